@@ -1,0 +1,56 @@
+"""End-to-end oracle for one synth.Problem: O1–O11 in the paper's order.
+
+build_tpfa -> Cartesian partition + open-box supports -> P^0 -> smoothing ->
+(fault-split level) -> A_c per level -> multibasis Richardson (+ dynamic stage).
+TEST INFRASTRUCTURE ONLY.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from . import basis as _basis
+from . import partition as _part
+from . import support as _sup
+from . import tpfa as _tpfa
+from .cycle import Level, iterate
+
+
+def cartesian_level(prob, A_T, sweeps=None, fixed=None):
+    part, M, _ = _part.cartesian(prob.nx, prob.ny, prob.nz, prob.block)
+    pat = _sup.box_pattern(prob.nx, prob.ny, prob.nz, prob.block)
+    P0 = _basis.indicator(part, pat)
+    ms = prob.max_sweeps if sweeps is None else sweeps
+    fx = prob.fixed_sweeps if fixed is None else fixed
+    P, n, deltas = _basis.smooth(P0, A_T, prob.omega, ms, prob.sweep_tol, fx)
+    return dict(part=part, M=M, pattern=pat, P=P, sweeps=n, deltas=deltas)
+
+
+def split_level(prob, A_T, cart, sweeps=None, fixed=None):
+    spart, Ms = _part.fault_split(prob, cart["part"])
+    pat = _sup.flood_pattern(prob, cart["part"], cart["pattern"], spart, Ms)
+    P0 = _basis.indicator(spart, pat)
+    ms = prob.max_sweeps if sweeps is None else sweeps
+    fx = prob.fixed_sweeps if fixed is None else fixed
+    P, n, deltas = _basis.smooth(P0, A_T, prob.omega, ms, prob.sweep_tol, fx)
+    return dict(part=spart, M=Ms, pattern=pat, P=P, sweeps=n, deltas=deltas)
+
+
+def run(prob, sweeps=None, fixed_sweeps=None, fixed_iters=None, max_iter=None,
+        record_dynamic=False, x0=None):
+    A_T, A, q, trans = _tpfa.build(prob)
+    cart = cartesian_level(prob, A_T, sweeps, fixed_sweeps)
+    levels_info = [cart]
+    if prob.split_level:
+        levels_info.append(split_level(prob, A_T, cart, sweeps, fixed_sweeps))
+    levels = [Level(li["P"].matrix(), A) for li in levels_info]
+    dyn = None
+    if prob.dynamic:
+        dyn = dict(nx=prob.nx, ny=prob.ny, nz=prob.nz, edges=prob.dyn_edges,
+                   max_blocks=prob.dyn_max_blocks)
+    fi = prob.fixed_iters if fixed_iters is None else fixed_iters
+    mi = prob.max_iter if max_iter is None else max_iter
+    x0 = np.zeros(prob.N) if x0 is None else x0
+    sol = iterate(A, q, x0, levels, prob.omega_s, prob.nu, prob.post_smooth,
+                  prob.cycle_tol, mi, fi, dyn, record_dynamic)
+    return dict(A_T=A_T, A=A, q=q, trans=trans, levels_info=levels_info, levels=levels,
+                sol=sol)
