@@ -1,0 +1,329 @@
+"""Thin Python binding over libmsb's C ABI (include/msb.h): argument marshalling
+only.  Every arithmetic step of the hot path runs in the library's CUDA kernels.
+
+Arrays may be torch tensors (CUDA or CPU) or NumPy arrays; they are passed to the
+library as raw pointers (host or device — the library detects which).  Device
+memory for the library's own handles comes from the PyTorch caching allocator
+through the context's allocator hook.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from typing import Optional, Sequence
+
+import numpy as np
+
+from . import _lib as L
+
+OK, NOT_CONVERGED = 0, 1
+_ERRNAMES = {-1: "EINVAL", -2: "EDIM", -3: "EZERO_DIAG", -4: "ESINGULAR",
+             -5: "EINCONSISTENT", -6: "EDIVERGED", -7: "ENOMEM", -8: "ECUDA"}
+
+
+class MsbError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"{_ERRNAMES.get(code, code)}: {msg}")
+        self.code = code
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def _ptr(a, dtype=np.float64):
+    """Raw pointer of a contiguous torch tensor / numpy array (None -> NULL)."""
+    if a is None:
+        return None
+    torch = None
+    try:
+        import torch as _t
+        torch = _t
+    except Exception:  # pragma: no cover
+        pass
+    if torch is not None and isinstance(a, torch.Tensor):
+        want = {np.float64: torch.float64, np.int32: torch.int32}[dtype]
+        if a.dtype != want or not a.is_contiguous():
+            raise TypeError(f"expected contiguous {want} tensor, got {a.dtype}")
+        return C.c_void_p(a.data_ptr())
+    if not isinstance(a, np.ndarray) or a.dtype != dtype or not a.flags.c_contiguous:
+        raise TypeError(f"expected contiguous numpy {np.dtype(dtype)} array")
+    return C.c_void_p(a.ctypes.data)
+
+
+class Context:
+    """msb_ctx on one CUDA device and stream (default: torch's current stream)."""
+
+    def __init__(self, device: int = 0, stream=None, torch_alloc: bool = True):
+        self.lib = L.load()
+        torch = _torch()
+        if not torch.cuda.is_available():
+            raise MsbError(-8, "no CUDA device: libmsb has no CPU path")
+        self.device = device
+        if stream is None:
+            stream = torch.cuda.current_stream(device)
+        self.stream = stream
+        handle = C.c_void_p(stream.cuda_stream)
+        self._keep = []
+        if torch_alloc:
+            dev = device
+
+            def _alloc(nbytes, user):
+                try:
+                    return torch.cuda.caching_allocator_alloc(int(nbytes), dev, self.stream)
+                except Exception:
+                    return None
+
+            def _free(ptr, user):
+                torch.cuda.caching_allocator_delete(ptr)
+
+            af, ff = L.ALLOC_FN(_alloc), L.FREE_FN(_free)
+        else:
+            af, ff = L.ALLOC_FN(), L.FREE_FN()
+        self._keep += [af, ff]
+        h = C.c_void_p()
+        st = self.lib.msb_ctx_create(C.byref(h), device, handle, af, ff, None)
+        if st != OK:
+            raise MsbError(st, "msb_ctx_create failed")
+        self.h = h
+
+    def check(self, st: int, what: str) -> int:
+        if st < 0:
+            raise MsbError(st, f"{what}: {self.lib.msb_last_error(self.h).decode()}")
+        return st
+
+    def launch_count(self) -> int:
+        return int(self.lib.msb_launch_count())
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.msb_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def _grid(nx, ny, nz, dx=1.0, dy=1.0, dz=1.0):
+    return L.Grid(int(nx), int(ny), int(nz), float(dx), float(dy), float(dz))
+
+
+class Operator:
+    """build_tpfa(grid, K, wells) — row a1.  K: (3N,) float64 SoA kx|ky|kz."""
+
+    def __init__(self, ctx: Context, nx, ny, nz, K, src_cells, src_rates, mult=None, mob=None,
+                 dx=1.0, dy=1.0, dz=1.0):
+        self.ctx = ctx
+        self.nx, self.ny, self.nz = int(nx), int(ny), int(nz)
+        self.N = self.nx * self.ny * self.nz
+        self.grid = _grid(nx, ny, nz, dx, dy, dz)
+        cells = np.asarray(src_cells, dtype=np.int64)
+        rates = np.asarray(src_rates, dtype=np.float64)
+        arr = (L.Source * max(1, len(cells)))()
+        for t, (c, r) in enumerate(zip(cells, rates)):
+            arr[t].cell = int(c)
+            arr[t].rate = float(r)
+        h = C.c_void_p()
+        st = ctx.lib.msb_build_tpfa(ctx.h, C.byref(self.grid), _ptr(K), _ptr(mult), _ptr(mob),
+                                    arr, len(cells), C.byref(h))
+        ctx.check(st, "msb_build_tpfa")
+        self.h = h
+
+    @property
+    def n_faces(self):
+        nx, ny, nz = self.nx, self.ny, self.nz
+        return (nx - 1) * ny * nz + nx * (ny - 1) * nz + nx * ny * (nz - 1)
+
+    def set_mobility(self, mob):
+        self.ctx.check(self.ctx.lib.msb_op_set_mobility(self.ctx.h, self.h, _ptr(mob)),
+                       "msb_op_set_mobility")
+
+    def export(self):
+        T = np.empty(self.n_faces)
+        q = np.empty(self.N)
+        self.ctx.check(self.ctx.lib.msb_op_export(self.ctx.h, self.h, _ptr(T), _ptr(q)),
+                       "msb_op_export")
+        return T, q
+
+    def apply(self, x, y):
+        self.ctx.check(self.ctx.lib.msb_op_apply(self.ctx.h, self.h, _ptr(x), _ptr(y)),
+                       "msb_op_apply")
+
+    def transport_upwind(self, p, S, phi, mu_w, mu_o, dt, mob_out=None):
+        n = C.c_int32()
+        self.ctx.check(self.ctx.lib.msb_transport_upwind(self.ctx.h, self.h, _ptr(p), _ptr(S),
+                                                         _ptr(phi), float(mu_w), float(mu_o),
+                                                         float(dt), _ptr(mob_out), C.byref(n)),
+                       "msb_transport_upwind")
+        return n.value
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.ctx.lib.msb_op_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def partition_cartesian(ctx: Context, nx, ny, nz, block, part_out=None):
+    g = _grid(nx, ny, nz)
+    M = C.c_int32()
+    ctx.check(ctx.lib.msb_partition_cartesian(ctx.h, C.byref(g), int(block[0]), int(block[1]),
+                                              int(block[2]), _ptr(part_out, np.int32), C.byref(M)),
+              "msb_partition_cartesian")
+    return M.value
+
+
+class Level:
+    """A (P, R = P^T, A_c) triple on one coarse partition."""
+
+    def __init__(self, ctx: Context, handle):
+        self.ctx = ctx
+        self.h = handle
+
+    # --- constructors (row a2)
+    @classmethod
+    def cartesian(cls, ctx: Context, op: Operator, block):
+        h = C.c_void_p()
+        nnz = C.c_int64()
+        ctx.check(ctx.lib.msb_level_create_cartesian(ctx.h, op.h, int(block[0]), int(block[1]),
+                                                     int(block[2]), C.byref(h), C.byref(nnz)),
+                  "msb_level_create_cartesian")
+        lev = cls(ctx, h)
+        lev.N = op.N
+        return lev
+
+    @classmethod
+    def split(cls, ctx: Context, op: Operator, parent: "Level"):
+        h = C.c_void_p()
+        nnz = C.c_int64()
+        ctx.check(ctx.lib.msb_level_create_split(ctx.h, op.h, parent.h, C.byref(h), C.byref(nnz)),
+                  "msb_level_create_split")
+        lev = cls(ctx, h)
+        lev.N = op.N
+        return lev
+
+    @classmethod
+    def constant(cls, ctx: Context, op: Operator, part, M: int):
+        h = C.c_void_p()
+        ctx.check(ctx.lib.msb_level_create_constant(ctx.h, op.h, _ptr(part, np.int32), int(M),
+                                                    C.byref(h)), "msb_level_create_constant")
+        lev = cls(ctx, h)
+        lev.N = op.N
+        return lev
+
+    def info(self, with_part=False):
+        M, nnz, W = C.c_int32(), C.c_int64(), C.c_int32()
+        part = np.empty(self.N, dtype=np.int32) if with_part else None
+        self.ctx.check(self.ctx.lib.msb_level_info(self.ctx.h, self.h, C.byref(M), C.byref(nnz),
+                                                   C.byref(W), _ptr(part, np.int32)),
+                       "msb_level_info")
+        out = dict(M=M.value, nnz=nnz.value, W=W.value)
+        if with_part:
+            out["part"] = part
+        return out
+
+    # --- row a3
+    def smooth(self, op: Operator, max_sweeps: int, omega: float = 2.0 / 3.0, tol: float = 1e-3):
+        n = C.c_int32()
+        last = C.c_double()
+        deltas = np.zeros(max(1, max_sweeps))
+        st = self.ctx.lib.msb_smooth_basis(self.ctx.h, self.h, op.h, int(max_sweeps),
+                                           float(omega), float(tol), C.byref(n), C.byref(last),
+                                           _ptr(deltas))
+        self.ctx.check(st, "msb_smooth_basis")
+        return n.value, last.value, deltas[:n.value], st
+
+    # --- rows a4, a5
+    def assemble(self, op: Operator):
+        self.ctx.check(self.ctx.lib.msb_coarse_assemble(self.ctx.h, self.h, op.h),
+                       "msb_coarse_assemble")
+
+    def export(self, with_Ac=False):
+        info = self.info()
+        N, nnz, M = self.N, info["nnz"], info["M"]
+        rowptr = np.empty(N + 1, dtype=np.int64)
+        cols = np.empty(nnz, dtype=np.int32)
+        vals = np.empty(nnz)
+        Ac = np.empty((M, M)) if with_Ac else None
+        self.ctx.check(self.ctx.lib.msb_level_export(self.ctx.h, self.h,
+                                                     C.c_void_p(rowptr.ctypes.data),
+                                                     _ptr(cols, np.int32), _ptr(vals),
+                                                     _ptr(Ac) if Ac is not None else None),
+                       "msb_level_export")
+        return rowptr, cols, vals, Ac
+
+    def import_values(self, vals):
+        self.ctx.check(self.ctx.lib.msb_level_import_values(self.ctx.h, self.h, _ptr(vals)),
+                       "msb_level_import_values")
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.ctx.lib.msb_level_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Solver:
+    """ms_iterate(b, tol) — rows a6–a11 (Eq. 8, Richardson, optional dynamic stage)."""
+
+    def __init__(self, ctx: Context, op: Operator, levels: Sequence[Level], omega_s=2.0 / 3.0,
+                 nu=1, post_smooth=False, dynamic=False, edges=(0.1, 0.5), max_blocks=1024):
+        self.ctx = ctx
+        self.op = op
+        self.levels = list(levels)
+        arr = (C.c_void_p * max(1, len(self.levels)))(*[lv.h.value for lv in self.levels])
+        h = C.c_void_p()
+        ctx.check(ctx.lib.msb_solver_create(ctx.h, op.h, arr, len(self.levels), float(omega_s),
+                                            int(nu), int(bool(post_smooth)), int(bool(dynamic)),
+                                            float(edges[0]), float(edges[1]), int(max_blocks),
+                                            C.byref(h)), "msb_solver_create")
+        self.h = h
+
+    def add_dynamic_basis(self, dp, part_out=None):
+        M = C.c_int32()
+        self.ctx.check(self.ctx.lib.msb_add_dynamic_basis(self.ctx.h, self.h, _ptr(dp), C.byref(M),
+                                                          _ptr(part_out, np.int32)),
+                       "msb_add_dynamic_basis")
+        return M.value
+
+    def iterate(self, x, b=None, tol=1e-6, max_iter=1000, fixed_iters=0, history=True):
+        """x: in x0 / out x (torch CUDA tensor or numpy array).  Returns a dict."""
+        n = C.c_int32()
+        cap = max(max_iter, fixed_iters) + 2
+        res = np.zeros(cap) if history else None
+        dyn = np.zeros(cap, dtype=np.int32) if history else None
+        st = self.ctx.lib.msb_ms_iterate(self.ctx.h, self.h, _ptr(b), _ptr(x), float(tol),
+                                         int(max_iter), int(fixed_iters), C.byref(n),
+                                         _ptr(res) if history else None,
+                                         _ptr(dyn, np.int32) if history else None)
+        self.ctx.check(st, "msb_ms_iterate")
+        k = n.value
+        out = dict(iters=k, status=st, converged=(st == OK and fixed_iters == 0))
+        if history:
+            out["res"] = res[:k + 1].copy()
+            out["dyn_M"] = dyn[:k].copy()
+        return out
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.ctx.lib.msb_solver_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

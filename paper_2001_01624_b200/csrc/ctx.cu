@@ -1,0 +1,199 @@
+// Context, allocation, host|dev staging, error reporting, device scan.
+#include "internal.cuh"
+
+namespace msb {
+
+std::atomic<int64_t> g_launches{0};
+
+msb_status set_error(msb_ctx ctx, msb_status code, const char* fmt, ...) {
+  if (ctx) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(ctx->err, sizeof(ctx->err), fmt, ap);
+    va_end(ap);
+  }
+  return code;
+}
+
+void* dalloc(msb_ctx ctx, size_t bytes) {
+  if (bytes == 0) bytes = 16;
+  if (ctx->alloc) return ctx->alloc(bytes, ctx->user);
+  void* p = nullptr;
+  if (cudaMalloc(&p, bytes) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  return p;
+}
+
+void dfree(msb_ctx ctx, void* p) {
+  if (!p) return;
+  if (ctx->free_fn) {
+    ctx->free_fn(p, ctx->user);
+    return;
+  }
+  cudaFree(p);
+}
+
+bool is_device_ptr(const void* p) {
+  if (!p) return false;
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+const void* stage_in(msb_ctx ctx, const void* p, size_t bytes, void** owned) {
+  *owned = nullptr;
+  if (!p) return nullptr;
+  if (is_device_ptr(p)) return p;
+  void* d = dalloc(ctx, bytes);
+  if (!d) return nullptr;
+  if (cudaMemcpyAsync(d, p, bytes, cudaMemcpyHostToDevice, ctx->stream) != cudaSuccess) {
+    dfree(ctx, d);
+    return nullptr;
+  }
+  *owned = d;
+  return d;
+}
+
+cudaError_t copy_out(msb_ctx ctx, void* dst, const void* src_dev, size_t bytes) {
+  if (!dst || bytes == 0) return cudaSuccess;
+  cudaError_t e = cudaMemcpyAsync(dst, src_dev, bytes, cudaMemcpyDefault, ctx->stream);
+  if (e != cudaSuccess) return e;
+  if (!is_device_ptr(dst)) return cudaStreamSynchronize(ctx->stream);
+  return cudaSuccess;
+}
+
+cudaError_t copy_in(msb_ctx ctx, void* dst_dev, const void* src, size_t bytes) {
+  if (!src || bytes == 0) return cudaSuccess;
+  cudaError_t e = cudaMemcpyAsync(dst_dev, src, bytes, cudaMemcpyDefault, ctx->stream);
+  if (e != cudaSuccess) return e;
+  // pageable host memory may be reused by the caller right after return
+  if (!is_device_ptr(src)) return cudaStreamSynchronize(ctx->stream);
+  return cudaSuccess;
+}
+
+msb_status sync(msb_ctx ctx) {
+  cudaError_t e = cudaStreamSynchronize(ctx->stream);
+  if (e != cudaSuccess) return set_error(ctx, MSB_ECUDA, "stream sync: %s", cudaGetErrorString(e));
+  return MSB_OK;
+}
+
+// ---------------------------------------------------------------- exclusive scan (int32)
+static constexpr int SCAN_BLOCK = 1024;
+
+__global__ void k_scan_block(const int32_t* __restrict__ in, int32_t* __restrict__ out,
+                             int32_t* __restrict__ sums, int64_t n) {
+  __shared__ int32_t warp_tot[32];
+  int64_t i = (int64_t)blockIdx.x * SCAN_BLOCK + threadIdx.x;
+  int32_t v = i < n ? in[i] : 0;
+  int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int32_t x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) warp_tot[w] = x;
+  __syncthreads();
+  if (w == 0) {
+    int32_t t = warp_tot[lane];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int32_t y = __shfl_up_sync(0xffffffffu, t, o);
+      if (lane >= o) t += y;
+    }
+    warp_tot[lane] = t;
+  }
+  __syncthreads();
+  int32_t base = w > 0 ? warp_tot[w - 1] : 0;
+  if (i < n) out[i] = base + x - v;
+  if (threadIdx.x == SCAN_BLOCK - 1) sums[blockIdx.x] = base + x;
+}
+
+__global__ void k_scan_add(int32_t* __restrict__ out, const int32_t* __restrict__ offs, int64_t n) {
+  int64_t i = (int64_t)blockIdx.x * SCAN_BLOCK + threadIdx.x;
+  if (i < n) out[i] += offs[blockIdx.x];
+}
+
+msb_status scan_exclusive(msb_ctx ctx, const int32_t* in, int32_t* out, int64_t n,
+                          int32_t* total) {
+  int64_t nb = (n + SCAN_BLOCK - 1) / SCAN_BLOCK;
+  if (nb == 0) {
+    if (total) *total = 0;
+    return MSB_OK;
+  }
+  int32_t* sums = dalloc_n<int32_t>(ctx, nb + 1);
+  int32_t* offs = dalloc_n<int32_t>(ctx, nb + 1);
+  if (!sums || !offs) return set_error(ctx, MSB_ENOMEM, "scan scratch");
+  k_scan_block<<<(unsigned)nb, SCAN_BLOCK, 0, ctx->stream>>>(in, out, sums, n);
+  MSB_LAUNCH_CHECK(ctx);
+  msb_status st = MSB_OK;
+  if (nb > 1) {
+    int32_t t = 0;
+    st = scan_exclusive(ctx, sums, offs, nb, &t);
+    if (st != MSB_OK) return st;
+    k_scan_add<<<(unsigned)nb, SCAN_BLOCK, 0, ctx->stream>>>(out, offs, n);
+    MSB_LAUNCH_CHECK(ctx);
+  }
+  if (total) {
+    int32_t last_out = 0, last_in = 0;
+    MSB_CUDA_TRY(ctx, cudaMemcpyAsync(&last_out, out + n - 1, 4, cudaMemcpyDeviceToHost, ctx->stream));
+    MSB_CUDA_TRY(ctx, cudaMemcpyAsync(&last_in, in + n - 1, 4, cudaMemcpyDeviceToHost, ctx->stream));
+    MSB_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    *total = last_out + last_in;
+  }
+  dfree(ctx, sums);
+  dfree(ctx, offs);
+  return st;
+}
+
+}  // namespace msb
+
+// ---------------------------------------------------------------- ABI
+extern "C" {
+
+msb_status msb_ctx_create(msb_ctx* out, int device, void* cuda_stream, msb_alloc_fn alloc,
+                          msb_free_fn free_fn, void* user) {
+  if (!out) return MSB_EINVAL;
+  *out = nullptr;
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
+    cudaGetLastError();
+    return MSB_ECUDA;
+  }
+  if (device < 0 || device >= n) return MSB_EINVAL;
+  if (cudaSetDevice(device) != cudaSuccess) return MSB_ECUDA;
+  msb_ctx c = new msb_ctx_s();
+  c->device = device;
+  c->stream = (cudaStream_t)cuda_stream;
+  c->alloc = alloc;
+  c->free_fn = free_fn;
+  c->user = user;
+  cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device);
+  *out = c;
+  return MSB_OK;
+}
+
+msb_status msb_ctx_destroy(msb_ctx ctx) {
+  if (!ctx) return MSB_EINVAL;
+  delete ctx;
+  return MSB_OK;
+}
+
+msb_status msb_ctx_set_stream(msb_ctx ctx, void* s) {
+  if (!ctx) return MSB_EINVAL;
+  ctx->stream = (cudaStream_t)s;
+  return MSB_OK;
+}
+
+const char* msb_last_error(msb_ctx ctx) { return ctx ? ctx->err : "null context"; }
+
+const char* msb_version(void) { return "libmsb 0.1 sm_100a"; }
+
+int64_t msb_launch_count(void) { return msb::g_launches.load(); }
+
+}  // extern "C"

@@ -1,0 +1,675 @@
+// Rows a6–a11: the multibasis Richardson cycle (Eq. 8) and the
+// dynamic Δp stage.
+//
+// Kernels (all HBM-bound, fp64, one thread per cell, coalesced SoA loads):
+//   k_jacobi        x_out = x + ω_s D_A^{-1}(b - A x)           (a7; first kernel of an
+//                   iteration also reduces ||b - A x||^2 -> stop test, a11)
+//   k_res_restrict  r = b - A x, rc += P^T r                      (a6 + a8; warp-segmented
+//                   sums over runs of equal columns, one fp64 atomic per run)
+//   k_gemv          xc = A_c^{-1} rc                              (a5, coarse.cu)
+//   k_prolong       x += P xc                                     (a9; row gather)
+// Stop test on the device: per-block partial sums of r^2, the last block to arrive
+// sums them in block order (deterministic), records ρ_k and sets `done`; every
+// later kernel of the enqueued chunk sees `done` and returns at once, so the host
+// only synchronises once per chunk of iterations.
+#include <algorithm>
+#include <cmath>
+
+#include "internal.cuh"
+
+struct IterState {
+  int done;
+  int k;          // completed iterations
+  int arrive;
+  int converged;
+  int diverged;
+  int max_iter;
+  int fixed;
+  int pad;
+  double tol;
+  double bscale;  // ||b|| (1 if b = 0)
+  double r0;
+};
+
+namespace msb {
+
+constexpr int CT = 256;  // cycle kernel block size
+
+struct StencilT {
+  const double* Tx;
+  const double* Ty;
+  const double* Tz;
+  int nx, ny, nz;
+};
+
+// r = b - A x at cell c (gauge: A_00 doubled); returns r and D_A.
+__device__ __forceinline__ double residual_at(const StencilT& S, const double* __restrict__ x,
+                                              const double* __restrict__ b, int64_t c,
+                                              double* DA) {
+  int64_t sxy = (int64_t)S.nx * S.ny;
+  int i = (int)(c % S.nx), j = (int)((c / S.nx) % S.ny), k = (int)(c / sxy);
+  double txp = S.Tx[c], typ = S.Ty[c], tzp = S.Tz[c];
+  double txm = i > 0 ? S.Tx[c - 1] : 0.0;
+  double tym = j > 0 ? S.Ty[c - S.nx] : 0.0;
+  double tzm = k > 0 ? S.Tz[c - sxy] : 0.0;
+  double D = txp + txm + typ + tym + tzp + tzm;
+  double off = 0.0;
+  if (k > 0) off += tzm * x[c - sxy];
+  if (j > 0) off += tym * x[c - S.nx];
+  if (i > 0) off += txm * x[c - 1];
+  if (i < S.nx - 1) off += txp * x[c + 1];
+  if (j < S.ny - 1) off += typ * x[c + S.nx];
+  if (k < S.nz - 1) off += tzp * x[c + sxy];
+  double dA = (c == 0) ? 2.0 * D : D;
+  *DA = dA;
+  return b[c] - (dA * x[c] - off);
+}
+
+__device__ __forceinline__ double block_sum(double v) {
+  __shared__ double sh[32];
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = v;
+  __syncthreads();
+  double w = (threadIdx.x < (blockDim.x >> 5)) ? sh[threadIdx.x] : 0.0;
+  if (threadIdx.x < 32)
+    for (int o = 16; o > 0; o >>= 1) w += __shfl_xor_sync(0xffffffffu, w, o);
+  return w;  // valid in warp 0
+}
+
+// Deterministic global sum of per-block values; the last block finalises the stop test.
+// mode 0: stop test on ||r||; mode 1: store ||b|| into st->bscale.
+__device__ void norm_epilogue(double v, double* __restrict__ partials, IterState* st,
+                              double* __restrict__ res, int mode) {
+  __shared__ int last;
+  double bs = block_sum(v);
+  if (threadIdx.x == 0) {
+    partials[blockIdx.x] = bs;
+    __threadfence();
+    int t = atomicAdd(&st->arrive, 1);
+    last = (t == (int)gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  double s = 0.0;
+  for (int t = threadIdx.x; t < (int)gridDim.x; t += blockDim.x) s += *(volatile double*)(partials + t);
+  double tot = block_sum(s);
+  if (threadIdx.x == 0) {
+    st->arrive = 0;
+    double nrm = sqrt(tot);
+    if (mode == 1) {
+      st->bscale = nrm > 0.0 ? nrm : 1.0;
+    } else {
+      int k = st->k;
+      double rho = nrm / st->bscale;
+      res[k] = rho;
+      if (k == 0) st->r0 = nrm;
+      int done = 0;
+      if (st->fixed > 0) {
+        if (k >= st->fixed) {
+          done = 1;
+          st->converged = rho <= st->tol;
+        }
+      } else {
+        if (rho <= st->tol) {
+          done = 1;
+          st->converged = 1;
+        } else if (k >= st->max_iter) {
+          done = 1;
+        }
+      }
+      if (!(nrm <= 1e6 * st->r0) && st->r0 > 0.0) {  // also catches NaN
+        done = 1;
+        st->diverged = 1;
+      }
+      if (done) st->done = 1;
+      else st->k = k + 1;
+    }
+    __threadfence();
+  }
+}
+
+__global__ void __launch_bounds__(CT) k_norm(StencilT S, const double* __restrict__ x,
+                                             const double* __restrict__ b, int mode,
+                                             double* __restrict__ partials, IterState* st,
+                                             double* __restrict__ res) {
+  if (mode == 0 && *(volatile int*)&st->done) return;
+  int64_t N = (int64_t)S.nx * S.ny * S.nz;
+  int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  double v = 0.0;
+  if (c < N) {
+    if (mode == 1) {
+      v = b[c] * b[c];
+    } else {
+      double dA;
+      double r = residual_at(S, x, b, c, &dA);
+      v = r * r;
+    }
+  }
+  norm_epilogue(v, partials, st, res, mode);
+}
+
+__global__ void __launch_bounds__(CT) k_jacobi(StencilT S, const double* __restrict__ x,
+                                               double* __restrict__ xo,
+                                               const double* __restrict__ b, double omega,
+                                               int first, double* __restrict__ partials,
+                                               IterState* st, double* __restrict__ res) {
+  if (*(volatile int*)&st->done) return;
+  int64_t N = (int64_t)S.nx * S.ny * S.nz;
+  int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  double v = 0.0;
+  if (c < N) {
+    double dA;
+    double r = residual_at(S, x, b, c, &dA);
+    xo[c] = x[c] + omega * (r / dA);
+    v = r * r;
+  }
+  if (first) norm_epilogue(v, partials, st, res, 0);
+}
+
+struct LevelView {
+  int kind, W, nx, ny, nb0, nb1;
+  int64_t N;
+  const int32_t* tab;
+  const int32_t* col;
+  const double* P;
+};
+
+__device__ __forceinline__ int lv_col(const LevelView& L, int64_t c, int i, int j, int k, int s) {
+  if (L.kind == 1) return L.col[(int64_t)s * L.N + c];
+  int jx = L.tab[2 * i + (s & 1)], jy = L.tab[2 * (L.nx + j) + ((s >> 1) & 1)],
+      jz = L.tab[2 * (L.nx + L.ny + k) + (s >> 2)];
+  if (jx < 0 || jy < 0 || jz < 0) return -1;
+  return jx + L.nb0 * (jy + L.nb1 * jz);
+}
+
+// Sum val over runs of equal key in consecutive lanes; the last lane of each run
+// with key >= 0 adds the run total to out[key].
+__device__ __forceinline__ void warp_segmented_add(int key, double val, double* __restrict__ out) {
+  const unsigned full = 0xffffffffu;
+  int lane = threadIdx.x & 31;
+  int prev = __shfl_up_sync(full, key, 1);
+  int head = (lane == 0) || (prev != key);
+  // segment start lane for each lane
+  unsigned heads = __ballot_sync(full, head);
+  int start = 31 - __clz(heads & ((2u << lane) - 1u));
+  double s = val;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    double y = __shfl_up_sync(full, s, o);
+    if (lane - o >= start) s += y;
+  }
+  int next = __shfl_down_sync(full, key, 1);
+  int tail = (lane == 31) || (next != key);
+  if (tail && key >= 0) atomicAdd(out + key, s);
+}
+
+__global__ void __launch_bounds__(CT) k_res_restrict(StencilT S, LevelView L,
+                                                     const double* __restrict__ x,
+                                                     const double* __restrict__ b,
+                                                     double* __restrict__ rc, int first,
+                                                     double* __restrict__ partials, IterState* st,
+                                                     double* __restrict__ res) {
+  if (*(volatile int*)&st->done) return;
+  int64_t N = L.N;
+  int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  bool in = c < N;
+  int64_t cc = in ? c : N - 1;
+  int64_t sxy = (int64_t)S.nx * S.ny;
+  int i = (int)(cc % S.nx), j = (int)((cc / S.nx) % S.ny), k = (int)(cc / sxy);
+  double r = 0.0;
+  if (in) {
+    double dA;
+    r = residual_at(S, x, b, c, &dA);
+  }
+  if (L.kind == 0) {
+#pragma unroll
+    for (int s = 0; s < 8; ++s) {
+      int key = in ? lv_col(L, cc, i, j, k, s) : -1;
+      double v = key >= 0 ? L.P[(int64_t)s * N + c] * r : 0.0;
+      warp_segmented_add(key, v, rc);
+    }
+  } else {
+    for (int s = 0; s < L.W; ++s) {
+      int key = in ? L.col[(int64_t)s * N + c] : -1;
+      double v = key >= 0 ? L.P[(int64_t)s * N + c] * r : 0.0;
+      warp_segmented_add(key, v, rc);
+    }
+  }
+  if (first) norm_epilogue(r * r, partials, st, res, 0);
+}
+
+__global__ void __launch_bounds__(CT) k_prolong(LevelView L, double* __restrict__ x,
+                                                const double* __restrict__ xc, const int* done) {
+  if (*(volatile const int*)done) return;
+  int64_t N = L.N;
+  int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= N) return;
+  int64_t sxy = (int64_t)L.nx * L.ny;
+  int i = (int)(c % L.nx), j = (int)((c / L.nx) % L.ny), k = (int)(c / sxy);
+  double acc = 0.0;
+  if (L.kind == 0) {
+#pragma unroll
+    for (int s = 0; s < 8; ++s) {
+      int key = lv_col(L, c, i, j, k, s);
+      if (key >= 0) acc += L.P[(int64_t)s * N + c] * xc[key];
+    }
+  } else {
+    for (int s = 0; s < L.W; ++s) {
+      int key = L.col[(int64_t)s * N + c];
+      if (key >= 0) acc += L.P[(int64_t)s * N + c] * xc[key];
+    }
+  }
+  x[c] += acc;
+}
+
+__global__ void k_zero_if(double* __restrict__ p, int n, const int* done) {
+  if (*(volatile const int*)done) return;
+  int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < n) p[t] = 0.0;
+}
+
+// ---------------------------------------------------------------- dynamic partition kernels
+__global__ void k_dp(const double* __restrict__ x, const double* __restrict__ xp, int64_t N,
+                     double* __restrict__ dp, unsigned long long* __restrict__ mx) {
+  int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  double a = 0.0;
+  if (c < N) {
+    double d = x[c] - xp[c];
+    dp[c] = d;
+    a = fabs(d);
+  }
+  for (int o = 16; o > 0; o >>= 1) a = fmax(a, __shfl_xor_sync(0xffffffffu, a, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(mx, (unsigned long long)__double_as_longlong(a));
+}
+
+__global__ void k_absmax_vec(const double* __restrict__ dp, int64_t N, unsigned long long* mx) {
+  int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  double a = c < N ? fabs(dp[c]) : 0.0;
+  for (int o = 16; o > 0; o >>= 1) a = fmax(a, __shfl_xor_sync(0xffffffffu, a, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(mx, (unsigned long long)__double_as_longlong(a));
+}
+
+__global__ void k_bins(const double* __restrict__ dp, int64_t N, const unsigned long long* mx,
+                       double e0, double e1, int32_t* __restrict__ bins) {
+  int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= N) return;
+  double m = __longlong_as_double((long long)*mx);
+  double a = fabs(dp[c]);
+  bins[c] = (a >= e0 * m) + (a >= e1 * m);
+}
+
+__global__ void k_sizes(const int32_t* __restrict__ lab, int64_t N, int32_t* __restrict__ cnt) {
+  int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c < N) atomicAdd(cnt + lab[c], 1);
+}
+
+// counts[0] = #roots with size >= smin; counts[1..3] = bin b has a small component
+__global__ void k_merge_count(const int32_t* __restrict__ lab, const int32_t* __restrict__ cnt,
+                              const int32_t* __restrict__ bins, int64_t N, int smin,
+                              int32_t* __restrict__ counts) {
+  int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= N) return;
+  if (lab[c] != (int32_t)c) return;
+  if (cnt[c] >= smin) atomicAdd(counts, 1);
+  else atomicExch(counts + 1 + bins[c], 1);
+}
+
+__global__ void k_merge_rep(const int32_t* __restrict__ lab, const int32_t* __restrict__ cnt,
+                            const int32_t* __restrict__ bins, int64_t N, int smin,
+                            int32_t* __restrict__ rep) {
+  int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= N) return;
+  if (cnt[lab[c]] < smin) atomicMin(rep + bins[c], (int32_t)c);
+}
+
+__global__ void k_merge_label(int32_t* __restrict__ lab, const int32_t* __restrict__ cnt,
+                              const int32_t* __restrict__ bins, int64_t N, int smin,
+                              const int32_t* __restrict__ rep, int32_t* __restrict__ out) {
+  int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= N) return;
+  int32_t r = lab[c];
+  out[c] = cnt[r] < smin ? rep[bins[c]] : r;
+}
+
+__global__ void k_refill_const(const int32_t* __restrict__ part, int64_t N, int32_t* __restrict__ col,
+                               double* __restrict__ P) {
+  int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= N) return;
+  col[c] = part[c];
+  P[c] = 1.0;
+}
+
+}  // namespace msb
+
+using namespace msb;
+
+static StencilT stencil(msb_op op) { return StencilT{op->Tx, op->Ty, op->Tz, op->nx, op->ny, op->nz}; }
+
+static LevelView view(msb_level L) {
+  return LevelView{L->kind, L->W, L->nx, L->ny, L->nb[0], L->nb[1], L->N, L->tab, L->col,
+                   L->P[L->cur]};
+}
+
+// Build the dynamic constant-basis stage from dp (device, length N) into s->dyn_level.
+static msb_status build_dynamic(msb_ctx ctx, msb_solver s, const double* dp, int32_t* M_out,
+                                int32_t* part_out) {
+  msb_op op = s->op;
+  int64_t N = op->N;
+  cudaStream_t st = ctx->stream;
+  unsigned long long* mx = reinterpret_cast<unsigned long long*>(s->scratch_i);
+  int32_t* counts = s->scratch_i + 2;
+  int32_t* rep = s->scratch_i + 8;
+  MSB_CUDA_TRY(ctx, cudaMemsetAsync(mx, 0, 8, st));
+  k_absmax_vec<<<grid_for(N, 256), 256, 0, st>>>(dp, N, mx);
+  MSB_LAUNCH_CHECK(ctx);
+  unsigned long long hm = 0;
+  MSB_CUDA_TRY(ctx, cudaMemcpyAsync(&hm, mx, 8, cudaMemcpyDeviceToHost, st));
+  MSB_CUDA_TRY(ctx, cudaStreamSynchronize(st));
+  double m;
+  memcpy(&m, &hm, 8);
+  if (!(m > 0.0)) {  // max|Δp| = 0: stage skipped
+    *M_out = 0;
+    return MSB_OK;
+  }
+  k_bins<<<grid_for(N, 256), 256, 0, st>>>(dp, N, mx, s->edge0, s->edge1, s->bins);
+  MSB_LAUNCH_CHECK(ctx);
+  msb_status rc = cc_label(ctx, op, s->bins, s->lab, false, nullptr);
+  if (rc) return rc;
+  MSB_CUDA_TRY(ctx, cudaMemsetAsync(s->cnt, 0, N * sizeof(int32_t), st));
+  k_sizes<<<grid_for(N, 256), 256, 0, st>>>(s->lab, N, s->cnt);
+  MSB_LAUNCH_CHECK(ctx);
+  int smin = 1;
+  while (true) {
+    MSB_CUDA_TRY(ctx, cudaMemsetAsync(counts, 0, 4 * sizeof(int32_t), st));
+    k_merge_count<<<grid_for(N, 256), 256, 0, st>>>(s->lab, s->cnt, s->bins, N, smin, counts);
+    MSB_LAUNCH_CHECK(ctx);
+    int32_t hc[4];
+    MSB_CUDA_TRY(ctx, cudaMemcpyAsync(hc, counts, sizeof(hc), cudaMemcpyDeviceToHost, st));
+    MSB_CUDA_TRY(ctx, cudaStreamSynchronize(st));
+    int nb = hc[0] + hc[1] + hc[2] + hc[3];
+    if (nb <= s->dyn_max || (int64_t)smin > N) break;
+    smin *= 2;
+  }
+  int32_t big[3] = {INT32_MAX, INT32_MAX, INT32_MAX};
+  MSB_CUDA_TRY(ctx, cudaMemcpyAsync(rep, big, sizeof(big), cudaMemcpyHostToDevice, st));
+  k_merge_rep<<<grid_for(N, 256), 256, 0, st>>>(s->lab, s->cnt, s->bins, N, smin, rep);
+  MSB_LAUNCH_CHECK(ctx);
+  k_merge_label<<<grid_for(N, 256), 256, 0, st>>>(s->lab, s->cnt, s->bins, N, smin, rep, s->ids);
+  MSB_LAUNCH_CHECK(ctx);
+  int32_t M = 0;
+  // canonical numbering: labels are minimum cells of their blocks
+  rc = canonical_number(ctx, N, s->ids, s->lab, s->cnt /* 2N scratch: cnt|bins reused */, &M);
+  if (rc) return rc;
+  msb_level D = s->dyn_level;
+  k_refill_const<<<grid_for(N, 256), 256, 0, st>>>(s->lab, N, D->col, D->P[0]);
+  MSB_LAUNCH_CHECK(ctx);
+  MSB_CUDA_TRY(ctx, cudaMemcpyAsync(D->part, s->lab, N * sizeof(int32_t), cudaMemcpyDeviceToDevice, st));
+  D->cur = 0;
+  D->M = M;
+  rc = coarse_assemble_dense(ctx, D, op);
+  if (rc) return rc;
+  if (part_out) MSB_CUDA_TRY(ctx, copy_out(ctx, part_out, D->part, N * sizeof(int32_t)));
+  *M_out = M;
+  return MSB_OK;
+}
+
+extern "C" {
+
+msb_status msb_solver_create(msb_ctx ctx, msb_op op, const msb_level* levels, int32_t n_levels,
+                             double omega_s, int32_t nu, int32_t post_smooth, int32_t dyn_enable,
+                             double dyn_edge0, double dyn_edge1, int32_t dyn_max_blocks,
+                             msb_solver* out) {
+  if (!ctx || !op || !out || n_levels < 0 || (n_levels > 0 && !levels) || nu < 0)
+    return set_error(ctx, MSB_EINVAL, "msb_solver_create args");
+  if (n_levels == 0 && !dyn_enable) return set_error(ctx, MSB_EINVAL, "solver needs a level");
+  msb_solver s = new msb_solver_s();
+  s->ctx = ctx;
+  s->op = op;
+  s->omega_s = omega_s;
+  s->nu = nu;
+  s->post = post_smooth ? 1 : 0;
+  s->dyn = dyn_enable ? 1 : 0;
+  s->edge0 = dyn_edge0;
+  s->edge1 = dyn_edge1;
+  s->dyn_max = dyn_max_blocks > 0 ? dyn_max_blocks : 1024;
+  int maxM = 1;
+  for (int l = 0; l < n_levels; ++l) {
+    msb_level L = levels[l];
+    if (!L || L->N != op->N) return set_error(ctx, MSB_EDIM, "level %d size mismatch", l);
+    if (!L->co.ready) return set_error(ctx, MSB_EINVAL, "level %d not assembled", l);
+    s->levels.push_back(L);
+    maxM = std::max(maxM, L->M);
+  }
+  int64_t N = op->N;
+  if (s->dyn) maxM = std::max(maxM, s->dyn_max + 3);
+  s->maxM = maxM;
+  MSB_ALLOC(ctx, s->xbuf[0], double, N);
+  MSB_ALLOC(ctx, s->xbuf[1], double, N);
+  MSB_ALLOC(ctx, s->rc, double, maxM + 2);
+  MSB_ALLOC(ctx, s->xc, double, maxM + 2);
+  MSB_ALLOC(ctx, s->partials, double, grid_for(N, CT) + 32);
+  s->st = dalloc_n<IterState>(ctx, 1);
+  if (!s->st) return set_error(ctx, MSB_ENOMEM, "solver state");
+  if (s->dyn) {
+    MSB_ALLOC(ctx, s->xprev, double, N);
+    MSB_ALLOC(ctx, s->r, double, N);
+    MSB_ALLOC(ctx, s->lab, int32_t, N);
+    MSB_ALLOC(ctx, s->ids, int32_t, N);
+    MSB_ALLOC(ctx, s->cnt, int32_t, 2 * N);
+    s->bins = s->cnt + N;  // bins live in the second half of the cnt scratch
+    MSB_ALLOC(ctx, s->scratch_i, int32_t, 64);
+    // constant-basis level reused across iterations
+    msb_level D = new msb_level_s();
+    D->ctx = ctx;
+    D->kind = 1;
+    D->N = N;
+    D->W = 1;
+    D->nnz = N;
+    D->nx = op->nx; D->ny = op->ny; D->nz = op->nz;
+    MSB_ALLOC(ctx, D->P[0], double, N);
+    MSB_ALLOC(ctx, D->P[1], double, N);
+    MSB_ALLOC(ctx, D->col, int32_t, N);
+    MSB_ALLOC(ctx, D->part, int32_t, N);
+    int cap = s->dyn_max + 3;
+    MSB_ALLOC(ctx, D->co.Ac, double, (int64_t)cap * cap);
+    MSB_ALLOC(ctx, D->co.L, double, (int64_t)cap * cap);
+    MSB_ALLOC(ctx, D->co.Ainv, double, (int64_t)cap * cap);
+    D->co.cap = cap;
+    s->dyn_level = D;
+  }
+  // bins must not alias cnt during counting: give them their own buffer
+  if (s->dyn) {
+    int32_t* b;
+    MSB_ALLOC(ctx, b, int32_t, N);
+    s->bins = b;
+  }
+  *out = s;
+  return MSB_OK;
+}
+
+msb_status msb_add_dynamic_basis(msb_ctx ctx, msb_solver s, const double* dp, int32_t* M_dyn_out,
+                                 int32_t* part_out) {
+  if (!ctx || !s || !dp) return set_error(ctx, MSB_EINVAL, "msb_add_dynamic_basis: null");
+  if (!s->dyn) return set_error(ctx, MSB_EINVAL, "solver created without dynamic stage");
+  void* o = nullptr;
+  const double* d = (const double*)stage_in(ctx, dp, s->op->N * sizeof(double), &o);
+  int32_t M = 0;
+  msb_status st = build_dynamic(ctx, s, d, &M, part_out);
+  if (o) {
+    cudaStreamSynchronize(ctx->stream);
+    dfree(ctx, o);
+  }
+  if (st) return st;
+  if (M == 0) s->dyn_level->M = 0;
+  if (M_dyn_out) *M_dyn_out = M;
+  return sync(ctx);
+}
+
+// Enqueue one stage (level L) on x buffers; `first` marks the iteration's first kernel.
+static msb_status enqueue_stage(msb_ctx ctx, msb_solver s, msb_level L, const double* b, int& cur,
+                                bool& first) {
+  msb_op op = s->op;
+  int64_t N = op->N;
+  cudaStream_t st = ctx->stream;
+  StencilT S = stencil(op);
+  LevelView V = view(L);
+  unsigned g = grid_for(N, CT);
+  const int* done = &s->st->done;
+  auto jac = [&]() -> msb_status {
+    for (int v = 0; v < s->nu; ++v) {
+      k_jacobi<<<g, CT, 0, st>>>(S, s->xbuf[cur], s->xbuf[cur ^ 1], b, s->omega_s, first ? 1 : 0,
+                                 s->partials, s->st, s->res_dev);
+      MSB_LAUNCH_CHECK(ctx);
+      first = false;
+      cur ^= 1;
+    }
+    return MSB_OK;
+  };
+  auto corr = [&]() -> msb_status {
+    k_zero_if<<<grid_for(L->M, 256), 256, 0, st>>>(s->rc, L->M, done);
+    MSB_LAUNCH_CHECK(ctx);
+    k_res_restrict<<<g, CT, 0, st>>>(S, V, s->xbuf[cur], b, s->rc, first ? 1 : 0, s->partials,
+                                     s->st, s->res_dev);
+    MSB_LAUNCH_CHECK(ctx);
+    first = false;
+    coarse_solve_dense(ctx, L->co, s->rc, s->xc, done);
+    k_prolong<<<g, CT, 0, st>>>(V, s->xbuf[cur], s->xc, done);
+    MSB_LAUNCH_CHECK(ctx);
+    return MSB_OK;
+  };
+  msb_status rc;
+  if (s->post) {
+    if ((rc = corr())) return rc;
+    if ((rc = jac())) return rc;
+  } else {
+    if ((rc = jac())) return rc;
+    if ((rc = corr())) return rc;
+  }
+  return MSB_OK;
+}
+
+msb_status msb_ms_iterate(msb_ctx ctx, msb_solver s, const double* b, double* x, double tol,
+                          int32_t max_iter, int32_t fixed_iters, int32_t* iters_out,
+                          double* res_hist, int32_t* dyn_M_hist) {
+  if (!ctx || !s || !x) return set_error(ctx, MSB_EINVAL, "msb_ms_iterate: null");
+  if (max_iter < 0 || fixed_iters < 0) return set_error(ctx, MSB_EINVAL, "negative iteration count");
+  msb_op op = s->op;
+  int64_t N = op->N;
+  cudaStream_t st = ctx->stream;
+  int cap = std::max(max_iter, fixed_iters) + 2;
+  if (s->res_cap < cap) {
+    dfree(ctx, s->res_dev);
+    MSB_ALLOC(ctx, s->res_dev, double, cap);
+    s->res_cap = cap;
+  }
+  void* ob = nullptr;
+  const double* db = b ? (const double*)stage_in(ctx, b, N * sizeof(double), &ob) : op->q;
+  if (!db) return set_error(ctx, MSB_ENOMEM, "rhs staging");
+  MSB_CUDA_TRY(ctx, cudaMemcpyAsync(s->xbuf[0], x, N * sizeof(double), cudaMemcpyDefault, st));
+  IterState h{};
+  h.max_iter = max_iter;
+  h.fixed = fixed_iters;
+  h.tol = tol;
+  h.bscale = 1.0;
+  MSB_CUDA_TRY(ctx, cudaMemcpyAsync(s->st, &h, sizeof(h), cudaMemcpyHostToDevice, st));
+  StencilT S = stencil(op);
+  unsigned g = grid_for(N, CT);
+  k_norm<<<g, CT, 0, st>>>(S, s->xbuf[0], db, 1, s->partials, s->st, s->res_dev);
+  MSB_LAUNCH_CHECK(ctx);
+  int cur = 0;
+  int target = fixed_iters > 0 ? fixed_iters : max_iter;
+  std::vector<int> cur_after;  // buffer holding x_k
+  cur_after.push_back(0);
+  std::vector<int32_t> dynM;
+  IterState hs{};
+  msb_status rc = MSB_OK;
+  if (!s->dyn) {
+    const int chunk = 8;
+    int issued = 0;
+    while (true) {
+      int n = std::min(chunk, target - issued);
+      for (int t = 0; t < n; ++t) {
+        bool first = true;
+        for (msb_level L : s->levels)
+          if ((rc = enqueue_stage(ctx, s, L, db, cur, first))) return rc;
+        cur_after.push_back(cur);
+      }
+      issued += n;
+      if (issued >= target) {
+        k_norm<<<g, CT, 0, st>>>(S, s->xbuf[cur], db, 0, s->partials, s->st, s->res_dev);
+        MSB_LAUNCH_CHECK(ctx);
+      }
+      MSB_CUDA_TRY(ctx, cudaMemcpyAsync(&hs, s->st, sizeof(hs), cudaMemcpyDeviceToHost, st));
+      MSB_CUDA_TRY(ctx, cudaStreamSynchronize(st));
+      if (hs.done || issued >= target) break;
+    }
+  } else {
+    // dynamic stage: host-synchronous per iteration (M_dyn is data dependent)
+    while (true) {
+      k_norm<<<g, CT, 0, st>>>(S, s->xbuf[cur], db, 0, s->partials, s->st, s->res_dev);
+      MSB_LAUNCH_CHECK(ctx);
+      MSB_CUDA_TRY(ctx, cudaMemcpyAsync(&hs, s->st, sizeof(hs), cudaMemcpyDeviceToHost, st));
+      MSB_CUDA_TRY(ctx, cudaStreamSynchronize(st));
+      if (hs.done) break;
+      int k = hs.k;  // iteration about to run (1-based)
+      int32_t M = 0;
+      if (k >= 2) {
+        k_dp<<<grid_for(N, 256), 256, 0, st>>>(s->xbuf[cur], s->xprev, N, s->r,
+                                               reinterpret_cast<unsigned long long*>(s->scratch_i));
+        count_launch();
+        if ((rc = build_dynamic(ctx, s, s->r, &M, nullptr))) return rc;
+      }
+      dynM.push_back(M);
+      MSB_CUDA_TRY(ctx, cudaMemcpyAsync(s->xprev, s->xbuf[cur], N * sizeof(double),
+                                        cudaMemcpyDeviceToDevice, st));
+      bool first = false;  // norm already taken
+      for (msb_level L : s->levels)
+        if ((rc = enqueue_stage(ctx, s, L, db, cur, first))) return rc;
+      if (M > 0)
+        if ((rc = enqueue_stage(ctx, s, s->dyn_level, db, cur, first))) return rc;
+      cur_after.push_back(cur);
+    }
+  }
+  int k = hs.k;
+  int xb = cur_after[std::min<size_t>(k, cur_after.size() - 1)];
+  MSB_CUDA_TRY(ctx, cudaMemcpyAsync(x, s->xbuf[xb], N * sizeof(double), cudaMemcpyDefault, st));
+  if (res_hist)
+    MSB_CUDA_TRY(ctx, cudaMemcpyAsync(res_hist, s->res_dev, (k + 1) * sizeof(double),
+                                      cudaMemcpyDefault, st));
+  MSB_CUDA_TRY(ctx, cudaStreamSynchronize(st));
+  if (ob) dfree(ctx, ob);
+  if (dyn_M_hist) {
+    for (size_t t = 0; t < dynM.size() && (int)t < cap; ++t) dyn_M_hist[t] = dynM[t];
+  }
+  if (iters_out) *iters_out = k;
+  if (hs.diverged) return set_error(ctx, MSB_EDIVERGED, "residual grew by more than 1e6");
+  if (fixed_iters > 0) return MSB_OK;
+  if (!hs.converged) return MSB_NOT_CONVERGED;
+  return MSB_OK;
+}
+
+msb_status msb_solver_destroy(msb_solver s) {
+  if (!s) return MSB_EINVAL;
+  msb_ctx ctx = s->ctx;
+  dfree(ctx, s->xbuf[0]);
+  dfree(ctx, s->xbuf[1]);
+  dfree(ctx, s->xprev);
+  dfree(ctx, s->r);
+  dfree(ctx, s->rc);
+  dfree(ctx, s->xc);
+  dfree(ctx, s->partials);
+  dfree(ctx, s->st);
+  dfree(ctx, s->res_dev);
+  dfree(ctx, s->lab);
+  dfree(ctx, s->ids);
+  dfree(ctx, s->cnt);
+  dfree(ctx, s->bins);
+  dfree(ctx, s->scratch_i);
+  if (s->dyn_level) level_free(s->dyn_level);
+  delete s;
+  return MSB_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,326 @@
+// Row a2 (fault-split partition + flood-fill supports) and the partition half of
+// row a10 (Δp-binned dynamic partition).
+//
+// Connected components use lock-free union-find (hook the larger root under the
+// smaller with atomicCAS, path-halving finds, then full compression).  Roots only
+// ever move to smaller indices, so the final root of a component is its minimum
+// node index — exactly the canonical "ascending minimum cell index" numbering of
+// the oracle after an exclusive scan over root flags.
+#include <algorithm>
+
+#include "internal.cuh"
+
+namespace msb {
+
+__device__ __forceinline__ int32_t uf_find(int32_t* __restrict__ par, int32_t x) {
+  int32_t p = par[x];
+  while (p != x) {
+    int32_t g = par[p];
+    if (g != p) par[x] = g;  // path halving (benign race: values only decrease)
+    x = p;
+    p = g;
+  }
+  return x;
+}
+
+__device__ __forceinline__ void uf_union(int32_t* __restrict__ par, int32_t a, int32_t b) {
+  while (true) {
+    a = uf_find(par, a);
+    b = uf_find(par, b);
+    if (a == b) return;
+    int32_t hi = a > b ? a : b, lo = a > b ? b : a;
+    int32_t old = atomicCAS(par + hi, hi, lo);
+    if (old == hi) return;
+    a = old;  // hi got hooked meanwhile; retry from its new parent
+    b = lo;
+  }
+}
+
+__global__ void k_iota(int32_t* __restrict__ p, int64_t n) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) p[i] = (int32_t)i;
+}
+
+__global__ void k_compress(int32_t* __restrict__ par, int64_t n) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) par[i] = uf_find(par, (int32_t)i);
+}
+
+// Cells joined across +x/+y/+z faces when klass matches and (optionally) the face
+// is open (multiplier == 1).
+__global__ void k_cc_cells(const int32_t* __restrict__ klass, const uint8_t* __restrict__ open,
+                           int nx, int ny, int nz, int32_t* __restrict__ par) {
+  int64_t N = (int64_t)nx * ny * nz;
+  int64_t sxy = (int64_t)nx * ny;
+  int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= N) return;
+  int i = (int)(c % nx), j = (int)((c / nx) % ny), k = (int)(c / sxy);
+  uint8_t o = open ? open[c] : 7;
+  int32_t kc = klass[c];
+  if (i < nx - 1 && (o & 1) && klass[c + 1] == kc) uf_union(par, (int32_t)c, (int32_t)(c + 1));
+  if (j < ny - 1 && (o & 2) && klass[c + nx] == kc) uf_union(par, (int32_t)c, (int32_t)(c + nx));
+  if (k < nz - 1 && (o & 4) && klass[c + sxy] == kc) uf_union(par, (int32_t)c, (int32_t)(c + sxy));
+}
+
+__global__ void k_root_flags(const int32_t* __restrict__ lab, int64_t n, int32_t* __restrict__ f) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) f[i] = lab[i] == (int32_t)i;
+}
+
+__global__ void k_gather_ids(const int32_t* __restrict__ lab, const int32_t* __restrict__ ids,
+                             int64_t n, int32_t* __restrict__ out) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = ids[lab[i]];
+}
+
+// lab[i] must be a cell index that is its own label for the representative cell.
+msb_status canonical_number(msb_ctx ctx, int64_t N, const int32_t* lab, int32_t* out,
+                            int32_t* scratch, int32_t* M_out) {
+  int32_t* flags = scratch;
+  int32_t* ids = scratch + N;
+  k_root_flags<<<grid_for(N, 256), 256, 0, ctx->stream>>>(lab, N, flags);
+  MSB_LAUNCH_CHECK(ctx);
+  int32_t M = 0;
+  msb_status st = scan_exclusive(ctx, flags, ids, N, &M);
+  if (st != MSB_OK) return st;
+  k_gather_ids<<<grid_for(N, 256), 256, 0, ctx->stream>>>(lab, ids, N, out);
+  MSB_LAUNCH_CHECK(ctx);
+  *M_out = M;
+  return MSB_OK;
+}
+
+msb_status cc_label(msb_ctx ctx, msb_op op, const int32_t* klass, int32_t* lab, bool use_open,
+                    int32_t*) {
+  int64_t N = op->N;
+  k_iota<<<grid_for(N, 256), 256, 0, ctx->stream>>>(lab, N);
+  MSB_LAUNCH_CHECK(ctx);
+  k_cc_cells<<<grid_for(N, 256), 256, 0, ctx->stream>>>(klass, use_open ? op->open : nullptr,
+                                                        op->nx, op->ny, op->nz, lab);
+  MSB_LAUNCH_CHECK(ctx);
+  k_compress<<<grid_for(N, 256), 256, 0, ctx->stream>>>(lab, N);
+  MSB_LAUNCH_CHECK(ctx);
+  return MSB_OK;
+}
+
+// ---------------------------------------------------------------- flood-fill supports
+// Nodes (s, c) of the parent Cartesian level's active slots; node id = s*N + c.
+// Joined across open faces when the neighbour holds the same column in slot s.
+__global__ void k_cc_slots(const int32_t* __restrict__ tab, const uint8_t* __restrict__ open,
+                           int nx, int ny, int nz, int32_t* __restrict__ par) {
+  int64_t N = (int64_t)nx * ny * nz;
+  int64_t sxy = (int64_t)nx * ny;
+  int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= N) return;
+  int i = (int)(c % nx), j = (int)((c / nx) % ny), k = (int)(c / sxy);
+  uint8_t o = open[c];
+  const int32_t* tx = tab + 2 * i;
+  const int32_t* ty = tab + 2 * (nx + j);
+  const int32_t* tz = tab + 2 * (nx + ny + k);
+  for (int s = 0; s < 8; ++s) {
+    int px = s & 1, py = (s >> 1) & 1, pz = s >> 2;
+    int jx = tx[px], jy = ty[py], jz = tz[pz];
+    if (jx < 0 || jy < 0 || jz < 0) continue;
+    int32_t a = (int32_t)(s * N + c);
+    if (i < nx - 1 && (o & 1) && tab[2 * (i + 1) + px] == jx) uf_union(par, a, a + 1);
+    if (j < ny - 1 && (o & 2) && tab[2 * (nx + j + 1) + py] == jy) uf_union(par, a, (int32_t)(a + nx));
+    if (k < nz - 1 && (o & 4) && tab[2 * (nx + ny + k + 1) + pz] == jz)
+      uf_union(par, a, (int32_t)(a + sxy));
+  }
+}
+
+constexpr int KCH = 6;  // max distinct split blocks attached to one box component
+
+// Attach each cell's split block to the component of its own-parent slot node.
+__global__ void k_attach(const int32_t* __restrict__ par, const int32_t* __restrict__ ppart,
+                         const int32_t* __restrict__ spart, int nbx, int nby, int64_t N,
+                         int32_t* __restrict__ lists, int* __restrict__ overflow) {
+  int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= N) return;
+  int J = ppart[c];
+  int s = (J % nbx & 1) | (((J / nbx) % nby & 1) << 1) | ((J / (nbx * nby) & 1) << 2);
+  int32_t root = par[(int64_t)s * N + c];
+  int32_t child = spart[c];
+  int32_t* L = lists + (int64_t)root * KCH;
+  for (int t = 0; t < KCH; ++t) {
+    int32_t old = atomicCAS(L + t, -1, child);
+    if (old == -1 || old == child) return;
+  }
+  atomicExch(overflow, 1);
+}
+
+__device__ __forceinline__ int gather_cols(const int32_t* __restrict__ tab,
+                                           const int32_t* __restrict__ par,
+                                           const int32_t* __restrict__ lists, int nx, int ny,
+                                           int64_t N, int64_t c, int* cols, int cap) {
+  int i = (int)(c % nx), j = (int)((c / nx) % ny), k = (int)(c / ((int64_t)nx * ny));
+  const int32_t* tx = tab + 2 * i;
+  const int32_t* ty = tab + 2 * (nx + j);
+  const int32_t* tz = tab + 2 * (nx + ny + k);
+  int n = 0;
+  for (int s = 0; s < 8; ++s) {
+    if (tx[s & 1] < 0 || ty[(s >> 1) & 1] < 0 || tz[s >> 2] < 0) continue;
+    int32_t root = par[(int64_t)s * N + c];
+    const int32_t* L = lists + (int64_t)root * KCH;
+    for (int t = 0; t < KCH; ++t) {
+      int32_t v = L[t];
+      if (v < 0) break;
+      bool dup = false;
+      for (int u = 0; u < n; ++u) dup |= cols[u] == v;
+      if (dup) continue;
+      if (n < cap) {
+        int p = n;
+        while (p > 0 && cols[p - 1] > v) {
+          cols[p] = cols[p - 1];
+          --p;
+        }
+        cols[p] = v;
+      }
+      ++n;
+    }
+  }
+  return n;
+}
+
+__global__ void k_flood_count(const int32_t* __restrict__ tab, const int32_t* __restrict__ par,
+                              const int32_t* __restrict__ lists, int nx, int ny, int64_t N,
+                              int* __restrict__ wmax, unsigned long long* __restrict__ nnz) {
+  int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= N) return;
+  int cols[64];
+  int n = gather_cols(tab, par, lists, nx, ny, N, c, cols, 64);
+  atomicMax(wmax, n);
+  atomicAdd(nnz, (unsigned long long)n);
+}
+
+__global__ void k_flood_fill(const int32_t* __restrict__ tab, const int32_t* __restrict__ par,
+                             const int32_t* __restrict__ lists, const int32_t* __restrict__ spart,
+                             int nx, int ny, int64_t N, int W, int32_t* __restrict__ col,
+                             double* __restrict__ P0, double* __restrict__ P1) {
+  int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= N) return;
+  int cols[64];
+  int n = gather_cols(tab, par, lists, nx, ny, N, c, cols, 64);
+  int own = spart[c];
+  for (int s = 0; s < W; ++s) {
+    int v = s < n ? cols[s] : -1;
+    col[(int64_t)s * N + c] = v;
+    double p = (v >= 0 && v == own) ? 1.0 : 0.0;
+    P0[(int64_t)s * N + c] = p;
+    P1[(int64_t)s * N + c] = 0.0;
+  }
+}
+
+__global__ void k_fill_i32(int32_t* __restrict__ p, int64_t n, int32_t v) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) p[i] = v;
+}
+
+__global__ void k_nbs_ell2(const int32_t* __restrict__ col, int W, int nx, int ny, int nz,
+                           int8_t* __restrict__ nbs) {
+  int64_t N = (int64_t)nx * ny * nz;
+  int64_t sxy = (int64_t)nx * ny;
+  int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= N) return;
+  int i = (int)(c % nx), j = (int)((c / nx) % ny), k = (int)(c / sxy);
+  int64_t nb[6] = {c - sxy, c - nx, c - 1, c + 1, c + nx, c + sxy};
+  bool ex[6] = {k > 0, j > 0, i > 0, i < nx - 1, j < ny - 1, k < nz - 1};
+  for (int s = 0; s < W; ++s) {
+    int jc = col[(int64_t)s * N + c];
+    for (int d = 0; d < 6; ++d) {
+      int r = -1;
+      if (jc >= 0 && ex[d]) {
+        for (int t = 0; t < W; ++t) {
+          int v = col[(int64_t)t * N + nb[d]];
+          if (v == jc) {
+            r = t;
+            break;
+          }
+        }
+      }
+      nbs[((int64_t)d * W + s) * N + c] = (int8_t)r;
+    }
+  }
+}
+
+}  // namespace msb
+
+using namespace msb;
+
+extern "C" msb_status msb_level_create_split(msb_ctx ctx, msb_op op, msb_level parent,
+                                             msb_level* out, int64_t* nnz_out) {
+  if (!ctx || !op || !parent || !out) return set_error(ctx, MSB_EINVAL, "split level: null");
+  if (parent->kind != 0) return set_error(ctx, MSB_EINVAL, "split level needs a Cartesian parent");
+  int64_t N = op->N;
+  if (8 * N >= (int64_t)INT32_MAX) return set_error(ctx, MSB_EINVAL, "grid too large for split level");
+  // 1. split partition: components of each parent block over open faces
+  int32_t *lab, *spart, *scratch;
+  MSB_ALLOC(ctx, lab, int32_t, N);
+  MSB_ALLOC(ctx, spart, int32_t, N);
+  MSB_ALLOC(ctx, scratch, int32_t, 2 * N);
+  msb_status st = cc_label(ctx, op, parent->part, lab, true, nullptr);
+  if (st) return st;
+  int32_t Ms = 0;
+  st = canonical_number(ctx, N, lab, spart, scratch, &Ms);
+  if (st) return st;
+  // 2. components of each parent support box (slot nodes) over open faces
+  int32_t* par;
+  MSB_ALLOC(ctx, par, int32_t, 8 * N);
+  k_iota<<<grid_for(8 * N, 256), 256, 0, ctx->stream>>>(par, 8 * N);
+  MSB_LAUNCH_CHECK(ctx);
+  k_cc_slots<<<grid_for(N, 256), 256, 0, ctx->stream>>>(parent->tab, op->open, op->nx, op->ny,
+                                                        op->nz, par);
+  MSB_LAUNCH_CHECK(ctx);
+  k_compress<<<grid_for(8 * N, 256), 256, 0, ctx->stream>>>(par, 8 * N);
+  MSB_LAUNCH_CHECK(ctx);
+  // 3. attach split blocks to box components; gather columns per cell
+  int32_t* lists;
+  MSB_ALLOC(ctx, lists, int32_t, 8 * N * KCH);
+  k_fill_i32<<<grid_for(8 * N * KCH, 256), 256, 0, ctx->stream>>>(lists, 8 * N * KCH, -1);
+  MSB_LAUNCH_CHECK(ctx);
+  int* flags = dalloc_n<int>(ctx, 2);
+  unsigned long long* dnnz = dalloc_n<unsigned long long>(ctx, 1);
+  MSB_CUDA_TRY(ctx, cudaMemsetAsync(flags, 0, 2 * sizeof(int), ctx->stream));
+  MSB_CUDA_TRY(ctx, cudaMemsetAsync(dnnz, 0, 8, ctx->stream));
+  k_attach<<<grid_for(N, 256), 256, 0, ctx->stream>>>(par, parent->part, spart, parent->nb[0],
+                                                      parent->nb[1], N, lists, flags);
+  MSB_LAUNCH_CHECK(ctx);
+  k_flood_count<<<grid_for(N, 128), 128, 0, ctx->stream>>>(parent->tab, par, lists, op->nx, op->ny,
+                                                           N, flags + 1, dnnz);
+  MSB_LAUNCH_CHECK(ctx);
+  int hf[2];
+  unsigned long long hn = 0;
+  MSB_CUDA_TRY(ctx, cudaMemcpyAsync(hf, flags, sizeof(hf), cudaMemcpyDeviceToHost, ctx->stream));
+  MSB_CUDA_TRY(ctx, cudaMemcpyAsync(&hn, dnnz, 8, cudaMemcpyDeviceToHost, ctx->stream));
+  MSB_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  if (hf[0]) return set_error(ctx, MSB_EINVAL, "split level: more than %d blocks per box component", KCH);
+  int W = hf[1];
+  if (W > 64 || W > 127) return set_error(ctx, MSB_EINVAL, "split level: %d supports per cell", W);
+  msb_level L = new msb_level_s();
+  L->ctx = ctx;
+  L->kind = 1;
+  L->N = N;
+  L->M = Ms;
+  L->W = W;
+  L->nnz = (int64_t)hn;
+  L->nx = op->nx; L->ny = op->ny; L->nz = op->nz;
+  L->part = spart;
+  MSB_ALLOC(ctx, L->col, int32_t, (int64_t)W * N);
+  MSB_ALLOC(ctx, L->P[0], double, (int64_t)W * N);
+  MSB_ALLOC(ctx, L->P[1], double, (int64_t)W * N);
+  MSB_ALLOC(ctx, L->nbs, int8_t, (int64_t)6 * W * N);
+  k_flood_fill<<<grid_for(N, 128), 128, 0, ctx->stream>>>(parent->tab, par, lists, spart, op->nx,
+                                                          op->ny, N, W, L->col, L->P[0], L->P[1]);
+  MSB_LAUNCH_CHECK(ctx);
+  k_nbs_ell2<<<grid_for(N, 128), 128, 0, ctx->stream>>>(L->col, W, op->nx, op->ny, op->nz, L->nbs);
+  MSB_LAUNCH_CHECK(ctx);
+  MSB_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  dfree(ctx, lab);
+  dfree(ctx, scratch);
+  dfree(ctx, par);
+  dfree(ctx, lists);
+  dfree(ctx, flags);
+  dfree(ctx, dnnz);
+  if (nnz_out) *nnz_out = L->nnz;
+  *out = L;
+  return MSB_OK;
+}

@@ -1,0 +1,177 @@
+// Row a12 (auxiliary, config 4): face fluxes, explicit single-point-upstream
+// transport of water saturation, and the upstream total mobility for the next
+// pressure step (PAPER.md:41 sequential splitting, :101 single-point upstream;
+// readings A17, A18).  Quadratic relative permeabilities:
+//   λ_w = S^2/μ_w, λ_o = (1-S)^2/μ_o, λ_t = λ_w + λ_o, f_w = λ_w/λ_t.
+// fw_max' is the largest forward-difference slope of f_w on the grid S = k/1000
+// (the same rule in the oracle), so both sides pick the same sub-step count.
+#include <algorithm>
+#include <cmath>
+
+#include "internal.cuh"
+
+namespace msb {
+
+__device__ __host__ __forceinline__ double fw(double S, double muw, double muo) {
+  double lw = S * S / muw, lo = (1.0 - S) * (1.0 - S) / muo;
+  return lw / (lw + lo);
+}
+
+__device__ __forceinline__ double lam_t(double S, double muw, double muo) {
+  return S * S / muw + (1.0 - S) * (1.0 - S) / muo;
+}
+
+struct FluxView {
+  const double* Tx;
+  const double* Ty;
+  const double* Tz;
+  int nx, ny, nz;
+};
+
+// outflow_i = Σ_{faces} max(F_out, 0) + q_i^-   (q^- = -min(q, 0)); reduce min φ/out.
+__global__ void k_cfl(FluxView F, const double* __restrict__ p, const double* __restrict__ q,
+                      const double* __restrict__ phi, double vol,
+                      unsigned long long* __restrict__ minbits) {
+  int64_t N = (int64_t)F.nx * F.ny * F.nz;
+  int64_t sxy = (int64_t)F.nx * F.ny;
+  int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  double v = INFINITY;
+  if (c < N) {
+    int i = (int)(c % F.nx), j = (int)((c / F.nx) % F.ny), k = (int)(c / sxy);
+    double out = 0.0;
+    double pc = p[c];
+    if (i < F.nx - 1) out += fmax(F.Tx[c] * (pc - p[c + 1]), 0.0);
+    if (i > 0) out += fmax(F.Tx[c - 1] * (pc - p[c - 1]), 0.0);
+    if (j < F.ny - 1) out += fmax(F.Ty[c] * (pc - p[c + F.nx]), 0.0);
+    if (j > 0) out += fmax(F.Ty[c - F.nx] * (pc - p[c - F.nx]), 0.0);
+    if (k < F.nz - 1) out += fmax(F.Tz[c] * (pc - p[c + sxy]), 0.0);
+    if (k > 0) out += fmax(F.Tz[c - sxy] * (pc - p[c - sxy]), 0.0);
+    out += fmax(-q[c], 0.0);
+    if (out > 0.0) v = phi[c] * vol / out;
+  }
+  for (int o = 16; o > 0; o >>= 1) v = fmin(v, __shfl_xor_sync(0xffffffffu, v, o));
+  if ((threadIdx.x & 31) == 0) atomicMin(minbits, (unsigned long long)__double_as_longlong(v));
+}
+
+__global__ void k_transport_step(FluxView F, const double* __restrict__ p,
+                                 const double* __restrict__ q, const double* __restrict__ phi,
+                                 double vol, double muw, double muo, double h,
+                                 const double* __restrict__ S, double* __restrict__ So) {
+  int64_t N = (int64_t)F.nx * F.ny * F.nz;
+  int64_t sxy = (int64_t)F.nx * F.ny;
+  int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= N) return;
+  int i = (int)(c % F.nx), j = (int)((c / F.nx) % F.ny), k = (int)(c / sxy);
+  double pc = p[c], sc = S[c];
+  double fc = fw(sc, muw, muo);
+  double net = 0.0;
+  // flux F = T (p_c - p_l) leaves c when positive
+  auto face = [&](double T, int64_t l) {
+    double Fl = T * (pc - p[l]);
+    if (Fl > 0.0) net -= Fl * fc;
+    else net -= Fl * fw(S[l], muw, muo);  // inflow: -F > 0 carries f_w(S_l)
+  };
+  if (k > 0) face(F.Tz[c - sxy], c - sxy);
+  if (j > 0) face(F.Ty[c - F.nx], c - F.nx);
+  if (i > 0) face(F.Tx[c - 1], c - 1);
+  if (i < F.nx - 1) face(F.Tx[c], c + 1);
+  if (j < F.ny - 1) face(F.Ty[c], c + F.nx);
+  if (k < F.nz - 1) face(F.Tz[c], c + sxy);
+  double qc = q[c];
+  if (qc > 0.0) net += qc;           // injected water, f_w = 1
+  else net += qc * fc;               // produced at f_w(S_c)
+  So[c] = sc + h / (phi[c] * vol) * net;
+}
+
+// Upstream total mobility per face (compact face layout); ties (F = 0) -> lower cell.
+__global__ void k_upstream_mob(FluxView F, const double* __restrict__ p, const double* __restrict__ S,
+                               double muw, double muo, double* __restrict__ mob) {
+  int64_t N = (int64_t)F.nx * F.ny * F.nz;
+  int64_t sxy = (int64_t)F.nx * F.ny;
+  int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= N) return;
+  int nx = F.nx, ny = F.ny, nz = F.nz;
+  int i = (int)(c % nx), j = (int)((c / nx) % ny), k = (int)(c / sxy);
+  int64_t nfx = (int64_t)(nx - 1) * ny * nz;
+  int64_t nfy = (int64_t)nx * (ny - 1) * nz;
+  double pc = p[c];
+  if (i < nx - 1) {
+    int64_t l = c + 1;
+    double s = (pc - p[l] >= 0.0) ? S[c] : S[l];
+    mob[i + (int64_t)(nx - 1) * (j + (int64_t)ny * k)] = lam_t(s, muw, muo);
+  }
+  if (j < ny - 1) {
+    int64_t l = c + nx;
+    double s = (pc - p[l] >= 0.0) ? S[c] : S[l];
+    mob[nfx + i + (int64_t)nx * (j + (int64_t)(ny - 1) * k)] = lam_t(s, muw, muo);
+  }
+  if (k < nz - 1) {
+    int64_t l = c + sxy;
+    double s = (pc - p[l] >= 0.0) ? S[c] : S[l];
+    mob[nfx + nfy + c] = lam_t(s, muw, muo);
+  }
+}
+
+}  // namespace msb
+
+using namespace msb;
+
+extern "C" msb_status msb_transport_upwind(msb_ctx ctx, msb_op op, const double* p, double* S,
+                                           const double* phi, double mu_w, double mu_o, double dt,
+                                           double* mob_out, int32_t* substeps_out) {
+  if (!ctx || !op || !p || !S || !phi) return set_error(ctx, MSB_EINVAL, "transport: null");
+  if (!(mu_w > 0) || !(mu_o > 0) || !(dt >= 0)) return set_error(ctx, MSB_EINVAL, "transport: bad args");
+  int64_t N = op->N;
+  cudaStream_t st = ctx->stream;
+  FluxView F{op->Tx, op->Ty, op->Tz, op->nx, op->ny, op->nz};
+  double vol = op->dx * op->dy * op->dz;
+  // fw_max' on the uniform grid k/1000 (forward differences), as in the oracle
+  double fmaxd = 0.0;
+  for (int t = 0; t < 1000; ++t) {
+    double a = fw(t / 1000.0, mu_w, mu_o), b = fw((t + 1) / 1000.0, mu_w, mu_o);
+    fmaxd = std::max(fmaxd, (b - a) * 1000.0);
+  }
+  unsigned long long* mb = dalloc_n<unsigned long long>(ctx, 1);
+  double inf = INFINITY;
+  MSB_CUDA_TRY(ctx, cudaMemcpyAsync(mb, &inf, 8, cudaMemcpyHostToDevice, st));
+  k_cfl<<<grid_for(N, 256), 256, 0, st>>>(F, p, op->q, phi, vol, mb);
+  MSB_LAUNCH_CHECK(ctx);
+  unsigned long long hb = 0;
+  MSB_CUDA_TRY(ctx, cudaMemcpyAsync(&hb, mb, 8, cudaMemcpyDeviceToHost, st));
+  MSB_CUDA_TRY(ctx, cudaStreamSynchronize(st));
+  double mn;
+  memcpy(&mn, &hb, 8);
+  int nsub = 1;
+  if (std::isfinite(mn) && fmaxd > 0.0) {
+    double dt_cfl = 0.5 * mn / fmaxd;
+    nsub = std::max(1, (int)std::ceil(dt / dt_cfl));
+  }
+  double h = dt / nsub;
+  double* tmp = dalloc_n<double>(ctx, N);
+  if (!tmp) return set_error(ctx, MSB_ENOMEM, "transport scratch");
+  double* a = S;
+  double* b = tmp;
+  for (int t = 0; t < nsub; ++t) {
+    k_transport_step<<<grid_for(N, 256), 256, 0, st>>>(F, p, op->q, phi, vol, mu_w, mu_o, h, a, b);
+    MSB_LAUNCH_CHECK(ctx);
+    std::swap(a, b);
+  }
+  if (a != S) MSB_CUDA_TRY(ctx, cudaMemcpyAsync(S, a, N * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  if (mob_out) {
+    int64_t nf = (int64_t)(op->nx - 1) * op->ny * op->nz + (int64_t)op->nx * (op->ny - 1) * op->nz +
+                 (int64_t)op->nx * op->ny * (op->nz - 1);
+    bool dev = is_device_ptr(mob_out);
+    double* d = dev ? mob_out : dalloc_n<double>(ctx, nf);
+    k_upstream_mob<<<grid_for(N, 256), 256, 0, st>>>(F, p, S, mu_w, mu_o, d);
+    MSB_LAUNCH_CHECK(ctx);
+    if (!dev) {
+      MSB_CUDA_TRY(ctx, copy_out(ctx, mob_out, d, nf * sizeof(double)));
+      dfree(ctx, d);
+    }
+  }
+  MSB_CUDA_TRY(ctx, cudaStreamSynchronize(st));
+  dfree(ctx, tmp);
+  dfree(ctx, mb);
+  if (substeps_out) *substeps_out = nsub;
+  return MSB_OK;
+}

@@ -1,0 +1,215 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on the
+same seeded synthetic inputs (synth/).  Tolerances (BASELINE.json north_star,
+SURVEY.md §8.c protocol):
+  T, q           <= 1 ulp
+  P              exact zeros where the oracle has zeros, else |ΔP|/P <= 1e-10,
+                 after the same sweep count; sweeps-to-tol identical
+  A_c            entrywise <= 1e-12 max|A_c| (GPU assembles from the oracle's P)
+  x              ||Δx||_2/||x||_2 <= 1e-9 at equal iteration counts
+  iterations     |k_gpu - k_oracle| <= 1 in free mode
+  labels         integer partitions bit-exact (same Δp input)
+"""
+import numpy as np
+import pytest
+
+from synth.configs import make_problem, random_problem
+
+pytestmark = pytest.mark.gpu
+
+P_RTOL = 1e-10
+X_RTOL = 1e-9
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    from paper_2001_01624_b200 import Context
+    return Context(0)
+
+
+def _oracle_level(prob, sweeps, fixed, split=False):
+    from oracle import pipeline as opl
+    from oracle import tpfa
+    A_T, A, q, _ = tpfa.build(prob)
+    cart = opl.cartesian_level(prob, A_T, sweeps, fixed)
+    if not split:
+        return A_T, A, q, cart
+    return A_T, A, q, cart, opl.split_level(prob, A_T, cart, sweeps, fixed)
+
+
+def _assert_P(rowptr, cols, vals, basis):
+    pat = basis.pattern
+    assert np.array_equal(rowptr, pat.indptr.astype(np.int64))
+    assert np.array_equal(cols, pat.indices.astype(np.int32))
+    ref = basis.vals
+    zero = ref == 0.0
+    assert np.all(vals[zero] == 0.0), "GPU nonzero where oracle is exactly zero"
+    rel = np.abs(vals[~zero] - ref[~zero]) / np.abs(ref[~zero])
+    assert rel.max(initial=0.0) <= P_RTOL, rel.max()
+
+
+# ---------------------------------------------------------------- row a1
+@pytest.mark.parametrize("case", ["config1", "faulted3d", "nonunit"])
+def test_tpfa_parity(ctx, case):
+    from oracle import tpfa
+    from paper_2001_01624_b200.pipeline import build_operator
+    if case == "config1":
+        prob = make_problem(1)
+    elif case == "faulted3d":
+        prob = make_problem(3, shape=(18, 33, 10))
+    else:
+        prob = random_problem(3, 7, 5, 4, (2, 2, 2), sigma=2.0, dx=2.0, dy=0.5, dz=3.0)
+    op = build_operator(ctx, prob)
+    T, q = op.export()
+    tr = tpfa.transmissibilities(prob)
+    Tor = np.concatenate([t[2] for t in tr])
+    assert np.all(np.abs(T - Tor) <= np.spacing(np.abs(Tor)))
+    assert np.array_equal(q, prob.rhs())
+
+
+# ---------------------------------------------------------------- rows a2, a3
+BASIS_CASES = {
+    "config1_full": (lambda: make_problem(1), 200, True),
+    "config2_recipe_ragged": (lambda: make_problem(2, shape=(26, 47, 23)), 25, True),
+    "random_ragged": (lambda: random_problem(1, 23, 17, 7, (5, 4, 3), sigma=2.0), 40, True),
+    "config2_recipe_tol": (lambda: make_problem(2, shape=(24, 44, 20)), 300, False),
+    "2d_odd": (lambda: random_problem(2, 35, 21, 1, (7, 7, 1), sigma=1.0), 60, True),
+}
+
+
+@pytest.mark.parametrize("name", list(BASIS_CASES))
+def test_basis_parity(ctx, name):
+    from paper_2001_01624_b200 import Level
+    from paper_2001_01624_b200.pipeline import build_operator
+    mk, sweeps, fixed = BASIS_CASES[name]
+    prob = mk()
+    A_T, A, q, cart = _oracle_level(prob, sweeps, fixed)
+    op = build_operator(ctx, prob)
+    lev = Level.cartesian(ctx, op, prob.block)
+    info = lev.info()
+    assert info["M"] == cart["M"] and info["nnz"] == cart["pattern"].nnz
+    n, last, deltas, st = lev.smooth(op, sweeps, prob.omega, -1.0 if fixed else prob.sweep_tol)
+    assert n == cart["sweeps"], (n, cart["sweeps"])
+    assert np.allclose(deltas, cart["deltas"], rtol=1e-9, atol=1e-15)
+    rowptr, cols, vals, _ = lev.export()
+    _assert_P(rowptr, cols, vals, cart["P"])
+    part = lev.info(with_part=True)["part"]
+    assert np.array_equal(part, cart["part"].astype(np.int32))
+
+
+def test_basis_invariants_on_gpu(ctx):
+    """Partition of unity, bounds and single-support ones, directly on GPU output."""
+    from paper_2001_01624_b200 import Level
+    from paper_2001_01624_b200.pipeline import build_operator
+    prob = random_problem(4, 31, 19, 9, (6, 5, 3), sigma=2.5)
+    op = build_operator(ctx, prob)
+    lev = Level.cartesian(ctx, op, prob.block)
+    lev.smooth(op, 50, 2.0 / 3.0, -1.0)
+    rowptr, cols, vals, _ = lev.export()
+    rows = np.repeat(np.arange(prob.N), np.diff(rowptr))
+    rs = np.bincount(rows, weights=vals, minlength=prob.N)
+    assert np.max(np.abs(rs - 1.0)) <= 1e-14
+    assert vals.min() >= 0.0 and vals.max() <= 1.0
+    single = np.diff(rowptr) == 1
+    assert np.all(vals[np.repeat(single, np.diff(rowptr))] == 1.0)
+
+
+# ---------------------------------------------------------------- rows a4, a5
+@pytest.mark.parametrize("shape", [(24, 44, 20), (23, 17, 7)])
+def test_rap_parity_lockstep(ctx, shape):
+    """GPU RAP from the oracle's P (imported) against scipy P^T A P."""
+    from oracle import coarse
+    from paper_2001_01624_b200 import Level
+    from paper_2001_01624_b200.pipeline import build_operator
+    prob = make_problem(2, shape=shape) if shape[0] == 24 else random_problem(
+        5, *shape, (5, 4, 3), sigma=2.0)
+    A_T, A, q, cart = _oracle_level(prob, 20, True)
+    op = build_operator(ctx, prob)
+    lev = Level.cartesian(ctx, op, prob.block)
+    lev.import_values(np.ascontiguousarray(cart["P"].vals))
+    lev.assemble(op)
+    _, _, _, Ac = lev.export(with_Ac=True)
+    ref = coarse.galerkin(cart["P"].matrix(), A)
+    assert np.max(np.abs(Ac - ref)) <= 1e-12 * np.abs(ref).max()
+
+
+# ---------------------------------------------------------------- rows a6–a11
+def _gpu_full(ctx, prob, sweeps=None, fixed_sweeps=None, fixed_iters=None, max_iter=None):
+    from paper_2001_01624_b200 import pipeline as gp
+    r = gp.run(ctx, prob, sweeps, fixed_sweeps, fixed_iters, max_iter)
+    r["x_host"] = r["x"].cpu().numpy()
+    return r
+
+
+def _oracle_full(prob, sweeps=None, fixed_sweeps=None, fixed_iters=None, max_iter=None):
+    from oracle import pipeline as opl
+    return opl.run(prob, sweeps, fixed_sweeps, fixed_iters, max_iter)
+
+
+CYCLE_CASES = {
+    "config1_full": lambda: make_problem(1),
+    "config2_recipe": lambda: make_problem(2, shape=(24, 44, 20), max_sweeps=300),
+    "post_nu2_ragged": lambda: random_problem(6, 23, 17, 7, (5, 4, 3), sigma=1.5,
+                                              post_smooth=True, nu=2, max_sweeps=40),
+}
+
+
+@pytest.mark.parametrize("name", list(CYCLE_CASES))
+def test_cycle_parity(ctx, name):
+    prob = CYCLE_CASES[name]()
+    orc = _oracle_full(prob)
+    k_or = orc["sol"]["iters"]
+    assert orc["sol"]["converged"]
+    # free mode: iteration counts within ±1
+    g = _gpu_full(ctx, prob)
+    assert abs(g["sol"]["iters"] - k_or) <= 1, (g["sol"]["iters"], k_or)
+    # fixed mode at the oracle's count: pressure relative L2 <= 1e-9
+    g2 = _gpu_full(ctx, prob, fixed_iters=k_or)
+    xo = orc["sol"]["x"]
+    err = np.linalg.norm(g2["x_host"] - xo) / np.linalg.norm(xo)
+    assert err <= X_RTOL, err
+    assert np.allclose(g2["sol"]["res"], orc["sol"]["res"], rtol=1e-6, atol=0)
+
+
+def test_cycle_fixed_small_counts(ctx):
+    """Exactly K cycles including K = 1 and a first residual check."""
+    prob = random_problem(7, 16, 12, 5, (4, 4, 5), sigma=1.0, max_sweeps=30)
+    orc = _oracle_full(prob, fixed_iters=3)
+    g = _gpu_full(ctx, prob, fixed_iters=3)
+    assert g["sol"]["iters"] == 3
+    xo = orc["sol"]["x"]
+    assert np.linalg.norm(g["x_host"] - xo) / np.linalg.norm(xo) <= X_RTOL
+
+
+def test_zero_rhs_zero_iterations(ctx):
+    import torch
+    from paper_2001_01624_b200 import pipeline as gp
+    prob = random_problem(8, 10, 8, 1, (5, 4, 1), max_sweeps=10)
+    op = gp.build_operator(ctx, prob)
+    levels, _ = gp.build_levels(ctx, op, prob)
+    s = gp.make_solver(ctx, op, levels, prob)
+    x = torch.zeros(prob.N, dtype=torch.float64, device="cuda")
+    b = torch.zeros(prob.N, dtype=torch.float64, device="cuda")
+    out = s.iterate(x, b, 1e-6, 100)
+    assert out["iters"] == 0 and out["status"] == 0
+
+
+def test_line_drive_closed_form_gpu(ctx):
+    """Uniform K, source plane x=0, sink plane x=nx-1: p(x) = -x q / T."""
+    import torch
+    from synth.configs import Problem
+    from paper_2001_01624_b200 import pipeline as gp
+    nx, ny, nz = 15, 7, 5
+    N = nx * ny * nz
+    k = np.full(N, 2.0)
+    cells = np.arange(N)
+    i = cells % nx
+    src = np.concatenate([cells[i == 0], cells[i == nx - 1]])
+    rates = np.concatenate([np.full((i == 0).sum(), 0.5), np.full((i == nx - 1).sum(), -0.5)])
+    prob = Problem("ld", nx, ny, nz, k, k.copy(), k.copy(), src, rates, (5, 7, 5),
+                   max_sweeps=100, sweep_tol=1e-6, cycle_tol=1e-10)
+    r = gp.run(ctx, prob)
+    assert r["sol"]["converged"]
+    assert np.max(np.abs(r["x"].cpu().numpy() + i * 0.25)) < 1e-8
