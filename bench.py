@@ -1,0 +1,349 @@
+#!/usr/bin/env python
+"""bench.py — MsRSB basis smoothing + iterative multiscale cycle on one B200.
+
+Workload (BASELINE.json configs[1], "config2"): 60x220x85 = 1,122,000 cells, fp64
+TPFA, synthetic SPE10-shaped K (synth/, seed 2), 5-spot source columns, 6x11x5
+coarse blocks (M = 3,400), ω = 2/3, smoothing to δ <= 1e-3 or 300 sweeps, then the
+Richardson multiscale cycle (pre-Jacobi ν = 1, ω_s = 2/3) to ||r|| <= 1e-6 ||b||.
+
+One timed STEP = the whole hot path on HBM-resident inputs: build_tpfa ->
+Cartesian partition/supports -> smooth_basis -> coarse_assemble (RAP + Cholesky +
+inverse) -> ms_iterate.  Phases are timed with CUDA events on the library stream.
+value = basis smoothing sweeps/s (smoothing phase); ms_per_iteration = cycle phase /
+iterations.  e2e = the same metric with the whole step driven from pinned host
+buffers through the C ABI (K in, pressure out, copies inside the timed region).
+
+--impl reference runs the CPU oracle (oracle/) as it stands on a bounded sample of
+the same workload (rank 0 only).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "basis smoothing sweeps/s & ms per multiscale iteration; achieved HBM GB/s vs peak"
+WORKLOAD = "config2: 60x220x85 (1.122M cells) fp64 TPFA, channelized synthetic K, 6x11x5 blocks"
+
+
+def _peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {"hbm_gbs": 6650.0, "_fallback": True}
+
+
+def _dist():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def _cpu_info():
+    cores = os.cpu_count()
+    model = ""
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except Exception:
+        pass
+    return cores, model
+
+
+# ----------------------------------------------------------------------------- oracle arm
+def oracle_sample(prob, sweeps=10, iters=5):
+    """Time the CPU oracle as it stands (single thread) on a bounded sample."""
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    from oracle import basis as ob
+    from oracle import partition as opart
+    from oracle import support as osup
+    from oracle import tpfa as otpfa
+    from oracle.cycle import Level, stage
+
+    A_T, A, q, _ = otpfa.build(prob)
+    part, M, _ = opart.cartesian(prob.nx, prob.ny, prob.nz, prob.block)
+    pat = osup.box_pattern(prob.nx, prob.ny, prob.nz, prob.block)
+    P = ob.indicator(part, pat)
+    t0 = time.perf_counter()
+    for _ in range(sweeps):
+        P, _ = ob.sweep(P, A_T, prob.omega)
+    t_sw = time.perf_counter() - t0
+    out = dict(sweeps=sweeps, sweep_s=t_sw, sweeps_per_s=sweeps / t_sw)
+    if iters > 0:
+        import numpy as np
+        lev = Level(P.matrix(), A)
+        x = np.zeros(prob.N)
+        DA = A.diagonal()
+        t0 = time.perf_counter()
+        for _ in range(iters):
+            x = stage(A, DA, q, x, lev, prob.omega_s, prob.nu, prob.post_smooth)
+            np.linalg.norm(q - A @ x)
+        t_it = time.perf_counter() - t0
+        out.update(iters=iters, ms_per_iteration=1e3 * t_it / iters)
+    return out
+
+
+def run_reference(args):
+    ws, rank, _ = _dist()
+    if rank != 0:
+        return 0
+    from synth.configs import make_problem
+    prob = make_problem(2)
+    cores, model = _cpu_info()
+    for _ in range(args.warmup):
+        oracle_sample(prob, sweeps=1, iters=0)
+    times, sweeps = [], 0
+    res = None
+    for _ in range(args.steps):
+        res = oracle_sample(prob, sweeps=args.ref_sweeps, iters=0)
+        times.append(res["sweep_s"])
+        sweeps += res["sweeps"]
+    tot = sum(times)
+    value = sweeps / tot
+    it = oracle_sample(prob, sweeps=1, iters=3)
+    sample = (f"{args.ref_sweeps} oracle MsRSB sweeps per step on the full config2 grid "
+              f"(SciPy SpGEMM, 1 thread); ms/iteration from 3 oracle cycles")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "sweeps/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * tot / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "l2": "n/a (CPU)"},
+        "ms_per_iteration": it["ms_per_iteration"],
+        "cpu_baseline": {"value": value, "unit": "sweeps/s", "cores": 1, "kind": "oracle",
+                         "sample": sample, "cpu": model, "host_cores": cores},
+        "e2e": {"value": value, "unit": "sweeps/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ----------------------------------------------------------------------------- GPU arm
+class Clocks:
+    def __init__(self, idx):
+        self.idx = idx
+        self.p = None
+        self.path = os.path.join(ROOT, "gpurun_out", f"clocks_{idx}.csv")
+
+    def start(self):
+        os.makedirs(os.path.dirname(self.path), exist_ok=True)
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.f = open(self.path, "w")
+            self.p = subprocess.Popen(["nvidia-smi", f"--id={self.idx}", f"--query-gpu={q}",
+                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        try:
+            self.p.wait(timeout=5)
+        except Exception:
+            self.p.kill()
+        self.f.close()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            parts = [s.strip() for s in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx = float(parts[2])
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        sm.sort()
+        med = sm[len(sm) // 2] if sm else None
+        return {"sm_mhz": med, "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def run_gpu(args):
+    import numpy as np
+    import torch
+
+    ws, rank, local = _dist()
+    torch.cuda.set_device(local)
+    dist = None
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl")
+    from paper_2001_01624_b200 import Context, Level, Operator, Solver
+    from paper_2001_01624_b200 import pipeline as gp
+    from synth.configs import make_problem
+
+    prob = make_problem(2)
+    if args.max_iter:
+        prob.max_iter = args.max_iter
+    N = prob.N
+    stream = torch.cuda.current_stream()
+    ctx = Context(local, stream)
+    K_host = torch.from_numpy(gp.problem_K(prob)).pin_memory()
+    K_dev = K_host.to(f"cuda:{local}")
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=f"cuda:{local}")  # 256 MB > L2
+
+    def step(K, x_out=None, timers=None):
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
+        ev[0].record(stream)
+        op = Operator(ctx, prob.nx, prob.ny, prob.nz, K, prob.src_cells, prob.src_rates)
+        lev = Level.cartesian(ctx, op, prob.block)
+        ev[1].record(stream)
+        n, last, deltas, _ = lev.smooth(op, prob.max_sweeps, prob.omega, prob.sweep_tol)
+        ev[2].record(stream)
+        lev.assemble(op)
+        solver = Solver(ctx, op, [lev], prob.omega_s, prob.nu, prob.post_smooth)
+        x = torch.zeros(N, dtype=torch.float64, device=f"cuda:{local}")
+        ev[3].record(stream)
+        sol = solver.iterate(x, None, prob.cycle_tol, prob.max_iter, 0, history=True)
+        ev[4].record(stream)
+        if x_out is not None:
+            x_out.copy_(x, non_blocking=True)
+        torch.cuda.synchronize()
+        t = [ev[i].elapsed_time(ev[i + 1]) for i in range(4)]
+        info = dict(sweeps=n, iters=sol["iters"], t_setup=t[0], t_smooth=t[1], t_coarse=t[2],
+                    t_cycle=t[3], t_step=sum(t), res=float(sol["res"][-1]))
+        solver.close(); lev.close(); op.close()
+        return info
+
+    for _ in range(args.warmup):
+        step(K_dev)
+    clocks = Clocks(local)
+    flush.zero_()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    launches0 = ctx.launch_count()
+    clocks.start()
+    infos = []
+    for _ in range(args.steps):
+        flush.zero_()  # L2 flush between steps (256 MB write)
+        infos.append(step(K_dev))
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    launches = ctx.launch_count() - launches0
+    if dist:
+        dist.barrier()
+
+    # e2e: pinned host K in, pressure out, through the C ABI (copies inside the region)
+    x_host = torch.empty(N, dtype=torch.float64).pin_memory()
+    e2e = []
+    for _ in range(max(1, min(args.steps, 3))):
+        flush.zero_()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        inf = step(K_host, x_out=x_host)
+        e2e.append((time.perf_counter() - t0, inf["sweeps"]))
+
+    t_smooth = sum(i["t_smooth"] for i in infos) / 1e3
+    t_cycle = sum(i["t_cycle"] for i in infos) / 1e3
+    t_step = sum(i["t_step"] for i in infos) / 1e3
+    sweeps = sum(i["sweeps"] for i in infos)
+    iters = sum(i["iters"] for i in infos)
+    vals = torch.tensor([t_smooth, t_cycle, t_step], dtype=torch.float64, device=f"cuda:{local}")
+    if dist:
+        dist.all_reduce(vals, op=dist.ReduceOp.MAX)
+    t_smooth, t_cycle, t_step = vals.tolist()
+    if rank != 0:
+        return 0
+
+    # algorithmic bytes: sweep = 16 nnz + 8 faces; cycle stage =
+    # 16 nnz + 8 faces + 40 N + 8 M^2 (dense inverse GEMV)
+    nnz, faces, M = 6964260, prob.n_faces, 3400
+    b_sweep = 16 * nnz + 8 * faces
+    b_iter = 16 * nnz + 8 * faces + 40 * N + 8 * M * M
+    peaks = _peaks()
+    peak = peaks["hbm_gbs"]
+    per_sweep = t_smooth / sweeps
+    per_iter = t_cycle / max(1, iters)
+    gbs_sweep = b_sweep / per_sweep / 1e9
+    gbs_iter = b_iter / per_iter / 1e9
+    # dominant kernel by time share inside the step
+    if t_cycle >= t_smooth:
+        dom = dict(kernel="cycle iteration (k_jacobi+k_res_restrict+k_gemv+k_prolong)",
+                   achieved=gbs_iter, bytes=b_iter)
+    else:
+        dom = dict(kernel="k_sweep_cart", achieved=gbs_sweep, bytes=b_sweep)
+    value = ws * sweeps / t_smooth
+    cores, model = _cpu_info()
+    cpu = None
+    if not args.no_cpu_baseline:
+        s = oracle_sample(prob, sweeps=args.cpu_sweeps, iters=args.cpu_iters)
+        cpu = {"value": s["sweeps_per_s"], "unit": "sweeps/s", "cores": 1, "kind": "oracle",
+               "sample": f"{args.cpu_sweeps} oracle sweeps + {args.cpu_iters} oracle cycles on "
+                         f"the full config2 grid, single thread",
+               "ms_per_iteration": s.get("ms_per_iteration"), "cpu": model, "host_cores": cores}
+    e2e_t = sum(t for t, _ in e2e)
+    e2e_sw = sum(n for _, n in e2e)
+    line = {
+        "metric": METRIC, "value": value, "unit": "sweeps/s", "n_gpus": ws,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t_step / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": WORKLOAD, "grid": [60, 220, 85], "coarse_blocks": [6, 11, 5],
+                   "l2": "flushed between steps (256 MB write)",
+                   "parallelism": f"replicas x{ws}" if ws > 1 else "single GPU"},
+        "ms_per_iteration": 1e3 * per_iter,
+        "ms_per_sweep": 1e3 * per_sweep,
+        "sweeps_per_step": sweeps / args.steps, "iterations_per_step": iters / args.steps,
+        "final_rel_residual": infos[-1]["res"],
+        "phase_ms": {k: sum(i[k] for i in infos) / args.steps
+                     for k in ("t_setup", "t_smooth", "t_coarse", "t_cycle")},
+        "hbm": {"sweep_gbs": gbs_sweep, "cycle_gbs": gbs_iter, "peak_gbs": peak,
+                "sweep_frac": gbs_sweep / peak, "cycle_frac": gbs_iter / peak,
+                "sweep_frac_nominal_8tbs": gbs_sweep / 8000.0,
+                "cycle_frac_nominal_8tbs": gbs_iter / 8000.0},
+        "roofline": {"bound": "hbm", "kernel": dom["kernel"], "achieved": dom["achieved"],
+                     "peak": peak, "unit": "GB/s", "frac": dom["achieved"] / peak,
+                     "traffic": None, "algorithmic_bytes_per_launch": dom["bytes"],
+                     "peak_source": "measured (MEASURED_PEAKS.json hbm_gbs)"
+                     if not peaks.get("_fallback") else "fallback (B200_PROFILING.md)"},
+        "cpu_baseline": cpu,
+        "e2e": {"value": e2e_sw / e2e_t, "unit": "sweeps/s",
+                "ms_per_step": 1e3 * e2e_t / len(e2e),
+                "h2d_bytes_per_step": 3 * N * 8, "d2h_bytes_per_step": N * 8},
+        "gpu_launches": launches,
+        "clocks": clk,
+    }
+    print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--max-iter", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sweeps", type=int, default=20)
+    ap.add_argument("--cpu-iters", type=int, default=10)
+    ap.add_argument("--ref-sweeps", type=int, default=5)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_gpu(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -68,14 +68,21 @@ class Context:
         if torch_alloc:
             dev = device
 
+            t_alloc = torch.cuda.caching_allocator_alloc
+            t_free = torch.cuda.caching_allocator_delete
+            stream_ = self.stream
+
             def _alloc(nbytes, user):
                 try:
-                    return torch.cuda.caching_allocator_alloc(int(nbytes), dev, self.stream)
+                    return t_alloc(int(nbytes), dev, stream_)
                 except Exception:
                     return None
 
             def _free(ptr, user):
-                torch.cuda.caching_allocator_delete(ptr)
+                try:
+                    t_free(ptr)
+                except Exception:  # interpreter shutdown: the process is exiting anyway
+                    pass
 
             af, ff = L.ALLOC_FN(_alloc), L.FREE_FN(_free)
         else:

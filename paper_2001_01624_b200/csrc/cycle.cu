@@ -408,9 +408,21 @@ static msb_status build_dynamic(msb_ctx ctx, msb_solver s, const double* dp, int
   MSB_CUDA_TRY(ctx, cudaMemcpyAsync(D->part, s->lab, N * sizeof(int32_t), cudaMemcpyDeviceToDevice, st));
   D->cur = 0;
   D->M = M;
-  rc = coarse_assemble_dense(ctx, D, op);
-  if (rc) return rc;
   if (part_out) MSB_CUDA_TRY(ctx, copy_out(ctx, part_out, D->part, N * sizeof(int32_t)));
+  if (getenv("MSB_DEBUG")) {
+    MSB_CUDA_TRY(ctx, cudaStreamSynchronize(st));
+    fprintf(stderr, "[msb] dynamic partition M=%d smin=%d\n", M, smin);
+  }
+  rc = coarse_assemble_dense(ctx, D, op);
+  if (getenv("MSB_DEBUG")) {
+    std::vector<double> h((size_t)M * M);
+    cudaMemcpy(h.data(), D->co.Ac, h.size() * 8, cudaMemcpyDeviceToHost);
+    for (int a = 0; a < std::min(M, 6); ++a) {
+      for (int b = 0; b < std::min(M, 6); ++b) fprintf(stderr, " %12.6g", h[(size_t)a * M + b]);
+      fprintf(stderr, "\n");
+    }
+  }
+  if (rc) return rc;
   *M_out = M;
   return MSB_OK;
 }

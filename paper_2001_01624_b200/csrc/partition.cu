@@ -41,9 +41,19 @@ __global__ void k_iota(int32_t* __restrict__ p, int64_t n) {
   if (i < n) p[i] = (int32_t)i;
 }
 
+// Compression after all unions: read-only walk to the root (no path-halving writes,
+// which could overwrite another thread's already-compressed entry with a non-root
+// ancestor), then each thread writes only its own entry.
 __global__ void k_compress(int32_t* __restrict__ par, int64_t n) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) par[i] = uf_find(par, (int32_t)i);
+  if (i >= n) return;
+  int32_t x = (int32_t)i;
+  int32_t p = *(volatile int32_t*)(par + x);
+  while (p != x) {
+    x = p;
+    p = *(volatile int32_t*)(par + x);
+  }
+  par[i] = x;
 }
 
 // Cells joined across +x/+y/+z faces when klass matches and (optionally) the face

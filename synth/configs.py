@@ -195,11 +195,12 @@ def _config3(shape=None, seed=2, **kw) -> Problem:
         # proportional placement on reduced grids; partial planes end on block
         # boundaries (multiples of by) as in the full config
         by = p.block[1]
-        fx1, fx2 = max(1, nx // 3) - 1, max(2, (2 * nx) // 3) - 1
+        # planes placed strictly inside coarse blocks so that they split them
+        fx1, fx2 = nx // 3, min(nx - 2, (2 * nx) // 3 + 1)
         nby = -(-ny // by)
         j1 = by * max(1, (7 * nby) // 10)
         j2 = by * max(1, (3 * nby) // 10)
-        fy1, fy2 = max(1, ny // 3) - 1, max(2, (2 * ny) // 3) - 1
+        fy1, fy2 = ny // 3, min(ny - 2, (2 * ny) // 3 + 1)
         faults = [("x", fx1, 0, min(j1, ny), 0.0), ("x", fx2, min(j2, ny), ny, 0.0),
                   ("y", fy1, 0, nx, 1e-3), ("y", fy2, 0, nx, 1e-3)]
     mx, my, mz = fault_multipliers(nx, ny, nz, faults)
