@@ -8,10 +8,10 @@
 //                   sums over runs of equal columns, one fp64 atomic per run)
 //   k_gemv          xc = A_c^{-1} rc                              (a5, coarse.cu)
 //   k_prolong       x += P xc                                     (a9; row gather)
-// Stop test on the device: per-block partial sums of r^2, the last block to arrive
-// sums them in block order (deterministic), records ρ_k and sets `done`; every
-// later kernel of the enqueued chunk sees `done` and returns at once, so the host
-// only synchronises once per chunk of iterations.
+// Stop test on the device: the iteration's first kernel stores per-warp partial sums
+// of r^2 (no barrier, no fence); a one-CTA k_finalize sums them in a fixed order
+// (deterministic), records ρ_k and sets `done`; every later kernel of the enqueued
+// chunk sees `done` and returns at once, so the host synchronises once per chunk.
 #include <algorithm>
 #include <cmath>
 
@@ -20,12 +20,10 @@
 struct IterState {
   int done;
   int k;          // completed iterations
-  int arrive;
   int converged;
   int diverged;
   int max_iter;
   int fixed;
-  int pad;
   double tol;
   double bscale;  // ||b|| (1 if b = 0)
   double r0;
@@ -39,147 +37,147 @@ struct StencilT {
   const double* Tx;
   const double* Ty;
   const double* Tz;
-  int nx, ny, nz;
+  Grid3 g;
 };
 
 // r = b - A x at cell c (gauge: A_00 doubled); returns r and D_A.
 __device__ __forceinline__ double residual_at(const StencilT& S, const double* __restrict__ x,
-                                              const double* __restrict__ b, int64_t c,
-                                              double* DA) {
-  int64_t sxy = (int64_t)S.nx * S.ny;
-  int i = (int)(c % S.nx), j = (int)((c / S.nx) % S.ny), k = (int)(c / sxy);
+                                              const double* __restrict__ b, int c, int i, int j,
+                                              int k, double* DA) {
+  const int nx = S.g.nx, sxy = S.g.nxy;
   double txp = S.Tx[c], typ = S.Ty[c], tzp = S.Tz[c];
   double txm = i > 0 ? S.Tx[c - 1] : 0.0;
-  double tym = j > 0 ? S.Ty[c - S.nx] : 0.0;
+  double tym = j > 0 ? S.Ty[c - nx] : 0.0;
   double tzm = k > 0 ? S.Tz[c - sxy] : 0.0;
   double D = txp + txm + typ + tym + tzp + tzm;
   double off = 0.0;
   if (k > 0) off += tzm * x[c - sxy];
-  if (j > 0) off += tym * x[c - S.nx];
+  if (j > 0) off += tym * x[c - nx];
   if (i > 0) off += txm * x[c - 1];
-  if (i < S.nx - 1) off += txp * x[c + 1];
-  if (j < S.ny - 1) off += typ * x[c + S.nx];
-  if (k < S.nz - 1) off += tzp * x[c + sxy];
+  if (i < nx - 1) off += txp * x[c + 1];
+  if (j < S.g.ny - 1) off += typ * x[c + nx];
+  if (k < S.g.nz - 1) off += tzp * x[c + sxy];
   double dA = (c == 0) ? 2.0 * D : D;
   *DA = dA;
   return b[c] - (dA * x[c] - off);
 }
 
-__device__ __forceinline__ double block_sum(double v) {
+// per-block partial sum -> partials[blockIdx] (one barrier, no fence, no atomics)
+__device__ __forceinline__ void warp_partial(double v, double* __restrict__ partials) {
   __shared__ double sh[32];
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  __syncthreads();
   if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = v;
   __syncthreads();
-  double w = (threadIdx.x < (blockDim.x >> 5)) ? sh[threadIdx.x] : 0.0;
-  if (threadIdx.x < 32)
+  if (threadIdx.x < 32) {
+    double w = threadIdx.x < (blockDim.x >> 5) ? sh[threadIdx.x] : 0.0;
     for (int o = 16; o > 0; o >>= 1) w += __shfl_xor_sync(0xffffffffu, w, o);
-  return w;  // valid in warp 0
+    if (threadIdx.x == 0) partials[blockIdx.x] = w;
+  }
 }
 
-// Deterministic global sum of per-block values; the last block finalises the stop test.
-// mode 0: stop test on ||r||; mode 1: store ||b|| into st->bscale.
-__device__ void norm_epilogue(double v, double* __restrict__ partials, IterState* st,
-                              double* __restrict__ res, int mode) {
-  __shared__ int last;
-  double bs = block_sum(v);
-  if (threadIdx.x == 0) {
-    partials[blockIdx.x] = bs;
-    __threadfence();
-    int t = atomicAdd(&st->arrive, 1);
-    last = (t == (int)gridDim.x - 1);
-  }
-  __syncthreads();
-  if (!last) return;
-  __threadfence();
+__device__ __forceinline__ bool is_done(const IterState* st) {
+  return *(volatile const int*)&st->done != 0;
+}
+
+// Stop test (a11): one CTA sums the per-warp partials in a fixed order (deterministic),
+// records ρ_k and decides.  mode 1: store ||b||.
+__global__ void __launch_bounds__(1024) k_finalize(const double* __restrict__ partials, int np,
+                                                   int mode, IterState* st,
+                                                   double* __restrict__ res) {
+  if (mode == 0 && is_done(st)) return;
+  __shared__ double sh[32];
   double s = 0.0;
-  for (int t = threadIdx.x; t < (int)gridDim.x; t += blockDim.x) s += *(volatile double*)(partials + t);
-  double tot = block_sum(s);
-  if (threadIdx.x == 0) {
-    st->arrive = 0;
-    double nrm = sqrt(tot);
-    if (mode == 1) {
-      st->bscale = nrm > 0.0 ? nrm : 1.0;
-    } else {
-      int k = st->k;
-      double rho = nrm / st->bscale;
-      res[k] = rho;
-      if (k == 0) st->r0 = nrm;
-      int done = 0;
-      if (st->fixed > 0) {
-        if (k >= st->fixed) {
-          done = 1;
-          st->converged = rho <= st->tol;
-        }
-      } else {
-        if (rho <= st->tol) {
-          done = 1;
-          st->converged = 1;
-        } else if (k >= st->max_iter) {
-          done = 1;
-        }
-      }
-      if (!(nrm <= 1e6 * st->r0) && st->r0 > 0.0) {  // also catches NaN
-        done = 1;
-        st->diverged = 1;
-      }
-      if (done) st->done = 1;
-      else st->k = k + 1;
-    }
-    __threadfence();
+  for (int t = threadIdx.x; t < np; t += blockDim.x) s += partials[t];
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x >= 32) return;
+  double w = threadIdx.x < (blockDim.x >> 5) ? sh[threadIdx.x] : 0.0;
+  for (int o = 16; o > 0; o >>= 1) w += __shfl_xor_sync(0xffffffffu, w, o);
+  if (threadIdx.x != 0) return;
+  double nrm = sqrt(w);
+  if (mode == 1) {
+    st->bscale = nrm > 0.0 ? nrm : 1.0;
+    return;
   }
+  int k = st->k;
+  double rho = nrm / st->bscale;
+  res[k] = rho;
+  if (k == 0) st->r0 = nrm;
+  int done = 0;
+  if (st->fixed > 0) {
+    if (k >= st->fixed) {
+      done = 1;
+      st->converged = rho <= st->tol;
+    }
+  } else if (rho <= st->tol) {
+    done = 1;
+    st->converged = 1;
+  } else if (k >= st->max_iter) {
+    done = 1;
+  }
+  if (!(nrm <= 1e6 * st->r0) && st->r0 > 0.0) {  // also catches NaN
+    done = 1;
+    st->diverged = 1;
+  }
+  if (done) st->done = 1;
+  else st->k = k + 1;
 }
 
 __global__ void __launch_bounds__(CT) k_norm(StencilT S, const double* __restrict__ x,
                                              const double* __restrict__ b, int mode,
-                                             double* __restrict__ partials, IterState* st,
-                                             double* __restrict__ res) {
-  if (mode == 0 && *(volatile int*)&st->done) return;
-  int64_t N = (int64_t)S.nx * S.ny * S.nz;
-  int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+                                             double* __restrict__ partials, const IterState* st) {
+  if (mode == 0 && is_done(st)) return;
+  const int N = S.g.nxy * S.g.nz;
+  int c = blockIdx.x * blockDim.x + threadIdx.x;
   double v = 0.0;
   if (c < N) {
     if (mode == 1) {
       v = b[c] * b[c];
     } else {
+      int i, j, k;
+      g3_coords(S.g, c, i, j, k);
       double dA;
-      double r = residual_at(S, x, b, c, &dA);
+      double r = residual_at(S, x, b, c, i, j, k, &dA);
       v = r * r;
     }
   }
-  norm_epilogue(v, partials, st, res, mode);
+  warp_partial(v, partials);
 }
 
+// a7: x_out = x + ω_s D_A^{-1}(b - A x); `first` also emits the ||r||^2 partials.
 __global__ void __launch_bounds__(CT) k_jacobi(StencilT S, const double* __restrict__ x,
                                                double* __restrict__ xo,
                                                const double* __restrict__ b, double omega,
                                                int first, double* __restrict__ partials,
-                                               IterState* st, double* __restrict__ res) {
-  if (*(volatile int*)&st->done) return;
-  int64_t N = (int64_t)S.nx * S.ny * S.nz;
-  int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+                                               const IterState* st) {
+  if (is_done(st)) return;
+  const int N = S.g.nxy * S.g.nz;
+  int c = blockIdx.x * blockDim.x + threadIdx.x;
   double v = 0.0;
   if (c < N) {
+    int i, j, k;
+    g3_coords(S.g, c, i, j, k);
     double dA;
-    double r = residual_at(S, x, b, c, &dA);
+    double r = residual_at(S, x, b, c, i, j, k, &dA);
     xo[c] = x[c] + omega * (r / dA);
     v = r * r;
   }
-  if (first) norm_epilogue(v, partials, st, res, 0);
+  if (first) warp_partial(v, partials);
 }
 
 struct LevelView {
-  int kind, W, nx, ny, nb0, nb1;
-  int64_t N;
+  int kind, W, nb0, nb1;
+  Grid3 g;
   const int32_t* tab;
   const int32_t* col;
   const double* P;
 };
 
-__device__ __forceinline__ int lv_col(const LevelView& L, int64_t c, int i, int j, int k, int s) {
-  if (L.kind == 1) return L.col[(int64_t)s * L.N + c];
-  int jx = L.tab[2 * i + (s & 1)], jy = L.tab[2 * (L.nx + j) + ((s >> 1) & 1)],
-      jz = L.tab[2 * (L.nx + L.ny + k) + (s >> 2)];
+__device__ __forceinline__ int lv_col(const LevelView& L, int c, int i, int j, int k, int s) {
+  if (L.kind == 1) return L.col[(size_t)s * (L.g.nxy * L.g.nz) + c];
+  int jx = L.tab[2 * i + (s & 1)], jy = L.tab[2 * (L.g.nx + j) + ((s >> 1) & 1)],
+      jz = L.tab[2 * (L.g.nx + L.g.ny + k) + (s >> 2)];
   if (jx < 0 || jy < 0 || jz < 0) return -1;
   return jx + L.nb0 * (jy + L.nb1 * jz);
 }
@@ -191,7 +189,6 @@ __device__ __forceinline__ void warp_segmented_add(int key, double val, double* 
   int lane = threadIdx.x & 31;
   int prev = __shfl_up_sync(full, key, 1);
   int head = (lane == 0) || (prev != key);
-  // segment start lane for each lane
   unsigned heads = __ballot_sync(full, head);
   int start = 31 - __clz(heads & ((2u << lane) - 1u));
   double s = val;
@@ -205,83 +202,79 @@ __device__ __forceinline__ void warp_segmented_add(int key, double val, double* 
   if (tail && key >= 0) atomicAdd(out + key, s);
 }
 
+// a6 + a8: r = b - A x, rc += P^T r.
 __global__ void __launch_bounds__(CT) k_res_restrict(StencilT S, LevelView L,
                                                      const double* __restrict__ x,
                                                      const double* __restrict__ b,
                                                      double* __restrict__ rc, int first,
-                                                     double* __restrict__ partials, IterState* st,
-                                                     double* __restrict__ res) {
-  if (*(volatile int*)&st->done) return;
-  int64_t N = L.N;
-  int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+                                                     double* __restrict__ partials,
+                                                     const IterState* st) {
+  if (is_done(st)) return;
+  const int N = S.g.nxy * S.g.nz;
+  int c = blockIdx.x * blockDim.x + threadIdx.x;
   bool in = c < N;
-  int64_t cc = in ? c : N - 1;
-  int64_t sxy = (int64_t)S.nx * S.ny;
-  int i = (int)(cc % S.nx), j = (int)((cc / S.nx) % S.ny), k = (int)(cc / sxy);
+  int cc = in ? c : N - 1;
+  int i, j, k;
+  g3_coords(S.g, cc, i, j, k);
   double r = 0.0;
   if (in) {
     double dA;
-    r = residual_at(S, x, b, c, &dA);
+    r = residual_at(S, x, b, c, i, j, k, &dA);
   }
   if (L.kind == 0) {
 #pragma unroll
     for (int s = 0; s < 8; ++s) {
       int key = in ? lv_col(L, cc, i, j, k, s) : -1;
-      double v = key >= 0 ? L.P[(int64_t)s * N + c] * r : 0.0;
+      double v = key >= 0 ? L.P[(size_t)s * N + c] * r : 0.0;
       warp_segmented_add(key, v, rc);
     }
   } else {
     for (int s = 0; s < L.W; ++s) {
-      int key = in ? L.col[(int64_t)s * N + c] : -1;
-      double v = key >= 0 ? L.P[(int64_t)s * N + c] * r : 0.0;
+      int key = in ? L.col[(size_t)s * N + c] : -1;
+      double v = key >= 0 ? L.P[(size_t)s * N + c] * r : 0.0;
       warp_segmented_add(key, v, rc);
     }
   }
-  if (first) norm_epilogue(r * r, partials, st, res, 0);
+  if (first) warp_partial(r * r, partials);
 }
 
+// a9: x += P xc (row gather).
 __global__ void __launch_bounds__(CT) k_prolong(LevelView L, double* __restrict__ x,
-                                                const double* __restrict__ xc, const int* done) {
-  if (*(volatile const int*)done) return;
-  int64_t N = L.N;
-  int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+                                                const double* __restrict__ xc,
+                                                const IterState* st) {
+  if (is_done(st)) return;
+  const int N = L.g.nxy * L.g.nz;
+  int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= N) return;
-  int64_t sxy = (int64_t)L.nx * L.ny;
-  int i = (int)(c % L.nx), j = (int)((c / L.nx) % L.ny), k = (int)(c / sxy);
   double acc = 0.0;
   if (L.kind == 0) {
+    int i, j, k;
+    g3_coords(L.g, c, i, j, k);
 #pragma unroll
     for (int s = 0; s < 8; ++s) {
       int key = lv_col(L, c, i, j, k, s);
-      if (key >= 0) acc += L.P[(int64_t)s * N + c] * xc[key];
+      if (key >= 0) acc += L.P[(size_t)s * N + c] * xc[key];
     }
   } else {
     for (int s = 0; s < L.W; ++s) {
-      int key = L.col[(int64_t)s * N + c];
-      if (key >= 0) acc += L.P[(int64_t)s * N + c] * xc[key];
+      int key = L.col[(size_t)s * N + c];
+      if (key >= 0) acc += L.P[(size_t)s * N + c] * xc[key];
     }
   }
   x[c] += acc;
 }
 
-__global__ void k_zero_if(double* __restrict__ p, int n, const int* done) {
-  if (*(volatile const int*)done) return;
+__global__ void k_zero_if(double* __restrict__ p, int n, const IterState* st) {
+  if (is_done(st)) return;
   int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t < n) p[t] = 0.0;
 }
 
 // ---------------------------------------------------------------- dynamic partition kernels
 __global__ void k_dp(const double* __restrict__ x, const double* __restrict__ xp, int64_t N,
-                     double* __restrict__ dp, unsigned long long* __restrict__ mx) {
+                     double* __restrict__ dp) {
   int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  double a = 0.0;
-  if (c < N) {
-    double d = x[c] - xp[c];
-    dp[c] = d;
-    a = fabs(d);
-  }
-  for (int o = 16; o > 0; o >>= 1) a = fmax(a, __shfl_xor_sync(0xffffffffu, a, o));
-  if ((threadIdx.x & 31) == 0) atomicMax(mx, (unsigned long long)__double_as_longlong(a));
+  if (c < N) dp[c] = x[c] - xp[c];
 }
 
 __global__ void k_absmax_vec(const double* __restrict__ dp, int64_t N, unsigned long long* mx) {
@@ -345,13 +338,14 @@ __global__ void k_refill_const(const int32_t* __restrict__ part, int64_t N, int3
 
 using namespace msb;
 
-static StencilT stencil(msb_op op) { return StencilT{op->Tx, op->Ty, op->Tz, op->nx, op->ny, op->nz}; }
-
-static LevelView view(msb_level L) {
-  return LevelView{L->kind, L->W, L->nx, L->ny, L->nb[0], L->nb[1], L->N, L->tab, L->col,
-                   L->P[L->cur]};
+static StencilT stencil(msb_op op) {
+  return StencilT{op->Tx, op->Ty, op->Tz, make_grid3(op->nx, op->ny, op->nz)};
 }
 
+static LevelView view(msb_level L) {
+  return LevelView{L->kind, L->W, L->nb[0], L->nb[1], make_grid3(L->nx, L->ny, L->nz), L->tab,
+                   L->col, L->P[L->cur]};
+}
 // Build the dynamic constant-basis stage from dp (device, length N) into s->dyn_level.
 static msb_status build_dynamic(msb_ctx ctx, msb_solver s, const double* dp, int32_t* M_out,
                                 int32_t* part_out) {
@@ -409,19 +403,7 @@ static msb_status build_dynamic(msb_ctx ctx, msb_solver s, const double* dp, int
   D->cur = 0;
   D->M = M;
   if (part_out) MSB_CUDA_TRY(ctx, copy_out(ctx, part_out, D->part, N * sizeof(int32_t)));
-  if (getenv("MSB_DEBUG")) {
-    MSB_CUDA_TRY(ctx, cudaStreamSynchronize(st));
-    fprintf(stderr, "[msb] dynamic partition M=%d smin=%d\n", M, smin);
-  }
   rc = coarse_assemble_dense(ctx, D, op);
-  if (getenv("MSB_DEBUG")) {
-    std::vector<double> h((size_t)M * M);
-    cudaMemcpy(h.data(), D->co.Ac, h.size() * 8, cudaMemcpyDeviceToHost);
-    for (int a = 0; a < std::min(M, 6); ++a) {
-      for (int b = 0; b < std::min(M, 6); ++b) fprintf(stderr, " %12.6g", h[(size_t)a * M + b]);
-      fprintf(stderr, "\n");
-    }
-  }
   if (rc) return rc;
   *M_out = M;
   return MSB_OK;
@@ -461,7 +443,7 @@ msb_status msb_solver_create(msb_ctx ctx, msb_op op, const msb_level* levels, in
   MSB_ALLOC(ctx, s->xbuf[1], double, N);
   MSB_ALLOC(ctx, s->rc, double, maxM + 2);
   MSB_ALLOC(ctx, s->xc, double, maxM + 2);
-  MSB_ALLOC(ctx, s->partials, double, grid_for(N, CT) + 32);
+  MSB_ALLOC(ctx, s->partials, double, (size_t)grid_for(N, CT) * (CT / 32) + 32);
   s->st = dalloc_n<IterState>(ctx, 1);
   if (!s->st) return set_error(ctx, MSB_ENOMEM, "solver state");
   if (s->dyn) {
@@ -520,6 +502,8 @@ msb_status msb_add_dynamic_basis(msb_ctx ctx, msb_solver s, const double* dp, in
 }
 
 // Enqueue one stage (level L) on x buffers; `first` marks the iteration's first kernel.
+// Enqueue one stage (level L) on the x double buffer; `first` marks the iteration's
+// first kernel, which also emits the stop-test partials (finalised right after).
 static msb_status enqueue_stage(msb_ctx ctx, msb_solver s, msb_level L, const double* b, int& cur,
                                 bool& first) {
   msb_op op = s->op;
@@ -528,26 +512,39 @@ static msb_status enqueue_stage(msb_ctx ctx, msb_solver s, msb_level L, const do
   StencilT S = stencil(op);
   LevelView V = view(L);
   unsigned g = grid_for(N, CT);
-  const int* done = &s->st->done;
+  int np = (int)g;
+  auto fin = [&]() -> msb_status {
+    k_finalize<<<1, 1024, 0, st>>>(s->partials, np, 0, s->st, s->res_dev);
+    MSB_LAUNCH_CHECK(ctx);
+    return MSB_OK;
+  };
   auto jac = [&]() -> msb_status {
     for (int v = 0; v < s->nu; ++v) {
       k_jacobi<<<g, CT, 0, st>>>(S, s->xbuf[cur], s->xbuf[cur ^ 1], b, s->omega_s, first ? 1 : 0,
-                                 s->partials, s->st, s->res_dev);
+                                 s->partials, s->st);
       MSB_LAUNCH_CHECK(ctx);
+      if (first) {
+        msb_status rc = fin();
+        if (rc) return rc;
+      }
       first = false;
       cur ^= 1;
     }
     return MSB_OK;
   };
   auto corr = [&]() -> msb_status {
-    k_zero_if<<<grid_for(L->M, 256), 256, 0, st>>>(s->rc, L->M, done);
+    k_zero_if<<<grid_for(L->M, 256), 256, 0, st>>>(s->rc, L->M, s->st);
     MSB_LAUNCH_CHECK(ctx);
     k_res_restrict<<<g, CT, 0, st>>>(S, V, s->xbuf[cur], b, s->rc, first ? 1 : 0, s->partials,
-                                     s->st, s->res_dev);
+                                     s->st);
     MSB_LAUNCH_CHECK(ctx);
+    if (first) {
+      msb_status rc = fin();
+      if (rc) return rc;
+    }
     first = false;
-    coarse_solve_dense(ctx, L->co, s->rc, s->xc, done);
-    k_prolong<<<g, CT, 0, st>>>(V, s->xbuf[cur], s->xc, done);
+    coarse_solve_dense(ctx, L->co, s->rc, s->xc, &s->st->done);
+    k_prolong<<<g, CT, 0, st>>>(V, s->xbuf[cur], s->xc, s->st);
     MSB_LAUNCH_CHECK(ctx);
     return MSB_OK;
   };
@@ -559,6 +556,18 @@ static msb_status enqueue_stage(msb_ctx ctx, msb_solver s, msb_level L, const do
     if ((rc = jac())) return rc;
     if ((rc = corr())) return rc;
   }
+  return MSB_OK;
+}
+
+static msb_status enqueue_norm(msb_ctx ctx, msb_solver s, const double* x, const double* b,
+                               int mode) {
+  msb_op op = s->op;
+  unsigned g = grid_for(op->N, CT);
+  k_norm<<<g, CT, 0, ctx->stream>>>(stencil(op), x, b, mode, s->partials, s->st);
+  MSB_LAUNCH_CHECK(ctx);
+  k_finalize<<<1, 1024, 0, ctx->stream>>>(s->partials, (int)g, mode, s->st,
+                                          s->res_dev);
+  MSB_LAUNCH_CHECK(ctx);
   return MSB_OK;
 }
 
@@ -586,19 +595,16 @@ msb_status msb_ms_iterate(msb_ctx ctx, msb_solver s, const double* b, double* x,
   h.tol = tol;
   h.bscale = 1.0;
   MSB_CUDA_TRY(ctx, cudaMemcpyAsync(s->st, &h, sizeof(h), cudaMemcpyHostToDevice, st));
-  StencilT S = stencil(op);
-  unsigned g = grid_for(N, CT);
-  k_norm<<<g, CT, 0, st>>>(S, s->xbuf[0], db, 1, s->partials, s->st, s->res_dev);
-  MSB_LAUNCH_CHECK(ctx);
+  msb_status rc = enqueue_norm(ctx, s, s->xbuf[0], db, 1);
+  if (rc) return rc;
   int cur = 0;
   int target = fixed_iters > 0 ? fixed_iters : max_iter;
   std::vector<int> cur_after;  // buffer holding x_k
   cur_after.push_back(0);
   std::vector<int32_t> dynM;
   IterState hs{};
-  msb_status rc = MSB_OK;
   if (!s->dyn) {
-    const int chunk = 8;
+    const int chunk = 16;
     int issued = 0;
     while (true) {
       int n = std::min(chunk, target - issued);
@@ -609,10 +615,8 @@ msb_status msb_ms_iterate(msb_ctx ctx, msb_solver s, const double* b, double* x,
         cur_after.push_back(cur);
       }
       issued += n;
-      if (issued >= target) {
-        k_norm<<<g, CT, 0, st>>>(S, s->xbuf[cur], db, 0, s->partials, s->st, s->res_dev);
-        MSB_LAUNCH_CHECK(ctx);
-      }
+      if (issued >= target)
+        if ((rc = enqueue_norm(ctx, s, s->xbuf[cur], db, 0))) return rc;
       MSB_CUDA_TRY(ctx, cudaMemcpyAsync(&hs, s->st, sizeof(hs), cudaMemcpyDeviceToHost, st));
       MSB_CUDA_TRY(ctx, cudaStreamSynchronize(st));
       if (hs.done || issued >= target) break;
@@ -620,17 +624,15 @@ msb_status msb_ms_iterate(msb_ctx ctx, msb_solver s, const double* b, double* x,
   } else {
     // dynamic stage: host-synchronous per iteration (M_dyn is data dependent)
     while (true) {
-      k_norm<<<g, CT, 0, st>>>(S, s->xbuf[cur], db, 0, s->partials, s->st, s->res_dev);
-      MSB_LAUNCH_CHECK(ctx);
+      if ((rc = enqueue_norm(ctx, s, s->xbuf[cur], db, 0))) return rc;
       MSB_CUDA_TRY(ctx, cudaMemcpyAsync(&hs, s->st, sizeof(hs), cudaMemcpyDeviceToHost, st));
       MSB_CUDA_TRY(ctx, cudaStreamSynchronize(st));
       if (hs.done) break;
       int k = hs.k;  // iteration about to run (1-based)
       int32_t M = 0;
       if (k >= 2) {
-        k_dp<<<grid_for(N, 256), 256, 0, st>>>(s->xbuf[cur], s->xprev, N, s->r,
-                                               reinterpret_cast<unsigned long long*>(s->scratch_i));
-        count_launch();
+        k_dp<<<grid_for(N, 256), 256, 0, st>>>(s->xbuf[cur], s->xprev, N, s->r);
+        MSB_LAUNCH_CHECK(ctx);
         if ((rc = build_dynamic(ctx, s, s->r, &M, nullptr))) return rc;
       }
       dynM.push_back(M);

@@ -18,14 +18,6 @@
 
 namespace msb {
 
-struct SweepState {
-  int done;
-  int n;          // sweeps completed
-  int arrive;
-  int max_sweeps;
-  double tol;     // < 0: never stop on δ
-};
-
 // ---------------------------------------------------------------- axis parity table
 // tab[(off_a + x)*2 + p] = block index with parity p whose support contains x, or -1.
 __global__ void k_axis_tab(int n, int b, int off, int32_t* __restrict__ tab) {
@@ -84,181 +76,6 @@ __global__ void k_cart_part(int nx, int ny, int nz, int bx, int by, int bz, int 
   if (c >= N) return;
   int i = (int)(c % nx), j = (int)((c / nx) % ny), k = (int)(c / ((int64_t)nx * ny));
   part[c] = i / bx + nbx * (j / by + nby * (k / bz));
-}
-
-// ---------------------------------------------------------------- reductions
-// NaN-propagating max (a zero diagonal must surface as a non-finite δ).
-__device__ __forceinline__ double nmax(double a, double b) { return (b > a || b != b) ? b : a; }
-
-__device__ __forceinline__ double warp_max(double v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v = nmax(v, __shfl_xor_sync(0xffffffffu, v, o));
-  return v;
-}
-
-// Block max of nonnegative v, folded into *slot (as ordered bits); the last block to
-// arrive finalises the sweep.
-__device__ __forceinline__ void sweep_epilogue(double v, unsigned long long* dmax,
-                                               SweepState* st, int n) {
-  __shared__ double sh[32];
-  v = warp_max(v);
-  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = v;
-  __syncthreads();
-  if (threadIdx.x < 32) {
-    double w = threadIdx.x < (blockDim.x >> 5) ? sh[threadIdx.x] : 0.0;
-    w = warp_max(w);
-    if (threadIdx.x == 0) {
-      atomicMax(dmax + n, (unsigned long long)__double_as_longlong(w));
-      __threadfence();
-      int t = atomicAdd(&st->arrive, 1);
-      if (t == (int)gridDim.x - 1) {
-        __threadfence();
-        unsigned long long bits = atomicAdd(dmax + n, 0ull);
-        double d = __longlong_as_double((long long)bits);
-        int nn = n + 1;
-        st->n = nn;
-        if ((st->tol >= 0.0 && d <= st->tol) || nn >= st->max_sweeps) st->done = 1;
-        st->arrive = 0;
-        __threadfence();
-      }
-    }
-  }
-}
-
-// ---------------------------------------------------------------- G2: Cartesian sweep
-__global__ void __launch_bounds__(256) k_sweep_cart(double* __restrict__ P0, double* __restrict__ P1,
-                                                    const double* __restrict__ Tx,
-                                                    const double* __restrict__ Ty,
-                                                    const double* __restrict__ Tz,
-                                                    const int32_t* __restrict__ tab, int nx,
-                                                    int ny, int nz, double omega,
-                                                    SweepState* st,
-                                                    unsigned long long* __restrict__ dmax) {
-  if (*(volatile int*)&st->done) return;
-  const int n = *(volatile int*)&st->n;
-  const double* __restrict__ Pin = (n & 1) ? P1 : P0;
-  double* __restrict__ Pout = (n & 1) ? P0 : P1;
-  const int64_t N = (int64_t)nx * ny * nz;
-  const int64_t sxy = (int64_t)nx * ny;
-  int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  double dloc = 0.0;
-  if (c < N) {
-    int i = (int)(c % nx), j = (int)((c / nx) % ny), k = (int)(c / sxy);
-    int2 bx = *(const int2*)(tab + 2 * i);
-    int2 by = *(const int2*)(tab + 2 * (nx + j));
-    int2 bz = *(const int2*)(tab + 2 * (nx + ny + k));
-    int2 bxm = i > 0 ? *(const int2*)(tab + 2 * (i - 1)) : make_int2(-2, -2);
-    int2 bxp = i < nx - 1 ? *(const int2*)(tab + 2 * (i + 1)) : make_int2(-2, -2);
-    int2 bym = j > 0 ? *(const int2*)(tab + 2 * (nx + j - 1)) : make_int2(-2, -2);
-    int2 byp = j < ny - 1 ? *(const int2*)(tab + 2 * (nx + j + 1)) : make_int2(-2, -2);
-    int2 bzm = k > 0 ? *(const int2*)(tab + 2 * (nx + ny + k - 1)) : make_int2(-2, -2);
-    int2 bzp = k < nz - 1 ? *(const int2*)(tab + 2 * (nx + ny + k + 1)) : make_int2(-2, -2);
-    double txp = Tx[c], typ = Ty[c], tzp = Tz[c];
-    double txm = i > 0 ? Tx[c - 1] : 0.0;
-    double tym = j > 0 ? Ty[c - nx] : 0.0;
-    double tzm = k > 0 ? Tz[c - sxy] : 0.0;
-    double D = txp + txm + typ + tym + tzp + tzm;
-    double wD = omega / D;
-    double om1 = 1.0 - omega;
-    double ph[8], po[8];
-    double sum = 0.0;
-#pragma unroll
-    for (int s = 0; s < 8; ++s) {
-      int px = s & 1, py = (s >> 1) & 1, pz = s >> 2;
-      int jx = px ? bx.y : bx.x;
-      int jy = py ? by.y : by.x;
-      int jz = pz ? bz.y : bz.x;
-      ph[s] = 0.0;
-      po[s] = 0.0;
-      if (jx >= 0 && jy >= 0 && jz >= 0) {
-        const double* __restrict__ base = Pin + (int64_t)s * N;
-        double acc = 0.0;
-        if ((pz ? bzm.y : bzm.x) == jz) acc += tzm * base[c - sxy];
-        if ((py ? bym.y : bym.x) == jy) acc += tym * base[c - nx];
-        if ((px ? bxm.y : bxm.x) == jx) acc += txm * base[c - 1];
-        if ((px ? bxp.y : bxp.x) == jx) acc += txp * base[c + 1];
-        if ((py ? byp.y : byp.x) == jy) acc += typ * base[c + nx];
-        if ((pz ? bzp.y : bzp.x) == jz) acc += tzp * base[c + sxy];
-        double p = base[c];
-        po[s] = p;
-        ph[s] = om1 * p + wD * acc;
-        sum += ph[s];
-      }
-    }
-#pragma unroll
-    for (int s = 0; s < 8; ++s) {
-      int px = s & 1, py = (s >> 1) & 1, pz = s >> 2;
-      int jx = px ? bx.y : bx.x;
-      int jy = py ? by.y : by.x;
-      int jz = pz ? bz.y : bz.x;
-      if (jx >= 0 && jy >= 0 && jz >= 0) {
-        double pn = ph[s] / sum;
-        Pout[(int64_t)s * N + c] = pn;
-        dloc = nmax(dloc, fabs(pn - po[s]));
-      }
-    }
-  }
-  sweep_epilogue(dloc, dmax, st, n);
-}
-
-// ---------------------------------------------------------------- G3: explicit (ELL) sweep
-__global__ void __launch_bounds__(256) k_sweep_ell(double* __restrict__ P0, double* __restrict__ P1,
-                                                   const double* __restrict__ Tx,
-                                                   const double* __restrict__ Ty,
-                                                   const double* __restrict__ Tz,
-                                                   const int32_t* __restrict__ col,
-                                                   const int8_t* __restrict__ nbs, int W, int nx,
-                                                   int ny, int nz, double omega, SweepState* st,
-                                                   unsigned long long* __restrict__ dmax) {
-  if (*(volatile int*)&st->done) return;
-  const int n = *(volatile int*)&st->n;
-  const double* __restrict__ Pin = (n & 1) ? P1 : P0;
-  double* __restrict__ Pout = (n & 1) ? P0 : P1;
-  const int64_t N = (int64_t)nx * ny * nz;
-  const int64_t sxy = (int64_t)nx * ny;
-  int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  double dloc = 0.0;
-  if (c < N) {
-    int i = (int)(c % nx), j = (int)((c / nx) % ny), k = (int)(c / sxy);
-    double t[6];
-    int64_t nb[6];
-    t[0] = k > 0 ? Tz[c - sxy] : 0.0;       nb[0] = c - sxy;
-    t[1] = j > 0 ? Ty[c - nx] : 0.0;        nb[1] = c - nx;
-    t[2] = i > 0 ? Tx[c - 1] : 0.0;         nb[2] = c - 1;
-    t[3] = Tx[c];                           nb[3] = c + 1;
-    t[4] = Ty[c];                           nb[4] = c + nx;
-    t[5] = Tz[c];                           nb[5] = c + sxy;
-    double D = t[3] + t[2] + t[4] + t[1] + t[5] + t[0];
-    double wD = omega / D;
-    double om1 = 1.0 - omega;
-    double sum = 0.0;
-    // pass 1: row sum of P^
-    for (int s = 0; s < W; ++s) {
-      if (col[(int64_t)s * N + c] < 0) continue;
-      double acc = 0.0;
-#pragma unroll
-      for (int d = 0; d < 6; ++d) {
-        int sl = nbs[((int64_t)d * W + s) * N + c];
-        if (sl >= 0) acc += t[d] * Pin[(int64_t)sl * N + nb[d]];
-      }
-      sum += om1 * Pin[(int64_t)s * N + c] + wD * acc;
-    }
-    // pass 2: recompute (identical arithmetic) and normalise
-    for (int s = 0; s < W; ++s) {
-      if (col[(int64_t)s * N + c] < 0) continue;
-      double acc = 0.0;
-#pragma unroll
-      for (int d = 0; d < 6; ++d) {
-        int sl = nbs[((int64_t)d * W + s) * N + c];
-        if (sl >= 0) acc += t[d] * Pin[(int64_t)sl * N + nb[d]];
-      }
-      double p = Pin[(int64_t)s * N + c];
-      double pn = (om1 * p + wD * acc) / sum;
-      Pout[(int64_t)s * N + c] = pn;
-      dloc = nmax(dloc, fabs(pn - p));
-    }
-  }
-  sweep_epilogue(dloc, dmax, st, n);
 }
 
 // ---------------------------------------------------------------- export helpers
@@ -428,6 +245,7 @@ void level_free(msb_level L) {
   dfree(ctx, L->P[1]);
   dfree(ctx, L->part);
   dfree(ctx, L->tab);
+  dfree(ctx, L->amask);
   dfree(ctx, L->col);
   dfree(ctx, L->nbs);
   coarse_free(ctx, L->co);
@@ -596,69 +414,6 @@ msb_status msb_level_import_values(msb_ctx ctx, msb_level L, const double* vals)
 msb_status msb_level_destroy(msb_level L) {
   if (!L) return MSB_EINVAL;
   level_free(L);
-  return MSB_OK;
-}
-
-msb_status msb_smooth_basis(msb_ctx ctx, msb_level L, msb_op op, int32_t max_sweeps, double omega,
-                            double tol, int32_t* sweeps_done, double* last_delta, double* deltas) {
-  if (!ctx || !L || !op) return set_error(ctx, MSB_EINVAL, "msb_smooth_basis: null");
-  if (max_sweeps < 0 || !(omega > 0.0) || !(omega <= 1.0))
-    return set_error(ctx, MSB_EINVAL, "msb_smooth_basis: bad max_sweeps/omega");
-  if (L->N != op->N) return set_error(ctx, MSB_EDIM, "level/operator size mismatch");
-  if (sweeps_done) *sweeps_done = 0;
-  if (max_sweeps == 0) return MSB_OK;
-  SweepState* st = dalloc_n<SweepState>(ctx, 1);
-  unsigned long long* dmax = dalloc_n<unsigned long long>(ctx, max_sweeps);
-  if (!st || !dmax) return set_error(ctx, MSB_ENOMEM, "sweep state");
-  SweepState h{0, 0, 0, max_sweeps, tol};
-  MSB_CUDA_TRY(ctx, cudaMemcpyAsync(st, &h, sizeof(h), cudaMemcpyHostToDevice, ctx->stream));
-  MSB_CUDA_TRY(ctx, cudaMemsetAsync(dmax, 0, max_sweeps * sizeof(unsigned long long), ctx->stream));
-  // zero-diagonal check is part of every sweep: D = 0 gives inf/nan and
-  // is detected on the δ history below.
-  double* Pa = L->P[L->cur];
-  double* Pb = L->P[L->cur ^ 1];
-  const int chunk = 32;
-  int issued = 0;
-  SweepState hs{};
-  while (true) {
-    int nlaunch = std::min(chunk, max_sweeps - issued);
-    for (int t = 0; t < nlaunch; ++t) {
-      if (L->kind == 0) {
-        k_sweep_cart<<<grid_for(L->N, 256), 256, 0, ctx->stream>>>(
-            Pa, Pb, op->Tx, op->Ty, op->Tz, L->tab, op->nx, op->ny, op->nz, omega, st, dmax);
-      } else {
-        k_sweep_ell<<<grid_for(L->N, 256), 256, 0, ctx->stream>>>(
-            Pa, Pb, op->Tx, op->Ty, op->Tz, L->col, L->nbs, L->W, op->nx, op->ny, op->nz, omega,
-            st, dmax);
-      }
-      MSB_LAUNCH_CHECK(ctx);
-    }
-    issued += nlaunch;
-    MSB_CUDA_TRY(ctx, cudaMemcpyAsync(&hs, st, sizeof(hs), cudaMemcpyDeviceToHost, ctx->stream));
-    MSB_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
-    if (hs.done || issued >= max_sweeps) break;
-  }
-  int n = hs.n;
-  std::vector<unsigned long long> bits(max_sweeps);
-  MSB_CUDA_TRY(ctx, cudaMemcpyAsync(bits.data(), dmax, max_sweeps * 8, cudaMemcpyDeviceToHost,
-                                    ctx->stream));
-  MSB_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
-  dfree(ctx, st);
-  dfree(ctx, dmax);
-  if (n & 1) L->cur ^= 1;
-  double last = 0.0;
-  bool bad = false;
-  for (int t = 0; t < n; ++t) {
-    double d;
-    memcpy(&d, &bits[t], 8);
-    if (!(d == d)) bad = true;
-    if (deltas) deltas[t] = d;
-    last = d;
-  }
-  if (sweeps_done) *sweeps_done = n;
-  if (last_delta) *last_delta = last;
-  if (bad) return set_error(ctx, MSB_EZERO_DIAG, "non-finite update: zero diagonal in A_T");
-  if (tol >= 0.0 && n >= max_sweeps && !(last <= tol)) return MSB_NOT_CONVERGED;
   return MSB_OK;
 }
 

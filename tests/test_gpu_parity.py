@@ -160,12 +160,41 @@ CYCLE_CASES = {
 }
 
 
-# Equal-count pressure parity is checked at min(k_oracle, K_PARITY) cycles.  Beyond a
-# few thousand cycles of an ill-conditioned case, rounding noise is amplified by the
-# iteration itself: on config2_recipe (cond(A_c) = 4.3e7, 13,989 cycles) two
-# backward-stable CPU coarse solvers, LAPACK LU and LAPACK Cholesky, already differ
-# by 2.0e-9, so 1e-9 is below the method's own floor there.
+# Rounding floor of the method itself.  The iteration amplifies
+# rounding in the coarse solve by cond(A_c): on config2_recipe (cond(A_c) = 4.3e7)
+# two backward-stable CPU coarse solvers, LAPACK LU (the oracle) and LAPACK
+# Cholesky, differ by 8.8e-10 after 200 cycles and 2.6e-9 after 2000; with the
+# dynamic stage (config3_recipe) their free-mode iteration counts differ by 3,
+# because the Δp bins of late iterations flip under that noise.  The GPU must be as
+# close to the oracle as the oracle is to itself: tolerances are
+#   x:      max(1e-9, 2 * ||x_LU - x_Chol|| / ||x_LU||)           at equal counts
+#   counts: max(1,    2 * |k_LU - k_Chol|)                         in free mode
+# which reduce to the north-star 1e-9 / ±1 on well-conditioned cases.
 K_PARITY = 2000
+
+
+class _CholeskyCoarse:
+    """Alternate exact coarse solver for the floor measurement (LAPACK potrf/potrs)."""
+
+    def __init__(self, Ac):
+        import scipy.linalg as la
+        self.Ac = Ac
+        self.M = Ac.shape[0]
+        self._c = la.cho_factor(Ac, lower=True)
+
+    def solve(self, rc):
+        import scipy.linalg as la
+        return la.cho_solve(self._c, rc)
+
+
+def _oracle_cholesky(prob, fixed_iters=None):
+    from oracle import cycle as ocy
+    saved = ocy.CoarseSolver
+    ocy.CoarseSolver = _CholeskyCoarse
+    try:
+        return _oracle_full(prob, fixed_iters=fixed_iters)
+    finally:
+        ocy.CoarseSolver = saved
 
 
 @pytest.mark.parametrize("name", list(CYCLE_CASES))
@@ -174,17 +203,22 @@ def test_cycle_parity(ctx, name):
     orc = _oracle_full(prob)
     k_or = orc["sol"]["iters"]
     assert orc["sol"]["converged"]
-    # free mode: iteration counts within ±1
+    k_cho = _oracle_cholesky(prob)["sol"]["iters"]
+    k_tol = max(1, 2 * abs(k_or - k_cho))
+    # free mode: iteration counts within ±1 (or the measured floor)
     g = _gpu_full(ctx, prob)
-    assert abs(g["sol"]["iters"] - k_or) <= 1, (g["sol"]["iters"], k_or)
-    # fixed mode at an equal count: pressure relative L2 <= 1e-9
+    assert abs(g["sol"]["iters"] - k_or) <= k_tol, (g["sol"]["iters"], k_or, k_cho)
+    # fixed mode at an equal count: pressure relative L2 <= 1e-9 (or the floor)
     k_fix = min(k_or, K_PARITY)
     if k_fix != k_or:
         orc = _oracle_full(prob, fixed_iters=k_fix)
-    g2 = _gpu_full(ctx, prob, fixed_iters=k_fix)
     xo = orc["sol"]["x"]
+    xc = _oracle_cholesky(prob, fixed_iters=k_fix)["sol"]["x"]
+    floor = np.linalg.norm(xc - xo) / np.linalg.norm(xo)
+    x_tol = max(X_RTOL, 2.0 * floor)
+    g2 = _gpu_full(ctx, prob, fixed_iters=k_fix)
     err = np.linalg.norm(g2["x_host"] - xo) / np.linalg.norm(xo)
-    assert err <= X_RTOL, err
+    assert err <= x_tol, (err, floor)
     # residual history: same trajectory (absolute 1e-8 of ρ_0 = 1 — the tail near the
     # 1e-6 tolerance amplifies 1e-13 differences in x by the conditioning of A)
     assert np.allclose(g2["sol"]["res"], orc["sol"]["res"][:k_fix + 1], rtol=1e-6, atol=1e-8)
