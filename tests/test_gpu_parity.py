@@ -213,15 +213,21 @@ def test_cycle_parity(ctx, name):
     if k_fix != k_or:
         orc = _oracle_full(prob, fixed_iters=k_fix)
     xo = orc["sol"]["x"]
-    xc = _oracle_cholesky(prob, fixed_iters=k_fix)["sol"]["x"]
+    cho = _oracle_cholesky(prob, fixed_iters=k_fix)["sol"]
+    xc = cho["x"]
     floor = np.linalg.norm(xc - xo) / np.linalg.norm(xo)
     x_tol = max(X_RTOL, 2.0 * floor)
     g2 = _gpu_full(ctx, prob, fixed_iters=k_fix)
     err = np.linalg.norm(g2["x_host"] - xo) / np.linalg.norm(xo)
     assert err <= x_tol, (err, floor)
-    # residual history: same trajectory (absolute 1e-8 of ρ_0 = 1 — the tail near the
-    # 1e-6 tolerance amplifies 1e-13 differences in x by the conditioning of A)
-    assert np.allclose(g2["sol"]["res"], orc["sol"]["res"][:k_fix + 1], rtol=1e-6, atol=1e-8)
+    # residual history: same trajectory.  Absolute 1e-8 of ρ_0 = 1 (the tail near the
+    # 1e-6 tolerance amplifies 1e-13 differences in x by the conditioning of A), or
+    # twice the LU-vs-Cholesky oracle spread when the dynamic stage makes the tail
+    # chaotic (its Δp bins flip under rounding noise).
+    ro = orc["sol"]["res"][:k_fix + 1]
+    r_floor = float(np.max(np.abs(cho["res"][:k_fix + 1] - ro)))
+    assert np.all(np.abs(g2["sol"]["res"] - ro) <= max(1e-8, 2.0 * r_floor) + 1e-6 * np.abs(ro)), \
+        r_floor
 
 
 def test_cycle_fixed_small_counts(ctx):
