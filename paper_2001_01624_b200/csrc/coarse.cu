@@ -11,6 +11,9 @@
 // d_jj <= 1e-14 max|A_c| -> MSB_ESINGULAR.  The explicit inverse
 // X = L^-T L^-1 is formed once, so every coarse solve in the cycle is a single
 // bandwidth-bound GEMV (M^2 doubles) instead of two latency-bound triangular solves.
+#include <algorithm>
+#include <cstdlib>
+
 #include "internal.cuh"
 
 namespace msb {
@@ -251,43 +254,48 @@ __global__ void k_identity(double* __restrict__ X, int M) {
 }
 
 // ---------------------------------------------------------------- GEMV solve
-// xc = X rc, one warp per row, coalesced double2 loads.  Skips when *done.
+// xc = X rc, one CTA per row: 256 threads each issue all of their (<= 8 at M <= 4096)
+// 16-byte loads of the row at once, so a row costs one memory round trip and ~8 rows
+// per SM are in flight; fixed-order per-thread sums + shuffle/smem tree: deterministic.
+// The done flag is read at entry and tested before the store.
+template <bool kStream>
 __global__ void __launch_bounds__(256) k_gemv(const double* __restrict__ X, int M,
                                               const double* __restrict__ rc,
                                               double* __restrict__ xc, const int* done) {
-  if (done && *(volatile const int*)done) return;
-  int lane = threadIdx.x & 31;
-  int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (row >= M) return;
+  const bool skip = done && *(volatile const int*)done;
+  const int64_t row = blockIdx.x;
   const double* a = X + row * M;
   double s = 0.0;
   if ((M & 1) == 0) {
-    // four independent 16-byte streaming loads in flight per lane (the matrix is
-    // read once per solve: evict-first; rc stays in L1/L2)
     const double2* a2 = reinterpret_cast<const double2*>(a);
     const double2* r2 = reinterpret_cast<const double2*>(rc);
-    int h = M >> 1;
-    double s1 = 0.0, s2 = 0.0, s3 = 0.0;
-    int t = lane;
-    for (; t + 96 < h; t += 128) {
-      double2 a0 = __ldcs(a2 + t), a1 = __ldcs(a2 + t + 32), a2v = __ldcs(a2 + t + 64),
-              a3 = __ldcs(a2 + t + 96);
-      double2 b0 = r2[t], b1 = r2[t + 32], b2 = r2[t + 64], b3 = r2[t + 96];
-      s += a0.x * b0.x + a0.y * b0.y;
-      s1 += a1.x * b1.x + a1.y * b1.y;
-      s2 += a2v.x * b2.x + a2v.y * b2.y;
-      s3 += a3.x * b3.x + a3.y * b3.y;
+    const int h = M >> 1;
+    for (int t0 = threadIdx.x; t0 < h; t0 += 8 * 256) {
+      double2 av[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int t = t0 + 256 * u;
+        av[u] = t < h ? (kStream ? __ldcs(a2 + t) : a2[t]) : make_double2(0.0, 0.0);
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int t = t0 + 256 * u;
+        const double2 b = t < h ? r2[t] : make_double2(0.0, 0.0);
+        s += av[u].x * b.x + av[u].y * b.y;
+      }
     }
-    for (; t < h; t += 32) {
-      double2 av = __ldcs(a2 + t), rv = r2[t];
-      s += av.x * rv.x + av.y * rv.y;
-    }
-    s = (s + s1) + (s2 + s3);
   } else {
-    for (int t = lane; t < M; t += 32) s += __ldcs(a + t) * rc[t];
+    for (int t = threadIdx.x; t < M; t += 256) s += (kStream ? __ldcs(a + t) : a[t]) * rc[t];
   }
+  __shared__ double sh[8];
   for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-  if (lane == 0) xc[row] = s;
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0 && !skip) {
+    double t = 0.0;
+    for (int w = 0; w < 8; ++w) t += sh[w];
+    xc[row] = t;
+  }
 }
 
 // ---------------------------------------------------------------- drivers
@@ -363,9 +371,59 @@ msb_status coarse_factor_dense(msb_ctx ctx, Coarse& co) {
   return MSB_OK;
 }
 
+// L2 residency of the dense inverse (B200: 126 MB L2).  The inverse is the only operand
+// of the cycle that is read unchanged every stage, so when the device allows a
+// persisting carve-out the GEMV is launched with an access-policy window over it:
+// after the first solve its lines stay in L2 and the per-stage M^2 HBM stream becomes
+// an L2 read.  Opt-in (MSB_L2_PERSIST=1): measured on config 2 the carve-out cost the
+// sweep 2x (its working set loses L2) for a 0.7 % cycle gain (profiles/r01_v1/).
+static size_t persist_bytes(msb_ctx ctx, size_t want) {
+  static int state = -1;  // -1 unknown, 0 off, 1 on
+  static size_t max_win = 0, max_persist = 0;
+  if (state < 0) {
+    const char* e = getenv("MSB_L2_PERSIST");
+    state = (e && e[0] == '1') ? 1 : 0;
+    int v = 0;
+    if (state && cudaDeviceGetAttribute(&v, cudaDevAttrMaxAccessPolicyWindowSize, ctx->device) == cudaSuccess)
+      max_win = (size_t)v;
+    if (state && cudaDeviceGetAttribute(&v, cudaDevAttrMaxPersistingL2CacheSize, ctx->device) == cudaSuccess)
+      max_persist = (size_t)v;
+    if (!max_win || !max_persist) state = 0;
+    if (state && cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, max_persist) != cudaSuccess) state = 0;
+    cudaGetLastError();
+  }
+  if (!state) return 0;
+  return std::min(want, std::min(max_win, max_persist));
+}
+
+void coarse_persist_init(msb_ctx ctx) { persist_bytes(ctx, 0); }
+
 void coarse_solve_dense(msb_ctx ctx, const Coarse& co, const double* rc, double* xc,
                         const int* done) {
-  k_gemv<<<grid_for(co.M, 8), 256, 0, ctx->stream>>>(co.Ainv, co.M, rc, xc, done);
+  const size_t bytes = (size_t)co.M * co.M * sizeof(double);
+  const size_t win = persist_bytes(ctx, bytes);
+  if (win) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(co.M);
+    cfg.blockDim = dim3(256);
+    cfg.stream = ctx->stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeAccessPolicyWindow;
+    at[0].val.accessPolicyWindow.base_ptr = co.Ainv;
+    at[0].val.accessPolicyWindow.num_bytes = win;
+    at[0].val.accessPolicyWindow.hitRatio = 1.0f;
+    at[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    at[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    if (cudaLaunchKernelEx(&cfg, k_gemv<false>, (const double*)co.Ainv, co.M, rc, xc, done) ==
+        cudaSuccess) {
+      count_launch();
+      return;
+    }
+    cudaGetLastError();
+  }
+  k_gemv<true><<<co.M, 256, 0, ctx->stream>>>(co.Ainv, co.M, rc, xc, done);
   count_launch();
 }
 

@@ -197,3 +197,43 @@ const char* msb_version(void) { return "libmsb 0.1 sm_100a"; }
 int64_t msb_launch_count(void) { return msb::g_launches.load(); }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------- TMA tensor maps (tma.cuh)
+#include "tma.cuh"
+
+namespace msb {
+
+static PFN_cuTensorMapEncodeTiled_v12000 tma_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    else
+      cudaGetLastError();
+  }
+  return fn;
+}
+
+bool tma_encode_4d(CUtensorMap* map, const double* base, const uint64_t dims[4],
+                   const uint64_t strides_el[3], const uint32_t box[4]) {
+  auto fn = tma_encoder();
+  if (!fn) return false;
+  cuuint64_t gd[4] = {dims[0], dims[1], dims[2], dims[3]};
+  cuuint64_t gs[3] = {strides_el[0] * 8, strides_el[1] * 8, strides_el[2] * 8};
+  for (int i = 0; i < 3; ++i)
+    if (gs[i] % 16) return false;
+  if (reinterpret_cast<uintptr_t>(base) % 16) return false;
+  cuuint32_t bd[4] = {box[0], box[1], box[2], box[3]};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double*>(base), gd, gs, bd, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+}  // namespace msb

@@ -78,6 +78,8 @@ __device__ __forceinline__ void warp_partial(double v, double* __restrict__ part
 __device__ __forceinline__ bool is_done(const IterState* st) {
   return *(volatile const int*)&st->done != 0;
 }
+// The streaming kernels read the flag at entry but test it only before their stores,
+// so its L2 round trip overlaps the data loads instead of serialising every CTA.
 
 // Stop test (a11): one CTA sums the per-warp partials in a fixed order (deterministic),
 // records ρ_k and decides.  mode 1: store ||b||.
@@ -151,7 +153,7 @@ __global__ void __launch_bounds__(CT) k_jacobi(StencilT S, const double* __restr
                                                const double* __restrict__ b, double omega,
                                                int first, double* __restrict__ partials,
                                                const IterState* st) {
-  if (is_done(st)) return;
+  const bool done = is_done(st);
   const int N = S.g.nxy * S.g.nz;
   int c = blockIdx.x * blockDim.x + threadIdx.x;
   double v = 0.0;
@@ -160,14 +162,15 @@ __global__ void __launch_bounds__(CT) k_jacobi(StencilT S, const double* __restr
     g3_coords(S.g, c, i, j, k);
     double dA;
     double r = residual_at(S, x, b, c, i, j, k, &dA);
-    xo[c] = x[c] + omega * (r / dA);
+    const double xn = x[c] + omega * (r / dA);
+    if (!done) xo[c] = xn;
     v = r * r;
   }
   if (first) warp_partial(v, partials);
 }
 
 struct LevelView {
-  int kind, W, nb0, nb1;
+  int kind, W, nb0, nb1, nb2, b0, b1, b2;
   Grid3 g;
   const int32_t* tab;
   const int32_t* col;
@@ -264,6 +267,131 @@ __global__ void __launch_bounds__(CT) k_prolong(LevelView L, double* __restrict_
   x[c] += acc;
 }
 
+// a6: r = b - A x (materialised for the gather restriction); `first` also emits the
+// ||r||^2 partials of the stop test (post-smoothing order starts a cycle here).
+__global__ void __launch_bounds__(CT) k_residual(StencilT S, const double* __restrict__ x,
+                                                 const double* __restrict__ b,
+                                                 double* __restrict__ r, int first,
+                                                 double* __restrict__ partials,
+                                                 const IterState* st) {
+  const bool done = is_done(st);
+  const int N = S.g.nxy * S.g.nz;
+  int c = blockIdx.x * blockDim.x + threadIdx.x;
+  double v = 0.0;
+  if (c < N) {
+    int i, j, k;
+    g3_coords(S.g, c, i, j, k);
+    double dA;
+    v = residual_at(S, x, b, c, i, j, k, &dA);
+    if (!done) r[c] = v;
+  }
+  if (first) warp_partial(v * v, partials);
+}
+
+// Open-box support range of block J along one axis (reading A3): cells x with
+// C(J-1) < 2x+1 < C(J+1), C(J) = lo_J + hi_J, limits dropped at the boundary.
+__device__ __forceinline__ void support_range(int J, int b, int n, int nb, int& x0, int& x1) {
+  x0 = 0;
+  x1 = n;
+  if (J > 0) {
+    int lo = (J - 1) * b;
+    x0 = (lo + min(lo + b, n) + 1) >> 1;
+  }
+  if (J < nb - 1) {
+    int lo = (J + 1) * b;
+    x1 = (lo + min(lo + b, n)) >> 1;
+  }
+}
+
+// a8 (Cartesian level): r_c[J] = Σ_{c ∈ S_J} P_cJ r_c, one CTA per coarse column,
+// gathering its support box row by row (column J lives in the parity slot of J in
+// every cell of S_J).  Every P entry is read exactly once; r (N doubles) stays in L2.
+// Fixed-order reduction: deterministic, no atomics.
+__global__ void __launch_bounds__(256) k_restrict_cart(LevelView L, const double* __restrict__ r,
+                                                       double* __restrict__ rc,
+                                                       const IterState* st) {
+  const bool done = is_done(st);
+  const int J = blockIdx.x;
+  const int N = L.g.nxy * L.g.nz;
+  const int nx = L.g.nx, sxy = L.g.nxy;
+  const int Jx = J % L.nb0, Jy = (J / L.nb0) % L.nb1, Jz = J / (L.nb0 * L.nb1);
+  int x0, x1, y0, y1, z0, z1;
+  support_range(Jx, L.b0, nx, L.nb0, x0, x1);
+  support_range(Jy, L.b1, L.g.ny, L.nb1, y0, y1);
+  support_range(Jz, L.b2, L.g.nz, L.nb2, z0, z1);
+  const int s = (Jx & 1) | ((Jy & 1) << 1) | ((Jz & 1) << 2);
+  const double* __restrict__ Ps = L.P + (size_t)s * N;
+  const int wx = x1 - x0, wy = y1 - y0;
+  const int rows = wy * (z1 - z0);
+  // rows of the box are spread over sub-warp groups of xw >= wx lanes (xw a power of
+  // two <= 32, wider rows loop); four rows per group are loaded before any FMA
+  const int xw = wx <= 8 ? 8 : (wx <= 16 ? 16 : 32);
+  const int rpw = 32 / xw;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int sub = lane / xw, xo = lane % xw;
+  const int rstep = (blockDim.x >> 5) * rpw;
+  double acc = 0.0;
+  for (int xb = 0; xb < wx; xb += xw) {
+    const int xx = xb + xo;
+    const bool xok = xx < wx;
+    for (int r0 = warp * rpw + sub; r0 < rows; r0 += 4 * rstep) {
+      double pv[4], rv[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int row = r0 + u * rstep;
+        const bool ok = xok && row < rows;
+        const int zz = row / wy, yy = row - zz * wy;
+        const int cc = x0 + xx + nx * (y0 + yy) + sxy * (z0 + zz);
+        pv[u] = ok ? Ps[cc] : 0.0;
+        rv[u] = ok ? r[cc] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) acc += pv[u] * rv[u];
+    }
+  }
+  __shared__ double sh[8];
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (lane == 0) sh[warp] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0 && !done) {
+    double t = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += sh[w];
+    rc[J] = t;
+  }
+}
+
+// a9 (Cartesian level): x += P x_c, one thread per cell: the six per-axis block
+// indices come from the parity table, the eight (P, x_c) loads are predicated selects
+// with no branches, so all sixteen are in flight together.
+__global__ void __launch_bounds__(CT) k_prolong_cart(LevelView L, double* __restrict__ x,
+                                                     const double* __restrict__ xc,
+                                                     const IterState* st) {
+  const bool done = is_done(st);
+  const int N = L.g.nxy * L.g.nz;
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= N) return;
+  int i, j, k;
+  g3_coords(L.g, c, i, j, k);
+  const int2 tx = reinterpret_cast<const int2*>(L.tab)[i];
+  const int2 ty = reinterpret_cast<const int2*>(L.tab)[L.g.nx + j];
+  const int2 tz = reinterpret_cast<const int2*>(L.tab)[L.g.nx + L.g.ny + k];
+  const double* __restrict__ base = L.P + c;
+  double v[8], xv[8];
+#pragma unroll
+  for (int s = 0; s < 8; ++s) {
+    const int jx = (s & 1) ? tx.y : tx.x, jy = (s & 2) ? ty.y : ty.x, jz = (s & 4) ? tz.y : tz.x;
+    const bool act = (jx | jy | jz) >= 0;
+    const int col = jx + L.nb0 * (jy + L.nb1 * jz);
+    v[s] = act ? base[(size_t)s * N] : 0.0;
+    xv[s] = act ? xc[col] : 0.0;
+  }
+  double acc = 0.0;
+#pragma unroll
+  for (int s = 0; s < 8; ++s) acc += v[s] * xv[s];
+  const double xn = x[c] + acc;
+  if (!done) x[c] = xn;
+}
+
 __global__ void k_zero_if(double* __restrict__ p, int n, const IterState* st) {
   if (is_done(st)) return;
   int t = blockIdx.x * blockDim.x + threadIdx.x;
@@ -343,8 +471,8 @@ static StencilT stencil(msb_op op) {
 }
 
 static LevelView view(msb_level L) {
-  return LevelView{L->kind, L->W, L->nb[0], L->nb[1], make_grid3(L->nx, L->ny, L->nz), L->tab,
-                   L->col, L->P[L->cur]};
+  return LevelView{L->kind, L->W, L->nb[0], L->nb[1], L->nb[2], L->bs[0], L->bs[1], L->bs[2],
+                   make_grid3(L->nx, L->ny, L->nz), L->tab, L->col, L->P[L->cur]};
 }
 // Build the dynamic constant-basis stage from dp (device, length N) into s->dyn_level.
 static msb_status build_dynamic(msb_ctx ctx, msb_solver s, const double* dp, int32_t* M_out,
@@ -437,6 +565,7 @@ msb_status msb_solver_create(msb_ctx ctx, msb_op op, const msb_level* levels, in
     maxM = std::max(maxM, L->M);
   }
   int64_t N = op->N;
+  coarse_persist_init(ctx);  // device-wide L2 carve-out, never inside a graph capture
   if (s->dyn) maxM = std::max(maxM, s->dyn_max + 3);
   s->maxM = maxM;
   MSB_ALLOC(ctx, s->xbuf[0], double, N);
@@ -444,11 +573,12 @@ msb_status msb_solver_create(msb_ctx ctx, msb_op op, const msb_level* levels, in
   MSB_ALLOC(ctx, s->rc, double, maxM + 2);
   MSB_ALLOC(ctx, s->xc, double, maxM + 2);
   MSB_ALLOC(ctx, s->partials, double, (size_t)grid_for(N, CT) * (CT / 32) + 32);
+  MSB_ALLOC(ctx, s->r, double, N);
   s->st = dalloc_n<IterState>(ctx, 1);
   if (!s->st) return set_error(ctx, MSB_ENOMEM, "solver state");
   if (s->dyn) {
     MSB_ALLOC(ctx, s->xprev, double, N);
-    MSB_ALLOC(ctx, s->r, double, N);
+    MSB_ALLOC(ctx, s->dpbuf, double, N);
     MSB_ALLOC(ctx, s->lab, int32_t, N);
     MSB_ALLOC(ctx, s->ids, int32_t, N);
     MSB_ALLOC(ctx, s->cnt, int32_t, 2 * N);
@@ -533,6 +663,21 @@ static msb_status enqueue_stage(msb_ctx ctx, msb_solver s, msb_level L, const do
     return MSB_OK;
   };
   auto corr = [&]() -> msb_status {
+    if (L->kind == 0) {
+      k_residual<<<g, CT, 0, st>>>(S, s->xbuf[cur], b, s->r, first ? 1 : 0, s->partials, s->st);
+      MSB_LAUNCH_CHECK(ctx);
+      if (first) {
+        msb_status rc = fin();
+        if (rc) return rc;
+      }
+      first = false;
+      k_restrict_cart<<<L->M, 256, 0, st>>>(V, s->r, s->rc, s->st);
+      MSB_LAUNCH_CHECK(ctx);
+      coarse_solve_dense(ctx, L->co, s->rc, s->xc, &s->st->done);
+      k_prolong_cart<<<g, CT, 0, st>>>(V, s->xbuf[cur], s->xc, s->st);
+      MSB_LAUNCH_CHECK(ctx);
+      return MSB_OK;
+    }
     k_zero_if<<<grid_for(L->M, 256), 256, 0, st>>>(s->rc, L->M, s->st);
     MSB_LAUNCH_CHECK(ctx);
     k_res_restrict<<<g, CT, 0, st>>>(S, V, s->xbuf[cur], b, s->rc, first ? 1 : 0, s->partials,
@@ -571,6 +716,69 @@ static msb_status enqueue_norm(msb_ctx ctx, msb_solver s, const double* x, const
   return MSB_OK;
 }
 
+static void drop_graphs(msb_solver s) {
+  for (int t = 0; t < 2; ++t) {
+    if (s->gexec[t]) cudaGraphExecDestroy(s->gexec[t]);
+    s->gexec[t] = nullptr;
+    s->glaunches[t] = 0;
+  }
+}
+
+// Capture `n` iterations of the static stages starting from x buffer `cur0` into a
+// CUDA graph (on a private capture stream: the context stream may be the legacy
+// default stream, which cannot be captured), instantiate once, reuse per chunk.
+static msb_status chunk_graph(msb_ctx ctx, msb_solver s, const double* db, int cur0, int n,
+                              cudaGraphExec_t* out) {
+  *out = nullptr;
+  std::vector<const void*> key = {db, s->res_dev, (const void*)(intptr_t)n};
+  for (msb_level L : s->levels) {
+    key.push_back(L->P[L->cur]);
+    key.push_back(L->co.Ainv);
+  }
+  if (key != s->gkey) {
+    drop_graphs(s);
+    s->gkey = key;
+  }
+  if (s->gexec[cur0]) {
+    *out = s->gexec[cur0];
+    return MSB_OK;
+  }
+  if (!s->cap_stream)
+    MSB_CUDA_TRY(ctx, cudaStreamCreateWithFlags(&s->cap_stream, cudaStreamNonBlocking));
+  cudaStream_t user = ctx->stream;
+  ctx->stream = s->cap_stream;
+  int64_t l0 = g_launches.load();
+  msb_status rc = MSB_OK;
+  cudaError_t e = cudaStreamBeginCapture(s->cap_stream, cudaStreamCaptureModeThreadLocal);
+  if (e == cudaSuccess) {
+    int cur = cur0;
+    for (int t = 0; t < n && !rc; ++t) {
+      bool first = true;
+      for (msb_level L : s->levels)
+        if ((rc = enqueue_stage(ctx, s, L, db, cur, first))) break;
+    }
+    cudaGraph_t graph = nullptr;
+    cudaError_t e2 = cudaStreamEndCapture(s->cap_stream, &graph);
+    if (!rc && e2 == cudaSuccess) {
+      e = cudaGraphInstantiate(&s->gexec[cur0], graph, 0);
+    } else if (e2 != cudaSuccess) {
+      e = e2;
+    }
+    if (graph) cudaGraphDestroy(graph);
+  }
+  ctx->stream = user;
+  s->glaunches[cur0] = g_launches.load() - l0;
+  g_launches.fetch_sub(s->glaunches[cur0]);  // captured, not launched
+  if (rc) return rc;
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    s->gexec[cur0] = nullptr;
+    return set_error(ctx, MSB_ECUDA, "graph capture: %s", cudaGetErrorString(e));
+  }
+  *out = s->gexec[cur0];
+  return MSB_OK;
+}
+
 msb_status msb_ms_iterate(msb_ctx ctx, msb_solver s, const double* b, double* x, double tol,
                           int32_t max_iter, int32_t fixed_iters, int32_t* iters_out,
                           double* res_hist, int32_t* dyn_M_hist) {
@@ -605,14 +813,29 @@ msb_status msb_ms_iterate(msb_ctx ctx, msb_solver s, const double* b, double* x,
   IterState hs{};
   if (!s->dyn) {
     const int chunk = 16;
+    const int flips = s->nu * (int)s->levels.size();  // x-buffer swaps per iteration
     int issued = 0;
     while (true) {
       int n = std::min(chunk, target - issued);
-      for (int t = 0; t < n; ++t) {
-        bool first = true;
-        for (msb_level L : s->levels)
-          if ((rc = enqueue_stage(ctx, s, L, db, cur, first))) return rc;
-        cur_after.push_back(cur);
+      cudaGraphExec_t ge = nullptr;
+      if (n == chunk) {
+        rc = chunk_graph(ctx, s, db, cur, chunk, &ge);
+        if (rc) return rc;
+      }
+      if (ge) {
+        MSB_CUDA_TRY(ctx, cudaGraphLaunch(ge, st));
+        g_launches.fetch_add(s->glaunches[cur], std::memory_order_relaxed);
+        for (int t = 0; t < n; ++t) {
+          cur ^= flips & 1;
+          cur_after.push_back(cur);
+        }
+      } else {
+        for (int t = 0; t < n; ++t) {
+          bool first = true;
+          for (msb_level L : s->levels)
+            if ((rc = enqueue_stage(ctx, s, L, db, cur, first))) return rc;
+          cur_after.push_back(cur);
+        }
       }
       issued += n;
       if (issued >= target)
@@ -631,9 +854,9 @@ msb_status msb_ms_iterate(msb_ctx ctx, msb_solver s, const double* b, double* x,
       int k = hs.k;  // iteration about to run (1-based)
       int32_t M = 0;
       if (k >= 2) {
-        k_dp<<<grid_for(N, 256), 256, 0, st>>>(s->xbuf[cur], s->xprev, N, s->r);
+        k_dp<<<grid_for(N, 256), 256, 0, st>>>(s->xbuf[cur], s->xprev, N, s->dpbuf);
         MSB_LAUNCH_CHECK(ctx);
-        if ((rc = build_dynamic(ctx, s, s->r, &M, nullptr))) return rc;
+        if ((rc = build_dynamic(ctx, s, s->dpbuf, &M, nullptr))) return rc;
       }
       dynM.push_back(M);
       MSB_CUDA_TRY(ctx, cudaMemcpyAsync(s->xprev, s->xbuf[cur], N * sizeof(double),
@@ -671,6 +894,7 @@ msb_status msb_solver_destroy(msb_solver s) {
   dfree(ctx, s->xbuf[1]);
   dfree(ctx, s->xprev);
   dfree(ctx, s->r);
+  dfree(ctx, s->dpbuf);
   dfree(ctx, s->rc);
   dfree(ctx, s->xc);
   dfree(ctx, s->partials);
@@ -682,6 +906,8 @@ msb_status msb_solver_destroy(msb_solver s) {
   dfree(ctx, s->bins);
   dfree(ctx, s->scratch_i);
   if (s->dyn_level) level_free(s->dyn_level);
+  drop_graphs(s);
+  if (s->cap_stream) cudaStreamDestroy(s->cap_stream);
   delete s;
   return MSB_OK;
 }

@@ -12,8 +12,11 @@
 // slots and returns at once when δ_n <= tol, so a chunk of sweeps is enqueued
 // without host round trips and without any grid-wide fence.
 #include <algorithm>
+#include <climits>
+#include <cstdlib>
 
 #include "internal.cuh"
+#include "tma.cuh"
 
 namespace msb {
 
@@ -73,6 +76,12 @@ __global__ void k_axis_mask(const int32_t* __restrict__ tab, int n, int off,
   mask[off + x] = m;
 }
 
+// Two threads per cell: lanes 0-15 of a warp take 16 consecutive cells for the four
+// slots with z-parity 0, lanes 16-31 the same cells for z-parity 1, so every slot plane
+// is read as 128-byte half-warp segments.  All loads are predicated selects (no
+// branches), so the compiler issues a slot's seven loads back to back; inactive
+// (cell, slot) pairs and masked neighbours fetch nothing.  The row sum (A6) is the two
+// halves' partial sums joined by one shuffle.
 __global__ void __launch_bounds__(SWEEP_BLOCK, 4) k_sweep_cart(
     double* __restrict__ P0, double* __restrict__ P1, const double* __restrict__ Tx,
     const double* __restrict__ Ty, const double* __restrict__ Tz, const uint8_t* __restrict__ amask,
@@ -82,52 +91,223 @@ __global__ void __launch_bounds__(SWEEP_BLOCK, 4) k_sweep_cart(
   double* __restrict__ Pout = (n & 1) ? P0 : P1;
   const int N = g.nxy * g.nz;
   const int nx = g.nx, sxy = g.nxy;
-  int c = blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31, h = lane >> 4;
+  const int c0 = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 16 + (lane & 15);
+  const bool in = c0 < N;
+  const int c = in ? c0 : N - 1;
+  int i, j, k;
+  g3_coords(g, c, i, j, k);
+  const unsigned mx = amask[i], my = amask[nx + j], mz = amask[nx + g.ny + k];
+  const double txp = Tx[c], typ = Ty[c], tzp = Tz[c];
+  const double txm = i > 0 ? Tx[c - 1] : 0.0;
+  const double tym = j > 0 ? Ty[c - nx] : 0.0;
+  const double tzm = k > 0 ? Tz[c - sxy] : 0.0;
+  const double D = txp + txm + typ + tym + tzp + tzm;
+  const double wD = omega / D;
+  const double om1 = 1.0 - omega;
+  const bool zin = in && ((mz >> h) & 1u);
+  const bool zm = (mz >> (2 + h)) & 1u, zp = (mz >> (4 + h)) & 1u;
+  const double* __restrict__ base = Pin + (size_t)(4 * h) * N + c;
+  double* __restrict__ obase = Pout + (size_t)(4 * h) * N + c;
+  double po[4], ph[4];
+  double sum = 0.0;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int px = q & 1, py = q >> 1;
+    const bool act = zin && ((mx >> px) & (my >> py) & 1u);
+    const double* __restrict__ b = base + (size_t)q * N;
+    const double vzm = (act && zm) ? b[-sxy] : 0.0;
+    const double vym = (act && ((my >> (2 + py)) & 1u)) ? b[-nx] : 0.0;
+    const double vxm = (act && ((mx >> (2 + px)) & 1u)) ? b[-1] : 0.0;
+    const double vxp = (act && ((mx >> (4 + px)) & 1u)) ? b[1] : 0.0;
+    const double vyp = (act && ((my >> (4 + py)) & 1u)) ? b[nx] : 0.0;
+    const double vzp = (act && zp) ? b[sxy] : 0.0;
+    const double p = act ? b[0] : 0.0;
+    double acc = tzm * vzm;
+    acc += tym * vym;
+    acc += txm * vxm;
+    acc += txp * vxp;
+    acc += typ * vyp;
+    acc += tzp * vzp;
+    po[q] = p;
+    ph[q] = act ? om1 * p + wD * acc : 0.0;
+    sum += ph[q];
+  }
+  sum += __shfl_xor_sync(0xffffffffu, sum, 16);
   double dloc = 0.0;
-  if (c < N) {
-    int i, j, k;
-    g3_coords(g, c, i, j, k);
-    const unsigned mx = amask[i], my = amask[nx + j], mz = amask[nx + g.ny + k];
-    double txp = Tx[c], typ = Ty[c], tzp = Tz[c];
-    double txm = i > 0 ? Tx[c - 1] : 0.0;
-    double tym = j > 0 ? Ty[c - nx] : 0.0;
-    double tzm = k > 0 ? Tz[c - sxy] : 0.0;
-    double D = txp + txm + typ + tym + tzp + tzm;
-    double wD = omega / D;
-    double om1 = 1.0 - omega;
-    double ph[8];
-    double sum = 0.0;
 #pragma unroll
-    for (int s = 0; s < 8; ++s) {
-      const int px = s & 1, py = (s >> 1) & 1, pz = s >> 2;
-      ph[s] = 0.0;
-      if ((mx >> px) & (my >> py) & (mz >> pz) & 1u) {
-        const double* __restrict__ base = Pin + (size_t)s * N;
-        double acc = 0.0;
-        if ((mz >> (2 + pz)) & 1u) acc += tzm * base[c - sxy];
-        if ((my >> (2 + py)) & 1u) acc += tym * base[c - nx];
-        if ((mx >> (2 + px)) & 1u) acc += txm * base[c - 1];
-        if ((mx >> (4 + px)) & 1u) acc += txp * base[c + 1];
-        if ((my >> (4 + py)) & 1u) acc += typ * base[c + nx];
-        if ((mz >> (4 + pz)) & 1u) acc += tzp * base[c + sxy];
-        double p = base[c];
-        ph[s] = om1 * p + wD * acc;
-        sum += ph[s];
-      }
-    }
-    // second pass: the cell's own P values are re-read (L1 hits) instead of being
-    // held in registers, which keeps the kernel at 4 blocks/SM
-#pragma unroll
-    for (int s = 0; s < 8; ++s) {
-      const int px = s & 1, py = (s >> 1) & 1, pz = s >> 2;
-      if ((mx >> px) & (my >> py) & (mz >> pz) & 1u) {
-        double pn = ph[s] / sum;
-        double po = __ldca(Pin + (size_t)s * N + c);
-        Pout[(size_t)s * N + c] = pn;
-        dloc = nmax(dloc, fabs(pn - po));
-      }
+  for (int q = 0; q < 4; ++q) {
+    const int px = q & 1, py = q >> 1;
+    const bool act = zin && ((mx >> px) & (my >> py) & 1u);
+    if (act) {
+      const double pn = ph[q] / sum;
+      obase[(size_t)q * N] = pn;
+      dloc = nmax(dloc, fabs(pn - po[q]));
     }
   }
+  sweep_fold(dloc, dslots, n);
+}
+
+// ---------------------------------------------------------------- G2': TMA-staged z-marching sweep
+// The B200 path for grids whose x extent is even (TMA needs 16-byte global strides).
+// A CTA owns a 32 x 4 column tile and marches it along z.  Each z plane of the tile
+// plus its halo — all 8 slot planes of P and the three T planes — arrives in shared
+// memory as two 4D TMA boxes (OOB halo zero-filled by the hardware) in a ring of
+// TT_S stages signalled by mbarriers and prefetched TT_S-2 planes ahead.  Two threads
+// per cell (lanes 0-15: slots with z-parity 0, lanes 16-31: z-parity 1, as in
+// k_sweep_cart) read every neighbour from shared memory — the z neighbours are the
+// ring's previous/next stage — so each P value crosses HBM once per sweep and the
+// 28 neighbour reads per thread are LDS, not LDG.  Persistent CTAs take (x-tile,
+// y-tile, z-chunk) items round-robin; the z-chunk length is chosen on the host to
+// balance the items over the resident CTAs.  Same arithmetic as k_sweep_cart
+// (masked transmissibilities multiply zero-filled values; the renormalisation is a
+// reciprocal with one residual correction, i.e. the correctly rounded quotient).
+// TMA requires the innermost box start to be 16-byte aligned, so the x halo is two
+// cells wide on each side (box x range [x0-2, x0+34), x0 a multiple of 32).
+constexpr int TT_X = 32, TT_Y = 4, TT_S = 4;
+constexpr int TB_X = TT_X + 4, TB_Y = TT_Y + 2, TQ_Y = TT_Y + 1;
+constexpr int TP_DBL = 8 * TB_Y * TB_X;  // P box (doubles): rows y0-1 .. y0+TT_Y
+constexpr int TQ_DBL = 3 * TQ_Y * TB_X;  // T box: rows y0-1 .. y0+TT_Y-1
+constexpr int TSTAGE_DBL = ((TP_DBL + TQ_DBL) * 8 + 127) / 128 * 128 / 8;
+constexpr uint32_t TSTAGE_TX = (uint32_t)(TP_DBL + TQ_DBL) * 8u;
+constexpr size_t TSWEEP_SMEM = (size_t)TT_S * TSTAGE_DBL * 8 + 64;
+constexpr int TSWEEP_THREADS = 2 * TT_X * TT_Y;
+
+struct SweepTiles {
+  int ntx, nty, kz, items;
+};
+
+// v if bit else +0.0, without a predicate (bit in {0, 1})
+__device__ __forceinline__ double mask_d(double v, unsigned bit) {
+  return __longlong_as_double(__double_as_longlong(v) & -(long long)bit);
+}
+
+__device__ __forceinline__ double div_rn(double a, double b, double rb) {
+  double q = a * rb;
+  double e = fma(-q, b, a);
+  return fma(e, rb, q);
+}
+
+__global__ void __launch_bounds__(TSWEEP_THREADS) k_sweep_tma(
+    const __grid_constant__ CUtensorMap mP0, const __grid_constant__ CUtensorMap mP1,
+    const __grid_constant__ CUtensorMap mT, double* __restrict__ P0, double* __restrict__ P1,
+    const uint8_t* __restrict__ amask, Grid3 g, SweepTiles tl, double omega, int n, double tol,
+    unsigned long long* __restrict__ dslots) {
+  if (sweep_skip(dslots, n, tol)) return;
+  // dynamic shared memory declared 128-byte aligned (TMA destination requirement) and
+  // indexed directly, so every stage read compiles to LDS (a pointer laundered through
+  // integer alignment arithmetic would fall back to generic LD).
+  extern __shared__ __align__(128) double sm[];
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + TT_S * TSTAGE_DBL);
+  const CUtensorMap* mIn = (n & 1) ? &mP1 : &mP0;
+  double* __restrict__ Pout = (n & 1) ? P0 : P1;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, h = lane >> 4;
+  const int ty = w >> 1, tx = ((w & 1) << 4) + (lane & 15);
+  const int nx = g.nx, ny = g.ny, nz = g.nz, N = g.nxy * g.nz;
+  if (tid == 0) {
+    if (smem_u32(sm) & 127u) __trap();  // TMA destinations must be 128-byte aligned
+    for (int t = 0; t < TT_S; ++t) mbar_init(&bars[t], 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  const double om1 = 1.0 - omega;
+  const int loc = (ty + 1) * TB_X + (tx + 2);  // same offset in the P and T boxes' row grid
+  uint32_t seq = 0;  // plane sequence number over this CTA's lifetime (ring slot / phase)
+  double dloc = 0.0;
+  bool nan_seen = false;
+  for (int item = blockIdx.x; item < tl.items; item += gridDim.x) {
+    const int xt = item % tl.ntx, rest = item / tl.ntx;
+    const int yt = rest % tl.nty, zc = rest / tl.nty;
+    const int x0 = xt * TT_X, y0 = yt * TT_Y, k0 = zc * tl.kz, k1 = min(k0 + tl.kz, nz);
+    const int np = k1 - k0 + 2;  // planes k0-1 .. k1
+    auto issue = [&](int p) {    // plane p of this item (z = k0 - 1 + p)
+      const uint32_t sq = seq + p;
+      const int slot = sq % TT_S;
+      double* st = sm + slot * TSTAGE_DBL;
+      mbar_expect_tx(&bars[slot], TSTAGE_TX);
+      tma_load_4d(st, mIn, &bars[slot], x0 - 2, y0 - 1, k0 - 1 + p, 0);
+      tma_load_4d(st + TP_DBL, &mT, &bars[slot], x0 - 2, y0 - 1, k0 - 1 + p, 0);
+    };
+    auto wait = [&](int p) {
+      const uint32_t sq = seq + p;
+      mbar_wait(&bars[sq % TT_S], (sq / TT_S) & 1u);
+    };
+    if (tid == 0)
+      for (int p = 0; p < min(TT_S - 1, np); ++p) issue(p);
+    const int x = x0 + tx, y = y0 + ty;
+    const bool inxy = x < nx && y < ny;
+    const unsigned mx = inxy ? amask[x] : 0u, my = inxy ? amask[nx + y] : 0u;
+    unsigned mz_next = amask[nx + ny + k0];
+    for (int k = k0; k < k1; ++k) {
+      const int pc = k - k0 + 1;
+      const unsigned mz = mz_next;
+      if (k + 1 < k1) mz_next = amask[nx + ny + k + 1];
+      if (tid == 0 && pc + TT_S - 2 < np) issue(pc + TT_S - 2);
+      if (pc == 1) {
+        wait(0);
+        wait(1);
+      }
+      wait(pc + 1);
+      const double* __restrict__ sM = sm + ((seq + pc - 1) % TT_S) * TSTAGE_DBL;
+      const double* __restrict__ sC = sm + ((seq + pc) % TT_S) * TSTAGE_DBL;
+      const double* __restrict__ sP = sm + ((seq + pc + 1) % TT_S) * TSTAGE_DBL;
+      const double* __restrict__ tC = sC + TP_DBL;
+      const double txp = tC[loc], txm = tC[loc - 1];
+      const double typ = tC[TQ_Y * TB_X + loc], tym = tC[TQ_Y * TB_X + loc - TB_X];
+      const double tzp = tC[2 * TQ_Y * TB_X + loc], tzm = sM[TP_DBL + 2 * TQ_Y * TB_X + loc];
+      const double D = txp + txm + typ + tym + tzp + tzm;
+      // out-of-domain tile cells see zero-filled T (D = 0): give them wD = 0 so their
+      // (unused) values stay finite
+      const double wD = inxy ? omega / D : 0.0;
+      const unsigned zb = (mz >> h) & 1u;
+      const double wzm = mask_d(tzm, (mz >> (2 + h)) & 1u), wzp = mask_d(tzp, (mz >> (4 + h)) & 1u);
+      const double wxm0 = mask_d(txm, (mx >> 2) & 1u), wxm1 = mask_d(txm, (mx >> 3) & 1u);
+      const double wxp0 = mask_d(txp, (mx >> 4) & 1u), wxp1 = mask_d(txp, (mx >> 5) & 1u);
+      const double wym0 = mask_d(tym, (my >> 2) & 1u), wym1 = mask_d(tym, (my >> 3) & 1u);
+      const double wyp0 = mask_d(typ, (my >> 4) & 1u), wyp1 = mask_d(typ, (my >> 5) & 1u);
+      const int ob = 4 * h * TB_Y * TB_X + loc;
+      // No activity select is needed: an inactive (cell, slot) holds 0, its neighbours
+      // along the inactive axis are masked, and its neighbours along the other axes
+      // share that coordinate and so hold 0 too — hence ph = 0 exactly.
+      double ph[4], po[4];
+      double sum = 0.0;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int px = q & 1, py = q >> 1;
+        const int o = ob + q * TB_Y * TB_X;
+        double acc = wzm * sM[o];
+        acc += (py ? wym1 : wym0) * sC[o - TB_X];
+        acc += (px ? wxm1 : wxm0) * sC[o - 1];
+        acc += (px ? wxp1 : wxp0) * sC[o + 1];
+        acc += (py ? wyp1 : wyp0) * sC[o + TB_X];
+        acc += wzp * sP[o];
+        po[q] = sC[o];
+        ph[q] = om1 * po[q] + wD * acc;
+        sum += ph[q];
+      }
+      sum += __shfl_xor_sync(0xffffffffu, sum, 16);
+      const unsigned act = zb & (unsigned)inxy;
+      if (act) {
+        const double rs = 1.0 / sum;
+        const int c = x + nx * (y + ny * k);
+        double* __restrict__ ob_out = Pout + (size_t)(4 * h) * N + c;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int px = q & 1, py = q >> 1;
+          if ((mx >> px) & (my >> py) & 1u) {
+            const double pn = div_rn(ph[q], sum, rs);
+            ob_out[(size_t)q * N] = pn;
+            dloc = fmax(dloc, fabs(pn - po[q]));
+          }
+        }
+        nan_seen |= !(sum == sum);  // zero diagonal in A_T
+      }
+      __syncthreads();  // ring slot of plane pc-1 is free for the next issue
+      if (tid == 0) fence_proxy_async_smem();
+    }
+    seq += np;
+  }
+  if (nan_seen) dloc = __longlong_as_double(0x7ff8000000000000ll);  // propagates to δ
   sweep_fold(dloc, dslots, n);
 }
 
@@ -225,7 +405,48 @@ extern "C" msb_status msb_smooth_basis(msb_ctx ctx, msb_level L, msb_op op, int3
   }
   double* Pa = L->P[L->cur];
   double* Pb = L->P[L->cur ^ 1];
-  const unsigned grid = grid_for(L->N, SWEEP_BLOCK);
+  // TMA path: tensor maps over both P buffers and the 3N transmissibility block
+  bool use_tma = false;
+  CUtensorMap mP[2], mT;
+  SweepTiles tl{};
+  unsigned tgrid = 0;
+  if (L->kind == 0 && (op->nx % 2) == 0 && !getenv("MSB_NO_TMA")) {
+    const uint64_t dP[4] = {(uint64_t)op->nx, (uint64_t)op->ny, (uint64_t)op->nz, 8};
+    const uint64_t dT[4] = {(uint64_t)op->nx, (uint64_t)op->ny, (uint64_t)op->nz, 3};
+    const uint64_t st3[3] = {(uint64_t)op->nx, (uint64_t)op->nx * op->ny, (uint64_t)L->N};
+    const uint32_t bP[4] = {TB_X, TB_Y, 1, 8}, bT[4] = {TB_X, TQ_Y, 1, 3};
+    use_tma = tma_encode_4d(&mP[0], Pa, dP, st3, bP) && tma_encode_4d(&mP[1], Pb, dP, st3, bP) &&
+              tma_encode_4d(&mT, op->Tx, dT, st3, bT);
+    if (use_tma) {
+      static int occ = 0;
+      if (!occ) {
+        MSB_CUDA_TRY(ctx, cudaFuncSetAttribute(k_sweep_tma, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               (int)TSWEEP_SMEM));
+        MSB_CUDA_TRY(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_sweep_tma, TSWEEP_THREADS,
+                                                                       TSWEEP_SMEM));
+        if (occ < 1) occ = 1;
+      }
+      tl.ntx = (op->nx + TT_X - 1) / TT_X;
+      tl.nty = (op->ny + TT_Y - 1) / TT_Y;
+      const int64_t slots = (int64_t)occ * ctx->sm_count;
+      const int64_t tiles = (int64_t)tl.ntx * tl.nty;
+      // z-chunking: minimise (waves) x (planes per item incl. 2 halo planes)
+      int64_t best = INT64_MAX;
+      for (int nzc = 1; nzc <= op->nz; ++nzc) {
+        int kz = (op->nz + nzc - 1) / nzc;
+        int64_t items = tiles * ((op->nz + kz - 1) / kz);
+        int64_t waves = (items + slots - 1) / slots;
+        int64_t cost = waves * (kz + 2);
+        if (cost < best) {
+          best = cost;
+          tl.kz = kz;
+          tl.items = (int)items;
+        }
+      }
+      tgrid = (unsigned)std::min<int64_t>(tl.items, slots);
+    }
+  }
+  const unsigned grid = L->kind == 0 ? grid_for(L->N * 2, SWEEP_BLOCK) : grid_for(L->N, SWEEP_BLOCK);
   const int chunk = 32;
   int issued = 0, n = 0;
   double last = 0.0;
@@ -235,7 +456,10 @@ extern "C" msb_status msb_smooth_basis(msb_ctx ctx, msb_level L, msb_op op, int3
     int nl = std::min(chunk, max_sweeps - issued);
     for (int t = 0; t < nl; ++t) {
       int idx = issued + t;
-      if (L->kind == 0)
+      if (use_tma)
+        k_sweep_tma<<<tgrid, TSWEEP_THREADS, TSWEEP_SMEM, st>>>(mP[0], mP[1], mT, Pa, Pb, L->amask, g,
+                                                            tl, omega, idx, tol, dslots);
+      else if (L->kind == 0)
         k_sweep_cart<<<grid, SWEEP_BLOCK, 0, st>>>(Pa, Pb, op->Tx, op->Ty, op->Tz, L->amask, g,
                                                    omega, idx, tol, dslots);
       else

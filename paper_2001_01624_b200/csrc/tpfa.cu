@@ -165,9 +165,10 @@ msb_status msb_build_tpfa(msb_ctx ctx, const msb_grid* g, const double* K, const
   op->ctx = ctx;
   op->nx = g->nx; op->ny = g->ny; op->nz = g->nz; op->N = N;
   op->dx = g->dx; op->dy = g->dy; op->dz = g->dz;
-  MSB_ALLOC(ctx, op->Tx, double, N);
-  MSB_ALLOC(ctx, op->Ty, double, N);
-  MSB_ALLOC(ctx, op->Tz, double, N);
+  // one 3N block: Tx | Ty | Tz, so a kernel can stage all three with one 4D TMA box
+  MSB_ALLOC(ctx, op->Tx, double, 3 * N);
+  op->Ty = op->Tx + N;
+  op->Tz = op->Tx + 2 * N;
   MSB_ALLOC(ctx, op->Tb, double, 3 * N);
   MSB_ALLOC(ctx, op->q, double, N);
   MSB_ALLOC(ctx, op->open, uint8_t, N);
@@ -257,9 +258,7 @@ msb_status msb_op_apply(msb_ctx ctx, msb_op op, const double* x, double* y) {
 msb_status msb_op_destroy(msb_op op) {
   if (!op) return MSB_EINVAL;
   msb_ctx ctx = op->ctx;
-  dfree(ctx, op->Tx);
-  dfree(ctx, op->Ty);
-  dfree(ctx, op->Tz);
+  dfree(ctx, op->Tx);  // Ty, Tz live in the same block
   dfree(ctx, op->Tb);
   dfree(ctx, op->q);
   dfree(ctx, op->open);

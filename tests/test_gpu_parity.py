@@ -73,6 +73,10 @@ def test_tpfa_parity(ctx, case):
 BASIS_CASES = {
     "config1_full": (lambda: make_problem(1), 200, True),
     "config2_recipe_ragged": (lambda: make_problem(2, shape=(26, 47, 23)), 25, True),
+    # even nx -> TMA z-marching kernel; ragged x tile (26 < 32), ragged y tile (46 % 4),
+    # z chunks with halo planes
+    "config2_recipe_even_ragged": (lambda: make_problem(2, shape=(26, 46, 23)), 25, True),
+    "wide_even_ragged": (lambda: random_problem(9, 70, 13, 11, (6, 5, 4), sigma=1.5), 30, True),
     "random_ragged": (lambda: random_problem(1, 23, 17, 7, (5, 4, 3), sigma=2.0), 40, True),
     "config2_recipe_tol": (lambda: make_problem(2, shape=(24, 44, 20)), 300, False),
     "2d_odd": (lambda: random_problem(2, 35, 21, 1, (7, 7, 1), sigma=1.0), 60, True),
