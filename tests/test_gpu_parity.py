@@ -327,3 +327,121 @@ def test_dynamic_labels_lockstep(ctx):
         M_g = s.add_dynamic_basis(np.ascontiguousarray(dp), part_g)
         assert M_g == M_o, name
         assert np.array_equal(part_g, part_o.astype(np.int32)), name
+
+
+# ---------------------------------------------------------------- row a12 (config 4)
+def test_transport_parity(ctx):
+    """Same p, S, λ in -> same S, sub-step count and upstream λ out (msb_transport_upwind)."""
+    import scipy.sparse.linalg as spla
+    import torch
+    from oracle import tpfa, transport
+    from oracle.grid import all_faces
+    from paper_2001_01624_b200.pipeline import build_operator
+    prob = make_problem(4, shape=(14, 26, 9))
+    rng = np.random.default_rng(3)
+    faces = all_faces(prob.nx, prob.ny, prob.nz)
+    S0 = rng.uniform(0.0, 0.9, prob.N)
+    p0 = rng.standard_normal(prob.N)
+    mob = transport.upstream_mobility(faces, p0, S0, 1.0, 5.0)
+    A_T, A, q, trans = tpfa.build(prob, mob)
+    p = spla.spsolve(A.tocsc(), q)
+    phi = np.full(prob.N, prob.phi)
+    dt = transport.step_size(prob, q, phi, 0.01)
+    S_or, n_or = transport.transport(trans, p, S0, phi, q, 1.0, 1.0, 5.0, dt)
+    mob_or = np.concatenate(transport.upstream_mobility(faces, p, S_or, 1.0, 5.0))
+    op = build_operator(ctx, prob, mob=np.ascontiguousarray(np.concatenate(mob)))
+    dev = "cuda"
+    S = torch.as_tensor(S0, device=dev)
+    mob_g = torch.empty(prob.n_faces, dtype=torch.float64, device=dev)
+    n_g = op.transport_upwind(torch.as_tensor(p, device=dev), S,
+                              torch.as_tensor(phi, device=dev), 1.0, 5.0, dt, mob_out=mob_g)
+    assert n_g == n_or
+    assert np.max(np.abs(S.cpu().numpy() - S_or)) <= 1e-13
+    # same upstream choice (same p); λ_t(S) differs only through S's rounding
+    assert np.allclose(mob_g.cpu().numpy(), mob_or, rtol=1e-12, atol=0.0)
+
+
+def test_config4_lockstep(ctx):
+    """Config-4 recipe on a reduced grid: per-step pressure (<= 1e-9 rel, equal counts),
+    saturation (<= 1e-9 abs) and free-mode per-step counts (±1)."""
+    from oracle import transport
+    from paper_2001_01624_b200 import pipeline as gp
+    prob = make_problem(4, shape=(18, 33, 10), max_sweeps=40, max_iter=20000)
+    steps, kw = 4, dict(k_adapt=5, pv_per_step=0.02)
+    free = transport.run(prob, steps=steps, **kw)
+    k_or = [r["iters"] for r in free["steps"]]
+    g_free = gp.run_sequential(ctx, prob, steps=steps, **kw)
+    for kg, ko in zip([r["iters"] for r in g_free["steps"]], k_or):
+        assert abs(kg - ko) <= 1, (kg, ko)
+    g = gp.run_sequential(ctx, prob, steps=steps, fixed_iters=k_or, keep_states=True, **kw)
+    assert g["init_sweeps"] == free["init_sweeps"]
+    for rg, ro in zip(g["steps"], free["steps"]):
+        assert rg["n_sub"] == ro["n_sub"]
+        assert np.linalg.norm(rg["p"] - ro["p"]) <= X_RTOL * np.linalg.norm(ro["p"])
+        assert np.max(np.abs(rg["S"] - ro["S"])) <= 1e-9
+
+
+# ---------------------------------------------------------------- full BASELINE sizes (bench launch config)
+def _full_sweep_lockstep(ctx, prob, pre_sweeps):
+    """GPU P^n exported, one oracle sweep from it, against the GPU's sweep n+1."""
+    from oracle import basis as ob
+    from oracle import partition as opart
+    from oracle import support as osup
+    from oracle import tpfa
+    from paper_2001_01624_b200 import Level
+    from paper_2001_01624_b200.pipeline import build_operator
+    A_T, _, _, _ = tpfa.build(prob)
+    pat = osup.box_pattern(prob.nx, prob.ny, prob.nz, prob.block)
+    part, M, _ = opart.cartesian(prob.nx, prob.ny, prob.nz, prob.block)
+    op = build_operator(ctx, prob)
+    lev = Level.cartesian(ctx, op, prob.block)
+    info = lev.info(with_part=True)
+    assert info["M"] == M and info["nnz"] == pat.nnz
+    assert np.array_equal(info["part"], part.astype(np.int32))
+    lev.smooth(op, pre_sweeps, prob.omega, -1.0)
+    rowptr, cols, vals_n, _ = lev.export()
+    assert np.array_equal(rowptr, pat.indptr.astype(np.int64))
+    assert np.array_equal(cols, pat.indices.astype(np.int32))
+    _, _, deltas, _ = lev.smooth(op, 1, prob.omega, -1.0)
+    _, _, vals_g, _ = lev.export()
+    ref, d_ref = ob.sweep(ob.Basis(pat, vals_n), A_T, prob.omega)
+    zero = ref.vals == 0.0
+    assert np.all(vals_g[zero] == 0.0)
+    rel = np.abs(vals_g[~zero] - ref.vals[~zero]) / ref.vals[~zero]
+    assert rel.max() <= P_RTOL, rel.max()
+    assert abs(deltas[0] - d_ref) <= 1e-12 * max(d_ref, 1e-300)
+    # partition of unity and bounds on the full grid
+    rows = np.repeat(np.arange(prob.N), np.diff(rowptr))
+    rs = np.bincount(rows, weights=vals_g, minlength=prob.N)
+    assert np.max(np.abs(rs - 1.0)) <= 1e-14
+    assert vals_g.min() >= 0.0 and vals_g.max() <= 1.0
+    return op, lev
+
+
+def test_full_config2_sweep_and_cycle_lockstep(ctx):
+    """BASELINE configs[1] at full size (1.122M cells, M = 3,400, nnz = 6,964,260):
+    one lockstep sweep, A_c, and one lockstep multiscale iteration."""
+    import torch
+    from oracle import coarse, tpfa
+    from oracle.cycle import Level as OLevel
+    from oracle.cycle import stage
+    from paper_2001_01624_b200 import Solver
+    prob = make_problem(2)
+    op, lev = _full_sweep_lockstep(ctx, prob, 40)
+    lev.assemble(op)
+    rowptr, cols, vals, Ac = lev.export(with_Ac=True)
+    _, A, q, _ = tpfa.build(prob)
+    import scipy.sparse as sp
+    P = sp.csr_matrix((vals, cols, rowptr), shape=(prob.N, 3400))
+    ref = coarse.galerkin(P, A)
+    assert np.max(np.abs(Ac - ref)) <= 1e-12 * np.abs(ref).max()
+    solver = Solver(ctx, op, [lev], prob.omega_s, prob.nu, prob.post_smooth)
+    x = torch.zeros(prob.N, dtype=torch.float64, device="cuda")
+    solver.iterate(x, None, prob.cycle_tol, 100, 5)
+    x5 = x.cpu().numpy()
+    solver.iterate(x, None, prob.cycle_tol, 100, 1)
+    x6 = x.cpu().numpy()
+    olev = OLevel(P, A)
+    x6_ref = stage(A, A.diagonal(), q, x5, olev, prob.omega_s, prob.nu, prob.post_smooth)
+    err = np.linalg.norm(x6 - x6_ref) / np.linalg.norm(x6_ref)
+    assert err <= X_RTOL, err
