@@ -1,0 +1,100 @@
+"""Run one BASELINE config at full size on cuda:0 and report phase timings, iteration
+counts and HBM fractions (CUDA events on the library stream).  Not the bench (bench.py
+is config 2); this is the config-5 / config-4 measurement harness.
+
+usage: python scripts/run_config.py 5 [--iters 20] [--sweeps 300]
+       python scripts/run_config.py 4 [--steps 100]
+"""
+import argparse
+import json
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+from paper_2001_01624_b200 import Context, Level, Solver  # noqa: E402
+from paper_2001_01624_b200 import pipeline as gp  # noqa: E402
+from synth.configs import make_problem  # noqa: E402
+
+
+def peak():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]
+    except Exception:
+        return 6650.0
+
+
+def ev(stream):
+    e = torch.cuda.Event(enable_timing=True)
+    e.record(stream)
+    return e
+
+
+def config_single(cfg, args):
+    prob = make_problem(cfg)
+    ctx = Context(0)
+    st = torch.cuda.current_stream()
+    t0 = time.perf_counter()
+    e0 = ev(st)
+    op = gp.build_operator(ctx, prob)
+    lev = Level.cartesian(ctx, op, prob.block)
+    e1 = ev(st)
+    n, last, deltas, _ = lev.smooth(op, args.sweeps or prob.max_sweeps, prob.omega,
+                                   -1.0 if prob.fixed_sweeps else prob.sweep_tol)
+    e2 = ev(st)
+    lev.assemble(op)
+    e3 = ev(st)
+    s = Solver(ctx, op, [lev], prob.omega_s, prob.nu, prob.post_smooth)
+    x = torch.zeros(prob.N, dtype=torch.float64, device="cuda")
+    fi = args.iters if args.iters else prob.fixed_iters
+    out = s.iterate(x, None, prob.cycle_tol, prob.max_iter, fi)
+    e4 = ev(st)
+    torch.cuda.synchronize()
+    info = lev.info()
+    nnz, M, N, nf = info["nnz"], info["M"], prob.N, prob.n_faces
+    t = [e0.elapsed_time(e1), e1.elapsed_time(e2), e2.elapsed_time(e3), e3.elapsed_time(e4)]
+    b_sweep = 16 * nnz + 8 * nf
+    b_iter = 16 * nnz + 8 * nf + 40 * N + 8 * M * M
+    ms_sweep = t[1] / max(1, n)
+    ms_iter = t[3] / max(1, out["iters"])
+    pk = peak()
+    rec = dict(config=cfg, N=N, M=M, nnz=nnz, sweeps=n, last_delta=last, iters=out["iters"],
+               final_res=float(out["res"][-1]), phase_ms=dict(setup=t[0], smooth=t[1], coarse=t[2],
+                                                               cycle=t[3]),
+               ms_per_sweep=ms_sweep, sweeps_per_s=1e3 / ms_sweep, ms_per_iteration=ms_iter,
+               sweep_gbs=b_sweep / ms_sweep / 1e6, iter_gbs=b_iter / ms_iter / 1e6,
+               sweep_frac=b_sweep / ms_sweep / 1e6 / pk, iter_frac=b_iter / ms_iter / 1e6 / pk,
+               wall_s=time.perf_counter() - t0)
+    print(json.dumps(rec), flush=True)
+
+
+def config4(args):
+    prob = make_problem(4)
+    ctx = Context(0)
+    t0 = time.perf_counter()
+    out = gp.run_sequential(ctx, prob, steps=args.steps)
+    torch.cuda.synchronize()
+    its = [r["iters"] for r in out["steps"]]
+    rec = dict(config=4, steps=args.steps, init_sweeps=out["init_sweeps"], total_iters=int(sum(its)),
+               per_step_iters=its, substeps=[r["n_sub"] for r in out["steps"]],
+               wall_s=time.perf_counter() - t0,
+               S_max=float(out["S"].max()), S_mean=float(out["S"].mean()))
+    print(json.dumps(rec), flush=True)
+
+
+if __name__ == "__main__":
+    ap = argparse.ArgumentParser()
+    ap.add_argument("config", type=int)
+    ap.add_argument("--iters", type=int, default=0)
+    ap.add_argument("--sweeps", type=int, default=0)
+    ap.add_argument("--steps", type=int, default=100)
+    a = ap.parse_args()
+    if a.config == 4:
+        config4(a)
+    else:
+        config_single(a.config, a)

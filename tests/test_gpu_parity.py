@@ -445,3 +445,31 @@ def test_full_config2_sweep_and_cycle_lockstep(ctx):
     x6_ref = stage(A, A.diagonal(), q, x5, olev, prob.omega_s, prob.nu, prob.post_smooth)
     err = np.linalg.norm(x6 - x6_ref) / np.linalg.norm(x6_ref)
     assert err <= X_RTOL, err
+
+
+def test_full_config5_sweep_lockstep_and_cycle(ctx):
+    """BASELINE configs[4] at full size (10M cells, M = 20,000, nnz = 68,090,100):
+    lockstep sweep + invariants, then one lockstep multiscale iteration against the
+    oracle's sparse (splu) coarse solve from the GPU-exported basis."""
+    import scipy.sparse as sp
+    import torch
+    from oracle import tpfa
+    from oracle.cycle import Level as OLevel
+    from oracle.cycle import stage
+    from paper_2001_01624_b200 import Solver
+    prob = make_problem(5)
+    op, lev = _full_sweep_lockstep(ctx, prob, 8)
+    lev.assemble(op)
+    rowptr, cols, vals, _ = lev.export()
+    assert len(vals) == 68090100
+    _, A, q, _ = tpfa.build(prob)
+    P = sp.csr_matrix((vals, cols, rowptr), shape=(prob.N, 20000))
+    solver = Solver(ctx, op, [lev], prob.omega_s, prob.nu, prob.post_smooth)
+    x = torch.zeros(prob.N, dtype=torch.float64, device="cuda")
+    solver.iterate(x, None, prob.cycle_tol, 100, 2)
+    x2 = x.cpu().numpy()
+    solver.iterate(x, None, prob.cycle_tol, 100, 1)
+    x3 = x.cpu().numpy()
+    x3_ref = stage(A, A.diagonal(), q, x2, OLevel(P, A), prob.omega_s, prob.nu, prob.post_smooth)
+    err = np.linalg.norm(x3 - x3_ref) / np.linalg.norm(x3_ref)
+    assert err <= X_RTOL, err
