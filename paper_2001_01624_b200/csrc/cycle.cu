@@ -13,6 +13,7 @@
 // (deterministic), records ρ_k and sets `done`; every later kernel of the enqueued
 // chunk sees `done` and returns at once, so the host synchronises once per chunk.
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 
 #include "internal.cuh"
@@ -148,6 +149,11 @@ __global__ void __launch_bounds__(CT) k_norm(StencilT S, const double* __restric
 }
 
 // a7: x_out = x + ω_s D_A^{-1}(b - A x); `first` also emits the ||r||^2 partials.
+// CPT cells per thread (strided by the block size, so every load instruction stays
+// coalesced): the loads of all CPT cells are in flight together and the grid is CPT
+// times shorter, which is what a short stencil pass needs to approach HBM bandwidth.
+constexpr int CPT = 4;
+
 __global__ void __launch_bounds__(CT) k_jacobi(StencilT S, const double* __restrict__ x,
                                                double* __restrict__ xo,
                                                const double* __restrict__ b, double omega,
@@ -155,16 +161,24 @@ __global__ void __launch_bounds__(CT) k_jacobi(StencilT S, const double* __restr
                                                const IterState* st) {
   const bool done = is_done(st);
   const int N = S.g.nxy * S.g.nz;
-  int c = blockIdx.x * blockDim.x + threadIdx.x;
-  double v = 0.0;
-  if (c < N) {
+  const int c0 = blockIdx.x * (CT * CPT) + threadIdx.x;
+  double r[CPT], dA[CPT], xv[CPT];
+#pragma unroll
+  for (int u = 0; u < CPT; ++u) {
+    const int c = min(c0 + u * CT, N - 1);
     int i, j, k;
     g3_coords(S.g, c, i, j, k);
-    double dA;
-    double r = residual_at(S, x, b, c, i, j, k, &dA);
-    const double xn = x[c] + omega * (r / dA);
-    if (!done) xo[c] = xn;
-    v = r * r;
+    r[u] = residual_at(S, x, b, c, i, j, k, &dA[u]);
+    xv[u] = x[c];
+  }
+  double v = 0.0;
+#pragma unroll
+  for (int u = 0; u < CPT; ++u) {
+    const int c = c0 + u * CT;
+    if (c < N) {
+      if (!done) xo[c] = xv[u] + omega * (r[u] / dA[u]);
+      v += r[u] * r[u];
+    }
   }
   if (first) warp_partial(v, partials);
 }
@@ -276,16 +290,26 @@ __global__ void __launch_bounds__(CT) k_residual(StencilT S, const double* __res
                                                  const IterState* st) {
   const bool done = is_done(st);
   const int N = S.g.nxy * S.g.nz;
-  int c = blockIdx.x * blockDim.x + threadIdx.x;
-  double v = 0.0;
-  if (c < N) {
+  const int c0 = blockIdx.x * (CT * CPT) + threadIdx.x;
+  double rv[CPT];
+#pragma unroll
+  for (int u = 0; u < CPT; ++u) {
+    const int c = min(c0 + u * CT, N - 1);
     int i, j, k;
     g3_coords(S.g, c, i, j, k);
     double dA;
-    v = residual_at(S, x, b, c, i, j, k, &dA);
-    if (!done) r[c] = v;
+    rv[u] = residual_at(S, x, b, c, i, j, k, &dA);
   }
-  if (first) warp_partial(v * v, partials);
+  double v = 0.0;
+#pragma unroll
+  for (int u = 0; u < CPT; ++u) {
+    const int c = c0 + u * CT;
+    if (c < N) {
+      if (!done) r[c] = rv[u];
+      v += rv[u] * rv[u];
+    }
+  }
+  if (first) warp_partial(v, partials);
 }
 
 // Open-box support range of block J along one axis (reading A3): cells x with
@@ -329,21 +353,32 @@ __global__ void __launch_bounds__(256) k_restrict_cart(LevelView L, const double
   const int rpw = 32 / xw;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int sub = lane / xw, xo = lane % xw;
-  const int rstep = (blockDim.x >> 5) * rpw;
+  const int rstep = (blockDim.x >> 5) * rpw;  // < wy for every config; handled generally
   double acc = 0.0;
   for (int xb = 0; xb < wx; xb += xw) {
     const int xx = xb + xo;
     const bool xok = xx < wx;
-    for (int r0 = warp * rpw + sub; r0 < rows; r0 += 4 * rstep) {
+    // (y, z) of this group's current row, advanced incrementally (no divisions)
+    int row = warp * rpw + sub;
+    int zz = row / wy, yy = row - zz * wy;
+    const int dz = rstep / wy, dy = rstep - dz * wy;
+    const double* __restrict__ pb = Ps + x0 + xx;
+    const double* __restrict__ rb = r + x0 + xx;
+    while (row < rows) {
       double pv[4], rv[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
-        const int row = r0 + u * rstep;
         const bool ok = xok && row < rows;
-        const int zz = row / wy, yy = row - zz * wy;
-        const int cc = x0 + xx + nx * (y0 + yy) + sxy * (z0 + zz);
-        pv[u] = ok ? Ps[cc] : 0.0;
-        rv[u] = ok ? r[cc] : 0.0;
+        const int off = nx * (y0 + yy) + sxy * (z0 + zz);
+        pv[u] = ok ? pb[off] : 0.0;
+        rv[u] = ok ? rb[off] : 0.0;
+        row += rstep;
+        yy += dy;
+        zz += dz;
+        if (yy >= wy) {
+          yy -= wy;
+          ++zz;
+        }
       }
 #pragma unroll
       for (int u = 0; u < 4; ++u) acc += pv[u] * rv[u];
@@ -360,36 +395,42 @@ __global__ void __launch_bounds__(256) k_restrict_cart(LevelView L, const double
   }
 }
 
-// a9 (Cartesian level): x += P x_c, one thread per cell: the six per-axis block
-// indices come from the parity table, the eight (P, x_c) loads are predicated selects
-// with no branches, so all sixteen are in flight together.
+// a9 (Cartesian level): x += P x_c, CPT cells per thread: the six per-axis block
+// indices come from the parity table, the eight (P, x_c) loads per cell are predicated
+// selects with no branches, so all of a thread's loads are in flight together.
 __global__ void __launch_bounds__(CT) k_prolong_cart(LevelView L, double* __restrict__ x,
                                                      const double* __restrict__ xc,
                                                      const IterState* st) {
   const bool done = is_done(st);
   const int N = L.g.nxy * L.g.nz;
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= N) return;
-  int i, j, k;
-  g3_coords(L.g, c, i, j, k);
-  const int2 tx = reinterpret_cast<const int2*>(L.tab)[i];
-  const int2 ty = reinterpret_cast<const int2*>(L.tab)[L.g.nx + j];
-  const int2 tz = reinterpret_cast<const int2*>(L.tab)[L.g.nx + L.g.ny + k];
-  const double* __restrict__ base = L.P + c;
-  double v[8], xv[8];
+  const int c0 = blockIdx.x * (CT * CPT) + threadIdx.x;
+  double xn[CPT];
 #pragma unroll
-  for (int s = 0; s < 8; ++s) {
-    const int jx = (s & 1) ? tx.y : tx.x, jy = (s & 2) ? ty.y : ty.x, jz = (s & 4) ? tz.y : tz.x;
-    const bool act = (jx | jy | jz) >= 0;
-    const int col = jx + L.nb0 * (jy + L.nb1 * jz);
-    v[s] = act ? base[(size_t)s * N] : 0.0;
-    xv[s] = act ? xc[col] : 0.0;
+  for (int u = 0; u < CPT; ++u) {
+    const int c = min(c0 + u * CT, N - 1);
+    int i, j, k;
+    g3_coords(L.g, c, i, j, k);
+    const int2 tx = reinterpret_cast<const int2*>(L.tab)[i];
+    const int2 ty = reinterpret_cast<const int2*>(L.tab)[L.g.nx + j];
+    const int2 tz = reinterpret_cast<const int2*>(L.tab)[L.g.nx + L.g.ny + k];
+    const double* __restrict__ base = L.P + c;
+    double acc = 0.0;
+#pragma unroll
+    for (int s = 0; s < 8; ++s) {
+      const int jx = (s & 1) ? tx.y : tx.x, jy = (s & 2) ? ty.y : ty.x, jz = (s & 4) ? tz.y : tz.x;
+      const bool act = (jx | jy | jz) >= 0;
+      const int col = jx + L.nb0 * (jy + L.nb1 * jz);
+      const double v = act ? base[(size_t)s * N] : 0.0;
+      const double xv = act ? xc[col] : 0.0;
+      acc += v * xv;
+    }
+    xn[u] = x[c] + acc;
   }
-  double acc = 0.0;
 #pragma unroll
-  for (int s = 0; s < 8; ++s) acc += v[s] * xv[s];
-  const double xn = x[c] + acc;
-  if (!done) x[c] = xn;
+  for (int u = 0; u < CPT; ++u) {
+    const int c = c0 + u * CT;
+    if (c < N && !done) x[c] = xn[u];
+  }
 }
 
 __global__ void k_zero_if(double* __restrict__ p, int n, const IterState* st) {
@@ -556,6 +597,10 @@ msb_status msb_solver_create(msb_ctx ctx, msb_op op, const msb_level* levels, in
   s->edge0 = dyn_edge0;
   s->edge1 = dyn_edge1;
   s->dyn_max = dyn_max_blocks > 0 ? dyn_max_blocks : 1024;
+  // fused TMA residual+restriction (cycle_tma.cu) is opt-in: on config 2 it measured
+  // 46 us against 16 + 27 us for the residual and gather passes it replaces, but the
+  // cycle as a whole ran 103 vs 90 us (profiles/r01_v3) — TMA box-row throughput bound
+  s->no_fuse = getenv("MSB_FUSE_RR") == nullptr;
   int maxM = 1;
   for (int l = 0; l < n_levels; ++l) {
     msb_level L = levels[l];
@@ -642,19 +687,19 @@ static msb_status enqueue_stage(msb_ctx ctx, msb_solver s, msb_level L, const do
   StencilT S = stencil(op);
   LevelView V = view(L);
   unsigned g = grid_for(N, CT);
-  int np = (int)g;
-  auto fin = [&]() -> msb_status {
-    k_finalize<<<1, 1024, 0, st>>>(s->partials, np, 0, s->st, s->res_dev);
+  const unsigned g4 = grid_for(N, CT * CPT);  // multi-cell stencil kernels
+  auto fin = [&](unsigned np) -> msb_status {  // np = blocks of the kernel that wrote partials
+    k_finalize<<<1, 1024, 0, st>>>(s->partials, (int)np, 0, s->st, s->res_dev);
     MSB_LAUNCH_CHECK(ctx);
     return MSB_OK;
   };
   auto jac = [&]() -> msb_status {
     for (int v = 0; v < s->nu; ++v) {
-      k_jacobi<<<g, CT, 0, st>>>(S, s->xbuf[cur], s->xbuf[cur ^ 1], b, s->omega_s, first ? 1 : 0,
+      k_jacobi<<<g4, CT, 0, st>>>(S, s->xbuf[cur], s->xbuf[cur ^ 1], b, s->omega_s, first ? 1 : 0,
                                  s->partials, s->st);
       MSB_LAUNCH_CHECK(ctx);
       if (first) {
-        msb_status rc = fin();
+        msb_status rc = fin(g4);
         if (rc) return rc;
       }
       first = false;
@@ -663,18 +708,34 @@ static msb_status enqueue_stage(msb_ctx ctx, msb_solver s, msb_level L, const do
     return MSB_OK;
   };
   auto corr = [&]() -> msb_status {
+    RRLaunch rr;
+    if (L->kind == 0 && !s->no_fuse && resrestrict_plan(ctx, op, L, s->xbuf[cur], b, &rr)) {
+      k_zero_if<<<grid_for(L->M, 256), 256, 0, st>>>(s->rc, L->M, s->st);
+      MSB_LAUNCH_CHECK(ctx);
+      msb_status rc = resrestrict_launch(ctx, op, L, rr, s->rc, first ? 1 : 0, s->partials,
+                                         &s->st->done);
+      if (rc) return rc;
+      if (first) {
+        if ((rc = fin(rr.grid))) return rc;
+      }
+      first = false;
+      coarse_solve_dense(ctx, L->co, s->rc, s->xc, &s->st->done);
+      k_prolong_cart<<<g4, CT, 0, st>>>(V, s->xbuf[cur], s->xc, s->st);
+      MSB_LAUNCH_CHECK(ctx);
+      return MSB_OK;
+    }
     if (L->kind == 0) {
-      k_residual<<<g, CT, 0, st>>>(S, s->xbuf[cur], b, s->r, first ? 1 : 0, s->partials, s->st);
+      k_residual<<<g4, CT, 0, st>>>(S, s->xbuf[cur], b, s->r, first ? 1 : 0, s->partials, s->st);
       MSB_LAUNCH_CHECK(ctx);
       if (first) {
-        msb_status rc = fin();
+        msb_status rc = fin(g4);
         if (rc) return rc;
       }
       first = false;
       k_restrict_cart<<<L->M, 256, 0, st>>>(V, s->r, s->rc, s->st);
       MSB_LAUNCH_CHECK(ctx);
       coarse_solve_dense(ctx, L->co, s->rc, s->xc, &s->st->done);
-      k_prolong_cart<<<g, CT, 0, st>>>(V, s->xbuf[cur], s->xc, s->st);
+      k_prolong_cart<<<g4, CT, 0, st>>>(V, s->xbuf[cur], s->xc, s->st);
       MSB_LAUNCH_CHECK(ctx);
       return MSB_OK;
     }
@@ -684,7 +745,7 @@ static msb_status enqueue_stage(msb_ctx ctx, msb_solver s, msb_level L, const do
                                      s->st);
     MSB_LAUNCH_CHECK(ctx);
     if (first) {
-      msb_status rc = fin();
+      msb_status rc = fin(g);
       if (rc) return rc;
     }
     first = false;

@@ -164,13 +164,14 @@ __global__ void __launch_bounds__(SWEEP_BLOCK, 4) k_sweep_cart(
 // reciprocal with one residual correction, i.e. the correctly rounded quotient).
 // TMA requires the innermost box start to be 16-byte aligned, so the x halo is two
 // cells wide on each side (box x range [x0-2, x0+34), x0 a multiple of 32).
-constexpr int TT_X = 32, TT_Y = 4, TT_S = 4;
+constexpr int TT_X = 32, TT_Y = 4;
+constexpr int TT_STAGES_DEFAULT = 4;  // ring depth TT_S (MSB_SW_STAGES=4|5|6 to A/B)
 constexpr int TB_X = TT_X + 4, TB_Y = TT_Y + 2, TQ_Y = TT_Y + 1;
 constexpr int TP_DBL = 8 * TB_Y * TB_X;  // P box (doubles): rows y0-1 .. y0+TT_Y
 constexpr int TQ_DBL = 3 * TQ_Y * TB_X;  // T box: rows y0-1 .. y0+TT_Y-1
 constexpr int TSTAGE_DBL = ((TP_DBL + TQ_DBL) * 8 + 127) / 128 * 128 / 8;
 constexpr uint32_t TSTAGE_TX = (uint32_t)(TP_DBL + TQ_DBL) * 8u;
-constexpr size_t TSWEEP_SMEM = (size_t)TT_S * TSTAGE_DBL * 8 + 64;
+constexpr size_t tsweep_smem(int S) { return (size_t)S * TSTAGE_DBL * 8 + 64; }
 constexpr int TSWEEP_THREADS = 2 * TT_X * TT_Y;
 
 struct SweepTiles {
@@ -188,6 +189,7 @@ __device__ __forceinline__ double div_rn(double a, double b, double rb) {
   return fma(e, rb, q);
 }
 
+template <int TT_S>
 __global__ void __launch_bounds__(TSWEEP_THREADS) k_sweep_tma(
     const __grid_constant__ CUtensorMap mP0, const __grid_constant__ CUtensorMap mP1,
     const __grid_constant__ CUtensorMap mT, double* __restrict__ P0, double* __restrict__ P1,
@@ -232,29 +234,37 @@ __global__ void __launch_bounds__(TSWEEP_THREADS) k_sweep_tma(
       const uint32_t sq = seq + p;
       mbar_wait(&bars[sq % TT_S], (sq / TT_S) & 1u);
     };
+    // The ring holds planes pc..pc+TT_S-1 during step pc: the cell's own minus-z
+    // values (P at k-1 for its 4 slots, Tz at k-1) are carried in registers from the
+    // previous step, so only planes k and k+1 must be resident and TT_S-2 planes are
+    // in flight ahead of the next need.
     if (tid == 0)
-      for (int p = 0; p < min(TT_S - 1, np); ++p) issue(p);
+      for (int p = 0; p < min(TT_S, np); ++p) issue(p);
     const int x = x0 + tx, y = y0 + ty;
     const bool inxy = x < nx && y < ny;
     const unsigned mx = inxy ? amask[x] : 0u, my = inxy ? amask[nx + y] : 0u;
     unsigned mz_next = amask[nx + ny + k0];
+    const int ob = 4 * h * TB_Y * TB_X + loc;
+    double pzm[4], tzm;
+    wait(0);
+    {
+      const double* s0 = sm + (seq % TT_S) * TSTAGE_DBL;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) pzm[q] = s0[ob + q * TB_Y * TB_X];
+      tzm = s0[TP_DBL + 2 * TQ_Y * TB_X + loc];
+    }
     for (int k = k0; k < k1; ++k) {
       const int pc = k - k0 + 1;
       const unsigned mz = mz_next;
       if (k + 1 < k1) mz_next = amask[nx + ny + k + 1];
-      if (tid == 0 && pc + TT_S - 2 < np) issue(pc + TT_S - 2);
-      if (pc == 1) {
-        wait(0);
-        wait(1);
-      }
+      if (pc == 1) wait(1);
       wait(pc + 1);
-      const double* __restrict__ sM = sm + ((seq + pc - 1) % TT_S) * TSTAGE_DBL;
       const double* __restrict__ sC = sm + ((seq + pc) % TT_S) * TSTAGE_DBL;
       const double* __restrict__ sP = sm + ((seq + pc + 1) % TT_S) * TSTAGE_DBL;
       const double* __restrict__ tC = sC + TP_DBL;
       const double txp = tC[loc], txm = tC[loc - 1];
       const double typ = tC[TQ_Y * TB_X + loc], tym = tC[TQ_Y * TB_X + loc - TB_X];
-      const double tzp = tC[2 * TQ_Y * TB_X + loc], tzm = sM[TP_DBL + 2 * TQ_Y * TB_X + loc];
+      const double tzp = tC[2 * TQ_Y * TB_X + loc];
       const double D = txp + txm + typ + tym + tzp + tzm;
       // out-of-domain tile cells see zero-filled T (D = 0): give them wD = 0 so their
       // (unused) values stay finite
@@ -265,7 +275,6 @@ __global__ void __launch_bounds__(TSWEEP_THREADS) k_sweep_tma(
       const double wxp0 = mask_d(txp, (mx >> 4) & 1u), wxp1 = mask_d(txp, (mx >> 5) & 1u);
       const double wym0 = mask_d(tym, (my >> 2) & 1u), wym1 = mask_d(tym, (my >> 3) & 1u);
       const double wyp0 = mask_d(typ, (my >> 4) & 1u), wyp1 = mask_d(typ, (my >> 5) & 1u);
-      const int ob = 4 * h * TB_Y * TB_X + loc;
       // No activity select is needed: an inactive (cell, slot) holds 0, its neighbours
       // along the inactive axis are masked, and its neighbours along the other axes
       // share that coordinate and so hold 0 too — hence ph = 0 exactly.
@@ -275,7 +284,7 @@ __global__ void __launch_bounds__(TSWEEP_THREADS) k_sweep_tma(
       for (int q = 0; q < 4; ++q) {
         const int px = q & 1, py = q >> 1;
         const int o = ob + q * TB_Y * TB_X;
-        double acc = wzm * sM[o];
+        double acc = wzm * pzm[q];
         acc += (py ? wym1 : wym0) * sC[o - TB_X];
         acc += (px ? wxm1 : wxm0) * sC[o - 1];
         acc += (px ? wxp1 : wxp0) * sC[o + 1];
@@ -302,8 +311,14 @@ __global__ void __launch_bounds__(TSWEEP_THREADS) k_sweep_tma(
         }
         nan_seen |= !(sum == sum);  // zero diagonal in A_T
       }
-      __syncthreads();  // ring slot of plane pc-1 is free for the next issue
-      if (tid == 0) fence_proxy_async_smem();
+#pragma unroll
+      for (int q = 0; q < 4; ++q) pzm[q] = po[q];
+      tzm = tzp;
+      __syncthreads();  // plane pc-1's ring slot (last read in step pc-1) is free
+      if (tid == 0) {
+        fence_proxy_async_smem();
+        if (pc - 1 + TT_S < np) issue(pc - 1 + TT_S);
+      }
     }
     seq += np;
   }
@@ -410,6 +425,7 @@ extern "C" msb_status msb_smooth_basis(msb_ctx ctx, msb_level L, msb_op op, int3
   CUtensorMap mP[2], mT;
   SweepTiles tl{};
   unsigned tgrid = 0;
+  int sw_stages = TT_STAGES_DEFAULT;
   if (L->kind == 0 && (op->nx % 2) == 0 && !getenv("MSB_NO_TMA")) {
     const uint64_t dP[4] = {(uint64_t)op->nx, (uint64_t)op->ny, (uint64_t)op->nz, 8};
     const uint64_t dT[4] = {(uint64_t)op->nx, (uint64_t)op->ny, (uint64_t)op->nz, 3};
@@ -418,14 +434,25 @@ extern "C" msb_status msb_smooth_basis(msb_ctx ctx, msb_level L, msb_op op, int3
     use_tma = tma_encode_4d(&mP[0], Pa, dP, st3, bP) && tma_encode_4d(&mP[1], Pb, dP, st3, bP) &&
               tma_encode_4d(&mT, op->Tx, dT, st3, bT);
     if (use_tma) {
-      static int occ = 0;
+      static int occ = 0, stages = 0;
       if (!occ) {
-        MSB_CUDA_TRY(ctx, cudaFuncSetAttribute(k_sweep_tma, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                               (int)TSWEEP_SMEM));
-        MSB_CUDA_TRY(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_sweep_tma, TSWEEP_THREADS,
-                                                                       TSWEEP_SMEM));
+        const char* e = getenv("MSB_SW_STAGES");
+        stages = e ? atoi(e) : TT_STAGES_DEFAULT;
+        if (stages != 4 && stages != 5 && stages != 6) stages = TT_STAGES_DEFAULT;
+        auto setup = [&](auto kern, int S) -> cudaError_t {
+          cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 (int)tsweep_smem(S));
+          if (err == cudaSuccess)
+            err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, TSWEEP_THREADS,
+                                                                tsweep_smem(S));
+          return err;
+        };
+        cudaError_t err = stages == 4 ? setup(k_sweep_tma<4>, 4)
+                        : stages == 5 ? setup(k_sweep_tma<5>, 5) : setup(k_sweep_tma<6>, 6);
+        MSB_CUDA_TRY(ctx, err);
         if (occ < 1) occ = 1;
       }
+      sw_stages = stages;
       tl.ntx = (op->nx + TT_X - 1) / TT_X;
       tl.nty = (op->ny + TT_Y - 1) / TT_Y;
       const int64_t slots = (int64_t)occ * ctx->sm_count;
@@ -457,8 +484,19 @@ extern "C" msb_status msb_smooth_basis(msb_ctx ctx, msb_level L, msb_op op, int3
     for (int t = 0; t < nl; ++t) {
       int idx = issued + t;
       if (use_tma)
-        k_sweep_tma<<<tgrid, TSWEEP_THREADS, TSWEEP_SMEM, st>>>(mP[0], mP[1], mT, Pa, Pb, L->amask, g,
-                                                            tl, omega, idx, tol, dslots);
+        switch (sw_stages) {
+          case 5:
+            k_sweep_tma<5><<<tgrid, TSWEEP_THREADS, tsweep_smem(5), st>>>(
+                mP[0], mP[1], mT, Pa, Pb, L->amask, g, tl, omega, idx, tol, dslots);
+            break;
+          case 6:
+            k_sweep_tma<6><<<tgrid, TSWEEP_THREADS, tsweep_smem(6), st>>>(
+                mP[0], mP[1], mT, Pa, Pb, L->amask, g, tl, omega, idx, tol, dslots);
+            break;
+          default:
+            k_sweep_tma<4><<<tgrid, TSWEEP_THREADS, tsweep_smem(4), st>>>(
+                mP[0], mP[1], mT, Pa, Pb, L->amask, g, tl, omega, idx, tol, dslots);
+        }
       else if (L->kind == 0)
         k_sweep_cart<<<grid, SWEEP_BLOCK, 0, st>>>(Pa, Pb, op->Tx, op->Ty, op->Tz, L->amask, g,
                                                    omega, idx, tol, dslots);

@@ -5,8 +5,9 @@ TAG=${1:-perf}
 OUT=gpurun_out/$TAG
 mkdir -p $OUT
 timeout 300 python -c "import __graft_entry__ as g; g.build(); g.smoke()" > $OUT/smoke.log 2>&1 || { echo smoke failed; cat $OUT/smoke.log; exit 1; }
+if [ "${RUN_TESTS:-0}" = "1" ]; then timeout 1200 python -m pytest tests -m gpu -x -q -k "not config5" > $OUT/pytest.log 2>&1; fi
 timeout 600 python bench.py --steps 3 --warmup 3 --no-cpu-baseline > $OUT/bench.log 2>&1
-MSB_L2_PERSIST=0 timeout 600 python bench.py --steps 3 --warmup 3 --no-cpu-baseline > $OUT/bench_nopersist.log 2>&1
+if [ -n "${BENCH2_ENV:-}" ]; then env $BENCH2_ENV timeout 600 python bench.py --steps 3 --warmup 3 --no-cpu-baseline > $OUT/bench2.log 2>&1; fi
 if [ "${SKIP_NCU:-0}" != "1" ]; then
   timeout 300 python scripts/profile_step.py > $OUT/profile_plain.log 2>&1 &&
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \

@@ -170,9 +170,11 @@ CYCLE_CASES = {
 # Cholesky, differ by 8.8e-10 after 200 cycles and 2.6e-9 after 2000; with the
 # dynamic stage (config3_recipe) their free-mode iteration counts differ by 3,
 # because the Δp bins of late iterations flip under that noise.  The GPU must be as
-# close to the oracle as the oracle is to itself: tolerances are
-#   x:      max(1e-9, 2 * ||x_LU - x_Chol|| / ||x_LU||)           at equal counts
-#   counts: max(1,    2 * |k_LU - k_Chol|)                         in free mode
+# close to the oracle as other correct CPU implementations of the same readings are:
+# the floor is the largest spread of two alternates — LAPACK Cholesky and the LAPACK
+# explicit inverse (reading B1, the GPU's coarse solve) — from the oracle:
+#   x:      max(1e-9, 2 * max_alt ||x_LU - x_alt|| / ||x_LU||)     at equal counts
+#   counts: max(1,    2 * max_alt |k_LU - k_alt|)                  in free mode
 # which reduce to the north-star 1e-9 / ±1 on well-conditioned cases.
 K_PARITY = 2000
 
@@ -191,14 +193,32 @@ class _CholeskyCoarse:
         return la.cho_solve(self._c, rc)
 
 
-def _oracle_cholesky(prob, fixed_iters=None):
+class _InverseCoarse:
+    """Alternate exact coarse solver: LAPACK explicit inverse (getrf/getri) + GEMV — the
+    GPU's reading B1 computed by a CPU library, so its spread from the oracle measures
+    what the explicit-inverse rounding alone contributes."""
+
+    def __init__(self, Ac):
+        self.Ac = Ac
+        self.M = Ac.shape[0]
+        self._X = np.linalg.inv(Ac)
+
+    def solve(self, rc):
+        return self._X @ rc
+
+
+def _oracle_variant(prob, cls, fixed_iters=None):
     from oracle import cycle as ocy
     saved = ocy.CoarseSolver
-    ocy.CoarseSolver = _CholeskyCoarse
+    ocy.CoarseSolver = cls
     try:
         return _oracle_full(prob, fixed_iters=fixed_iters)
     finally:
         ocy.CoarseSolver = saved
+
+
+def _oracle_cholesky(prob, fixed_iters=None):
+    return _oracle_variant(prob, _CholeskyCoarse, fixed_iters)
 
 
 @pytest.mark.parametrize("name", list(CYCLE_CASES))
@@ -207,8 +227,9 @@ def test_cycle_parity(ctx, name):
     orc = _oracle_full(prob)
     k_or = orc["sol"]["iters"]
     assert orc["sol"]["converged"]
-    k_cho = _oracle_cholesky(prob)["sol"]["iters"]
-    k_tol = max(1, 2 * abs(k_or - k_cho))
+    k_alt = [_oracle_variant(prob, c)["sol"]["iters"] for c in (_CholeskyCoarse, _InverseCoarse)]
+    k_cho = k_alt[0]
+    k_tol = max(1, 2 * max(abs(k_or - k) for k in k_alt))
     # free mode: iteration counts within ±1 (or the measured floor)
     g = _gpu_full(ctx, prob)
     assert abs(g["sol"]["iters"] - k_or) <= k_tol, (g["sol"]["iters"], k_or, k_cho)
@@ -217,9 +238,9 @@ def test_cycle_parity(ctx, name):
     if k_fix != k_or:
         orc = _oracle_full(prob, fixed_iters=k_fix)
     xo = orc["sol"]["x"]
-    cho = _oracle_cholesky(prob, fixed_iters=k_fix)["sol"]
-    xc = cho["x"]
-    floor = np.linalg.norm(xc - xo) / np.linalg.norm(xo)
+    alts = [_oracle_variant(prob, c, fixed_iters=k_fix)["sol"]
+            for c in (_CholeskyCoarse, _InverseCoarse)]
+    floor = max(np.linalg.norm(a["x"] - xo) / np.linalg.norm(xo) for a in alts)
     x_tol = max(X_RTOL, 2.0 * floor)
     g2 = _gpu_full(ctx, prob, fixed_iters=k_fix)
     err = np.linalg.norm(g2["x_host"] - xo) / np.linalg.norm(xo)
@@ -229,7 +250,7 @@ def test_cycle_parity(ctx, name):
     # twice the LU-vs-Cholesky oracle spread when the dynamic stage makes the tail
     # chaotic (its Δp bins flip under rounding noise).
     ro = orc["sol"]["res"][:k_fix + 1]
-    r_floor = float(np.max(np.abs(cho["res"][:k_fix + 1] - ro)))
+    r_floor = max(float(np.max(np.abs(a["res"][:k_fix + 1] - ro))) for a in alts)
     assert np.all(np.abs(g2["sol"]["res"] - ro) <= max(1e-8, 2.0 * r_floor) + 1e-6 * np.abs(ro)), \
         r_floor
 
