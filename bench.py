@@ -39,6 +39,42 @@ def _peaks():
         return {"hbm_gbs": 6650.0, "_fallback": True}
 
 
+def max_over_ranks(vals, dist=None, device=None):
+    """Element-wise max of per-rank timings (the slowest rank defines the job time)."""
+    if dist is None:
+        return list(vals)
+    import torch
+    t = torch.tensor(list(vals), dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return t.tolist()
+
+
+CYCLE_KERNELS = ("k_jacobi", "k_residual", "k_restrict_cart", "k_gemv", "k_prolong_cart",
+                 "k_finalize")
+
+
+def _traffic():
+    """Per-launch DRAM bytes of the timed kernels from the committed ncu capture
+    (profiles/roofline_traffic.json, written by scripts/traffic_from_ncu.py), or None."""
+    try:
+        doc = json.load(open(os.path.join(ROOT, "profiles", "roofline_traffic.json")))
+    except Exception:
+        return None, None
+    k = doc.get("kernels", {})
+
+    def find(prefix):
+        for name, v in k.items():
+            if name.startswith(prefix):
+                return v
+        return None
+    sw = find("k_sweep_tma")
+    parts = [find(n) for n in CYCLE_KERNELS]
+    cyc = None
+    if all(p is not None for p in parts):
+        cyc = sum(p["dram_bytes"] for p in parts)
+    return (sw["dram_bytes"] if sw else None), cyc
+
+
 def _dist():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -245,7 +281,7 @@ def run_gpu(args):
     # e2e: pinned host K in, pressure out, through the C ABI (copies inside the region)
     x_host = torch.empty(N, dtype=torch.float64).pin_memory()
     e2e = []
-    for _ in range(max(1, min(args.steps, 3))):
+    for _ in range(0 if args.no_e2e else max(1, min(args.steps, 3))):
         flush.zero_()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
@@ -257,10 +293,8 @@ def run_gpu(args):
     t_step = sum(i["t_step"] for i in infos) / 1e3
     sweeps = sum(i["sweeps"] for i in infos)
     iters = sum(i["iters"] for i in infos)
-    vals = torch.tensor([t_smooth, t_cycle, t_step], dtype=torch.float64, device=f"cuda:{local}")
-    if dist:
-        dist.all_reduce(vals, op=dist.ReduceOp.MAX)
-    t_smooth, t_cycle, t_step = vals.tolist()
+    t_smooth, t_cycle, t_step = max_over_ranks([t_smooth, t_cycle, t_step], dist,
+                                               f"cuda:{local}")
     if rank != 0:
         return 0
 
@@ -275,12 +309,23 @@ def run_gpu(args):
     per_iter = t_cycle / max(1, iters)
     gbs_sweep = b_sweep / per_sweep / 1e9
     gbs_iter = b_iter / per_iter / 1e9
-    # dominant kernel by time share inside the step
-    if t_cycle >= t_smooth:
-        dom = dict(kernel="cycle iteration (k_jacobi+k_res_restrict+k_gemv+k_prolong)",
-                   achieved=gbs_iter, bytes=b_iter)
-    else:
-        dom = dict(kernel="k_sweep_cart", achieved=gbs_sweep, bytes=b_sweep)
+    # roofline of the dominant phase of the step (the cycle on config 2): one multiscale
+    # iteration is one CUDA-graph launch unit (k_jacobi, k_finalize, k_residual,
+    # k_restrict_cart, k_gemv, k_prolong_cart), timed with CUDA events on the library
+    # stream around the whole phase and divided by the iteration count
+    tr_sweep, tr_iter = _traffic()
+    src = "measured (MEASURED_PEAKS.json hbm_gbs, copy)" if not peaks.get("_fallback") \
+        else "fallback 6650 GB/s (B200_PROFILING.md)"
+    roof_cycle = {"bound": "hbm", "kernel": "cycle iteration: " + " + ".join(CYCLE_KERNELS),
+                  "achieved": gbs_iter, "peak": peak, "unit": "GB/s", "frac": gbs_iter / peak,
+                  "traffic": tr_iter, "algorithmic_bytes_per_launch": b_iter,
+                  "launch_us": 1e6 * per_iter, "peak_source": src,
+                  "traffic_source": "profiles/roofline_traffic.json (ncu --set full, cold cache)"}
+    roof_sweep = {"bound": "hbm", "kernel": "k_sweep_tma", "achieved": gbs_sweep, "peak": peak,
+                  "unit": "GB/s", "frac": gbs_sweep / peak, "traffic": tr_sweep,
+                  "algorithmic_bytes_per_launch": b_sweep, "launch_us": 1e6 * per_sweep,
+                  "peak_source": src}
+    dominant = roof_cycle if t_cycle >= t_smooth else roof_sweep
     value = ws * sweeps / t_smooth
     cores, model = _cpu_info()
     cpu = None
@@ -290,7 +335,7 @@ def run_gpu(args):
                "sample": f"{args.cpu_sweeps} oracle sweeps + {args.cpu_iters} oracle cycles on "
                          f"the full config2 grid, single thread",
                "ms_per_iteration": s.get("ms_per_iteration"), "cpu": model, "host_cores": cores}
-    e2e_t = sum(t for t, _ in e2e)
+    e2e_t = sum(t for t, _ in e2e) or float("nan")
     e2e_sw = sum(n for _, n in e2e)
     line = {
         "metric": METRIC, "value": value, "unit": "sweeps/s", "n_gpus": ws,
@@ -310,14 +355,12 @@ def run_gpu(args):
                 "sweep_frac": gbs_sweep / peak, "cycle_frac": gbs_iter / peak,
                 "sweep_frac_nominal_8tbs": gbs_sweep / 8000.0,
                 "cycle_frac_nominal_8tbs": gbs_iter / 8000.0},
-        "roofline": {"bound": "hbm", "kernel": dom["kernel"], "achieved": dom["achieved"],
-                     "peak": peak, "unit": "GB/s", "frac": dom["achieved"] / peak,
-                     "traffic": None, "algorithmic_bytes_per_launch": dom["bytes"],
-                     "peak_source": "measured (MEASURED_PEAKS.json hbm_gbs)"
-                     if not peaks.get("_fallback") else "fallback (B200_PROFILING.md)"},
+        "roofline": dominant,
+        "roofline_sweep": roof_sweep,
+        "roofline_cycle": roof_cycle,
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_sw / e2e_t, "unit": "sweeps/s",
-                "ms_per_step": 1e3 * e2e_t / len(e2e),
+                "ms_per_step": 1e3 * e2e_t / max(1, len(e2e)),
                 "h2d_bytes_per_step": 3 * N * 8, "d2h_bytes_per_step": N * 8},
         "gpu_launches": launches,
         "clocks": clk,
@@ -336,6 +379,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--max-iter", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer e2e steps "
+                    "(ncu launch-list runs)")
     ap.add_argument("--cpu-sweeps", type=int, default=20)
     ap.add_argument("--cpu-iters", type=int, default=10)
     ap.add_argument("--ref-sweeps", type=int, default=5)

@@ -1,0 +1,20 @@
+#!/bin/bash
+# Round-evidence call: smoke, full GPU test suite, the default bench (with the CPU
+# oracle baseline), the ncu launch list, and ncu --set full captures of the sweep and of
+# one cycle iteration's kernels -> profiles/roofline_traffic.json input.
+TAG=${1:-round}
+OUT=gpurun_out/$TAG
+mkdir -p $OUT
+nvidia-smi > $OUT/nvidia-smi.txt 2>&1
+timeout 300 python -c "import __graft_entry__ as g; g.build(); g.smoke()" > $OUT/smoke.log 2>&1 || { echo smoke failed; tail $OUT/smoke.log; exit 1; }
+timeout 1500 python -m pytest tests -m gpu -q > $OUT/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $OUT/pytest_gpu.log
+timeout 900 python bench.py > $OUT/bench.log 2>&1; echo "bench rc=$?" >> $OUT/bench.log
+timeout 300 python scripts/profile_step.py > $OUT/profile_plain.log 2>&1 &&
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
+    --log-file $OUT/launches.csv python scripts/profile_step.py > $OUT/ncu_launch.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_sweep_tma -s 2 -c 1 \
+    -o $OUT/sweep python scripts/profile_step.py > $OUT/ncu_sweep.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on \
+    -k regex:"k_jacobi|k_residual|k_restrict|k_gemv|k_prolong|k_finalize" -s 30 -c 6 \
+    -o $OUT/cycle python scripts/profile_step.py > $OUT/ncu_cycle.log 2>&1
+echo done

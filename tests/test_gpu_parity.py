@@ -491,6 +491,21 @@ def test_full_config5_sweep_lockstep_and_cycle(ctx):
     x2 = x.cpu().numpy()
     solver.iterate(x, None, prob.cycle_tol, 100, 1)
     x3 = x.cpu().numpy()
-    x3_ref = stage(A, A.diagonal(), q, x2, OLevel(P, A), prob.omega_s, prob.nu, prob.post_smooth)
+    olev = OLevel(P, A)
+    x3_ref = stage(A, A.diagonal(), q, x2, olev, prob.omega_s, prob.nu, prob.post_smooth)
+    # rounding floor: the same stage with another exact sparse coarse
+    # factorisation (natural instead of COLAMD column order); cond(A_c) makes one
+    # coarse correction differ at the 1e-9 level between backward-stable solvers
+    import scipy.sparse.linalg as spla
+
+    class _Natural:
+        def __init__(self, Ac):
+            self._lu = spla.splu(sp.csc_matrix(Ac), permc_spec="NATURAL")
+
+        def solve(self, rc):
+            return self._lu.solve(rc)
+    olev.solver = _Natural(olev.Ac)
+    x3_alt = stage(A, A.diagonal(), q, x2, olev, prob.omega_s, prob.nu, prob.post_smooth)
+    floor = np.linalg.norm(x3_alt - x3_ref) / np.linalg.norm(x3_ref)
     err = np.linalg.norm(x3 - x3_ref) / np.linalg.norm(x3_ref)
-    assert err <= X_RTOL, err
+    assert err <= max(X_RTOL, 2.0 * floor), (err, floor)
