@@ -331,106 +331,129 @@ __device__ __forceinline__ void support_range(int J, int b, int n, int nb, int& 
 // gathering its support box row by row (column J lives in the parity slot of J in
 // every cell of S_J).  Every P entry is read exactly once; r (N doubles) stays in L2.
 // Fixed-order reduction: deterministic, no atomics.
-__global__ void __launch_bounds__(256) k_restrict_cart(LevelView L, const double* __restrict__ r,
-                                                       double* __restrict__ rc,
-                                                       const IterState* st) {
+// a8 (Cartesian level): r_c = P^T r.  One CTA per coarse (Jy, Jz) row of blocks
+// computes the restriction of all Jx of that row: it walks the (y, z) rows of the
+// (Jy, Jz) support box over the FULL x extent, reading both x-parity slot planes of
+// P and r with fully coalesced row loads (each P entry once; r shared by the two
+// parities), keeps per-thread partial sums per x position and parity, and finally sums
+// each column's x range from shared memory in a fixed order (deterministic, no
+// atomics).  Thread layout: XL lanes along x (XL = pow2 >= nx, <= 256) x RG row
+// groups; x positions beyond 256 take a second partial.
+constexpr int RR2_THREADS = 256;
+__global__ void __launch_bounds__(RR2_THREADS) k_restrict_cart(LevelView L,
+                                                               const double* __restrict__ r,
+                                                               double* __restrict__ rc,
+                                                               const IterState* st) {
   const bool done = is_done(st);
-  const int J = blockIdx.x;
   const int N = L.g.nxy * L.g.nz;
   const int nx = L.g.nx, sxy = L.g.nxy;
-  const int Jx = J % L.nb0, Jy = (J / L.nb0) % L.nb1, Jz = J / (L.nb0 * L.nb1);
-  int x0, x1, y0, y1, z0, z1;
-  support_range(Jx, L.b0, nx, L.nb0, x0, x1);
+  const int Jy = blockIdx.x % L.nb1, Jz = blockIdx.x / L.nb1;
+  int y0, y1, z0, z1;
   support_range(Jy, L.b1, L.g.ny, L.nb1, y0, y1);
   support_range(Jz, L.b2, L.g.nz, L.nb2, z0, z1);
-  const int s = (Jx & 1) | ((Jy & 1) << 1) | ((Jz & 1) << 2);
-  const double* __restrict__ Ps = L.P + (size_t)s * N;
-  const int wx = x1 - x0, wy = y1 - y0;
-  const int rows = wy * (z1 - z0);
-  // rows of the box are spread over sub-warp groups of xw >= wx lanes (xw a power of
-  // two <= 32, wider rows loop); four rows per group are loaded before any FMA
-  const int xw = wx <= 8 ? 8 : (wx <= 16 ? 16 : 32);
-  const int rpw = 32 / xw;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int sub = lane / xw, xo = lane % xw;
-  const int rstep = (blockDim.x >> 5) * rpw;  // < wy for every config; handled generally
-  double acc = 0.0;
-  for (int xb = 0; xb < wx; xb += xw) {
-    const int xx = xb + xo;
-    const bool xok = xx < wx;
-    // (y, z) of this group's current row, advanced incrementally (no divisions)
-    int row = warp * rpw + sub;
-    int zz = row / wy, yy = row - zz * wy;
-    const int dz = rstep / wy, dy = rstep - dz * wy;
-    const double* __restrict__ pb = Ps + x0 + xx;
-    const double* __restrict__ rb = r + x0 + xx;
-    while (row < rows) {
-      double pv[4], rv[4];
+  const int wy = y1 - y0, rows = wy * (z1 - z0);
+  const int sy = ((Jy & 1) << 1) | ((Jz & 1) << 2);
+  const double* __restrict__ P0 = L.P + (size_t)sy * N;        // x parity 0
+  const double* __restrict__ P1 = L.P + (size_t)(sy | 1) * N;  // x parity 1
+  const int XL = nx <= 32 ? 32 : (nx <= 64 ? 64 : (nx <= 128 ? 128 : 256));
+  const int RG = RR2_THREADS / XL;
+  const int xo = threadIdx.x % XL, rg = threadIdx.x / XL;
+  const bool x0ok = xo < nx, x1ok = xo + 256 < nx;
+  double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;  // parity 0/1 at xo and xo + 256
+  int row = rg;
+  int zz = row / wy, yy = row - zz * wy;
+  const int dz = RG / wy, dy = RG - dz * wy;
+  while (row < rows) {
+    double p0[4], p1[4], rv[4], q0[4], q1[4], rw[4];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const bool ok = xok && row < rows;
-        const int off = nx * (y0 + yy) + sxy * (z0 + zz);
-        pv[u] = ok ? pb[off] : 0.0;
-        rv[u] = ok ? rb[off] : 0.0;
-        row += rstep;
-        yy += dy;
-        zz += dz;
-        if (yy >= wy) {
-          yy -= wy;
-          ++zz;
-        }
+    for (int u = 0; u < 4; ++u) {
+      const bool ok = row < rows;
+      const size_t c = (size_t)nx * (y0 + yy) + (size_t)sxy * (z0 + zz) + xo;
+      p0[u] = (ok && x0ok) ? P0[c] : 0.0;
+      p1[u] = (ok && x0ok) ? P1[c] : 0.0;
+      rv[u] = (ok && x0ok) ? r[c] : 0.0;
+      q0[u] = (ok && x1ok) ? P0[c + 256] : 0.0;
+      q1[u] = (ok && x1ok) ? P1[c + 256] : 0.0;
+      rw[u] = (ok && x1ok) ? r[c + 256] : 0.0;
+      row += RG;
+      yy += dy;
+      zz += dz;
+      if (yy >= wy) {
+        yy -= wy;
+        ++zz;
       }
+    }
 #pragma unroll
-      for (int u = 0; u < 4; ++u) acc += pv[u] * rv[u];
+    for (int u = 0; u < 4; ++u) {
+      a0 += p0[u] * rv[u];
+      a1 += p1[u] * rv[u];
+      b0 += q0[u] * rw[u];
+      b1 += q1[u] * rw[u];
     }
   }
-  __shared__ double sh[8];
-  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-  if (lane == 0) sh[warp] = acc;
+  // per-(row group, parity, x) partials -> shared, summed over row groups in order
+  extern __shared__ double rsh[];  // [RG][2][XLX], XLX = 2 * XL (x and x + 256)
+  const int XLX = 2 * XL;
+  rsh[(rg * 2 + 0) * XLX + xo] = a0;
+  rsh[(rg * 2 + 1) * XLX + xo] = a1;
+  rsh[(rg * 2 + 0) * XLX + XL + xo] = b0;
+  rsh[(rg * 2 + 1) * XLX + XL + xo] = b1;
   __syncthreads();
-  if (threadIdx.x == 0 && !done) {
-    double t = 0.0;
-    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += sh[w];
-    rc[J] = t;
+  for (int t = threadIdx.x; t < 2 * XLX; t += blockDim.x) {
+    double v = 0.0;
+    for (int g = 0; g < RG; ++g) v += rsh[g * 2 * XLX + t];
+    rsh[RG * 2 * XLX + t] = v;  // totals [2][XLX] after the per-group block
+  }
+  __syncthreads();
+  const double* tot = rsh + RG * 2 * XLX;
+  for (int Jx = threadIdx.x; Jx < L.nb0; Jx += blockDim.x) {
+    int x0, x1;
+    support_range(Jx, L.b0, nx, L.nb0, x0, x1);
+    const double* tp = tot + (Jx & 1) * XLX;
+    double v = 0.0;
+    for (int x = x0; x < x1; ++x) v += tp[x < 256 ? x : XL + (x - 256)];
+    if (!done) rc[Jx + L.nb0 * (Jy + L.nb1 * Jz)] = v;
   }
 }
 
-// a9 (Cartesian level): x += P x_c, CPT cells per thread: the six per-axis block
-// indices come from the parity table, the eight (P, x_c) loads per cell are predicated
-// selects with no branches, so all of a thread's loads are in flight together.
+static inline size_t restrict_rows_smem(int nx) {
+  const int XL = nx <= 32 ? 32 : (nx <= 64 ? 64 : (nx <= 128 ? 128 : 256));
+  const int RG = RR2_THREADS / XL;
+  return (size_t)(RG + 1) * 2 * 2 * XL * sizeof(double);
+}
+
+// a9 (Cartesian level): x += P x_c, one thread per cell: the six per-axis block
+// indices come from the parity table, the eight (P, x_c) loads are predicated selects
+// with no branches, so all sixteen are in flight together.  (Four cells per thread, as
+// the stencil passes use, measured 27 us against 17 us here: the dependent x_c gathers
+// need the occupancy more than the extra loads in flight.)
 __global__ void __launch_bounds__(CT) k_prolong_cart(LevelView L, double* __restrict__ x,
                                                      const double* __restrict__ xc,
                                                      const IterState* st) {
   const bool done = is_done(st);
   const int N = L.g.nxy * L.g.nz;
-  const int c0 = blockIdx.x * (CT * CPT) + threadIdx.x;
-  double xn[CPT];
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= N) return;
+  int i, j, k;
+  g3_coords(L.g, c, i, j, k);
+  const int2 tx = reinterpret_cast<const int2*>(L.tab)[i];
+  const int2 ty = reinterpret_cast<const int2*>(L.tab)[L.g.nx + j];
+  const int2 tz = reinterpret_cast<const int2*>(L.tab)[L.g.nx + L.g.ny + k];
+  const double* __restrict__ base = L.P + c;
+  double v[8], xv[8];
 #pragma unroll
-  for (int u = 0; u < CPT; ++u) {
-    const int c = min(c0 + u * CT, N - 1);
-    int i, j, k;
-    g3_coords(L.g, c, i, j, k);
-    const int2 tx = reinterpret_cast<const int2*>(L.tab)[i];
-    const int2 ty = reinterpret_cast<const int2*>(L.tab)[L.g.nx + j];
-    const int2 tz = reinterpret_cast<const int2*>(L.tab)[L.g.nx + L.g.ny + k];
-    const double* __restrict__ base = L.P + c;
-    double acc = 0.0;
-#pragma unroll
-    for (int s = 0; s < 8; ++s) {
-      const int jx = (s & 1) ? tx.y : tx.x, jy = (s & 2) ? ty.y : ty.x, jz = (s & 4) ? tz.y : tz.x;
-      const bool act = (jx | jy | jz) >= 0;
-      const int col = jx + L.nb0 * (jy + L.nb1 * jz);
-      const double v = act ? base[(size_t)s * N] : 0.0;
-      const double xv = act ? xc[col] : 0.0;
-      acc += v * xv;
-    }
-    xn[u] = x[c] + acc;
+  for (int s = 0; s < 8; ++s) {
+    const int jx = (s & 1) ? tx.y : tx.x, jy = (s & 2) ? ty.y : ty.x, jz = (s & 4) ? tz.y : tz.x;
+    const bool act = (jx | jy | jz) >= 0;
+    const int col = jx + L.nb0 * (jy + L.nb1 * jz);
+    v[s] = act ? base[(size_t)s * N] : 0.0;
+    xv[s] = act ? xc[col] : 0.0;
   }
+  double acc = 0.0;
 #pragma unroll
-  for (int u = 0; u < CPT; ++u) {
-    const int c = c0 + u * CT;
-    if (c < N && !done) x[c] = xn[u];
-  }
+  for (int s = 0; s < 8; ++s) acc += v[s] * xv[s];
+  const double xn = x[c] + acc;
+  if (!done) x[c] = xn;
 }
 
 __global__ void k_zero_if(double* __restrict__ p, int n, const IterState* st) {
@@ -720,7 +743,7 @@ static msb_status enqueue_stage(msb_ctx ctx, msb_solver s, msb_level L, const do
       }
       first = false;
       coarse_solve_dense(ctx, L->co, s->rc, s->xc, &s->st->done);
-      k_prolong_cart<<<g4, CT, 0, st>>>(V, s->xbuf[cur], s->xc, s->st);
+      k_prolong_cart<<<g, CT, 0, st>>>(V, s->xbuf[cur], s->xc, s->st);
       MSB_LAUNCH_CHECK(ctx);
       return MSB_OK;
     }
@@ -732,10 +755,13 @@ static msb_status enqueue_stage(msb_ctx ctx, msb_solver s, msb_level L, const do
         if (rc) return rc;
       }
       first = false;
-      k_restrict_cart<<<L->M, 256, 0, st>>>(V, s->r, s->rc, s->st);
+      if (op->nx > 512)
+        return set_error(ctx, MSB_EINVAL, "Cartesian restriction supports nx <= 512 (nx=%d)", op->nx);
+      k_restrict_cart<<<L->nb[1] * L->nb[2], RR2_THREADS, restrict_rows_smem(op->nx), st>>>(
+          V, s->r, s->rc, s->st);
       MSB_LAUNCH_CHECK(ctx);
       coarse_solve_dense(ctx, L->co, s->rc, s->xc, &s->st->done);
-      k_prolong_cart<<<g4, CT, 0, st>>>(V, s->xbuf[cur], s->xc, s->st);
+      k_prolong_cart<<<g, CT, 0, st>>>(V, s->xbuf[cur], s->xc, s->st);
       MSB_LAUNCH_CHECK(ctx);
       return MSB_OK;
     }
