@@ -299,10 +299,11 @@ def run_gpu(args):
         return 0
 
     # algorithmic bytes: sweep = 16 nnz + 8 faces; cycle stage =
-    # 16 nnz + 8 faces + 40 N + 8 M^2 (dense inverse GEMV)
+    # 16 nnz + 8 faces + 40 N + coarse solve, the coarse solve reading the lower
+    # triangle of the symmetric A_c^{-1}: 8 M (M + 1) / 2
     nnz, faces, M = 6964260, prob.n_faces, 3400
     b_sweep = 16 * nnz + 8 * faces
-    b_iter = 16 * nnz + 8 * faces + 40 * N + 8 * M * M
+    b_iter = 16 * nnz + 8 * faces + 40 * N + 4 * M * (M + 1)
     peaks = _peaks()
     peak = peaks["hbm_gbs"]
     per_sweep = t_smooth / sweeps

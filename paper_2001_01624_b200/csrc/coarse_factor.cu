@@ -331,6 +331,7 @@ msb_status coarse_factor_dense(msb_ctx ctx, Coarse& co) {
   k_mirror_lower<<<g, dim3(32, 32), 0, s>>>(F, M);
   MSB_LAUNCH_CHECK(ctx);
   std::swap(co.L, co.Ainv);
+  if ((rc = coarse_pack_symmetric(ctx, co))) return rc;
   co.ready = true;
   return MSB_OK;
 }

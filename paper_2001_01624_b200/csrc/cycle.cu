@@ -821,6 +821,7 @@ static msb_status chunk_graph(msb_ctx ctx, msb_solver s, const double* db, int c
   for (msb_level L : s->levels) {
     key.push_back(L->P[L->cur]);
     key.push_back(L->co.Ainv);
+    key.push_back(L->co.Xp);
   }
   if (key != s->gkey) {
     drop_graphs(s);
