@@ -183,6 +183,18 @@ __device__ __forceinline__ double mask_d(double v, unsigned bit) {
   return __longlong_as_double(__double_as_longlong(v) & -(long long)bit);
 }
 
+// 1/x from the fp64 reciprocal seed (MUFU.RCP64H) and two Newton steps: accurate to
+// ~1 ulp (not correctly rounded) for the normal, positive D and row sums of the sweep;
+// div_rn below still returns the correctly rounded quotient from it.
+__device__ __forceinline__ double rcp_fast(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+}
+
 __device__ __forceinline__ double div_rn(double a, double b, double rb) {
   double q = a * rb;
   double e = fma(-q, b, a);
@@ -216,7 +228,6 @@ __global__ void __launch_bounds__(TSWEEP_THREADS) k_sweep_tma(
   const int loc = (ty + 1) * TB_X + (tx + 2);  // same offset in the P and T boxes' row grid
   uint32_t seq = 0;  // plane sequence number over this CTA's lifetime (ring slot / phase)
   double dloc = 0.0;
-  bool nan_seen = false;
   for (int item = blockIdx.x; item < tl.items; item += gridDim.x) {
     const int xt = item % tl.ntx, rest = item / tl.ntx;
     const int yt = rest % tl.nty, zc = rest / tl.nty;
@@ -246,7 +257,14 @@ __global__ void __launch_bounds__(TSWEEP_THREADS) k_sweep_tma(
     unsigned mz_next = amask[nx + ny + k0];
     const int ob = 4 * h * TB_Y * TB_X + loc;
     double pzm[4], tzm;
-    wait(0);
+    // one thread waits on the ring's mbarriers and the CTA barrier publishes the data:
+    // planes 0..2 before the first step, plane pc+2 at the end of step pc
+    if (tid == 0) {
+      wait(0);
+      wait(1);
+      if (np > 2) wait(2);
+    }
+    __syncthreads();
     {
       const double* s0 = sm + (seq % TT_S) * TSTAGE_DBL;
 #pragma unroll
@@ -257,8 +275,6 @@ __global__ void __launch_bounds__(TSWEEP_THREADS) k_sweep_tma(
       const int pc = k - k0 + 1;
       const unsigned mz = mz_next;
       if (k + 1 < k1) mz_next = amask[nx + ny + k + 1];
-      if (pc == 1) wait(1);
-      wait(pc + 1);
       const double* __restrict__ sC = sm + ((seq + pc) % TT_S) * TSTAGE_DBL;
       const double* __restrict__ sP = sm + ((seq + pc + 1) % TT_S) * TSTAGE_DBL;
       const double* __restrict__ tC = sC + TP_DBL;
@@ -268,7 +284,7 @@ __global__ void __launch_bounds__(TSWEEP_THREADS) k_sweep_tma(
       const double D = txp + txm + typ + tym + tzp + tzm;
       // out-of-domain tile cells see zero-filled T (D = 0): give them wD = 0 so their
       // (unused) values stay finite
-      const double wD = inxy ? omega / D : 0.0;
+      const double wD = inxy ? omega * rcp_fast(D) : 0.0;
       const unsigned zb = (mz >> h) & 1u;
       const double wzm = mask_d(tzm, (mz >> (2 + h)) & 1u), wzp = mask_d(tzp, (mz >> (4 + h)) & 1u);
       const double wxm0 = mask_d(txm, (mx >> 2) & 1u), wxm1 = mask_d(txm, (mx >> 3) & 1u);
@@ -297,7 +313,7 @@ __global__ void __launch_bounds__(TSWEEP_THREADS) k_sweep_tma(
       sum += __shfl_xor_sync(0xffffffffu, sum, 16);
       const unsigned act = zb & (unsigned)inxy;
       if (act) {
-        const double rs = 1.0 / sum;
+        const double rs = rcp_fast(sum);
         const int c = x + nx * (y + ny * k);
         double* __restrict__ ob_out = Pout + (size_t)(4 * h) * N + c;
 #pragma unroll
@@ -309,12 +325,12 @@ __global__ void __launch_bounds__(TSWEEP_THREADS) k_sweep_tma(
             dloc = fmax(dloc, fabs(pn - po[q]));
           }
         }
-        nan_seen |= !(sum == sum);  // zero diagonal in A_T
       }
 #pragma unroll
       for (int q = 0; q < 4; ++q) pzm[q] = po[q];
       tzm = tzp;
-      __syncthreads();  // plane pc-1's ring slot (last read in step pc-1) is free
+      if (tid == 0 && pc + 2 < np) wait(pc + 2);
+      __syncthreads();  // plane pc+2 is published; plane pc-1's ring slot is free
       if (tid == 0) {
         fence_proxy_async_smem();
         if (pc - 1 + TT_S < np) issue(pc - 1 + TT_S);
@@ -322,8 +338,22 @@ __global__ void __launch_bounds__(TSWEEP_THREADS) k_sweep_tma(
     }
     seq += np;
   }
-  if (nan_seen) dloc = __longlong_as_double(0x7ff8000000000000ll);  // propagates to δ
   sweep_fold(dloc, dslots, n);
+}
+
+// Zero diagonal of A_T: a cell with no open face (D_T = 0) has no
+// smoothing update.  Checked once per msb_smooth_basis call, so the sweep kernels need
+// no per-step NaN bookkeeping.
+__global__ void k_zero_diag(const double* __restrict__ Tx, const double* __restrict__ Ty,
+                            const double* __restrict__ Tz, Grid3 g, int* __restrict__ flag) {
+  const int N = g.nxy * g.nz;
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= N) return;
+  int i, j, k;
+  g3_coords(g, c, i, j, k);
+  const double D = Tx[c] + (i > 0 ? Tx[c - 1] : 0.0) + Ty[c] + (j > 0 ? Ty[c - g.nx] : 0.0) +
+                   Tz[c] + (k > 0 ? Tz[c - g.nxy] : 0.0);
+  if (!(D > 0.0)) atomicExch(flag, 1);
 }
 
 // ---------------------------------------------------------------- G3: explicit (ELL) sweep
@@ -407,6 +437,21 @@ extern "C" msb_status msb_smooth_basis(msb_ctx ctx, msb_level L, msb_op op, int3
   if (!dslots) return set_error(ctx, MSB_ENOMEM, "sweep state");
   MSB_CUDA_TRY(ctx, cudaMemsetAsync(dslots, 0, (size_t)max_sweeps * DSLOTS * 8, st));
   Grid3 g = make_grid3(op->nx, op->ny, op->nz);
+  {
+    int* zf = dalloc_n<int>(ctx, 1);
+    if (!zf) return set_error(ctx, MSB_ENOMEM, "zero-diagonal flag");
+    MSB_CUDA_TRY(ctx, cudaMemsetAsync(zf, 0, sizeof(int), st));
+    k_zero_diag<<<grid_for(op->N, 256), 256, 0, st>>>(op->Tx, op->Ty, op->Tz, g, zf);
+    MSB_LAUNCH_CHECK(ctx);
+    int hz = 0;
+    MSB_CUDA_TRY(ctx, cudaMemcpyAsync(&hz, zf, sizeof(int), cudaMemcpyDeviceToHost, st));
+    MSB_CUDA_TRY(ctx, cudaStreamSynchronize(st));
+    dfree(ctx, zf);
+    if (hz) {
+      dfree(ctx, dslots);
+      return set_error(ctx, MSB_EZERO_DIAG, "zero diagonal in A_T (a cell with no open face)");
+    }
+  }
   if (L->kind == 0 && !L->amask) {
     int tot = op->nx + op->ny + op->nz;
     MSB_ALLOC(ctx, L->amask, uint8_t, tot);

@@ -581,3 +581,24 @@ def test_full_config5_sweep_lockstep_and_cycle(ctx):
     floor = max(floors)
     err = np.linalg.norm(x3 - x3_ref) / np.linalg.norm(x3_ref)
     assert err <= max(X_RTOL, 2.0 * floor), (err, floors)
+
+
+def test_zero_diagonal_rejected_gpu(ctx):
+    """A cell sealed on all six faces has D_T = 0: smoothing fails loudly."""
+    from paper_2001_01624_b200 import Level
+    from paper_2001_01624_b200.api import MsbError
+    from paper_2001_01624_b200.pipeline import build_operator
+    prob = random_problem(11, 8, 6, 4, (4, 3, 2))
+    nx, ny, nz = prob.nx, prob.ny, prob.nz
+    i, j, k = 3, 2, 1
+    mx = np.ones((nz, ny, nx - 1))
+    my = np.ones((nz, ny - 1, nx))
+    mz = np.ones((nz - 1, ny, nx))
+    mx[k, j, i - 1] = mx[k, j, i] = 0.0
+    my[k, j - 1, i] = my[k, j, i] = 0.0
+    mz[k - 1, j, i] = mz[k, j, i] = 0.0
+    prob.mult_x, prob.mult_y, prob.mult_z = mx.ravel(), my.ravel(), mz.ravel()
+    op = build_operator(ctx, prob)
+    lev = Level.cartesian(ctx, op, prob.block)
+    with pytest.raises(MsbError, match="EZERO_DIAG"):
+        lev.smooth(op, 3, prob.omega, -1.0)
