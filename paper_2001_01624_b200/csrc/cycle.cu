@@ -711,11 +711,35 @@ static msb_status enqueue_stage(msb_ctx ctx, msb_solver s, msb_level L, const do
   LevelView V = view(L);
   unsigned g = grid_for(N, CT);
   const unsigned g4 = grid_for(N, CT * CPT);  // multi-cell stencil kernels
+  // With one pre-smoothed level and nu = 1 no kernel of an iteration writes the buffer
+  // holding x_{k-1}, so the stop test's finalize runs on a side branch in parallel with
+  // the rest of the iteration and is joined before the next iteration's first kernel
+  // (kernels that have not yet seen `done` then do harmless work).
+  const bool side = s->levels.size() == 1 && s->nu == 1 && !s->post && L->kind == 0 &&
+                    !getenv("MSB_SERIAL_FINALIZE");
   auto fin = [&](unsigned np) -> msb_status {  // np = blocks of the kernel that wrote partials
+    if (side) {
+      if (!s->side_stream) {
+        MSB_CUDA_TRY(ctx, cudaStreamCreateWithFlags(&s->side_stream, cudaStreamNonBlocking));
+        MSB_CUDA_TRY(ctx, cudaEventCreateWithFlags(&s->ev_fork, cudaEventDisableTiming));
+        MSB_CUDA_TRY(ctx, cudaEventCreateWithFlags(&s->ev_join, cudaEventDisableTiming));
+      }
+      MSB_CUDA_TRY(ctx, cudaEventRecord(s->ev_fork, st));
+      MSB_CUDA_TRY(ctx, cudaStreamWaitEvent(s->side_stream, s->ev_fork, 0));
+      k_finalize<<<1, 1024, 0, s->side_stream>>>(s->partials, (int)np, 0, s->st, s->res_dev);
+      MSB_LAUNCH_CHECK(ctx);
+      MSB_CUDA_TRY(ctx, cudaEventRecord(s->ev_join, s->side_stream));
+      s->pending_join = true;
+      return MSB_OK;
+    }
     k_finalize<<<1, 1024, 0, st>>>(s->partials, (int)np, 0, s->st, s->res_dev);
     MSB_LAUNCH_CHECK(ctx);
     return MSB_OK;
   };
+  if (first && s->pending_join) {
+    MSB_CUDA_TRY(ctx, cudaStreamWaitEvent(st, s->ev_join, 0));
+    s->pending_join = false;
+  }
   auto jac = [&]() -> msb_status {
     for (int v = 0; v < s->nu; ++v) {
       k_jacobi<<<g4, CT, 0, st>>>(S, s->xbuf[cur], s->xbuf[cur ^ 1], b, s->omega_s, first ? 1 : 0,
@@ -791,6 +815,14 @@ static msb_status enqueue_stage(msb_ctx ctx, msb_solver s, msb_level L, const do
   return MSB_OK;
 }
 
+static msb_status join_side(msb_ctx ctx, msb_solver s) {
+  if (s->pending_join) {
+    MSB_CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->stream, s->ev_join, 0));
+    s->pending_join = false;
+  }
+  return MSB_OK;
+}
+
 static msb_status enqueue_norm(msb_ctx ctx, msb_solver s, const double* x, const double* b,
                                int mode) {
   msb_op op = s->op;
@@ -845,6 +877,8 @@ static msb_status chunk_graph(msb_ctx ctx, msb_solver s, const double* db, int c
       for (msb_level L : s->levels)
         if ((rc = enqueue_stage(ctx, s, L, db, cur, first))) break;
     }
+    if (!rc) rc = join_side(ctx, s);  // the side branch rejoins before the capture ends
+    s->pending_join = false;
     cudaGraph_t graph = nullptr;
     cudaError_t e2 = cudaStreamEndCapture(s->cap_stream, &graph);
     if (!rc && e2 == cudaSuccess) {
@@ -926,6 +960,7 @@ msb_status msb_ms_iterate(msb_ctx ctx, msb_solver s, const double* b, double* x,
         }
       }
       issued += n;
+      if ((rc = join_side(ctx, s))) return rc;
       if (issued >= target)
         if ((rc = enqueue_norm(ctx, s, s->xbuf[cur], db, 0))) return rc;
       MSB_CUDA_TRY(ctx, cudaMemcpyAsync(&hs, s->st, sizeof(hs), cudaMemcpyDeviceToHost, st));
@@ -996,6 +1031,9 @@ msb_status msb_solver_destroy(msb_solver s) {
   if (s->dyn_level) level_free(s->dyn_level);
   drop_graphs(s);
   if (s->cap_stream) cudaStreamDestroy(s->cap_stream);
+  if (s->side_stream) cudaStreamDestroy(s->side_stream);
+  if (s->ev_fork) cudaEventDestroy(s->ev_fork);
+  if (s->ev_join) cudaEventDestroy(s->ev_join);
   delete s;
   return MSB_OK;
 }
