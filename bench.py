@@ -49,7 +49,8 @@ def max_over_ranks(vals, dist=None, device=None):
     return t.tolist()
 
 
-CYCLE_KERNELS = ("k_jacobi", "k_residual", "k_restrict_cart", "k_gemv", "k_prolong_cart",
+CYCLE_KERNELS = ("k_jacobi", "k_residual", "k_restrict_cart", "k_symv_tiles", "k_symv_reduce",
+                 "k_prolong_cart",
                  "k_finalize")
 
 

@@ -15,6 +15,6 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_sweep_tma -s 2 -c 1 \
     -o $OUT/sweep python scripts/profile_step.py > $OUT/ncu_sweep.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on \
-    -k regex:"k_jacobi|k_residual|k_restrict|k_gemv|k_prolong|k_finalize" -s 30 -c 6 \
+    -k regex:"k_jacobi|k_residual|k_restrict|k_symv|k_prolong|k_finalize" -s 35 -c 7 \
     -o $OUT/cycle python scripts/profile_step.py > $OUT/ncu_cycle.log 2>&1
 echo done
