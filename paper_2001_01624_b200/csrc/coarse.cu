@@ -12,6 +12,7 @@
 #include <cstdlib>
 
 #include "internal.cuh"
+#include "symv.cuh"
 
 namespace msb {
 
@@ -154,7 +155,6 @@ __global__ void __launch_bounds__(256) k_gemv(const double* __restrict__ X, int 
 // off the diagonal, its column contribution X_t^T r_bi (for block bj) into per-tile
 // partial slots; k_symv_reduce sums each output block's slots in a fixed order
 // (deterministic).  HBM bytes per solve: 4 M (M + 64) instead of 8 M^2.
-constexpr int ST = 64;
 
 __global__ void k_pack_lower(const double* __restrict__ X, int M, int ntb, double* __restrict__ Xp) {
   const int64_t t = blockIdx.x;  // tile index
@@ -175,77 +175,14 @@ constexpr int SYMV_T = 256;  // threads per tile: 8 double2 of the tile per thre
 __global__ void __launch_bounds__(SYMV_T) k_symv_tiles(const double* __restrict__ Xp, int M,
                                                        const double* __restrict__ rc,
                                                        double* __restrict__ part) {
-  const int64_t t = blockIdx.x;
-  int bi = (int)((sqrt(8.0 * (double)t + 1.0) - 1.0) * 0.5);
-  while ((int64_t)(bi + 1) * (bi + 2) / 2 <= t) ++bi;
-  while ((int64_t)bi * (bi + 1) / 2 > t) --bi;
-  const int bj = (int)(t - (int64_t)bi * (bi + 1) / 2);
-  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // columns 2tx, 2tx+1; rows ty + 8u
-  const double2* tile = reinterpret_cast<const double2*>(Xp + t * ST * ST);
-  double2 a[8];
-#pragma unroll
-  for (int u = 0; u < 8; ++u) a[u] = __ldcs(tile + (ty + 8 * u) * (ST / 2) + tx);
-  const int cj = bj * ST + 2 * tx;
-  const double r0 = cj < M ? rc[cj] : 0.0, r1 = cj + 1 < M ? rc[cj + 1] : 0.0;
-  double ri[8];
-#pragma unroll
-  for (int u = 0; u < 8; ++u) {
-    const int row = bi * ST + ty + 8 * u;
-    ri[u] = row < M ? rc[row] : 0.0;
-  }
-  // row contributions: sum over this thread's two columns, then over the warp (tx)
-  __shared__ double rows_sh[ST];
-  __shared__ double cols_sh[8][ST];
-#pragma unroll
-  for (int u = 0; u < 8; ++u) {
-    double v = a[u].x * r0 + a[u].y * r1;
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    if (tx == 0) rows_sh[ty + 8 * u] = v;
-  }
-  // column contributions (off-diagonal tiles): sum over this thread's eight rows
-  double c0 = 0.0, c1 = 0.0;
-#pragma unroll
-  for (int u = 0; u < 8; ++u) {
-    c0 += a[u].x * ri[u];
-    c1 += a[u].y * ri[u];
-  }
-  cols_sh[ty][2 * tx] = c0;
-  cols_sh[ty][2 * tx + 1] = c1;
-  __syncthreads();
-  double* pt = part + t * 2 * ST;
-  if (threadIdx.x < ST) {
-    pt[threadIdx.x] = rows_sh[threadIdx.x];
-  } else if (threadIdx.x < 2 * ST) {
-    const int c = threadIdx.x - ST;
-    double v = 0.0;
-    if (bi != bj)
-      for (int g = 0; g < 8; ++g) v += cols_sh[g][c];
-    pt[ST + c] = v;
-  }
+  symv_tile_body<false>(Xp, M, rc, part, blockIdx.x);
 }
 
-// xc[block b] = sum_{j <= b} row part of tile (b, j) + sum_{k > b} column part of (k, b):
-// four thread groups take every fourth contribution, then a fixed-order combine.
 __global__ void __launch_bounds__(4 * ST) k_symv_reduce(const double* __restrict__ part, int M,
                                                         int ntb, double* __restrict__ xc,
                                                         const int* done) {
   const bool skip = done && *(volatile const int*)done;
-  const int b = blockIdx.x, i = threadIdx.x & (ST - 1), g = threadIdx.x / ST;
-  const int64_t rowbase = (int64_t)b * (b + 1) / 2;
-  double v = 0.0;
-  for (int e = g; e < ntb; e += 4) {  // e <= b: row part of (b, e); e > b: column part of (e, b)
-    const int64_t off = e <= b ? (rowbase + e) * 2 * ST + i
-                               : ((int64_t)e * (e + 1) / 2 + b) * 2 * ST + ST + i;
-    v += part[off];
-  }
-  __shared__ double sh[4][ST];
-  sh[g][i] = v;
-  __syncthreads();
-  if (g == 0) {
-    const double tot = (sh[0][i] + sh[1][i]) + (sh[2][i] + sh[3][i]);
-    const int row = b * ST + i;
-    if (row < M && !skip) xc[row] = tot;
-  }
+  symv_reduce_body<false>(part, M, ntb, xc, blockIdx.x, skip);
 }
 
 msb_status coarse_pack_symmetric(msb_ctx ctx, Coarse& co) {

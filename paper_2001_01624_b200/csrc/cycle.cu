@@ -16,7 +16,10 @@
 #include <cstdlib>
 #include <cmath>
 
+#include <cooperative_groups.h>
+
 #include "internal.cuh"
+#include "symv.cuh"
 
 struct IterState {
   int done;
@@ -28,6 +31,7 @@ struct IterState {
   double tol;
   double bscale;  // ||b|| (1 if b = 0)
   double r0;
+  int cur;        // x buffer holding x_k (persistent cycle kernel)
 };
 
 namespace msb {
@@ -435,14 +439,13 @@ __device__ __forceinline__ void support_range(int J, int b, int n, int nb, int& 
 // atomics).  Thread layout: XL lanes along x (XL = pow2 >= nx, <= 256) x RG row
 // groups; x positions beyond 256 take a second partial.
 constexpr int RR2_THREADS = 256;
-__global__ void __launch_bounds__(RR2_THREADS) k_restrict_cart(LevelView L,
-                                                               const double* __restrict__ r,
-                                                               double* __restrict__ rc,
-                                                               const IterState* st) {
-  const bool done = is_done(st);
+template <bool CG>
+__device__ __forceinline__ void restrict_row_body(const LevelView& L, const double* r,
+                                                  double* __restrict__ rc, int unit,
+                                                  double* rsh, bool done) {
   const int N = L.g.nxy * L.g.nz;
   const int nx = L.g.nx, sxy = L.g.nxy;
-  const int Jy = blockIdx.x % L.nb1, Jz = blockIdx.x / L.nb1;
+  const int Jy = unit % L.nb1, Jz = unit / L.nb1;
   int y0, y1, z0, z1;
   support_range(Jy, L.b1, L.g.ny, L.nb1, y0, y1);
   support_range(Jz, L.b2, L.g.nz, L.nb2, z0, z1);
@@ -466,10 +469,10 @@ __global__ void __launch_bounds__(RR2_THREADS) k_restrict_cart(LevelView L,
       const size_t c = (size_t)nx * (y0 + yy) + (size_t)sxy * (z0 + zz) + xo;
       p0[u] = (ok && x0ok) ? P0[c] : 0.0;
       p1[u] = (ok && x0ok) ? P1[c] : 0.0;
-      rv[u] = (ok && x0ok) ? r[c] : 0.0;
+      rv[u] = (ok && x0ok) ? ld_mut<CG>(r + c) : 0.0;
       q0[u] = (ok && x1ok) ? P0[c + 256] : 0.0;
       q1[u] = (ok && x1ok) ? P1[c + 256] : 0.0;
-      rw[u] = (ok && x1ok) ? r[c + 256] : 0.0;
+      rw[u] = (ok && x1ok) ? ld_mut<CG>(r + c + 256) : 0.0;
       row += RG;
       yy += dy;
       zz += dz;
@@ -487,8 +490,7 @@ __global__ void __launch_bounds__(RR2_THREADS) k_restrict_cart(LevelView L,
     }
   }
   // per-(row group, parity, x) partials -> shared, summed over row groups in order
-  extern __shared__ double rsh[];  // [RG][2][XLX], XLX = 2 * XL (x and x + 256)
-  const int XLX = 2 * XL;
+  const int XLX = 2 * XL;  // rsh: [RG][2][XLX] then totals [2][XLX]
   rsh[(rg * 2 + 0) * XLX + xo] = a0;
   rsh[(rg * 2 + 1) * XLX + xo] = a1;
   rsh[(rg * 2 + 0) * XLX + XL + xo] = b0;
@@ -497,7 +499,7 @@ __global__ void __launch_bounds__(RR2_THREADS) k_restrict_cart(LevelView L,
   for (int t = threadIdx.x; t < 2 * XLX; t += blockDim.x) {
     double v = 0.0;
     for (int g = 0; g < RG; ++g) v += rsh[g * 2 * XLX + t];
-    rsh[RG * 2 * XLX + t] = v;  // totals [2][XLX] after the per-group block
+    rsh[RG * 2 * XLX + t] = v;
   }
   __syncthreads();
   const double* tot = rsh + RG * 2 * XLX;
@@ -509,6 +511,15 @@ __global__ void __launch_bounds__(RR2_THREADS) k_restrict_cart(LevelView L,
     for (int x = x0; x < x1; ++x) v += tp[x < 256 ? x : XL + (x - 256)];
     if (!done) rc[Jx + L.nb0 * (Jy + L.nb1 * Jz)] = v;
   }
+  __syncthreads();  // rsh is reused by the next unit of a persistent CTA
+}
+
+__global__ void __launch_bounds__(RR2_THREADS) k_restrict_cart(LevelView L,
+                                                               const double* __restrict__ r,
+                                                               double* __restrict__ rc,
+                                                               const IterState* st) {
+  extern __shared__ double rsh[];
+  restrict_row_body<false>(L, r, rc, blockIdx.x, rsh, is_done(st));
 }
 
 static inline size_t restrict_rows_smem(int nx) {
@@ -549,6 +560,191 @@ __global__ void __launch_bounds__(CT) k_prolong_cart(LevelView L, double* __rest
   for (int s = 0; s < 8; ++s) acc += v[s] * xv[s];
   const double xn = x[c] + acc;
   if (!done) x[c] = xn;
+}
+
+// ---------------------------------------------------------------- persistent cycle (rows a6–a11)
+// Opt-in (MSB_PERSIST=1).  Measured slower than the CUDA-graph chain of kernels:
+// 114 us vs 71.7 us per config-2 iteration, 1.21 vs 0.76 ms on config 5
+// (profiles/r01_v8) — six grid barriers per iteration, one register budget for all
+// phases and L2-only (cg) loads of the stencil inputs cost more than the launch ramps
+// they remove.
+// The whole Richardson solve for one pre-smoothed Cartesian level (ν = 1) as ONE
+// cooperative launch: phases Jacobi → stop test → residual → restriction → SYMV tiles →
+// SYMV reduce → prolongation, separated by grid-wide barriers, looping on the device
+// until the stop test fires.  At config-2 size every pass is ~50–70 MB, where a kernel
+// launch's ramp-up and drain cost ~6 µs (a plain 54 MB 5-read/1-write pass reaches only
+// 3.3 TB/s, scripts/probes/stream_probe.cu); resident CTAs start each phase's loads the
+// moment the barrier opens.  The stop test is evaluated redundantly by every CTA from
+// the per-CTA partials in one fixed order, so all CTAs take the same decision without
+// another barrier.  Data rewritten inside the launch (x, r, r_c, partials, x_c) is read
+// with ld.global.cg: no kernel boundary invalidates L1 between phases.
+struct PersistArgs {
+  StencilT S;
+  LevelView V;
+  const double* b;
+  double* xb0;
+  double* xb1;
+  double* r;
+  double* rc;
+  double* xc;
+  double* partials;
+  const double* Xp;
+  double* part;
+  int M, ntb;
+  long long nt;
+  double omega;
+  IterState* st;
+  double* res;
+  int cur0;
+};
+
+__device__ __forceinline__ double block_sum256(double v, double* sh32) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0) sh32[threadIdx.x >> 5] = v;
+  __syncthreads();
+  double w = 0.0;
+  if (threadIdx.x < 32) {
+    w = threadIdx.x < (blockDim.x >> 5) ? sh32[threadIdx.x] : 0.0;
+    for (int o = 16; o > 0; o >>= 1) w += __shfl_xor_sync(0xffffffffu, w, o);
+  }
+  __syncthreads();
+  return w;  // valid in warp 0
+}
+
+// r = b - A x at cell c with coherent loads of x (same order as residual_at)
+__device__ __forceinline__ double residual_cg(const StencilT& S, const double* x,
+                                              const double* __restrict__ b, int c, double* dAo,
+                                              double* xco) {
+  int i, j, k;
+  g3_coords(S.g, c, i, j, k);
+  const int nx = S.g.nx, sxy = S.g.nxy;
+  const double txp = S.Tx[c], typ = S.Ty[c], tzp = S.Tz[c];
+  const double txm = i > 0 ? S.Tx[c - 1] : 0.0;
+  const double tym = j > 0 ? S.Ty[c - nx] : 0.0;
+  const double tzm = k > 0 ? S.Tz[c - sxy] : 0.0;
+  const double D = txp + txm + typ + tym + tzp + tzm;
+  double off = 0.0;
+  if (k > 0) off += tzm * __ldcg(x + c - sxy);
+  if (j > 0) off += tym * __ldcg(x + c - nx);
+  if (i > 0) off += txm * __ldcg(x + c - 1);
+  if (i < nx - 1) off += txp * __ldcg(x + c + 1);
+  if (j < S.g.ny - 1) off += typ * __ldcg(x + c + nx);
+  if (k < S.g.nz - 1) off += tzp * __ldcg(x + c + sxy);
+  const double dA = (c == 0) ? 2.0 * D : D;
+  const double xc = __ldcg(x + c);
+  *dAo = dA;
+  *xco = xc;
+  return b[c] - (dA * xc - off);
+}
+
+__global__ void __launch_bounds__(256) k_cycle_persistent(PersistArgs A) {
+  namespace cgr = cooperative_groups;
+  cgr::grid_group grid = cgr::this_grid();
+  extern __shared__ double dsm[];  // restriction scratch
+  __shared__ double sh32[32];
+  __shared__ double wsh;
+  const StencilT& S = A.S;
+  const int N = S.g.nxy * S.g.nz;
+  const int gtid = blockIdx.x * blockDim.x + threadIdx.x, gsz = gridDim.x * blockDim.x;
+  IterState ls = *A.st;  // the stop-test state, identical in every CTA
+  int cur = A.cur0;
+  const bool writer = blockIdx.x == 0 && threadIdx.x == 0;
+  for (;;) {
+    const double* x0 = cur ? A.xb1 : A.xb0;
+    double* x1 = cur ? A.xb0 : A.xb1;
+    // a7: Jacobi, with the ||r||^2 partial of the stop test
+    double v = 0.0;
+    for (int c = gtid; c < N; c += gsz) {
+      double dA, xc;
+      const double r0 = residual_cg(S, x0, A.b, c, &dA, &xc);
+      x1[c] = xc + A.omega * (r0 / dA);
+      v += r0 * r0;
+    }
+    v = block_sum256(v, sh32);
+    if (threadIdx.x == 0) A.partials[blockIdx.x] = v;
+    grid.sync();
+    // a11: stop test — every CTA sums the partials in the same order
+    double w = 0.0;
+    for (int t = threadIdx.x; t < (int)gridDim.x; t += blockDim.x) w += __ldcg(A.partials + t);
+    w = block_sum256(w, sh32);
+    if (threadIdx.x == 0) wsh = w;
+    __syncthreads();
+    w = wsh;
+    {
+      const double nrm = sqrt(w);
+      const int k = ls.k;
+      const double rho = nrm / ls.bscale;
+      if (writer) A.res[k] = rho;
+      if (k == 0) ls.r0 = nrm;
+      int done = 0;
+      if (ls.fixed > 0) {
+        if (k >= ls.fixed) {
+          done = 1;
+          ls.converged = rho <= ls.tol;
+        }
+      } else if (rho <= ls.tol) {
+        done = 1;
+        ls.converged = 1;
+      } else if (k >= ls.max_iter) {
+        done = 1;
+      }
+      if (!(nrm <= 1e6 * ls.r0) && ls.r0 > 0.0) {
+        done = 1;
+        ls.diverged = 1;
+      }
+      if (done) {
+        ls.done = 1;
+        break;
+      }
+      ls.k = k + 1;
+    }
+    // a6: residual of the smoothed iterate
+    for (int c = gtid; c < N; c += gsz) {
+      double dA, xc;
+      A.r[c] = residual_cg(S, x1, A.b, c, &dA, &xc);
+    }
+    grid.sync();
+    // a8: restriction, one (Jy, Jz) row of coarse blocks per unit
+    for (int u = blockIdx.x; u < A.V.nb1 * A.V.nb2; u += gridDim.x)
+      restrict_row_body<true>(A.V, A.r, A.rc, u, dsm, false);
+    grid.sync();
+    // a5: x_c = A_c^{-1} r_c (symmetric GEMV)
+    for (long long t = blockIdx.x; t < A.nt; t += gridDim.x) symv_tile_body<true>(A.Xp, A.M, A.rc, A.part, t);
+    grid.sync();
+    for (int bb = blockIdx.x; bb < A.ntb; bb += gridDim.x)
+      symv_reduce_body<true>(A.part, A.M, A.ntb, A.xc, bb, false);
+    grid.sync();
+    // a9: prolongation
+    for (int c = gtid; c < N; c += gsz) {
+      int i, j, k;
+      g3_coords(A.V.g, c, i, j, k);
+      const int2 tx = reinterpret_cast<const int2*>(A.V.tab)[i];
+      const int2 ty = reinterpret_cast<const int2*>(A.V.tab)[A.V.g.nx + j];
+      const int2 tz = reinterpret_cast<const int2*>(A.V.tab)[A.V.g.nx + A.V.g.ny + k];
+      const double* __restrict__ base = A.V.P + c;
+      double acc = 0.0;
+#pragma unroll
+      for (int s = 0; s < 8; ++s) {
+        const int jx = (s & 1) ? tx.y : tx.x, jy = (s & 2) ? ty.y : ty.x, jz = (s & 4) ? tz.y : tz.x;
+        const bool act = (jx | jy | jz) >= 0;
+        const int col = jx + A.V.nb0 * (jy + A.V.nb1 * jz);
+        const double pv = act ? base[(size_t)s * N] : 0.0;
+        const double xv = act ? __ldcg(A.xc + col) : 0.0;
+        acc += pv * xv;
+      }
+      x1[c] = __ldcg(x1 + c) + acc;
+    }
+    cur ^= 1;
+    grid.sync();
+  }
+  if (writer) {
+    A.st->k = ls.k;
+    A.st->done = ls.done;
+    A.st->converged = ls.converged;
+    A.st->diverged = ls.diverged;
+    A.st->r0 = ls.r0;
+    A.st->cur = cur;
+  }
 }
 
 __global__ void k_zero_if(double* __restrict__ p, int n, const IterState* st) {
@@ -1048,6 +1244,48 @@ msb_status msb_ms_iterate(msb_ctx ctx, msb_solver s, const double* b, double* x,
   cur_after.push_back(0);
   std::vector<int32_t> dynM;
   IterState hs{};
+  const bool persist = !s->dyn && s->levels.size() == 1 && s->levels[0]->kind == 0 && !s->post &&
+                       s->nu == 1 && s->levels[0]->co.Xp && op->nx <= 512 && getenv("MSB_PERSIST");
+  if (persist) {
+    msb_level L = s->levels[0];
+    const size_t smem = restrict_rows_smem(op->nx);
+    int dev_coop = 0, occ = 0;
+    cudaDeviceGetAttribute(&dev_coop, cudaDevAttrCooperativeLaunch, ctx->device);
+    MSB_CUDA_TRY(ctx, cudaFuncSetAttribute(k_cycle_persistent,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    MSB_CUDA_TRY(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_cycle_persistent, 256,
+                                                                   smem));
+    if (dev_coop && occ > 0) {
+      PersistArgs A;
+      A.S = stencil(op);
+      A.V = view(L);
+      A.b = db;
+      A.xb0 = s->xbuf[0];
+      A.xb1 = s->xbuf[1];
+      A.r = s->r;
+      A.rc = s->rc;
+      A.xc = s->xc;
+      A.partials = s->partials;
+      A.Xp = L->co.Xp;
+      A.part = L->co.part;
+      A.M = L->M;
+      A.ntb = L->co.ntb;
+      A.nt = (long long)L->co.ntb * (L->co.ntb + 1) / 2;
+      A.omega = s->omega_s;
+      A.st = s->st;
+      A.res = s->res_dev;
+      A.cur0 = 0;
+      const unsigned grid = (unsigned)(occ * ctx->sm_count);
+      void* args[] = {&A};
+      MSB_CUDA_TRY(ctx, cudaLaunchCooperativeKernel((void*)k_cycle_persistent, grid, 256, args,
+                                                    smem, st));
+      count_launch();
+      MSB_CUDA_TRY(ctx, cudaMemcpyAsync(&hs, s->st, sizeof(hs), cudaMemcpyDeviceToHost, st));
+      MSB_CUDA_TRY(ctx, cudaStreamSynchronize(st));
+      cur_after.assign((size_t)hs.k + 1, hs.cur);
+      goto finish;
+    }
+  }
   if (!s->dyn) {
     const int chunk = 16;
     const int flips = s->nu * (int)s->levels.size();  // x-buffer swaps per iteration
@@ -1107,6 +1345,7 @@ msb_status msb_ms_iterate(msb_ctx ctx, msb_solver s, const double* b, double* x,
       cur_after.push_back(cur);
     }
   }
+finish:
   int k = hs.k;
   int xb = cur_after[std::min<size_t>(k, cur_after.size() - 1)];
   MSB_CUDA_TRY(ctx, cudaMemcpyAsync(x, s->xbuf[xb], N * sizeof(double), cudaMemcpyDefault, st));
