@@ -247,8 +247,8 @@ __global__ void __launch_bounds__(TSWEEP_THREADS) k_sweep_tma(
     };
     // The ring holds planes pc..pc+TT_S-1 during step pc: the cell's own minus-z
     // values (P at k-1 for its 4 slots, Tz at k-1) are carried in registers from the
-    // previous step, so only planes k and k+1 must be resident and TT_S-2 planes are
-    // in flight ahead of the next need.
+    // previous step, so only planes k and k+1 are read; plane pc's slot is refilled
+    // (with plane pc+TT_S) right after step pc, TT_S-2 steps before that plane is needed.
     if (tid == 0)
       for (int p = 0; p < min(TT_S, np); ++p) issue(p);
     const int x = x0 + tx, y = y0 + ty;
@@ -270,6 +270,11 @@ __global__ void __launch_bounds__(TSWEEP_THREADS) k_sweep_tma(
 #pragma unroll
       for (int q = 0; q < 4; ++q) pzm[q] = s0[ob + q * TB_Y * TB_X];
       tzm = s0[TP_DBL + 2 * TQ_Y * TB_X + loc];
+    }
+    __syncthreads();  // plane 0 is consumed: refill its slot with plane TT_S
+    if (tid == 0) {
+      fence_proxy_async_smem();
+      if (TT_S < np) issue(TT_S);
     }
     for (int k = k0; k < k1; ++k) {
       const int pc = k - k0 + 1;
@@ -330,10 +335,10 @@ __global__ void __launch_bounds__(TSWEEP_THREADS) k_sweep_tma(
       for (int q = 0; q < 4; ++q) pzm[q] = po[q];
       tzm = tzp;
       if (tid == 0 && pc + 2 < np) wait(pc + 2);
-      __syncthreads();  // plane pc+2 is published; plane pc-1's ring slot is free
+      __syncthreads();  // plane pc+2 is published; plane pc (read last in this step) is free
       if (tid == 0) {
         fence_proxy_async_smem();
-        if (pc - 1 + TT_S < np) issue(pc - 1 + TT_S);
+        if (pc + TT_S < np) issue(pc + TT_S);  // TT_S-2 steps before its wait
       }
     }
     seq += np;
