@@ -9,6 +9,8 @@ nvidia-smi > $OUT/nvidia-smi.txt 2>&1
 timeout 300 python -c "import __graft_entry__ as g; g.build(); g.smoke()" > $OUT/smoke.log 2>&1 || { echo smoke failed; tail $OUT/smoke.log; exit 1; }
 timeout 1500 python -m pytest tests -m gpu -q > $OUT/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $OUT/pytest_gpu.log
 timeout 900 python bench.py > $OUT/bench.log 2>&1; echo "bench rc=$?" >> $OUT/bench.log
+timeout 600 python scripts/run_config.py 5 > $OUT/config5.json 2>&1
+timeout 900 python scripts/run_config.py 4 --steps 100 > $OUT/config4.json 2>&1
 timeout 300 python scripts/profile_step.py > $OUT/profile_plain.log 2>&1 &&
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
     --log-file $OUT/launches.csv python scripts/profile_step.py > $OUT/ncu_launch.log 2>&1
