@@ -197,6 +197,25 @@ msb_status msb_ms_iterate(msb_ctx ctx, msb_solver s, const double* b, double* x,
                           double* res_hist, int32_t* dyn_M_hist);
 msb_status msb_solver_destroy(msb_solver s);
 
+/* ---------------------------------------------------------------- FGMRES (§8 NEXT-1)
+ * Flexible GMRES(restart) right-preconditioned by ONE multibasis cycle (Eq. 8 from x = 0)
+ * over the solver's static levels followed, when one is installed (M_dyn > 0), by its
+ * dynamic constant-basis stage — held fixed for the whole solve, as the paper builds
+ * dynamic partitions from the most recent nonlinear iteration (reading
+ * B6).  The paper's other outer solver.  Arnoldi with classical Gram-Schmidt applied twice,
+ * Givens rotations on the host; stops when the Arnoldi residual estimate
+ * |g_{j+1}| <= tol ||b|| (confirmed by the true residual at the restart boundary), at
+ * max_iter (MSB_NOT_CONVERGED), or after exactly fixed_iters > 0 steps.
+ * b, x: host|dev N doubles (NULL b = the operator's q; x in x0 / out x); restart in
+ * [1, 64]; res_hist: host array of (max(max_iter, fixed_iters) + 2 + #restarts)
+ * doubles or NULL (ρ_0, then the estimate after every step).  Workspace: (2 restart + 3) N
+ * doubles of device memory for the call.  Errors: MSB_EINVAL (null handle, restart out of
+ * range, no stage), MSB_ENOMEM, MSB_ECUDA; NaN in the Arnoldi estimate is not trapped
+ * (the run ends at max_iter with MSB_NOT_CONVERGED). */
+msb_status msb_fgmres(msb_ctx ctx, msb_solver s, const double* b, double* x, double tol,
+                      int32_t restart, int32_t max_iter, int32_t fixed_iters, int32_t* iters_out,
+                      double* res_hist);
+
 /* ---------------------------------------------------------------- config-4 transport (row a12)
  * Face fluxes F_f = T_f (p_i - p_l) with T including the current mobility, and
  * explicit single-point-upstream transport of water saturation S (

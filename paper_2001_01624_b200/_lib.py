@@ -57,6 +57,7 @@ SIGNATURES = {
     "msb_add_dynamic_basis": (i32, [p, p, p, pi32, p]),
     "msb_ms_iterate": (i32, [p, p, p, p, f64, i32, i32, pi32, p, p]),
     "msb_solver_destroy": (i32, [p]),
+    "msb_fgmres": (i32, [p, p, p, p, f64, i32, i32, i32, pi32, p]),
     "msb_transport_upwind": (i32, [p, p, p, p, p, f64, f64, f64, p, pi32]),
 }
 

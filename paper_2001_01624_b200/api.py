@@ -324,6 +324,19 @@ class Solver:
             out["dyn_M"] = dyn[:k].copy()
         return out
 
+    def fgmres(self, x, b=None, tol=1e-6, restart=20, max_iter=1000, fixed_iters=0):
+        """Flexible GMRES right-preconditioned by one multibasis cycle (§8 NEXT-1).
+        x: in x0 / out x.  Returns dict(iters, status, converged, res)."""
+        n = C.c_int32()
+        cap = max(max_iter, fixed_iters) + 2 + max(max_iter, fixed_iters) // max(1, restart) + 2
+        res = np.zeros(cap)
+        st = self.ctx.lib.msb_fgmres(self.ctx.h, self.h, _ptr(b), _ptr(x), float(tol), int(restart),
+                                     int(max_iter), int(fixed_iters), C.byref(n), _ptr(res))
+        self.ctx.check(st, "msb_fgmres")
+        k = n.value
+        return dict(iters=k, status=st, converged=(st == OK and fixed_iters == 0),
+                    res=res[:k + 1].copy())
+
     def close(self):
         if getattr(self, "h", None):
             self.ctx.lib.msb_solver_destroy(self.h)

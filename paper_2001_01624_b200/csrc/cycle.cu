@@ -1393,3 +1393,29 @@ msb_status msb_solver_destroy(msb_solver s) {
 }
 
 }  // extern "C"
+
+// z = M^{-1} v for FGMRES (fgmres.cu): one iteration of Eq. (8) over the solver's static
+// levels from x = 0 with right-hand side v (no stop test, no dynamic stage).
+namespace msb {
+msb_status solver_precondition(msb_ctx ctx, msb_solver s, const double* v, double* z) {
+  cudaStream_t st = ctx->stream;
+  const int64_t N = s->op->N;
+  IterState h{};
+  h.bscale = 1.0;
+  h.max_iter = 1;
+  MSB_CUDA_TRY(ctx, cudaMemcpyAsync(s->st, &h, sizeof(h), cudaMemcpyHostToDevice, st));
+  MSB_CUDA_TRY(ctx, cudaMemsetAsync(s->xbuf[0], 0, N * sizeof(double), st));
+  int cur = 0;
+  bool first = false;
+  msb_status rc;
+  for (msb_level L : s->levels)
+    if ((rc = enqueue_stage(ctx, s, L, v, cur, first))) return rc;
+  // the installed dynamic stage (msb_add_dynamic_basis, or the last one msb_ms_iterate
+  // built) stays fixed over the solve: reading B6
+  if (s->dyn && s->dyn_level && s->dyn_level->M > 0)
+    if ((rc = enqueue_stage(ctx, s, s->dyn_level, v, cur, first))) return rc;
+  MSB_CUDA_TRY(ctx, cudaMemcpyAsync(z, s->xbuf[cur], N * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  return MSB_OK;
+}
+}  // namespace msb
+

@@ -602,3 +602,116 @@ def test_zero_diagonal_rejected_gpu(ctx):
     lev = Level.cartesian(ctx, op, prob.block)
     with pytest.raises(MsbError, match="EZERO_DIAG"):
         lev.smooth(op, 3, prob.omega, -1.0)
+
+
+def _poison_torch_cache():
+    """Leave NaN in the blocks torch's caching allocator hands out next (both pools), so
+    a kernel that reads a buffer before writing it fails loudly instead of seeing the
+    zeros a fresh cudaMalloc happens to return."""
+    import torch
+    small = [torch.full((1 << 16,), float("nan"), dtype=torch.float64, device="cuda")
+             for _ in range(128)]
+    big = [torch.full((1 << 22,), float("nan"), dtype=torch.float64, device="cuda")
+           for _ in range(8)]
+    torch.cuda.synchronize()
+    del small, big
+
+
+@pytest.mark.parametrize("name", ["config1_dynamic", "ragged_odd", "even_ragged"])
+def test_pipeline_on_poisoned_memory(ctx, name):
+    """Whole path (TPFA, sweeps, RAP, factor, cycle) after the allocator cache is filled
+    with NaN: same iterate as the oracle — no kernel depends on zero-initialised memory."""
+    from oracle import pipeline as opl
+    from paper_2001_01624_b200 import pipeline as gp
+    prob = {"config1_dynamic": lambda: make_problem(1, shape=(32, 32), block=(8, 8, 1),
+                                                    max_sweeps=60, dynamic=True),
+            "ragged_odd": lambda: random_problem(6, 23, 17, 7, (5, 4, 3), sigma=1.5,
+                                                 max_sweeps=40),
+            "even_ragged": lambda: make_problem(2, shape=(26, 46, 23), max_sweeps=25)}[name]()
+    orc = opl.run(prob, fixed_iters=8)
+    _poison_torch_cache()
+    g = gp.run(ctx, prob, fixed_iters=8)
+    x = g["x"].cpu().numpy()
+    assert np.all(np.isfinite(x))
+    err = np.linalg.norm(x - orc["sol"]["x"]) / np.linalg.norm(orc["sol"]["x"])
+    assert err <= 1e-9, err
+
+
+# ---------------------------------------------------------------- §8 NEXT-1: FGMRES
+def _fgmres_dyn_case():
+    """Config 1 with a dynamic stage installed from the Δp of Richardson iterations 1 -> 2
+    (the "most recent nonlinear iteration" of PAPER.md:277), held fixed over the solve."""
+    from oracle import pipeline as opl
+    prob = make_problem(1)
+    x1 = opl.run(prob, fixed_iters=1)["sol"]["x"]
+    x2 = opl.run(prob, fixed_iters=2)["sol"]["x"]
+    prob.dynamic = True
+    return prob, x2 - x1
+
+
+FGMRES_CASES = {
+    "config1": lambda: (make_problem(1), None),
+    "config1_dynamic": _fgmres_dyn_case,
+    "config2_recipe": lambda: (make_problem(2, shape=(24, 44, 20), max_sweeps=300), None),
+    "ragged_odd": lambda: (random_problem(6, 23, 17, 7, (5, 4, 3), sigma=1.5, max_sweeps=40),
+                           None),
+}
+
+
+def _fgmres_alt_levels(levels, A, cls):
+    from oracle.cycle import Level as OLevel
+    out = []
+    for lvl in levels:
+        al = OLevel(lvl.P, A)
+        al.solver = cls(al.Ac)
+        out.append(al)
+    return out
+
+
+@pytest.mark.parametrize("name", list(FGMRES_CASES))
+def test_fgmres_parity(ctx, name):
+    """FGMRES(20) preconditioned by one multibasis cycle: free-mode step counts within
+    max(1, 2 x the alternates' spread) and the iterate at an equal step count within
+    max(1e-9, 2 x floor) — the floors from the same FGMRES with each alternate exact
+    coarse solver in the preconditioner.  GMRES is backward stable; the
+    GPU's CGS2 and the oracle's MGS build the same Arnoldi basis to rounding."""
+    import torch
+    from oracle import fgmres as og
+    from oracle import pipeline as opl
+    from paper_2001_01624_b200 import pipeline as gp
+    from oracle import partition as opart
+    from oracle.cycle import Level as OLevel, constant_basis
+    prob, dp = FGMRES_CASES[name]()
+    tol, m = 1e-6, 20
+    orc = opl.run(prob, fixed_iters=1)  # levels + operator
+    A, q, levels = orc["A"], orc["q"], list(orc["levels"])
+    if dp is not None:
+        part, M = opart.dynamic_partition(dp, prob.nx, prob.ny, prob.nz,
+                                          max_blocks=prob.dyn_max_blocks)
+        levels.append(OLevel(constant_basis(part, M), A))
+    kw = dict(omega_s=prob.omega_s, nu=prob.nu, post=prob.post_smooth, tol=tol, restart=m)
+    free = og.fgmres(A, q, np.zeros(prob.N), levels, max_iter=3000, **kw)
+    assert free["converged"]
+    k_alt = [og.fgmres(A, q, np.zeros(prob.N), _fgmres_alt_levels(levels, A, c), max_iter=3000,
+                       **kw)["iters"] for c in ALTERNATES]
+    k_tol = max(1, 2 * max(abs(free["iters"] - ka) for ka in k_alt))
+    _poison_torch_cache()
+    op = gp.build_operator(ctx, prob)
+    lv, _ = gp.build_levels(ctx, op, prob)
+    s = gp.make_solver(ctx, op, lv, prob)
+    if dp is not None:
+        assert s.add_dynamic_basis(np.ascontiguousarray(dp)) == M
+    x = torch.zeros(prob.N, dtype=torch.float64, device="cuda")
+    out = s.fgmres(x, None, tol=tol, restart=m, max_iter=3000)
+    assert out["converged"], (out["status"], out["iters"], free["iters"], out["res"][-3:])
+    assert abs(out["iters"] - free["iters"]) <= k_tol, (out["iters"], free["iters"], k_alt)
+    k = min(free["iters"], 25)
+    ref = og.fgmres(A, q, np.zeros(prob.N), levels, fixed_iters=k, **kw)
+    floors = [np.linalg.norm(og.fgmres(A, q, np.zeros(prob.N), _fgmres_alt_levels(levels, A, c),
+                                       fixed_iters=k, **kw)["x"] - ref["x"])
+              / np.linalg.norm(ref["x"]) for c in ALTERNATES]
+    x.zero_()
+    s.fgmres(x, None, tol=tol, restart=m, fixed_iters=k)
+    err = np.linalg.norm(x.cpu().numpy() - ref["x"]) / np.linalg.norm(ref["x"])
+    assert err <= max(X_RTOL, 2.0 * max(floors)), (err, floors)
+    assert np.allclose(out["res"][:5], free["res"][:5], rtol=1e-7, atol=1e-12)
