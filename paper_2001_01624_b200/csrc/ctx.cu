@@ -59,6 +59,21 @@ const void* stage_in(msb_ctx ctx, const void* p, size_t bytes, void** owned) {
   return d;
 }
 
+void* pinned_scratch(msb_ctx ctx, size_t bytes) {
+  if (ctx->pinned_bytes >= bytes) return ctx->pinned;
+  if (ctx->pinned) cudaFreeHost(ctx->pinned);
+  ctx->pinned = nullptr;
+  ctx->pinned_bytes = 0;
+  size_t cap = bytes < 65536 ? 65536 : bytes;
+  if (cudaHostAlloc(&ctx->pinned, cap, cudaHostAllocDefault) != cudaSuccess) {
+    cudaGetLastError();
+    ctx->pinned = nullptr;
+    return nullptr;
+  }
+  ctx->pinned_bytes = cap;
+  return ctx->pinned;
+}
+
 cudaError_t copy_out(msb_ctx ctx, void* dst, const void* src_dev, size_t bytes) {
   if (!dst || bytes == 0) return cudaSuccess;
   cudaError_t e = cudaMemcpyAsync(dst, src_dev, bytes, cudaMemcpyDefault, ctx->stream);
@@ -180,6 +195,7 @@ msb_status msb_ctx_create(msb_ctx* out, int device, void* cuda_stream, msb_alloc
 
 msb_status msb_ctx_destroy(msb_ctx ctx) {
   if (!ctx) return MSB_EINVAL;
+  if (ctx->pinned) cudaFreeHost(ctx->pinned);
   delete ctx;
   return MSB_OK;
 }

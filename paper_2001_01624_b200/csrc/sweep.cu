@@ -31,8 +31,8 @@ __device__ __forceinline__ bool sweep_skip(const unsigned long long* __restrict_
   __shared__ int skip;
   if (threadIdx.x < 32) {
     double d = 0.0;
-    if (n > 0 && tol >= 0.0 && threadIdx.x < DSLOTS)
-      d = __longlong_as_double((long long)dslots[(n - 1) * DSLOTS + threadIdx.x]);
+    if (n > 0 && tol >= 0.0 && threadIdx.x < DSLOTS)  // L2 read: written by the previous grid
+      d = __longlong_as_double((long long)__ldcg(dslots + (n - 1) * DSLOTS + threadIdx.x));
     for (int o = 16; o > 0; o >>= 1) d = nmax(d, __shfl_xor_sync(0xffffffffu, d, o));
     if (threadIdx.x == 0) skip = (n > 0 && tol >= 0.0 && d <= tol) ? 1 : 0;
   }
@@ -166,6 +166,7 @@ __global__ void __launch_bounds__(SWEEP_BLOCK, 4) k_sweep_cart(
 // cells wide on each side (box x range [x0-2, x0+34), x0 a multiple of 32).
 constexpr int TT_X = 32, TT_Y = 4;
 constexpr int TT_STAGES_DEFAULT = 4;  // ring depth TT_S (MSB_SW_STAGES=4|5|6 to A/B)
+constexpr int SW8_TY_DEFAULT = 4, SW8_STAGES_DEFAULT = 3;  // k_sweep_tma8 tile rows, ring depth
 constexpr int TB_X = TT_X + 4, TB_Y = TT_Y + 2, TQ_Y = TT_Y + 1;
 constexpr int TP_DBL = 8 * TB_Y * TB_X;  // P box (doubles): rows y0-1 .. y0+TT_Y
 constexpr int TQ_DBL = 3 * TQ_Y * TB_X;  // T box: rows y0-1 .. y0+TT_Y-1
@@ -346,6 +347,377 @@ __global__ void __launch_bounds__(TSWEEP_THREADS) k_sweep_tma(
   sweep_fold(dloc, dslots, n);
 }
 
+// ---------------------------------------------------------------- G2'': one thread per cell
+// Same TMA ring and arithmetic as k_sweep_tma, but each thread owns a cell and all 8
+// slots: the per-cell work (five T reads, D, 1/D, the twelve masked weights, the row
+// sum, 1/sum, the store address) is done once instead of twice, which cuts the issued
+// instructions per cell ~2x (the two-thread kernel is issue-bound: profiles/r01_v9).
+// The TMA issue cursor runs ahead across items, so the next item's first planes load
+// during the current item's last steps (no ring drain at item boundaries).
+template <int TY>
+struct SweepBox {
+  static constexpr int BX = TT_X + 4;           // 2-cell x halo (16-byte TMA start)
+  static constexpr int PPL = (TY + 2) * BX;     // one slot plane of the P box
+  static constexpr int TPL = (TY + 1) * BX;     // one face-direction plane of the T box
+  static constexpr int P_DBL = 8 * PPL;
+  static constexpr int T_DBL = 3 * TPL;
+  static constexpr int STAGE = ((P_DBL + T_DBL) * 8 + 127) / 128 * 128 / 8;
+  static constexpr uint32_t TX = (uint32_t)(P_DBL + T_DBL) * 8u;
+  static constexpr size_t smem(int S) { return (size_t)S * STAGE * 8 + 64; }
+};
+
+// v & m on both 32-bit halves (m all-ones or zero)
+__device__ __forceinline__ double and_mask32(double v, unsigned m) {
+  return __hiloint2double(__double2hiint(v) & (int)m, __double2loint(v) & (int)m);
+}
+
+__device__ __forceinline__ double and_mask(double v, unsigned long long m) {
+  return __longlong_as_double((long long)((unsigned long long)__double_as_longlong(v) & m));
+}
+
+template <int TY, int S>
+__global__ void __launch_bounds__(32 * TY) k_sweep_tma8(
+    const __grid_constant__ CUtensorMap mP0, const __grid_constant__ CUtensorMap mP1,
+    const __grid_constant__ CUtensorMap mT, double* __restrict__ P0, double* __restrict__ P1,
+    const uint8_t* __restrict__ amask, Grid3 g, SweepTiles tl, double omega, int n, double tol,
+    unsigned long long* __restrict__ dslots) {
+  using B = SweepBox<TY>;
+  if (sweep_skip(dslots, n, tol)) return;
+  extern __shared__ __align__(128) double sm[];
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + S * B::STAGE);
+  const CUtensorMap* mIn = (n & 1) ? &mP1 : &mP0;
+  double* __restrict__ Pout = (n & 1) ? P0 : P1;
+  const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;
+  const int nx = g.nx, ny = g.ny, nz = g.nz, nxy = g.nxy, N = g.nxy * g.nz;
+  if (tid == 0) {
+    if (smem_u32(sm) & 127u) __trap();  // TMA destinations must be 128-byte aligned
+    for (int t = 0; t < S; ++t) mbar_init(&bars[t], 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  // issue cursor (thread 0): item ci, plane cp of its cnp planes, ring sequence iss
+  const int tiles = tl.ntx * tl.nty;
+  int ci = blockIdx.x, cp = 0, cnp = 0;
+  uint32_t iss = 0;
+  auto planes_of = [&](int it) {
+    const int k0 = (it / tiles) * tl.kz;
+    return min(k0 + tl.kz, nz) - k0 + 2;
+  };
+  if (ci < tl.items) cnp = planes_of(ci);
+  auto issue_one = [&]() {
+    if (ci >= tl.items) return;
+    const int xt = ci % tl.ntx, yt = (ci / tl.ntx) % tl.nty, zc = ci / tiles;
+    const int slot = iss % S;
+    double* st = sm + slot * B::STAGE;
+    const int z = zc * tl.kz - 1 + cp;
+    mbar_expect_tx(&bars[slot], B::TX);
+    tma_load_4d(st, mIn, &bars[slot], xt * TT_X - 2, yt * TY - 1, z, 0);
+    tma_load_4d(st + B::P_DBL, &mT, &bars[slot], xt * TT_X - 2, yt * TY - 1, z, 0);
+    ++iss;
+    if (++cp == cnp) {
+      ci += gridDim.x;
+      cp = 0;
+      cnp = ci < tl.items ? planes_of(ci) : 0;
+    }
+  };
+  if (tid == 0)
+    for (int p = 0; p < S; ++p) issue_one();
+  const double om1 = 1.0 - omega;
+  const int loc = (ty + 1) * B::BX + (tx + 2);  // same offset in the P and T boxes' row grid
+  uint32_t seq = 0;  // ring sequence number of the current item's plane 0
+  double dloc = 0.0;
+  for (int item = blockIdx.x; item < tl.items; item += gridDim.x) {
+    const int xt = item % tl.ntx, yt = (item / tl.ntx) % tl.nty, zc = item / tiles;
+    const int x0 = xt * TT_X, y0 = yt * TY, k0 = zc * tl.kz, k1 = min(k0 + tl.kz, nz);
+    const int np = k1 - k0 + 2;  // planes k0-1 .. k1 (>= 3)
+    auto wait = [&](int p) {
+      const uint32_t sq = seq + p;
+      mbar_wait(&bars[sq % S], (sq / S) & 1u);
+    };
+    const int x = x0 + tx, y = y0 + ty;
+    const bool inxy = x < nx && y < ny;
+    const unsigned mx = inxy ? amask[x] : 0u, my = inxy ? amask[nx + y] : 0u;
+    // loop-invariant x/y neighbour masks (all-ones or zero)
+    const unsigned long long mxm0 = 0ull - ((mx >> 2) & 1u), mxm1 = 0ull - ((mx >> 3) & 1u);
+    const unsigned long long mxp0 = 0ull - ((mx >> 4) & 1u), mxp1 = 0ull - ((mx >> 5) & 1u);
+    const unsigned long long mym0 = 0ull - ((my >> 2) & 1u), mym1 = 0ull - ((my >> 3) & 1u);
+    const unsigned long long myp0 = 0ull - ((my >> 4) & 1u), myp1 = 0ull - ((my >> 5) & 1u);
+    unsigned mz_next = amask[nx + ny + k0];
+    double pzm[8], tzm;
+    if (tid == 0) {
+      wait(0);
+      wait(1);
+      wait(2);
+    }
+    __syncthreads();
+    {
+      const double* s0 = sm + (seq % S) * B::STAGE;
+#pragma unroll
+      for (int s = 0; s < 8; ++s) pzm[s] = s0[loc + s * B::PPL];
+      tzm = s0[B::P_DBL + 2 * B::TPL + loc];
+    }
+    __syncthreads();  // plane 0 is consumed
+    if (tid == 0) {
+      fence_proxy_async_smem();
+      issue_one();
+    }
+    double* __restrict__ pout = Pout + (size_t)(x + nx * y) + (size_t)k0 * nxy;
+    for (int k = k0; k < k1; ++k) {
+      const int pc = k - k0 + 1;
+      const unsigned mz = mz_next;
+      if (k + 1 < k1) mz_next = amask[nx + ny + k + 1];
+      const double* __restrict__ sC = sm + ((seq + pc) % S) * B::STAGE;
+      const double* __restrict__ sP = sm + ((seq + pc + 1) % S) * B::STAGE;
+      const double* __restrict__ tC = sC + B::P_DBL;
+      const double txp = tC[loc], txm = tC[loc - 1];
+      const double typ = tC[B::TPL + loc], tym = tC[B::TPL + loc - B::BX];
+      const double tzp = tC[2 * B::TPL + loc];
+      const double D = txp + txm + typ + tym + tzp + tzm;
+      const double wD = inxy ? omega * rcp_fast(D) : 0.0;
+      const double wxm0 = and_mask(txm, mxm0), wxm1 = and_mask(txm, mxm1);
+      const double wxp0 = and_mask(txp, mxp0), wxp1 = and_mask(txp, mxp1);
+      const double wym0 = and_mask(tym, mym0), wym1 = and_mask(tym, mym1);
+      const double wyp0 = and_mask(typ, myp0), wyp1 = and_mask(typ, myp1);
+      const double wzm0 = mask_d(tzm, (mz >> 2) & 1u), wzm1 = mask_d(tzm, (mz >> 3) & 1u);
+      const double wzp0 = mask_d(tzp, (mz >> 4) & 1u), wzp1 = mask_d(tzp, (mz >> 5) & 1u);
+      double ph[8], po[8];
+#pragma unroll
+      for (int s = 0; s < 8; ++s) {
+        const int px = s & 1, py = (s >> 1) & 1, pz = s >> 2;
+        const int o = loc + s * B::PPL;
+        double acc = (pz ? wzm1 : wzm0) * pzm[s];
+        acc += (py ? wym1 : wym0) * sC[o - B::BX];
+        acc += (px ? wxm1 : wxm0) * sC[o - 1];
+        acc += (px ? wxp1 : wxp0) * sC[o + 1];
+        acc += (py ? wyp1 : wyp0) * sC[o + B::BX];
+        acc += (pz ? wzp1 : wzp0) * sP[o];
+        po[s] = sC[o];
+        ph[s] = om1 * po[s] + wD * acc;
+      }
+      // row sum in the two-thread kernel's order: (z-parity-0 half) + (z-parity-1 half)
+      double slo = 0.0, shi = 0.0;
+#pragma unroll
+      for (int s = 0; s < 4; ++s) {
+        slo += ph[s];
+        shi += ph[4 + s];
+      }
+      const double sum = slo + shi;
+      if (inxy) {
+        const double rs = rcp_fast(sum);
+#pragma unroll
+        for (int s = 0; s < 8; ++s) {
+          const int px = s & 1, py = (s >> 1) & 1, pz = s >> 2;
+          if ((mx >> px) & (my >> py) & (mz >> pz) & 1u) {
+            const double pn = div_rn(ph[s], sum, rs);
+            pout[(size_t)s * N] = pn;
+            const double d = fabs(pn - po[s]);
+            dloc = d > dloc ? d : dloc;
+          }
+        }
+      }
+#pragma unroll
+      for (int s = 0; s < 8; ++s) pzm[s] = po[s];
+      tzm = tzp;
+      pout += nxy;
+      if (tid == 0 && pc + 2 < np) wait(pc + 2);
+      __syncthreads();  // plane pc+2 is published; plane pc (and after the last step, np-1) is free
+      if (tid == 0) {
+        fence_proxy_async_smem();
+        issue_one();
+        if (pc == np - 2) issue_one();
+      }
+    }
+    seq += np;
+  }
+  sweep_fold(dloc, dslots, n);
+}
+
+// Grid-wide barrier for the persistent multi-sweep launch (all CTAs co-resident: the
+// launch is cooperative).  The fences order this CTA's generic-proxy stores before the
+// arrive and the other CTAs' stores before this CTA's next TMA (async-proxy) loads.
+__device__ __forceinline__ void sweep_grid_sync(unsigned* bar, unsigned target) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+    atomicAdd(bar, 1u);
+    unsigned v;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
+    } while (v < target);
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+  }
+  __syncthreads();
+}
+
+// ---------------------------------------------------------------- G2-ws: warp-specialised ring
+// k_sweep_tma8's arithmetic with a producer/consumer ring instead of CTA barriers: one
+// producer warp (lane 0) streams the planes of all of this CTA's items through S stages,
+// waiting on per-stage "empty" mbarriers; each of the TY consumer warps (one tile row
+// of 32 cells) waits on the stage's "full" mbarrier, computes, and releases the plane
+// with one arrive.  Warps never wait for each other, only for data, so a warp can run
+// up to S-2 planes ahead of the slowest.  One launch runs `cnt` sweeps n0 .. n0+cnt-1
+// with a grid barrier between them (persistent, cooperative launch), so the per-launch
+// ramp and drain are paid once per chunk instead of once per sweep; the ring's phase
+// counters run on across sweeps.  Every sweep first tests δ of the previous one and the
+// whole grid stops at the same sweep (δ is final after the barrier).
+template <int TY, int S>
+__global__ void __launch_bounds__(32 * (TY + 1)) k_sweep_ws(
+    const __grid_constant__ CUtensorMap mP0, const __grid_constant__ CUtensorMap mP1,
+    const __grid_constant__ CUtensorMap mT, double* __restrict__ P0, double* __restrict__ P1,
+    const uint8_t* __restrict__ amask, Grid3 g, SweepTiles tl, double omega, int n0, int cnt,
+    double tol, unsigned long long* __restrict__ dslots, unsigned* __restrict__ gbar) {
+  using B = SweepBox<TY>;
+  extern __shared__ __align__(128) double sm[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm + S * B::STAGE);
+  uint64_t* empty = full + S;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nx = g.nx, ny = g.ny, nz = g.nz, nxy = g.nxy, N = g.nxy * g.nz;
+  const int tiles = tl.ntx * tl.nty;
+  if (tid == 0) {
+    if (smem_u32(sm) & 127u) __trap();  // TMA destinations must be 128-byte aligned
+    for (int t = 0; t < S; ++t) {
+      mbar_init(&full[t], 1);
+      mbar_init(&empty[t], TY);
+    }
+    mbar_fence_init();
+  }
+  uint32_t q = 0, seq = 0;  // ring sequence: producer issue count / consumer item base
+  for (int j = 0; j < cnt; ++j) {
+    const int n = n0 + j;
+    if (j > 0) sweep_grid_sync(gbar, (unsigned)j * gridDim.x);
+    if (sweep_skip(dslots, n, tol)) break;  // uniform: δ_{n-1} is final (its __syncthreads
+                                            // also publishes the barrier init)
+    double dloc = 0.0;
+    if (warp == TY) {  // producer
+      if (lane == 0) {
+        const CUtensorMap* mIn = (n & 1) ? &mP1 : &mP0;
+        for (int item = blockIdx.x; item < tl.items; item += gridDim.x) {
+          const int xt = item % tl.ntx, yt = (item / tl.ntx) % tl.nty, zc = item / tiles;
+          const int k0 = zc * tl.kz, np = min(k0 + tl.kz, nz) - k0 + 2;
+          for (int p = 0; p < np; ++p, ++q) {
+            const int slot = q % S;
+            if (q >= (uint32_t)S) mbar_wait(&empty[slot], ((q / S) - 1) & 1u);
+            double* st = sm + slot * B::STAGE;
+            mbar_expect_tx(&full[slot], B::TX);
+            tma_load_4d(st, mIn, &full[slot], xt * TT_X - 2, yt * TY - 1, k0 - 1 + p, 0);
+            tma_load_4d(st + B::P_DBL, &mT, &full[slot], xt * TT_X - 2, yt * TY - 1, k0 - 1 + p, 0);
+          }
+        }
+      }
+    } else {  // consumers: warp = tile row
+      double* __restrict__ Pout = (n & 1) ? P0 : P1;
+      const double om1 = 1.0 - omega;
+      const int tx = lane, ty = warp;
+      const int loc = (ty + 1) * B::BX + (tx + 2);
+      for (int item = blockIdx.x; item < tl.items; item += gridDim.x) {
+        const int xt = item % tl.ntx, yt = (item / tl.ntx) % tl.nty, zc = item / tiles;
+        const int x0 = xt * TT_X, y0 = yt * TY, k0 = zc * tl.kz, k1 = min(k0 + tl.kz, nz);
+        const int np = k1 - k0 + 2;
+        auto wait_full = [&](int p) {
+          const uint32_t sq = seq + p;
+          mbar_wait(&full[sq % S], (sq / S) & 1u);
+        };
+        auto release = [&](int p) {
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&empty[(seq + p) % S]);
+        };
+        const int x = x0 + tx, y = y0 + ty;
+        const bool inxy = x < nx && y < ny;
+        const unsigned mx = inxy ? amask[x] : 0u, my = inxy ? amask[nx + y] : 0u;
+        // loop-invariant x/y neighbour masks, one 32-bit word applied to both halves
+        const unsigned mxm0 = 0u - ((mx >> 2) & 1u), mxm1 = 0u - ((mx >> 3) & 1u);
+        const unsigned mxp0 = 0u - ((mx >> 4) & 1u), mxp1 = 0u - ((mx >> 5) & 1u);
+        const unsigned mym0 = 0u - ((my >> 2) & 1u), mym1 = 0u - ((my >> 3) & 1u);
+        const unsigned myp0 = 0u - ((my >> 4) & 1u), myp1 = 0u - ((my >> 5) & 1u);
+        // active slots of this column: bit s set iff x parity s&1 and y parity (s>>1)&1
+        // are supports here (the z parity is folded in per plane)
+        const unsigned axy = ((mx & 1u) ? 0x55u : 0u) | ((mx & 2u) ? 0xAAu : 0u);
+        const unsigned act_xy =
+            axy & (((my & 1u) ? 0x33u : 0u) | ((my & 2u) ? 0xCCu : 0u)) & (inxy ? 0xFFu : 0u);
+        unsigned mz_next = amask[nx + ny + k0];
+        double pzm[8], tzm;
+        wait_full(0);
+        {
+          const double* s0 = sm + (seq % S) * B::STAGE;
+#pragma unroll
+          for (int s = 0; s < 8; ++s) pzm[s] = s0[loc + s * B::PPL];
+          tzm = s0[B::P_DBL + 2 * B::TPL + loc];
+        }
+        release(0);
+        wait_full(1);
+        double* __restrict__ pout = Pout + (size_t)(x + nx * y) + (size_t)k0 * nxy;
+        for (int k = k0; k < k1; ++k) {
+          const int pc = k - k0 + 1;
+          const unsigned mz = mz_next;
+          if (k + 1 < k1) mz_next = amask[nx + ny + k + 1];
+          wait_full(pc + 1);
+          const double* __restrict__ sC = sm + ((seq + pc) % S) * B::STAGE;
+          const double* __restrict__ sP = sm + ((seq + pc + 1) % S) * B::STAGE;
+          const double* __restrict__ tC = sC + B::P_DBL;
+          const double txp = tC[loc], txm = tC[loc - 1];
+          const double typ = tC[B::TPL + loc], tym = tC[B::TPL + loc - B::BX];
+          const double tzp = tC[2 * B::TPL + loc];
+          const double D = txp + txm + typ + tym + tzp + tzm;
+          const double wD = inxy ? omega * rcp_fast(D) : 0.0;
+          const double wxm0 = and_mask32(txm, mxm0), wxm1 = and_mask32(txm, mxm1);
+          const double wxp0 = and_mask32(txp, mxp0), wxp1 = and_mask32(txp, mxp1);
+          const double wym0 = and_mask32(tym, mym0), wym1 = and_mask32(tym, mym1);
+          const double wyp0 = and_mask32(typ, myp0), wyp1 = and_mask32(typ, myp1);
+          const double wzm0 = and_mask32(tzm, 0u - ((mz >> 2) & 1u));
+          const double wzm1 = and_mask32(tzm, 0u - ((mz >> 3) & 1u));
+          const double wzp0 = and_mask32(tzp, 0u - ((mz >> 4) & 1u));
+          const double wzp1 = and_mask32(tzp, 0u - ((mz >> 5) & 1u));
+          double ph[8], po[8];
+#pragma unroll
+          for (int s = 0; s < 8; ++s) {
+            const int px = s & 1, py = (s >> 1) & 1, pz = s >> 2;
+            const int o = loc + s * B::PPL;
+            double acc = (pz ? wzm1 : wzm0) * pzm[s];
+            acc += (py ? wym1 : wym0) * sC[o - B::BX];
+            acc += (px ? wxm1 : wxm0) * sC[o - 1];
+            acc += (px ? wxp1 : wxp0) * sC[o + 1];
+            acc += (py ? wyp1 : wyp0) * sC[o + B::BX];
+            acc += (pz ? wzp1 : wzp0) * sP[o];
+            po[s] = sC[o];
+            ph[s] = om1 * po[s] + wD * acc;
+          }
+          release(pc);  // plane pc is read for the last time above
+          double slo = 0.0, shi = 0.0;
+#pragma unroll
+          for (int s = 0; s < 4; ++s) {
+            slo += ph[s];
+            shi += ph[4 + s];
+          }
+          const double sum = slo + shi;
+          // inactive (cell, slot) entries have ph = po = 0 exactly, so they add 0 to δ
+          // and only their stores need the activity predicate
+          const unsigned act = act_xy & (((mz & 1u) ? 0x0Fu : 0u) | ((mz & 2u) ? 0xF0u : 0u));
+          if (inxy) {
+            const double rs = rcp_fast(sum);
+            double* __restrict__ qo = pout;
+#pragma unroll
+            for (int s = 0; s < 8; ++s) {
+              const double pn = div_rn(ph[s], sum, rs);
+              if ((act >> s) & 1u) *qo = pn;
+              qo += N;
+              const double d = fabs(pn - po[s]);
+              dloc = d > dloc ? d : dloc;
+            }
+          }
+#pragma unroll
+          for (int s = 0; s < 8; ++s) pzm[s] = po[s];
+          tzm = tzp;
+          pout += nxy;
+        }
+        release(np - 1);
+        seq += np;
+      }
+    }
+    sweep_fold(dloc, dslots, n);
+  }
+}
+
 // Zero diagonal of A_T: a cell with no open face (D_T = 0) has no
 // smoothing update.  Checked once per msb_smooth_basis call, so the sweep kernels need
 // no per-step NaN bookkeeping.
@@ -421,6 +793,75 @@ __global__ void __launch_bounds__(SWEEP_BLOCK) k_sweep_ell(
   sweep_fold(dloc, dslots, n);
 }
 
+using SweepKern = void (*)(const CUtensorMap, const CUtensorMap, const CUtensorMap, double*,
+                           double*, const uint8_t*, Grid3, SweepTiles, double, int, double,
+                           unsigned long long*);
+using SweepKernMulti = void (*)(const CUtensorMap, const CUtensorMap, const CUtensorMap, double*,
+                                double*, const uint8_t*, Grid3, SweepTiles, double, int, int,
+                                double, unsigned long long*, unsigned*);
+struct SweepLaunch {
+  SweepKern kern = nullptr;        // one sweep per launch
+  SweepKernMulti multi = nullptr;  // a chunk of sweeps per (cooperative) launch
+  int threads = 0, ty = 0, occ = 0;
+  size_t smem = 0;
+};
+
+template <typename K>
+static cudaError_t sweep_setup_common(SweepLaunch* out, K kern, int threads, int ty, size_t smem) {
+  cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int occ = 0;
+  if (err == cudaSuccess) err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem);
+  if (err != cudaSuccess) return err;
+  out->threads = threads;
+  out->ty = ty;
+  out->occ = occ < 1 ? 1 : occ;
+  out->smem = smem;
+  return cudaSuccess;
+}
+static cudaError_t sweep_setup(SweepLaunch* out, SweepKern kern, int threads, int ty, size_t smem) {
+  out->kern = kern;
+  return sweep_setup_common(out, kern, threads, ty, smem);
+}
+static cudaError_t sweep_setup(SweepLaunch* out, SweepKernMulti kern, int threads, int ty,
+                               size_t smem) {
+  out->multi = kern;
+  return sweep_setup_common(out, kern, threads, ty, smem);
+}
+
+// Kernel choice (A/B knobs, read once per process): MSB_SW_KERNEL=1 two threads per cell
+// (MSB_SW_STAGES=4|5|6), =2 one thread per cell with CTA barriers (MSB_SW_TY=4|8,
+// MSB_SW_STAGES=3|4), default: warp-specialised persistent multi-sweep
+// (MSB_SW_TY=4|8, MSB_SW_STAGES=3|4|5).
+static cudaError_t sweep_variant(SweepLaunch* out) {
+  const char* ek = getenv("MSB_SW_KERNEL");
+  const char* es = getenv("MSB_SW_STAGES");
+  const char* ey = getenv("MSB_SW_TY");
+  const int kind = ek ? atoi(ek) : 3;
+  if (kind == 1) {
+    const int S = es ? atoi(es) : TT_STAGES_DEFAULT;
+    if (S == 5) return sweep_setup(out, k_sweep_tma<5>, TSWEEP_THREADS, TT_Y, tsweep_smem(5));
+    if (S == 6) return sweep_setup(out, k_sweep_tma<6>, TSWEEP_THREADS, TT_Y, tsweep_smem(6));
+    return sweep_setup(out, k_sweep_tma<4>, TSWEEP_THREADS, TT_Y, tsweep_smem(4));
+  }
+  const int S = es ? atoi(es) : SW8_STAGES_DEFAULT;
+  const int TY = ey ? atoi(ey) : SW8_TY_DEFAULT;
+  if (kind == 2) {
+    if (TY == 8) {
+      if (S == 4) return sweep_setup(out, k_sweep_tma8<8, 4>, 256, 8, SweepBox<8>::smem(4));
+      return sweep_setup(out, k_sweep_tma8<8, 3>, 256, 8, SweepBox<8>::smem(3));
+    }
+    if (S == 3) return sweep_setup(out, k_sweep_tma8<4, 3>, 128, 4, SweepBox<4>::smem(3));
+    return sweep_setup(out, k_sweep_tma8<4, 4>, 128, 4, SweepBox<4>::smem(4));
+  }
+  if (TY == 8) {
+    if (S == 3) return sweep_setup(out, k_sweep_ws<8, 3>, 288, 8, SweepBox<8>::smem(3) + 64);
+    return sweep_setup(out, k_sweep_ws<8, 4>, 288, 8, SweepBox<8>::smem(4) + 64);
+  }
+  if (S == 3) return sweep_setup(out, k_sweep_ws<4, 3>, 160, 4, SweepBox<4>::smem(3) + 64);
+  if (S == 5) return sweep_setup(out, k_sweep_ws<4, 5>, 160, 4, SweepBox<4>::smem(5) + 64);
+  return sweep_setup(out, k_sweep_ws<4, 4>, 160, 4, SweepBox<4>::smem(4) + 64);
+}
+
 }  // namespace msb
 
 using namespace msb;
@@ -438,9 +879,12 @@ extern "C" msb_status msb_smooth_basis(msb_ctx ctx, msb_level L, msb_op op, int3
   if (last_delta) *last_delta = 0.0;
   if (max_sweeps == 0) return MSB_OK;
   cudaStream_t st = ctx->stream;
-  unsigned long long* dslots = dalloc_n<unsigned long long>(ctx, (size_t)max_sweeps * DSLOTS);
+  // δ slots per sweep, then one 128-byte line for the multi-sweep grid barrier counter
+  unsigned long long* dslots =
+      dalloc_n<unsigned long long>(ctx, (size_t)max_sweeps * DSLOTS + DSLOTS);
   if (!dslots) return set_error(ctx, MSB_ENOMEM, "sweep state");
-  MSB_CUDA_TRY(ctx, cudaMemsetAsync(dslots, 0, (size_t)max_sweeps * DSLOTS * 8, st));
+  MSB_CUDA_TRY(ctx, cudaMemsetAsync(dslots, 0, ((size_t)max_sweeps * DSLOTS + DSLOTS) * 8, st));
+  unsigned* gbar = reinterpret_cast<unsigned*>(dslots + (size_t)max_sweeps * DSLOTS);
   Grid3 g = make_grid3(op->nx, op->ny, op->nz);
   {
     int* zf = dalloc_n<int>(ctx, 1);
@@ -470,42 +914,30 @@ extern "C" msb_status msb_smooth_basis(msb_ctx ctx, msb_level L, msb_op op, int3
   }
   double* Pa = L->P[L->cur];
   double* Pb = L->P[L->cur ^ 1];
-  // TMA path: tensor maps over both P buffers and the 3N transmissibility block
+  // TMA path: tensor maps over both P buffers and the 3N transmissibility block.
+  // Variants (A/B knobs): MSB_SW_KERNEL=1 selects the two-thread-per-cell kernel
+  // (MSB_SW_STAGES=4|5|6); the default one-thread-per-cell kernel takes
+  // MSB_SW_TY=4|8 tile rows and MSB_SW_STAGES=3|4 ring stages.
   bool use_tma = false;
   CUtensorMap mP[2], mT;
   SweepTiles tl{};
   unsigned tgrid = 0;
-  int sw_stages = TT_STAGES_DEFAULT;
+  SweepLaunch sl{};
   if (L->kind == 0 && (op->nx % 2) == 0 && !getenv("MSB_NO_TMA")) {
+    static SweepLaunch cached{};
+    if (!cached.kern) MSB_CUDA_TRY(ctx, sweep_variant(&cached));
+    sl = cached;
     const uint64_t dP[4] = {(uint64_t)op->nx, (uint64_t)op->ny, (uint64_t)op->nz, 8};
     const uint64_t dT[4] = {(uint64_t)op->nx, (uint64_t)op->ny, (uint64_t)op->nz, 3};
     const uint64_t st3[3] = {(uint64_t)op->nx, (uint64_t)op->nx * op->ny, (uint64_t)L->N};
-    const uint32_t bP[4] = {TB_X, TB_Y, 1, 8}, bT[4] = {TB_X, TQ_Y, 1, 3};
+    const uint32_t bP[4] = {TT_X + 4, (uint32_t)sl.ty + 2, 1, 8};
+    const uint32_t bT[4] = {TT_X + 4, (uint32_t)sl.ty + 1, 1, 3};
     use_tma = tma_encode_4d(&mP[0], Pa, dP, st3, bP) && tma_encode_4d(&mP[1], Pb, dP, st3, bP) &&
               tma_encode_4d(&mT, op->Tx, dT, st3, bT);
     if (use_tma) {
-      static int occ = 0, stages = 0;
-      if (!occ) {
-        const char* e = getenv("MSB_SW_STAGES");
-        stages = e ? atoi(e) : TT_STAGES_DEFAULT;
-        if (stages != 4 && stages != 5 && stages != 6) stages = TT_STAGES_DEFAULT;
-        auto setup = [&](auto kern, int S) -> cudaError_t {
-          cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                 (int)tsweep_smem(S));
-          if (err == cudaSuccess)
-            err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, TSWEEP_THREADS,
-                                                                tsweep_smem(S));
-          return err;
-        };
-        cudaError_t err = stages == 4 ? setup(k_sweep_tma<4>, 4)
-                        : stages == 5 ? setup(k_sweep_tma<5>, 5) : setup(k_sweep_tma<6>, 6);
-        MSB_CUDA_TRY(ctx, err);
-        if (occ < 1) occ = 1;
-      }
-      sw_stages = stages;
       tl.ntx = (op->nx + TT_X - 1) / TT_X;
-      tl.nty = (op->ny + TT_Y - 1) / TT_Y;
-      const int64_t slots = (int64_t)occ * ctx->sm_count;
+      tl.nty = (op->ny + sl.ty - 1) / sl.ty;
+      const int64_t slots = (int64_t)sl.occ * ctx->sm_count;
       const int64_t tiles = (int64_t)tl.ntx * tl.nty;
       // z-chunking: minimise (waves) x (planes per item incl. 2 halo planes)
       int64_t best = INT64_MAX;
@@ -528,38 +960,73 @@ extern "C" msb_status msb_smooth_basis(msb_ctx ctx, msb_level L, msb_op op, int3
   int issued = 0, n = 0;
   double last = 0.0;
   bool bad = false, done = false;
-  std::vector<unsigned long long> hb;
-  while (!done && issued < max_sweeps) {
-    int nl = std::min(chunk, max_sweeps - issued);
-    for (int t = 0; t < nl; ++t) {
-      int idx = issued + t;
-      if (use_tma)
-        switch (sw_stages) {
-          case 5:
-            k_sweep_tma<5><<<tgrid, TSWEEP_THREADS, tsweep_smem(5), st>>>(
-                mP[0], mP[1], mT, Pa, Pb, L->amask, g, tl, omega, idx, tol, dslots);
-            break;
-          case 6:
-            k_sweep_tma<6><<<tgrid, TSWEEP_THREADS, tsweep_smem(6), st>>>(
-                mP[0], mP[1], mT, Pa, Pb, L->amask, g, tl, omega, idx, tol, dslots);
-            break;
-          default:
-            k_sweep_tma<4><<<tgrid, TSWEEP_THREADS, tsweep_smem(4), st>>>(
-                mP[0], mP[1], mT, Pa, Pb, L->amask, g, tl, omega, idx, tol, dslots);
-        }
-      else if (L->kind == 0)
-        k_sweep_cart<<<grid, SWEEP_BLOCK, 0, st>>>(Pa, Pb, op->Tx, op->Ty, op->Tz, L->amask, g,
-                                                   omega, idx, tol, dslots);
-      else
-        k_sweep_ell<<<grid, SWEEP_BLOCK, 0, st>>>(Pa, Pb, op->Tx, op->Ty, op->Tz, L->col, L->nbs,
-                                                  L->W, g, omega, idx, tol, dslots);
-      MSB_LAUNCH_CHECK(ctx);
+  // Chunks of up to 32 sweeps are enqueued without host round trips; each chunk's δ slots
+  // are copied to pinned memory behind it, and the host reads chunk c while chunk c+1
+  // runs (two-deep pipeline).  Sweeps after convergence return at entry (δ_{n-1} <= tol),
+  // so the over-issued chunk costs one empty launch.
+  unsigned long long* hbuf =
+      static_cast<unsigned long long*>(pinned_scratch(ctx, 2 * (size_t)chunk * DSLOTS * 8));
+  if (!hbuf) {
+    dfree(ctx, dslots);
+    return set_error(ctx, MSB_ENOMEM, "pinned readback buffer");
+  }
+  cudaEvent_t ev[2] = {nullptr, nullptr};
+  for (auto& e : ev) MSB_CUDA_TRY(ctx, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  int c_first[2] = {0, 0}, c_n[2] = {0, 0};
+  auto launch_chunk = [&](int b) -> msb_status {
+    const int nl = std::min(chunk, max_sweeps - issued);
+    if (use_tma && sl.multi) {
+      // the chunk's sweeps in one cooperative launch (grid barrier between sweeps)
+      MSB_CUDA_TRY(ctx, cudaMemsetAsync(gbar, 0, sizeof(unsigned), st));
+      cudaLaunchConfig_t cfg{};
+      cfg.gridDim = dim3(tgrid);
+      cfg.blockDim = dim3(sl.threads);
+      cfg.dynamicSmemBytes = sl.smem;
+      cfg.stream = st;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeCooperative;
+      at[0].val.cooperative = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      MSB_CUDA_TRY(ctx, cudaLaunchKernelEx(&cfg, sl.multi, mP[0], mP[1], mT, Pa, Pb,
+                                           (const uint8_t*)L->amask, g, tl, omega, issued, nl, tol,
+                                           dslots, gbar));
+    } else {
+      for (int t = 0; t < nl; ++t) {
+        const int idx = issued + t;
+        if (use_tma)
+          sl.kern<<<tgrid, sl.threads, sl.smem, st>>>(mP[0], mP[1], mT, Pa, Pb, L->amask, g, tl,
+                                                      omega, idx, tol, dslots);
+        else if (L->kind == 0)
+          k_sweep_cart<<<grid, SWEEP_BLOCK, 0, st>>>(Pa, Pb, op->Tx, op->Ty, op->Tz, L->amask, g,
+                                                     omega, idx, tol, dslots);
+        else
+          k_sweep_ell<<<grid, SWEEP_BLOCK, 0, st>>>(Pa, Pb, op->Tx, op->Ty, op->Tz, L->col, L->nbs,
+                                                    L->W, g, omega, idx, tol, dslots);
+        MSB_LAUNCH_CHECK(ctx);
+      }
     }
-    hb.resize((size_t)nl * DSLOTS);
-    MSB_CUDA_TRY(ctx, cudaMemcpyAsync(hb.data(), dslots + (size_t)issued * DSLOTS,
-                                      hb.size() * 8, cudaMemcpyDeviceToHost, st));
-    MSB_CUDA_TRY(ctx, cudaStreamSynchronize(st));
-    for (int t = 0; t < nl && !done; ++t) {
+    MSB_CUDA_TRY(ctx, cudaMemcpyAsync(hbuf + (size_t)b * chunk * DSLOTS,
+                                      dslots + (size_t)issued * DSLOTS, (size_t)nl * DSLOTS * 8,
+                                      cudaMemcpyDeviceToHost, st));
+    MSB_CUDA_TRY(ctx, cudaEventRecord(ev[b], st));
+    c_first[b] = issued;
+    c_n[b] = nl;
+    issued += nl;
+    return MSB_OK;
+  };
+  msb_status lrc = MSB_OK;
+  int cb = 0;
+  if (max_sweeps > 0) lrc = launch_chunk(0);
+  while (!lrc) {
+    const bool more = issued < max_sweeps;
+    if (more && (lrc = launch_chunk(cb ^ 1))) break;
+    if (cudaEventSynchronize(ev[cb]) != cudaSuccess) {
+      lrc = set_error(ctx, MSB_ECUDA, "sweep chunk: %s", cudaGetErrorString(cudaGetLastError()));
+      break;
+    }
+    const unsigned long long* hb = hbuf + (size_t)cb * chunk * DSLOTS;
+    for (int t = 0; t < c_n[cb] && !done; ++t) {
       double d = 0.0;
       for (int q = 0; q < DSLOTS; ++q) {
         double v;
@@ -567,12 +1034,19 @@ extern "C" msb_status msb_smooth_basis(msb_ctx ctx, msb_level L, msb_op op, int3
         d = (v > d || v != v) ? v : d;
       }
       if (!(d == d)) bad = true;
-      if (deltas) deltas[issued + t] = d;
+      if (deltas) deltas[c_first[cb] + t] = d;
       last = d;
-      n = issued + t + 1;
+      n = c_first[cb] + t + 1;
       if (tol >= 0.0 && d <= tol) done = true;
     }
-    issued += nl;
+    if (done || !more) break;
+    cb ^= 1;
+  }
+  cudaStreamSynchronize(st);  // an over-issued chunk may still be running
+  for (auto& e : ev) cudaEventDestroy(e);
+  if (lrc) {
+    dfree(ctx, dslots);
+    return lrc;
   }
   dfree(ctx, dslots);
   if (n & 1) L->cur ^= 1;

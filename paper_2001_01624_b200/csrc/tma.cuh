@@ -51,6 +51,11 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
+// Plain arrive (count 1) on a consumer-release barrier.
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
 // Order this thread's earlier generic-proxy shared-memory accesses before later
 // async-proxy (TMA) writes to the same buffers.
 __device__ __forceinline__ void fence_proxy_async_smem() {
