@@ -18,6 +18,8 @@
 
 #include <cooperative_groups.h>
 
+#include <cstdio>
+
 #include "internal.cuh"
 #include "symv.cuh"
 
@@ -892,6 +894,82 @@ static msb_status build_dynamic(msb_ctx ctx, msb_solver s, const double* dp, int
   return MSB_OK;
 }
 
+// ---------------------------------------------------------------- L2 residency of P
+// P is read twice per iteration (restriction, prolongation) and, on the 1.1M-cell grid,
+// fits the device's persisting-L2 carve-out (8N doubles = 71.8 MB <= 82.9 MB on B200).
+// While a solve runs the carve-out is set to P's size and the library stream (and the
+// graph-capture stream) carry an access-policy window over P, so after the first
+// iteration P is served from L2 (ncu, direct launches: restriction DRAM reads 53 -> 0.3 MB).
+// The window covers only P's addresses, so the other kernels' accesses are unaffected.
+// When the solve returns, the streams' previous windows are restored, persisting lines
+// are reset and the carve-out is released, so the basis sweeps keep the whole L2.
+// Opt-in (MSB_L2_P=1) and skipped when P does not fit (config 5: 640 MB): measured on
+// config 2 the restriction's DRAM reads drop as intended, but the 74.6 MB set-aside
+// leaves the stencil passes 58 MB of normal L2 and the iteration runs 72.0 -> 74.4 us
+// (profiles/r01_v10).  A per-launch access-policy attribute had no effect at all; the
+// window has to be a stream attribute (and, for captured graphs, a kernel-node attribute).
+static void set_window(cudaStream_t st, const cudaAccessPolicyWindow& w) {
+  if (!st) return;
+  cudaStreamAttrValue sv{};
+  sv.accessPolicyWindow = w;
+  cudaStreamSetAttribute(st, cudaStreamAttributeAccessPolicyWindow, &sv);
+}
+
+static cudaAccessPolicyWindow p_window(msb_solver s) {
+  cudaAccessPolicyWindow w{};
+  w.base_ptr = const_cast<void*>(s->l2_base);
+  w.num_bytes = s->l2_bytes;
+  w.hitRatio = 1.0f;
+  w.hitProp = cudaAccessPropertyPersisting;
+  w.missProp = cudaAccessPropertyStreaming;
+  return w;
+}
+
+static void l2_begin(msb_ctx ctx, msb_solver s) {
+  s->l2_base = nullptr;
+  s->l2_bytes = 0;
+  const char* e = getenv("MSB_L2_P");
+  if (!(e && e[0] == '1') || s->levels.size() != 1 || s->levels[0]->kind != 0) return;
+  static size_t max_persist = (size_t)-1, max_win = 0;
+  if (max_persist == (size_t)-1) {
+    int v = 0, w = 0;
+    max_persist = cudaDeviceGetAttribute(&v, cudaDevAttrMaxPersistingL2CacheSize, ctx->device) ==
+                          cudaSuccess ? (size_t)v : 0;
+    max_win = cudaDeviceGetAttribute(&w, cudaDevAttrMaxAccessPolicyWindowSize, ctx->device) ==
+                      cudaSuccess ? (size_t)w : 0;
+    cudaGetLastError();
+  }
+  msb_level L = s->levels[0];
+  const size_t bytes = (size_t)8 * L->N * sizeof(double);
+  if (bytes > max_persist || bytes > max_win) return;
+  if (cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, bytes) != cudaSuccess) {
+    cudaGetLastError();
+    return;
+  }
+  cudaStreamAttrValue prev{};
+  if (ctx->stream &&
+      cudaStreamGetAttribute(ctx->stream, cudaStreamAttributeAccessPolicyWindow, &prev) == cudaSuccess)
+    s->l2_prev = prev.accessPolicyWindow;
+  else
+    s->l2_prev = cudaAccessPolicyWindow{};
+  cudaGetLastError();
+  s->l2_base = L->P[L->cur];
+  s->l2_bytes = bytes;
+  set_window(ctx->stream, p_window(s));
+  set_window(s->cap_stream, p_window(s));
+}
+
+static void l2_end(msb_ctx ctx, msb_solver s) {
+  if (!s->l2_bytes) return;
+  set_window(ctx->stream, s->l2_prev);
+  set_window(s->cap_stream, cudaAccessPolicyWindow{});
+  cudaCtxResetPersistingL2Cache();
+  cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, 0);
+  cudaGetLastError();
+  s->l2_base = nullptr;
+  s->l2_bytes = 0;
+}
+
 extern "C" {
 
 msb_status msb_solver_create(msb_ctx ctx, msb_op op, const msb_level* levels, int32_t n_levels,
@@ -1160,7 +1238,7 @@ static void drop_graphs(msb_solver s) {
 static msb_status chunk_graph(msb_ctx ctx, msb_solver s, const double* db, int cur0, int n,
                               cudaGraphExec_t* out) {
   *out = nullptr;
-  std::vector<const void*> key = {db, s->res_dev, (const void*)(intptr_t)n};
+  std::vector<const void*> key = {db, s->res_dev, (const void*)(intptr_t)n, s->l2_base};
   for (msb_level L : s->levels) {
     key.push_back(L->P[L->cur]);
     key.push_back(L->co.Ainv);
@@ -1174,8 +1252,10 @@ static msb_status chunk_graph(msb_ctx ctx, msb_solver s, const double* db, int c
     *out = s->gexec[cur0];
     return MSB_OK;
   }
-  if (!s->cap_stream)
+  if (!s->cap_stream) {
     MSB_CUDA_TRY(ctx, cudaStreamCreateWithFlags(&s->cap_stream, cudaStreamNonBlocking));
+    if (s->l2_bytes) set_window(s->cap_stream, p_window(s));
+  }
   cudaStream_t user = ctx->stream;
   ctx->stream = s->cap_stream;
   int64_t l0 = g_launches.load();
@@ -1192,6 +1272,21 @@ static msb_status chunk_graph(msb_ctx ctx, msb_solver s, const double* db, int c
     s->pending_join = false;
     cudaGraph_t graph = nullptr;
     cudaError_t e2 = cudaStreamEndCapture(s->cap_stream, &graph);
+    if (!rc && e2 == cudaSuccess && s->l2_bytes) {
+      // stream attributes are not captured: put the P window on every kernel node
+      size_t nn = 0;
+      cudaGraphGetNodes(graph, nullptr, &nn);
+      std::vector<cudaGraphNode_t> nodes(nn);
+      if (nn) cudaGraphGetNodes(graph, nodes.data(), &nn);
+      cudaKernelNodeAttrValue kv{};
+      kv.accessPolicyWindow = p_window(s);
+      for (cudaGraphNode_t nd : nodes) {
+        cudaGraphNodeType ty;
+        if (cudaGraphNodeGetType(nd, &ty) == cudaSuccess && ty == cudaGraphNodeTypeKernel)
+          cudaGraphKernelNodeSetAttribute(nd, cudaKernelNodeAttributeAccessPolicyWindow, &kv);
+      }
+      cudaGetLastError();
+    }
     if (!rc && e2 == cudaSuccess) {
       e = cudaGraphInstantiate(&s->gexec[cur0], graph, 0);
     } else if (e2 != cudaSuccess) {
@@ -1236,6 +1331,12 @@ msb_status msb_ms_iterate(msb_ctx ctx, msb_solver s, const double* b, double* x,
   h.tol = tol;
   h.bscale = 1.0;
   MSB_CUDA_TRY(ctx, cudaMemcpyAsync(s->st, &h, sizeof(h), cudaMemcpyHostToDevice, st));
+  l2_begin(ctx, s);
+  struct L2Guard {
+    msb_ctx ctx;
+    msb_solver s;
+    ~L2Guard() { l2_end(ctx, s); }
+  } l2_guard{ctx, s};
   msb_status rc = enqueue_norm(ctx, s, s->xbuf[0], db, 1);
   if (rc) return rc;
   int cur = 0;
@@ -1397,6 +1498,9 @@ msb_status msb_solver_destroy(msb_solver s) {
 // z = M^{-1} v for FGMRES (fgmres.cu): one iteration of Eq. (8) over the solver's static
 // levels from x = 0 with right-hand side v (no stop test, no dynamic stage).
 namespace msb {
+void solver_l2_begin(msb_ctx ctx, msb_solver s) { l2_begin(ctx, s); }
+void solver_l2_end(msb_ctx ctx, msb_solver s) { l2_end(ctx, s); }
+
 msb_status solver_precondition(msb_ctx ctx, msb_solver s, const double* v, double* z) {
   cudaStream_t st = ctx->stream;
   const int64_t N = s->op->N;

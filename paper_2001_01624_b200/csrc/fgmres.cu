@@ -97,6 +97,12 @@ extern "C" msb_status msb_fgmres(msb_ctx ctx, msb_solver s, const double* b, dou
   void* ob = nullptr;
   const double* db = b ? (const double*)stage_in(ctx, b, N * sizeof(double), &ob) : op->q;
   if (!db) return set_error(ctx, MSB_ENOMEM, "rhs staging");
+  solver_l2_begin(ctx, s);
+  struct L2Guard {
+    msb_ctx ctx;
+    msb_solver s;
+    ~L2Guard() { solver_l2_end(ctx, s); }
+  } l2_guard{ctx, s};
   double *V, *Z, *w, *xd, *part, *dots;
   MSB_ALLOC(ctx, V, double, (size_t)(m + 1) * N);
   MSB_ALLOC(ctx, Z, double, (size_t)m * N);

@@ -14,6 +14,7 @@ lev.smooth(op, 12, prob.omega, -1.0)
 lev.assemble(op)
 s = Solver(ctx, op, [lev], prob.omega_s, prob.nu, prob.post_smooth)
 x = torch.zeros(prob.N, dtype=torch.float64, device="cuda")
-out = s.iterate(x, None, 1e-6, 100, 12)
+its = int(sys.argv[2]) if len(sys.argv) > 2 else 12
+out = s.iterate(x, None, 1e-6, max(100, its), its)
 torch.cuda.synchronize()
 print("ok", out["iters"], out["res"][-1])
