@@ -1127,6 +1127,24 @@ static msb_status enqueue_stage(msb_ctx ctx, msb_solver s, msb_level L, const do
     cur ^= 1;
     return MSB_OK;
   };
+  // fused Jacobi + residual, TMA z-marching (jacres_tma.cu, opt-in MSB_JQ=1): Cartesian
+  // level, pre-smoothing, ν = 1, grid and b TMA-compatible (even nx, 16-byte aligned b)
+  bool jq = false;
+  if (!jr && L->kind == 0 && !s->post && s->nu == 1 && s->no_fuse) {
+    if (!s->jq) s->jq = new JQPlan();
+    if (!s->jq->ok || s->jq->b != b || s->jq->x[0] != s->xbuf[0] || s->jq->x[1] != s->xbuf[1])
+      jacres_tma_plan(ctx, op, s->xbuf[0], s->xbuf[1], b, s->jq);
+    jq = s->jq->ok;
+  }
+  auto jqres = [&]() -> msb_status {
+    msb_status rc = jacres_tma_launch(ctx, op, *s->jq, cur, s->xbuf[cur ^ 1], s->r, s->omega_s,
+                                      first ? 1 : 0, s->partials, &s->st->done);
+    if (rc) return rc;
+    if (first && (rc = fin(s->jq->grid))) return rc;
+    first = false;
+    cur ^= 1;
+    return MSB_OK;
+  };
   auto jac = [&]() -> msb_status {
     for (int v = 0; v < s->nu; ++v) {
       k_jacobi<<<g4, CT, 0, st>>>(S, s->xbuf[cur], s->xbuf[cur ^ 1], b, s->omega_s, first ? 1 : 0,
@@ -1159,7 +1177,7 @@ static msb_status enqueue_stage(msb_ctx ctx, msb_solver s, msb_level L, const do
       return MSB_OK;
     }
     if (L->kind == 0) {
-      if (!jr) {
+      if (!jr && !jq) {
         k_residual<<<g4, CT, 0, st>>>(S, s->xbuf[cur], b, s->r, first ? 1 : 0, s->partials, s->st);
         MSB_LAUNCH_CHECK(ctx);
         if (first) {
@@ -1198,7 +1216,7 @@ static msb_status enqueue_stage(msb_ctx ctx, msb_solver s, msb_level L, const do
     if ((rc = corr())) return rc;
     if ((rc = jac())) return rc;
   } else {
-    if ((rc = jr ? jacres() : jac())) return rc;
+    if ((rc = jr ? jacres() : (jq ? jqres() : jac()))) return rc;
     if ((rc = corr())) return rc;
   }
   return MSB_OK;
@@ -1484,6 +1502,7 @@ msb_status msb_solver_destroy(msb_solver s) {
   dfree(ctx, s->bins);
   dfree(ctx, s->scratch_i);
   if (s->dyn_level) level_free(s->dyn_level);
+  delete s->jq;
   drop_graphs(s);
   if (s->cap_stream) cudaStreamDestroy(s->cap_stream);
   if (s->side_stream) cudaStreamDestroy(s->side_stream);
