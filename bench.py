@@ -68,12 +68,15 @@ def _traffic():
             if name.startswith(prefix):
                 return v
         return None
-    sw = find("k_sweep_tma")
+    sw = find("k_sweep_ws")
+    sw_bytes = None
+    if sw:  # the persistent sweep kernel runs a chunk of sweeps per launch: per sweep
+        sw_bytes = sw.get("per_unit", sw)["dram_bytes"]
     parts = [find(n) for n in CYCLE_KERNELS]
     cyc = None
     if all(p is not None for p in parts):
         cyc = sum(p["dram_bytes"] for p in parts)
-    return (sw["dram_bytes"] if sw else None), cyc
+    return sw_bytes, cyc
 
 
 def _dist():
@@ -323,7 +326,8 @@ def run_gpu(args):
                   "traffic": tr_iter, "algorithmic_bytes_per_launch": b_iter,
                   "launch_us": 1e6 * per_iter, "peak_source": src,
                   "traffic_source": "profiles/roofline_traffic.json (ncu --set full, cold cache)"}
-    roof_sweep = {"bound": "hbm", "kernel": "k_sweep_tma", "achieved": gbs_sweep, "peak": peak,
+    roof_sweep = {"bound": "hbm", "kernel": "k_sweep_ws (one sweep; launched in chunks of 32)",
+                  "achieved": gbs_sweep, "peak": peak,
                   "unit": "GB/s", "frac": gbs_sweep / peak, "traffic": tr_sweep,
                   "algorithmic_bytes_per_launch": b_sweep, "launch_us": 1e6 * per_sweep,
                   "peak_source": src}

@@ -14,7 +14,7 @@ timeout 900 python scripts/run_config.py 4 --steps 100 > $OUT/config4.json 2>&1
 timeout 300 python scripts/profile_step.py > $OUT/profile_plain.log 2>&1 &&
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
     --log-file $OUT/launches.csv python scripts/profile_step.py > $OUT/ncu_launch.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_sweep_tma -s 2 -c 1 \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_sweep -c 1 \
     -o $OUT/sweep python scripts/profile_step.py > $OUT/ncu_sweep.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on \
     -k regex:"k_jacobi|k_residual|k_restrict|k_symv|k_prolong|k_finalize" -s 35 -c 7 \

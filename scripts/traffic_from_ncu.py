@@ -3,7 +3,10 @@
 kernel name.  bench.py reads it to fill roofline.traffic (ncu replays are cold-cache:
 the bytes include compulsory misses that a warm in-graph launch may hit in L2).
 
-usage: python scripts/traffic_from_ncu.py <report.ncu-rep> [more.ncu-rep ...]
+usage: python scripts/traffic_from_ncu.py [--units KERNEL=N ...] <report.ncu-rep> [...]
+  --units k_sweep_ws=12: the captured launch of KERNEL processed N units (the persistent
+  sweep kernel runs a chunk of sweeps per launch); dram_bytes/duration are also given per
+  unit ("per_unit").
 """
 import csv
 import io
@@ -39,9 +42,25 @@ def read(path):
 
 if __name__ == "__main__":
     allk = {}
-    for p in sys.argv[1:]:
+    units = {}
+    args = sys.argv[1:]
+    paths = []
+    while args:
+        a = args.pop(0)
+        if a == "--units":
+            k, n = args.pop(0).split("=")
+            units[k] = int(n)
+        else:
+            paths.append(a)
+    for p in paths:
         allk.update(read(p))
-    doc = {"source": [os.path.relpath(p, ROOT) for p in sys.argv[1:]],
+    for name, a in allk.items():
+        for k, n in units.items():
+            if name.startswith(k):
+                a["units_per_launch"] = n
+                a["per_unit"] = {"dram_bytes": a["dram_bytes"] / n,
+                                 "duration_us": a["duration_us"] / n}
+    doc = {"source": [os.path.relpath(p, ROOT) for p in paths],
            "note": "ncu --set full --clock-control none, cold cache per replay; per-launch means",
            "kernels": allk}
     path = os.path.join(ROOT, "profiles", "roofline_traffic.json")

@@ -294,6 +294,21 @@ def test_cycle_parity(ctx, name):
         r_floor
 
 
+@pytest.mark.parametrize("shape", [(24, 44, 20), (26, 46, 23)])
+def test_cycle_fused_jacres_opt_in(ctx, shape, monkeypatch):
+    """The opt-in fused Jacobi + residual kernel (MSB_JQ=1, jacres_tma.cu) gives the
+    oracle's iterate: fixed 12 cycles on even-nx grids, ragged y tile and z chunks."""
+    prob = make_problem(2, shape=shape, max_sweeps=25)
+    orc = _oracle_full(prob, fixed_iters=12)
+    monkeypatch.setenv("MSB_JQ", "1")
+    g = _gpu_full(ctx, prob, fixed_iters=12)
+    monkeypatch.delenv("MSB_JQ")
+    xo = orc["sol"]["x"]
+    err = np.linalg.norm(g["x_host"] - xo) / np.linalg.norm(xo)
+    assert err <= X_RTOL, err
+    assert np.allclose(g["sol"]["res"], orc["sol"]["res"][:13], rtol=1e-9, atol=1e-12)
+
+
 def test_cycle_fixed_small_counts(ctx):
     """Exactly K cycles including K = 1 and a first residual check."""
     prob = random_problem(7, 16, 12, 5, (4, 4, 5), sigma=1.0, max_sweeps=30)
