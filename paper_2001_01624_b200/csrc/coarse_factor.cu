@@ -15,11 +15,22 @@
 //   A_c^{-1} = W^T W                             (GEMM over the nonzero K range, lower
 //                                                 tiles, then mirrored)
 //
-// so all O(M^3) work is in one register-blocked fp64 GEMM (128x128 tiles, 8x8 per
-// thread, double-buffered shared memory) and the leaves (n <= 64) are one-CTA kernels.
-// Flops: M^3/3 (chol) + M^3/3 (inverse of L) + M^3/3 (W^T W) = M^3.
+// so all O(M^3) work is in plain GEMM / SYRK products and the leaves (n <= 64) are
+// one-CTA kernels.  The products go to cuBLAS (DGEMM/DSYRK: 33-36 TFLOP/s fp64 on B200
+// at these sizes, scripts/probes/dgemm_probe.py) — plain library GEMMs — resolved at run
+// time with dlopen so the library has no link dependency; without it (or with
+// MSB_OWN_DGEMM=1) they run on k_dgemm below, a register-blocked fp64 GEMM (128x128
+// tiles, 8x8 per thread, double-buffered shared memory; lower-tile and triangular-K
+// variants for the symmetric products).  Either way every step runs on the GPU.
+// Flops: M^3/3 (chol) + M^3/3 (inverse of L) + M^3/3 (W^T W, triangular K range on
+// k_dgemm; the DSYRK form does not skip W's zero upper triangle: M^3) ~ M^3 .. 5M^3/3.
 // Pivot test: d_jj <= 1e-14 max|A_c| -> MSB_ESINGULAR.
+#include <dlfcn.h>
+
 #include <algorithm>
+#include <cstdlib>
+
+#include <cublas_v2.h>
 
 #include "internal.cuh"
 
@@ -132,6 +143,70 @@ __global__ void __launch_bounds__(256) k_dgemm(int m, int n, int K, double alpha
   }
 }
 
+// ---------------------------------------------------------------- cuBLAS (run-time bound)
+struct BlasApi {
+  bool ok = false;
+  cublasHandle_t h = nullptr;
+  decltype(&cublasSetStream_v2) set_stream = nullptr;
+  decltype(&cublasDgemm_v2) dgemm = nullptr;
+  decltype(&cublasDsyrk_v2) dsyrk = nullptr;
+};
+
+static BlasApi* blas(msb_ctx ctx) {
+  static BlasApi api[64];
+  static bool tried[64];
+  const int d = ctx->device;
+  if (d < 0 || d >= 64) return nullptr;
+  if (!tried[d]) {
+    tried[d] = true;
+    const char* own = getenv("MSB_OWN_DGEMM");
+    if (own && own[0] == '1') return nullptr;
+    void* lib = dlopen("libcublas.so.12", RTLD_NOW | RTLD_GLOBAL);
+    if (!lib) lib = dlopen("libcublas.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!lib) return nullptr;
+    auto create = reinterpret_cast<decltype(&cublasCreate_v2)>(dlsym(lib, "cublasCreate_v2"));
+    BlasApi& a = api[d];
+    a.set_stream = reinterpret_cast<decltype(&cublasSetStream_v2)>(dlsym(lib, "cublasSetStream_v2"));
+    a.dgemm = reinterpret_cast<decltype(&cublasDgemm_v2)>(dlsym(lib, "cublasDgemm_v2"));
+    a.dsyrk = reinterpret_cast<decltype(&cublasDsyrk_v2)>(dlsym(lib, "cublasDsyrk_v2"));
+    auto set_mode =
+        reinterpret_cast<decltype(&cublasSetMathMode)>(dlsym(lib, "cublasSetMathMode"));
+    if (!create || !a.set_stream || !a.dgemm || !a.dsyrk) return nullptr;
+    int prev = -1;
+    cudaGetDevice(&prev);
+    cudaSetDevice(d);
+    const bool made = create(&a.h) == CUBLAS_STATUS_SUCCESS;
+    if (prev >= 0) cudaSetDevice(prev);
+    if (!made) return nullptr;
+    if (set_mode) set_mode(a.h, CUBLAS_PEDANTIC_MATH);  // plain fp64, no emulation
+    a.ok = true;
+  }
+  return api[d].ok ? &api[d] : nullptr;
+}
+
+// Row-major C (m x n, ldc) = alpha op(A) op(B) + beta C on cuBLAS (column-major): the
+// same memory read column-major is the transpose, so C^T = op(B)^T op(A)^T.
+template <bool TA, bool TB>
+static bool blas_gemm(msb_ctx ctx, int m, int n, int K, double alpha, const double* A,
+                      int64_t lda, const double* B, int64_t ldb, double beta, double* C,
+                      int64_t ldc) {
+  BlasApi* b = blas(ctx);
+  if (!b || b->set_stream(b->h, ctx->stream) != CUBLAS_STATUS_SUCCESS) return false;
+  return b->dgemm(b->h, TB ? CUBLAS_OP_T : CUBLAS_OP_N, TA ? CUBLAS_OP_T : CUBLAS_OP_N, n, m, K,
+                  &alpha, B, (int)ldb, A, (int)lda, &beta, C, (int)ldc) == CUBLAS_STATUS_SUCCESS;
+}
+
+// Row-major lower triangle of C (n x n) = alpha X + beta C with X = A A^T (at = false,
+// A n x k) or X = A^T A (at = true, A k x n); the row-major lower triangle is the
+// column-major upper one.
+static bool blas_syrk(msb_ctx ctx, bool at, int n, int k, double alpha, const double* A,
+                      int64_t lda, double beta, double* C, int64_t ldc) {
+  BlasApi* b = blas(ctx);
+  if (!b || b->set_stream(b->h, ctx->stream) != CUBLAS_STATUS_SUCCESS) return false;
+  return b->dsyrk(b->h, CUBLAS_FILL_MODE_UPPER, at ? CUBLAS_OP_N : CUBLAS_OP_T, n, k, &alpha, A,
+                  (int)lda, &beta, C, (int)ldc) == CUBLAS_STATUS_SUCCESS;
+}
+
 constexpr size_t GEMM_SMEM = 2 * 2 * GK * (GB + GPAD) * sizeof(double);
 
 template <bool TA, bool TB>
@@ -139,6 +214,11 @@ static msb_status gemm(msb_ctx ctx, int m, int n, int K, double alpha, const dou
                        const double* B, int64_t ldb, double beta, double* C, int64_t ldc,
                        bool lower = false, bool tri_k = false) {
   if (m <= 0 || n <= 0) return MSB_OK;
+  if (!lower && !tri_k && K > 0 &&
+      blas_gemm<TA, TB>(ctx, m, n, K, alpha, A, lda, B, ldb, beta, C, ldc)) {
+    count_launch();
+    return MSB_OK;
+  }
   static bool attr = false;
   if (!attr) {
     MSB_CUDA_TRY(ctx, cudaFuncSetAttribute(k_dgemm<TA, TB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -278,7 +358,10 @@ static msb_status chol_inv(msb_ctx ctx, double* F, double* Wb, int64_t ld, int n
   k_copy2d<<<grid_for((int64_t)n2 * n1, 256), 256, 0, ctx->stream>>>(F21, ld, W21, ld, n2, n1);
   MSB_LAUNCH_CHECK(ctx);
   // A22 -= L21 L21^T (lower tiles)
-  if ((rc = gemm<false, true>(ctx, n2, n2, n1, -1.0, F21, ld, F21, ld, 1.0, F22, ld, true))) return rc;
+  if (blas_syrk(ctx, false, n2, n1, -1.0, F21, ld, 1.0, F22, ld))
+    count_launch();
+  else if ((rc = gemm<false, true>(ctx, n2, n2, n1, -1.0, F21, ld, F21, ld, 1.0, F22, ld, true)))
+    return rc;
   if ((rc = chol_inv(ctx, F22, W22, ld, n2, amax, sing))) return rc;
   // triangular inverse (LAPACK dtrtri): T^T = W11^T L21^T (n1 x n2) into the free upper
   // block F12;  W21 = -W22 T
@@ -326,7 +409,10 @@ msb_status coarse_factor_dense(msb_ctx ctx, Coarse& co) {
   // A_c^{-1} = W^T W: lower tiles with the K range restricted to the nonzeros of W,
   // written over the factor buffer (L is no longer needed), then mirrored; swap so
   // that co.Ainv holds the inverse and co.L the inverse factor W.
-  if ((rc = gemm<true, false>(ctx, M, M, M, 1.0, Wb, M, Wb, M, 0.0, F, M, true, true))) return rc;
+  if (blas_syrk(ctx, true, M, M, 1.0, Wb, M, 0.0, F, M))
+    count_launch();
+  else if ((rc = gemm<true, false>(ctx, M, M, M, 1.0, Wb, M, Wb, M, 0.0, F, M, true, true)))
+    return rc;
   dim3 g((M + 31) / 32, (M + 31) / 32);
   k_mirror_lower<<<g, dim3(32, 32), 0, s>>>(F, M);
   MSB_LAUNCH_CHECK(ctx);
