@@ -6,7 +6,8 @@
  * Calls follow BASELINE.json north_star's problem statement:
  *   build_tpfa(grid, K, wells)        -> msb_build_tpfa
  *   build_partition / build_support   -> msb_partition_cartesian, msb_level_create_cartesian,
- *                                        msb_level_create_split
+ *                                        msb_level_create_split; NEXT-3: msb_partition_wells,
+ *                                        msb_partition_indicator, msb_level_create_general
  *   smooth_basis(P, iters, w)         -> msb_smooth_basis
  *   coarse_assemble(R, A, P) -> A_c   -> msb_coarse_assemble
  *   add_dynamic_basis(dp)             -> msb_add_dynamic_basis
@@ -135,6 +136,33 @@ msb_status msb_level_create_split(msb_ctx ctx, msb_op op, msb_level parent, msb_
  * (PAPER.md:260 caption).  part host|dev int32[N], values in [0, M). */
 msb_status msb_level_create_constant(msb_ctx ctx, msb_op op, const int32_t* part, int32_t M,
                                      msb_level* out);
+/* ---------------------------------------------------------------- static partitions (§8 NEXT-3)
+ * Well partition ("one for each well plus one to ensure partition of unity";
+ * SPEC.md:410-416; reading B9): well w owns the cells whose Chebyshev index distance to its
+ * nearest perforation is <= radius (a cell in reach of several wells joins the nearest,
+ * ties to the lower well index); block n_wells holds every other cell and is omitted when
+ * empty.  perf_ptr host int32[n_wells+1] (CSR offsets into perf_cells), perf_cells host
+ * int32[perf_ptr[n_wells]] cell indices; part host|dev int32[N] out; M_out host.
+ * Errors: MSB_EINVAL for radius < 0, a well without perforations or a cell outside the grid. */
+msb_status msb_partition_wells(msb_ctx ctx, const msb_grid* grid, const int32_t* perf_ptr,
+                               const int32_t* perf_cells, int32_t n_wells, int32_t radius,
+                               int32_t* part, int32_t* M_out);
+/* Indicator partition ("agglomerates cells into coarse blocks based on a
+ * flow indicator"; reading B10): bin_i = #{e : edges[e] <= |ind_i|}
+ * (absolute edges, strictly increasing, n_edges <= 8), connected components of equal bins
+ * over the grid faces, components below s_min merged into one block per bin with s_min
+ * doubling from 1 until at most max_blocks blocks remain (the dynamic stage's rule, A15);
+ * numbered by ascending minimum cell.  ind host|dev double[N]; part host|dev int32[N] out. */
+msb_status msb_partition_indicator(msb_ctx ctx, msb_op op, const double* ind, const double* edges,
+                                   int32_t n_edges, int32_t max_blocks, int32_t* part,
+                                   int32_t* M_out);
+/* Level on a general partition (§8 NEXT-3; reading B8): supports
+ * S_j = block j dilated by `halo` layers of the graph of A_T (faces with base T > 0),
+ * explicit ELL pattern with ascending columns (at most 16 per cell, else MSB_EINVAL),
+ * P := constant basis of the partition (P^0), ready for msb_smooth_basis (halo 0: the
+ * constant-basis level).  part host|dev int32[N], values in [0, M). */
+msb_status msb_level_create_general(msb_ctx ctx, msb_op op, const int32_t* part, int32_t M,
+                                    int32_t halo, msb_level* out, int64_t* nnz_out);
 /* Level facts: M, nnz, slot width W (planes), and the partition (host|dev int32[N], may be NULL). */
 msb_status msb_level_info(msb_ctx ctx, msb_level lev, int32_t* M, int64_t* nnz, int32_t* W,
                           int32_t* part);

@@ -87,6 +87,58 @@ def dynamic_partition(dp, nx, ny, nz, edges=(0.1, 0.5), max_blocks=1024):
     bins, m = dp_bins(dp, edges)
     if m == 0.0:
         return None, 0
+    return _bin_components(bins, nx, ny, nz, max_blocks)
+
+
+def indicator_partition(ind, nx, ny, nz, edges, max_blocks=1024):
+    """NEXT-3 static partition from a per-cell indicator ("agglomerates
+    cells into coarse blocks based on a flow indicator"): bin_i =
+    #{e in edges : e <= |ind_i|} with ABSOLUTE edges (reading B10), then the same
+    components and small-component rule as the dynamic partition (A15)."""
+    edges = list(edges)
+    if any(b <= a for a, b in zip(edges, edges[1:])):
+        raise ValueError("edges must be strictly increasing")
+    a = np.abs(np.asarray(ind, dtype=np.float64))
+    bins = np.zeros(len(a), dtype=np.int64)
+    for e in edges:
+        bins += (a >= e)
+    return _bin_components(bins, nx, ny, nz, max_blocks)
+
+
+def wells_partition(nx, ny, nz, wells, radius):
+    """NEXT-3 well partition ("one for each well plus one to ensure
+    partition of unity"; reading B9): block w holds the cells whose
+    Chebyshev index distance to the nearest perforation of well w is <= radius; a cell
+    in reach of several wells joins the nearest, ties to the lower well index; block
+    n_w holds every other cell and is omitted when empty.  Returns (part, M)."""
+    if radius < 0:
+        raise ValueError("radius must be >= 0")
+    N = nx * ny * nz
+    c = np.arange(N)
+    i, j, k = c % nx, (c // nx) % ny, c // (nx * ny)
+    best = np.full(N, np.iinfo(np.int64).max)
+    owner = np.full(N, -1, dtype=np.int64)
+    for w, cells in enumerate(wells):
+        cells = np.asarray(cells, dtype=np.int64)
+        if len(cells) == 0 or cells.min() < 0 or cells.max() >= N:
+            raise ValueError("well outside the grid or without perforations")
+        d = np.full(N, np.iinfo(np.int64).max)
+        for q in cells:
+            qi, qj, qk = q % nx, (q // nx) % ny, q // (nx * ny)
+            d = np.minimum(d, np.maximum(np.maximum(np.abs(i - qi), np.abs(j - qj)), np.abs(k - qk)))
+        take = d < best  # strict: an equal distance keeps the lower well index
+        best[take] = d[take]
+        owner[take] = w
+    n_w = len(wells)
+    part = np.where(best <= radius, owner, n_w)
+    M = n_w + int(np.any(part == n_w))
+    return part, M
+
+
+def _bin_components(bins, nx, ny, nz, max_blocks):
+    """Connected components of equal-bin cells over the grid faces, components smaller
+    than s_min merged into one block per bin, s_min doubling from 1 until at most
+    max_blocks blocks remain (A15); canonical numbering."""
     N = nx * ny * nz
     faces = all_faces(nx, ny, nz)
     left = np.concatenate([f[0] for f in faces])

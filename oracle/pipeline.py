@@ -35,6 +35,29 @@ def split_level(prob, A_T, cart, sweeps=None, fixed=None):
     return dict(part=spart, M=Ms, pattern=pat, P=P, sweeps=n, deltas=deltas)
 
 
+def general_level(prob, A_T, part, M, halo, sweeps=None, fixed=None):
+    """NEXT-3 level on a general partition: MsRSB from the constant basis on the
+    dilated supports."""
+    pat = _sup.dilated_pattern(part, M, A_T, halo)
+    P0 = _basis.indicator(np.asarray(part, dtype=np.int64), pat)
+    ms = prob.max_sweeps if sweeps is None else sweeps
+    fx = prob.fixed_sweeps if fixed is None else fixed
+    P, n, deltas = _basis.smooth(P0, A_T, prob.omega, ms, prob.sweep_tol, fx)
+    return dict(part=np.asarray(part, dtype=np.int64), M=M, pattern=pat, P=P, sweeps=n,
+                deltas=deltas)
+
+
+def static_partition(prob, spec):
+    """Partition of one NEXT-3 static level spec (synth.Problem.static_levels)."""
+    if spec["kind"] == "wells":
+        return _part.wells_partition(prob.nx, prob.ny, prob.nz, prob.wells(), spec["radius"])
+    if spec["kind"] == "indicator":
+        return _part.indicator_partition(prob.indicator(spec.get("field", "logk")), prob.nx,
+                                         prob.ny, prob.nz, spec["edges"],
+                                         spec.get("max_blocks", 1024))
+    raise ValueError(f"unknown static level kind {spec['kind']!r}")
+
+
 def run(prob, sweeps=None, fixed_sweeps=None, fixed_iters=None, max_iter=None,
         record_dynamic=False, x0=None):
     A_T, A, q, trans = _tpfa.build(prob)
@@ -42,6 +65,9 @@ def run(prob, sweeps=None, fixed_sweeps=None, fixed_iters=None, max_iter=None,
     levels_info = [cart]
     if prob.split_level:
         levels_info.append(split_level(prob, A_T, cart, sweeps, fixed_sweeps))
+    for spec in prob.static_levels:  # NEXT-3 (reading B11: after the general levels)
+        part, M = static_partition(prob, spec)
+        levels_info.append(general_level(prob, A_T, part, M, spec["halo"], sweeps, fixed_sweeps))
     levels = [Level(li["P"].matrix(), A) for li in levels_info]
     dyn = None
     if prob.dynamic:

@@ -125,6 +125,25 @@ def flood_pattern(prob, parent_part, parent_pattern, split_part, Ms):
     return _pattern_from_pairs(rows, cols, N, Ms)
 
 
+def dilated_pattern(part, M, A_T, halo):
+    """NEXT-3 supports of a general partition (requirement 2 of
+    PAPER.md:220; reading B8): S_j = Ω_j dilated by `halo` layers of the graph of A_T
+    (cells joined by a face with T != 0, so a sealing fault also bounds the support)."""
+    N = len(part)
+    part = np.asarray(part, dtype=np.int64)
+    S = sp.csr_matrix((np.ones(N), (np.arange(N), part)), shape=(N, M))
+    G = sp.csr_matrix(A_T, copy=True)
+    G.eliminate_zeros()  # a face with T = 0 is no edge
+    G.data[:] = 1.0
+    G = (G + sp.identity(N, format="csr")).tocsr()
+    for _ in range(halo):
+        S = (G @ S).tocsr()
+        S.data[:] = 1.0
+    S.eliminate_zeros()
+    S.sort_indices()
+    return S.astype(np.int8)
+
+
 def check_requirements(part, pattern):
     """Requirement 1–2 checks: every cell's own block column is
     in its row of the pattern.  Returns the number of violations."""

@@ -46,6 +46,9 @@ SIGNATURES = {
     "msb_level_create_cartesian": (i32, [p, p, i32, i32, i32, C.POINTER(p), pi64]),
     "msb_level_create_split": (i32, [p, p, p, C.POINTER(p), pi64]),
     "msb_level_create_constant": (i32, [p, p, p, i32, C.POINTER(p)]),
+    "msb_partition_wells": (i32, [p, C.POINTER(Grid), p, p, i32, i32, p, pi32]),
+    "msb_partition_indicator": (i32, [p, p, p, p, i32, i32, p, pi32]),
+    "msb_level_create_general": (i32, [p, p, p, i32, i32, C.POINTER(p), pi64]),
     "msb_level_info": (i32, [p, p, pi32, pi64, pi32, p]),
     "msb_level_export": (i32, [p, p, p, p, p, p]),
     "msb_level_import_values": (i32, [p, p, p]),

@@ -188,6 +188,32 @@ def partition_cartesian(ctx: Context, nx, ny, nz, block, part_out=None):
     return M.value
 
 
+def partition_wells(ctx: Context, nx, ny, nz, wells, radius, part_out=None):
+    """NEXT-3 well partition (msb_partition_wells); wells: sequence of cell-index arrays.
+    Returns (part int32[N], M)."""
+    g = _grid(nx, ny, nz)
+    ptr = np.zeros(len(wells) + 1, dtype=np.int32)
+    ptr[1:] = np.cumsum([len(w) for w in wells])
+    cells = np.ascontiguousarray(np.concatenate([np.asarray(w) for w in wells]), dtype=np.int32)
+    part = np.empty(nx * ny * nz, dtype=np.int32) if part_out is None else part_out
+    M = C.c_int32()
+    ctx.check(ctx.lib.msb_partition_wells(ctx.h, C.byref(g), _ptr(ptr, np.int32),
+                                          _ptr(cells, np.int32), len(wells), int(radius),
+                                          _ptr(part, np.int32), C.byref(M)), "msb_partition_wells")
+    return part, M.value
+
+
+def partition_indicator(ctx: Context, op: "Operator", ind, edges, max_blocks=1024, part_out=None):
+    """NEXT-3 indicator partition (msb_partition_indicator).  Returns (part int32[N], M)."""
+    e = np.ascontiguousarray(edges, dtype=np.float64)
+    part = np.empty(op.N, dtype=np.int32) if part_out is None else part_out
+    M = C.c_int32()
+    ctx.check(ctx.lib.msb_partition_indicator(ctx.h, op.h, _ptr(ind), _ptr(e) if len(e) else None,
+                                              len(e), int(max_blocks), _ptr(part, np.int32),
+                                              C.byref(M)), "msb_partition_indicator")
+    return part, M.value
+
+
 class Level:
     """A (P, R = P^T, A_c) triple on one coarse partition."""
 
@@ -222,6 +248,18 @@ class Level:
         h = C.c_void_p()
         ctx.check(ctx.lib.msb_level_create_constant(ctx.h, op.h, _ptr(part, np.int32), int(M),
                                                     C.byref(h)), "msb_level_create_constant")
+        lev = cls(ctx, h)
+        lev.N = op.N
+        return lev
+
+    @classmethod
+    def general(cls, ctx: Context, op: Operator, part, M: int, halo: int):
+        """NEXT-3 level on a general partition: supports = blocks dilated by `halo` layers."""
+        h = C.c_void_p()
+        nnz = C.c_int64()
+        ctx.check(ctx.lib.msb_level_create_general(ctx.h, op.h, _ptr(part, np.int32), int(M),
+                                                   int(halo), C.byref(h), C.byref(nnz)),
+                  "msb_level_create_general")
         lev = cls(ctx, h)
         lev.N = op.N
         return lev

@@ -356,6 +356,49 @@ __global__ void __launch_bounds__(CT) k_res_restrict(StencilT S, LevelView L,
   if (first) warp_partial(r * r, partials);
 }
 
+// a6 + a8 for explicit levels with few columns (M <= RRS_MAX_M: well, indicator and
+// dynamic partitions): the warp-segmented sums go to a per-CTA shared-memory copy of r_c
+// and each CTA adds its nonzero entries to global memory once, instead of one global
+// atomic per warp segment — with M = 6 (the well level) those ~70k atomics all hit six
+// addresses.  Grid-stride over cells with a fixed grid (rrs_grid()).
+constexpr int RRS_MAX_M = 4096;
+__global__ void __launch_bounds__(CT) k_res_restrict_small(StencilT S, LevelView L, int M,
+                                                           const double* __restrict__ x,
+                                                           const double* __restrict__ b,
+                                                           double* __restrict__ rc, int first,
+                                                           double* __restrict__ partials,
+                                                           const IterState* st) {
+  if (is_done(st)) return;
+  extern __shared__ double rsm[];
+  for (int m = threadIdx.x; m < M; m += blockDim.x) rsm[m] = 0.0;
+  __syncthreads();
+  const int N = S.g.nxy * S.g.nz;
+  const int stride = gridDim.x * blockDim.x;
+  double v2 = 0.0;
+  for (int base = blockIdx.x * blockDim.x; base < N; base += stride) {  // warp-uniform
+    const int c = base + threadIdx.x;
+    const bool in = c < N;
+    const int cc = in ? c : N - 1;
+    int i, j, k;
+    g3_coords(S.g, cc, i, j, k);
+    double r = 0.0;
+    if (in) {
+      double dA;
+      r = residual_at(S, x, b, c, i, j, k, &dA);
+    }
+    v2 += r * r;
+    for (int s2 = 0; s2 < L.W; ++s2) {
+      const int key = in ? L.col[(size_t)s2 * N + c] : -1;
+      const double v = key >= 0 ? L.P[(size_t)s2 * N + c] * r : 0.0;
+      warp_segmented_add(key, v, rsm);
+    }
+  }
+  __syncthreads();
+  for (int m = threadIdx.x; m < M; m += blockDim.x)
+    if (rsm[m] != 0.0) atomicAdd(rc + m, rsm[m]);
+  if (first) warp_partial(v2, partials);
+}
+
 // a9: x += P xc (row gather).
 __global__ void __launch_bounds__(CT) k_prolong(LevelView L, double* __restrict__ x,
                                                 const double* __restrict__ xc,
@@ -811,6 +854,21 @@ __global__ void k_merge_label(int32_t* __restrict__ lab, const int32_t* __restri
   out[c] = cnt[r] < smin ? rep[bins[c]] : r;
 }
 
+// NEXT-3 indicator partition: bin = #{e : edges[e] <= |ind|} (absolute edges)
+struct BinEdges {
+  int n;
+  double v[8];
+};
+__global__ void k_bins_abs(const double* __restrict__ ind, int64_t N, BinEdges E,
+                           int32_t* __restrict__ bins) {
+  int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= N) return;
+  const double a = fabs(ind[c]);
+  int b = 0;
+  for (int e = 0; e < E.n; ++e) b += a >= E.v[e];
+  bins[c] = b;
+}
+
 __global__ void k_refill_const(const int32_t* __restrict__ part, int64_t N, int32_t* __restrict__ col,
                                double* __restrict__ P) {
   int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -1198,11 +1256,19 @@ static msb_status enqueue_stage(msb_ctx ctx, msb_solver s, msb_level L, const do
     }
     k_zero_if<<<grid_for(L->M, 256), 256, 0, st>>>(s->rc, L->M, s->st);
     MSB_LAUNCH_CHECK(ctx);
-    k_res_restrict<<<g, CT, 0, st>>>(S, V, s->xbuf[cur], b, s->rc, first ? 1 : 0, s->partials,
-                                     s->st);
+    unsigned gpart = g;  // blocks that write stop-test partials
+    static const bool no_small = getenv("MSB_NO_RRS") != nullptr;
+    if (L->kind == 1 && L->M <= RRS_MAX_M && !no_small) {
+      gpart = (unsigned)std::min<int64_t>(g, 4 * ctx->sm_count);
+      k_res_restrict_small<<<gpart, CT, (size_t)L->M * sizeof(double), st>>>(
+          S, V, L->M, s->xbuf[cur], b, s->rc, first ? 1 : 0, s->partials, s->st);
+    } else {
+      k_res_restrict<<<g, CT, 0, st>>>(S, V, s->xbuf[cur], b, s->rc, first ? 1 : 0, s->partials,
+                                       s->st);
+    }
     MSB_LAUNCH_CHECK(ctx);
     if (first) {
-      msb_status rc = fin(g);
+      msb_status rc = fin(gpart);
       if (rc) return rc;
     }
     first = false;
@@ -1322,6 +1388,74 @@ static msb_status chunk_graph(msb_ctx ctx, msb_solver s, const double* db, int c
     return set_error(ctx, MSB_ECUDA, "graph capture: %s", cudaGetErrorString(e));
   }
   *out = s->gexec[cur0];
+  return MSB_OK;
+}
+
+msb_status msb_partition_indicator(msb_ctx ctx, msb_op op, const double* ind, const double* edges,
+                                   int32_t n_edges, int32_t max_blocks, int32_t* part,
+                                   int32_t* M_out) {
+  if (!ctx || !op || !ind || !M_out || n_edges < 0 || n_edges > 8 || (n_edges && !edges) ||
+      max_blocks < 1)
+    return set_error(ctx, MSB_EINVAL, "msb_partition_indicator: args");
+  BinEdges E{};
+  E.n = n_edges;
+  for (int e = 0; e < n_edges; ++e) {
+    E.v[e] = edges[e];
+    if (e > 0 && !(edges[e] > edges[e - 1]))
+      return set_error(ctx, MSB_EINVAL, "msb_partition_indicator: edges not strictly increasing");
+  }
+  const int64_t N = op->N;
+  const int nbin = n_edges + 1;
+  cudaStream_t st = ctx->stream;
+  void* o = nullptr;
+  const double* d = (const double*)stage_in(ctx, ind, N * sizeof(double), &o);
+  if (!d) return set_error(ctx, MSB_ENOMEM, "indicator staging");
+  int32_t *bins, *lab, *ids, *cnt, *scr;
+  MSB_ALLOC(ctx, bins, int32_t, N);
+  MSB_ALLOC(ctx, lab, int32_t, N);
+  MSB_ALLOC(ctx, ids, int32_t, N);
+  MSB_ALLOC(ctx, cnt, int32_t, 2 * N);
+  MSB_ALLOC(ctx, scr, int32_t, 2 * nbin + 2);
+  int32_t* counts = scr;         // [0] roots >= s_min, [1 + b] bin b has a small component
+  int32_t* rep = scr + nbin + 1;  // per bin: minimum cell of its small components
+  k_bins_abs<<<grid_for(N, 256), 256, 0, st>>>(d, N, E, bins);
+  MSB_LAUNCH_CHECK(ctx);
+  msb_status rc = cc_label(ctx, op, bins, lab, false, nullptr);
+  if (rc) return rc;
+  MSB_CUDA_TRY(ctx, cudaMemsetAsync(cnt, 0, N * sizeof(int32_t), st));
+  k_sizes<<<grid_for(N, 256), 256, 0, st>>>(lab, N, cnt);
+  MSB_LAUNCH_CHECK(ctx);
+  int smin = 1;
+  std::vector<int32_t> hc(nbin + 1);
+  while (true) {  // s_min doubles until at most max_blocks blocks remain (A15)
+    MSB_CUDA_TRY(ctx, cudaMemsetAsync(counts, 0, (nbin + 1) * sizeof(int32_t), st));
+    k_merge_count<<<grid_for(N, 256), 256, 0, st>>>(lab, cnt, bins, N, smin, counts);
+    MSB_LAUNCH_CHECK(ctx);
+    MSB_CUDA_TRY(ctx, cudaMemcpyAsync(hc.data(), counts, hc.size() * sizeof(int32_t),
+                                      cudaMemcpyDeviceToHost, st));
+    MSB_CUDA_TRY(ctx, cudaStreamSynchronize(st));
+    int64_t nb = 0;
+    for (int32_t v : hc) nb += v;
+    if (nb <= max_blocks || (int64_t)smin > N) break;
+    smin *= 2;
+  }
+  std::vector<int32_t> big(nbin, INT32_MAX);
+  MSB_CUDA_TRY(ctx, cudaMemcpyAsync(rep, big.data(), nbin * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+  k_merge_rep<<<grid_for(N, 256), 256, 0, st>>>(lab, cnt, bins, N, smin, rep);
+  MSB_LAUNCH_CHECK(ctx);
+  k_merge_label<<<grid_for(N, 256), 256, 0, st>>>(lab, cnt, bins, N, smin, rep, ids);
+  MSB_LAUNCH_CHECK(ctx);
+  int32_t M = 0;
+  if ((rc = canonical_number(ctx, N, ids, lab, cnt, &M))) return rc;
+  if (part) MSB_CUDA_TRY(ctx, copy_out(ctx, part, lab, N * sizeof(int32_t)));
+  MSB_CUDA_TRY(ctx, cudaStreamSynchronize(st));
+  dfree(ctx, bins);
+  dfree(ctx, lab);
+  dfree(ctx, ids);
+  dfree(ctx, cnt);
+  dfree(ctx, scr);
+  if (o) dfree(ctx, o);
+  *M_out = M;
   return MSB_OK;
 }
 

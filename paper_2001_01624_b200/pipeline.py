@@ -5,7 +5,7 @@ from __future__ import annotations
 
 import numpy as np
 
-from .api import Context, Level, Operator, Solver
+from .api import Context, Level, Operator, Solver, partition_indicator, partition_wells
 
 
 def problem_K(prob):
@@ -42,9 +42,25 @@ def build_levels(ctx: Context, op: Operator, prob, sweeps=None, fixed=None):
         # the split level starts from its own indicator (O6) and is smoothed the same way
         info.append(sp.smooth(op, ms, prob.omega, tol))
         levels.append(sp)
+    for spec in prob.static_levels:  # NEXT-3, after the general levels (reading B11)
+        part, M = static_partition(ctx, op, prob, spec)
+        lv = Level.general(ctx, op, part, M, spec["halo"])
+        info.append(lv.smooth(op, ms, prob.omega, tol))
+        levels.append(lv)
     for lv in levels:
         lv.assemble(op)
     return levels, info
+
+
+def static_partition(ctx: Context, op: Operator, prob, spec):
+    """Partition of one NEXT-3 static level spec on the GPU; inputs (well perforations,
+    the indicator field) come from the problem definition (synth)."""
+    if spec["kind"] == "wells":
+        return partition_wells(ctx, prob.nx, prob.ny, prob.nz, prob.wells(), spec["radius"])
+    if spec["kind"] == "indicator":
+        ind = np.ascontiguousarray(prob.indicator(spec.get("field", "logk")), dtype=np.float64)
+        return partition_indicator(ctx, op, ind, spec["edges"], spec.get("max_blocks", 1024))
+    raise ValueError(f"unknown static level kind {spec['kind']!r}")
 
 
 def make_solver(ctx: Context, op: Operator, levels, prob):

@@ -77,6 +77,36 @@ def config_single(cfg, args):
     print(json.dumps(rec), flush=True)
 
 
+def config_static(cfg, args):
+    """Config `cfg` solved with and without the NEXT-3 static levels (wells, MsRSB halo 2;
+    log-permeability indicator, constant basis): iterations and solve time."""
+    ctx = Context(0)
+    st = torch.cuda.current_stream()
+    W = {"kind": "wells", "radius": 2, "halo": 2}
+    I = {"kind": "indicator", "edges": (1.0, 2.5), "halo": 0, "max_blocks": 1024}
+    recs = []
+    for name, sl in (("cartesian", ()), ("cartesian+wells+logk", (W, I))):
+        prob = make_problem(cfg, static_levels=sl)
+        e0 = ev(st)
+        op = gp.build_operator(ctx, prob)
+        levels, info = gp.build_levels(ctx, op, prob)
+        e1 = ev(st)
+        s = gp.make_solver(ctx, op, levels, prob)
+        x = torch.zeros(prob.N, dtype=torch.float64, device="cuda")
+        s.iterate(x, None, prob.cycle_tol, prob.max_iter, 0)  # warm-up (graph capture)
+        x.zero_()
+        e2 = ev(st)
+        out = s.iterate(x, None, prob.cycle_tol, prob.max_iter, 0)
+        e3 = ev(st)
+        torch.cuda.synchronize()
+        recs.append(dict(levels=name, M=[lv.info()["M"] for lv in levels],
+                         sweeps=[i[0] for i in info], iters=out["iters"],
+                         converged=out["converged"], setup_ms=e0.elapsed_time(e1),
+                         solve_ms=e2.elapsed_time(e3),
+                         ms_per_iteration=e2.elapsed_time(e3) / max(1, out["iters"])))
+    print(json.dumps(dict(config=cfg, static_levels=recs)), flush=True)
+
+
 def config4(args):
     prob = make_problem(4)
     ctx = Context(0)
@@ -97,8 +127,11 @@ if __name__ == "__main__":
     ap.add_argument("--iters", type=int, default=0)
     ap.add_argument("--sweeps", type=int, default=0)
     ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--static", action="store_true", help="NEXT-3 static levels vs none")
     a = ap.parse_args()
-    if a.config == 4:
+    if a.static:
+        config_static(a.config, a)
+    elif a.config == 4:
         config4(a)
     else:
         config_single(a.config, a)

@@ -50,6 +50,9 @@ class Problem:
     fixed_iters: int = 0                  # config 5: exactly 20 iterations
     dyn_edges: tuple = (0.1, 0.5)
     dyn_max_blocks: int = 1024
+    # NEXT-3 static levels after the general ones, e.g. ({"kind": "wells", "radius": 2,
+    # "halo": 2}, {"kind": "indicator", "edges": (1.0,), "halo": 1, "max_blocks": 512})
+    static_levels: tuple = ()
 
     @property
     def N(self) -> int:
@@ -59,6 +62,23 @@ class Problem:
     def n_faces(self) -> int:
         nx, ny, nz = self.nx, self.ny, self.nz
         return (nx - 1) * ny * nz + nx * (ny - 1) * nz + nx * ny * (nz - 1)
+
+    def wells(self):
+        """Perforated cells grouped into wells: one well per (i, j) column of source
+        cells (fully penetrating 5-spot columns; a 2D source cell is its own well),
+        in order of first appearance."""
+        cols = {}
+        for c in self.src_cells.tolist():
+            key = c % (self.nx * self.ny)
+            cols.setdefault(key, []).append(c)
+        return [np.array(v, dtype=np.int64) for v in cols.values()]
+
+    def indicator(self, field="logk"):
+        """Per-cell static indicator: "logk" = log10(kx / min kx) >= 0 (the permeability
+        flow indicator of PAPER.md:360)."""
+        if field != "logk":
+            raise ValueError(field)
+        return np.log10(self.kx / self.kx.min())
 
     def rhs(self) -> np.ndarray:
         q = np.zeros(self.N)

@@ -734,3 +734,105 @@ def test_fgmres_parity(ctx, name):
     err = np.linalg.norm(x.cpu().numpy() - ref["x"]) / np.linalg.norm(ref["x"])
     assert err <= max(X_RTOL, 2.0 * max(floors)), (err, floors)
     assert np.allclose(out["res"][:5], free["res"][:5], rtol=1e-7, atol=1e-12)
+
+
+# ---------------------------------------------------------------- §8 NEXT-3: static levels
+def test_partition_wells_parity(ctx):
+    """Bit-exact well partitions (msb_partition_wells vs oracle.partition.wells_partition)."""
+    from oracle import partition as opart
+    from paper_2001_01624_b200.api import partition_wells
+    p = make_problem(2, shape=(24, 44, 20))
+    rng = np.random.default_rng(7)
+    rw = [rng.choice(7 * 6 * 5, size=int(rng.integers(1, 4)), replace=False) for _ in range(3)]
+    cases = [(p.nx, p.ny, p.nz, p.wells(), r) for r in (0, 2, 5)] + \
+            [(7, 6, 5, rw, r) for r in (0, 1, 3)] + [(9, 1, 1, [np.array([2]), np.array([6])], 2)]
+    for nx, ny, nz, wells, r in cases:
+        po, Mo = opart.wells_partition(nx, ny, nz, wells, r)
+        pg, Mg = partition_wells(ctx, nx, ny, nz, wells, r)
+        assert Mg == Mo and np.array_equal(pg, po.astype(np.int32)), (nx, ny, nz, r)
+
+
+def test_partition_indicator_parity(ctx):
+    """Bit-exact indicator partitions incl. the small-component merge (max_blocks)."""
+    from oracle import partition as opart
+    from paper_2001_01624_b200.api import partition_indicator
+    from paper_2001_01624_b200.pipeline import build_operator
+    p = make_problem(2, shape=(24, 44, 20))
+    op = build_operator(ctx, p)
+    rng = np.random.default_rng(9)
+    cases = [(p.indicator(), (1.0, 2.5), 1024), (p.indicator(), (1.0,), 4),
+             (rng.standard_normal(p.N) ** 3, (0.5, 2.0), 1024),
+             (rng.standard_normal(p.N) ** 3, (0.5, 2.0), 40), (np.full(p.N, 2.0), (1.0,), 10),
+             (rng.uniform(0, 1, p.N), (), 10)]
+    for ind, edges, mb in cases:
+        po, Mo = opart.indicator_partition(ind, p.nx, p.ny, p.nz, edges, mb)
+        pg, Mg = partition_indicator(ctx, op, np.ascontiguousarray(ind), edges, mb)
+        assert Mg == Mo and np.array_equal(pg, po.astype(np.int32)), (edges, mb)
+
+
+GENERAL_CASES = {
+    "wells_halo2": (lambda: make_problem(2, shape=(24, 44, 20)), {"kind": "wells", "radius": 2, "halo": 2}),
+    "indicator_halo1": (lambda: make_problem(2, shape=(24, 44, 20)),
+                        {"kind": "indicator", "edges": (1.0, 2.5), "halo": 1, "max_blocks": 256}),
+    "ragged_wells_halo3": (lambda: random_problem(6, 23, 17, 7, (5, 4, 3), sigma=1.5),
+                           {"kind": "wells", "radius": 1, "halo": 3}),
+    "indicator_halo0": (lambda: make_problem(2, shape=(24, 44, 20)),
+                        {"kind": "indicator", "edges": (1.0, 2.5), "halo": 0, "max_blocks": 256}),
+}
+
+
+@pytest.mark.parametrize("name", list(GENERAL_CASES))
+def test_general_level_parity(ctx, name):
+    """msb_level_create_general + msb_smooth_basis + msb_coarse_assemble vs the oracle's
+    dilated pattern and MsRSB smoothing: pattern exact, values <= 1e-10 after 25 fixed
+    sweeps, A_c to 1e-12 of max|A_c|."""
+    from oracle import pipeline as opl
+    from paper_2001_01624_b200 import pipeline as gp
+    from paper_2001_01624_b200.api import Level
+    prob, spec = GENERAL_CASES[name][0](), GENERAL_CASES[name][1]
+    A_T, A, q, _ = tpfa_build(prob)
+    part, M = opl.static_partition(prob, spec)
+    li = opl.general_level(prob, A_T, part, M, spec["halo"], sweeps=25, fixed=True)
+    op = gp.build_operator(ctx, prob)
+    lv = Level.general(ctx, op, part.astype(np.int32), M, spec["halo"])
+    n, last, deltas, _ = lv.smooth(op, 25, prob.omega, -1.0)
+    assert n == 25
+    rowptr, cols, vals, _ = lv.export()
+    _assert_P(rowptr, cols, vals, li["P"])
+    assert np.allclose(deltas[:25], li["deltas"], rtol=1e-9, atol=1e-15)
+    lv.assemble(op)
+    _, _, _, Ac = lv.export(with_Ac=True)
+    from oracle.coarse import galerkin
+    Ao = galerkin(li["P"].matrix(), A)
+    Ao = Ao.toarray() if hasattr(Ao, "toarray") else np.asarray(Ao)
+    assert np.max(np.abs(Ac - Ao)) <= 1e-12 * np.max(np.abs(Ao))
+
+
+def tpfa_build(prob):
+    from oracle import tpfa
+    return tpfa.build(prob)
+
+
+def test_static_levels_cycle_parity(ctx):
+    """Cartesian + well (MsRSB, halo 2) + permeability-indicator (constant basis) stages:
+    free-mode counts within the alternates' spread and the iterate at an equal count
+    within max(1e-9, 2 floor)."""
+    W = {"kind": "wells", "radius": 2, "halo": 2}
+    I = {"kind": "indicator", "edges": (1.0, 2.5), "halo": 0, "max_blocks": 256}
+    prob = make_problem(2, shape=(24, 44, 20), max_sweeps=300, max_iter=20000,
+                        static_levels=(W, I))
+    orc = _oracle_full(prob)
+    assert orc["sol"]["converged"]
+    k_or = orc["sol"]["iters"]
+    k_alt = [_oracle_variant(prob, c)["sol"]["iters"] for c in ALTERNATES]
+    k_tol = max(1, 2 * max(abs(k_or - k) for k in k_alt))
+    g = _gpu_full(ctx, prob)
+    assert abs(g["sol"]["iters"] - k_or) <= k_tol, (g["sol"]["iters"], k_or, k_alt)
+    k_fix = min(k_or, K_PARITY)
+    orf = _oracle_full(prob, fixed_iters=k_fix)
+    xo = orf["sol"]["x"]
+    alts = [_oracle_variant(prob, c, fixed_iters=k_fix)["sol"] for c in ALTERNATES]
+    floor = max(np.linalg.norm(a["x"] - xo) / np.linalg.norm(xo) for a in alts)
+    g2 = _gpu_full(ctx, prob, fixed_iters=k_fix)
+    err = np.linalg.norm(g2["x_host"] - xo) / np.linalg.norm(xo)
+    assert err <= max(X_RTOL, 2.0 * floor), (err, floor)
