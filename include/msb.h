@@ -224,6 +224,13 @@ msb_status msb_ms_iterate(msb_ctx ctx, msb_solver s, const double* b, double* x,
                           int32_t max_iter, int32_t fixed_iters, int32_t* iters_out,
                           double* res_hist, int32_t* dyn_M_hist);
 msb_status msb_solver_destroy(msb_solver s);
+/* Stage smoother (§8 NEXT-2): kind 0 = damped Jacobi with the solver's omega_s (reading A9,
+ * the default), kind 1 = the paper's ILU(0) in
+ * red-black cell ordering (reading B12): x <- x + (L U)^{-1}(b - A x), undamped, nu steps
+ * per stage, L U = the ILU(0) factors of the red-black permuted A.  The pivots are
+ * recomputed from the operator's current transmissibilities at the start of every
+ * msb_ms_iterate / msb_fgmres call.  Errors: MSB_EINVAL for another kind. */
+msb_status msb_solver_set_smoother(msb_ctx ctx, msb_solver s, int32_t kind);
 
 /* ---------------------------------------------------------------- FGMRES (§8 NEXT-1)
  * Flexible GMRES(restart) right-preconditioned by ONE multibasis cycle (Eq. 8 from x = 0)

@@ -61,16 +61,26 @@ def coarse_correction(A, b, x, level):
     return x + level.P @ xc
 
 
-def stage(A, DA, b, x, level, omega_s, nu, post):
+def smooth_step(A, DA, b, x, omega_s, nu, smoother=None):
+    """The stage smoother: damped Jacobi (reading A9) or, given an ILU(0) factor object
+    (oracle.ilu.RBILU0, NEXT-2), ν undamped ILU(0) steps."""
+    if smoother is None:
+        return jacobi(A, DA, b, x, omega_s, nu)
+    for _ in range(nu):
+        x = x + smoother.solve(residual(A, b, x))
+    return x
+
+
+def stage(A, DA, b, x, level, omega_s, nu, post, smoother=None):
     if post:
         x = coarse_correction(A, b, x, level)
-        return jacobi(A, DA, b, x, omega_s, nu)
-    x = jacobi(A, DA, b, x, omega_s, nu)
+        return smooth_step(A, DA, b, x, omega_s, nu, smoother)
+    x = smooth_step(A, DA, b, x, omega_s, nu, smoother)
     return coarse_correction(A, b, x, level)
 
 
 def iterate(A, b, x0, levels, omega_s=2.0 / 3.0, nu=1, post=False, tol=1e-6,
-            max_iter=1000, fixed_iters=0, dynamic=None, record_dynamic=False):
+            max_iter=1000, fixed_iters=0, dynamic=None, record_dynamic=False, smoother=None):
     """Run the multibasis Richardson iteration.
 
     dynamic: None or dict(nx=, ny=, nz=, edges=(0.1, 0.5), max_blocks=1024).
@@ -105,7 +115,7 @@ def iterate(A, b, x0, levels, omega_s=2.0 / 3.0, nu=1, post=False, tol=1e-6,
                     out["dyn"].append((k, part, M))
         x_prev_start = x_start
         for lev in stages:
-            x = stage(A, DA, b, x, lev, omega_s, nu, post)
+            x = stage(A, DA, b, x, lev, omega_s, nu, post, smoother)
         rk = float(np.linalg.norm(residual(A, b, x)))
         res.append(rk / scale)
         if rk > 1e6 * r0 and r0 > 0:

@@ -27,16 +27,16 @@ import scipy.sparse as sp
 from .cycle import stage
 
 
-def precondition(A, DA, v, levels, omega_s=2.0 / 3.0, nu=1, post=False):
+def precondition(A, DA, v, levels, omega_s=2.0 / 3.0, nu=1, post=False, smoother=None):
     """z = M^{-1} v: one multibasis cycle (Eq. 8) from x = 0 with right-hand side v."""
     z = np.zeros_like(v)
     for lev in levels:
-        z = stage(A, DA, v, z, lev, omega_s, nu, post)
+        z = stage(A, DA, v, z, lev, omega_s, nu, post, smoother)
     return z
 
 
 def fgmres(A, b, x0, levels, omega_s=2.0 / 3.0, nu=1, post=False, tol=1e-6, restart=30,
-           max_iter=1000, fixed_iters=0, precond=None):
+           max_iter=1000, fixed_iters=0, precond=None, smoother=None):
     """Returns dict(x, iters, res (true relative residual at each restart start and the
     Arnoldi estimate after each step), converged).  precond: optional callable v -> z
     replacing the multibasis cycle (pins: identity, exact inverse)."""
@@ -71,7 +71,7 @@ def fgmres(A, b, x0, levels, omega_s=2.0 / 3.0, nu=1, post=False, tol=1e-6, rest
         j_used = 0
         for j in range(m):
             Z[:, j] = (precond(V[:, j]) if precond is not None
-                       else precondition(A, DA, V[:, j], levels, omega_s, nu, post))
+                       else precondition(A, DA, V[:, j], levels, omega_s, nu, post, smoother))
             w = A @ Z[:, j]
             for i in range(j + 1):
                 H[i, j] = float(w @ V[:, i])

@@ -76,7 +76,18 @@ def run(prob, sweeps=None, fixed_sweeps=None, fixed_iters=None, max_iter=None,
     fi = prob.fixed_iters if fixed_iters is None else fixed_iters
     mi = prob.max_iter if max_iter is None else max_iter
     x0 = np.zeros(prob.N) if x0 is None else x0
+    smoother = make_smoother(prob, A)
     sol = iterate(A, q, x0, levels, prob.omega_s, prob.nu, prob.post_smooth,
-                  prob.cycle_tol, mi, fi, dyn, record_dynamic)
+                  prob.cycle_tol, mi, fi, dyn, record_dynamic, smoother)
     return dict(A_T=A_T, A=A, q=q, trans=trans, levels_info=levels_info, levels=levels,
-                sol=sol)
+                sol=sol, smoother=smoother)
+
+
+def make_smoother(prob, A):
+    """None = damped Jacobi (A9); "ilu0" = red-black ILU(0) (NEXT-2, reading B12)."""
+    if prob.smoother == "jacobi":
+        return None
+    if prob.smoother == "ilu0":
+        from .ilu import RBILU0
+        return RBILU0(A, prob.nx, prob.ny, prob.nz)
+    raise ValueError(f"unknown smoother {prob.smoother!r}")

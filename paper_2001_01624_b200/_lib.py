@@ -46,6 +46,7 @@ SIGNATURES = {
     "msb_level_create_cartesian": (i32, [p, p, i32, i32, i32, C.POINTER(p), pi64]),
     "msb_level_create_split": (i32, [p, p, p, C.POINTER(p), pi64]),
     "msb_level_create_constant": (i32, [p, p, p, i32, C.POINTER(p)]),
+    "msb_solver_set_smoother": (i32, [p, p, i32]),
     "msb_partition_wells": (i32, [p, C.POINTER(Grid), p, p, i32, i32, p, pi32]),
     "msb_partition_indicator": (i32, [p, p, p, p, i32, i32, p, pi32]),
     "msb_level_create_general": (i32, [p, p, p, i32, i32, C.POINTER(p), pi64]),

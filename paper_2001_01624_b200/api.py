@@ -324,8 +324,11 @@ class Level:
 class Solver:
     """ms_iterate(b, tol) — rows a6–a11 (Eq. 8, Richardson, optional dynamic stage)."""
 
+    SMOOTHERS = {"jacobi": 0, "ilu0": 1}
+
     def __init__(self, ctx: Context, op: Operator, levels: Sequence[Level], omega_s=2.0 / 3.0,
-                 nu=1, post_smooth=False, dynamic=False, edges=(0.1, 0.5), max_blocks=1024):
+                 nu=1, post_smooth=False, dynamic=False, edges=(0.1, 0.5), max_blocks=1024,
+                 smoother="jacobi"):
         self.ctx = ctx
         self.op = op
         self.levels = list(levels)
@@ -336,6 +339,14 @@ class Solver:
                                             float(edges[0]), float(edges[1]), int(max_blocks),
                                             C.byref(h)), "msb_solver_create")
         self.h = h
+        if smoother != "jacobi":
+            self.set_smoother(smoother)
+
+    def set_smoother(self, smoother):
+        """"jacobi" (damped, omega_s) or "ilu0" (red-black ILU(0), NEXT-2)."""
+        self.ctx.check(self.ctx.lib.msb_solver_set_smoother(self.ctx.h, self.h,
+                                                            self.SMOOTHERS[smoother]),
+                       "msb_solver_set_smoother")
 
     def add_dynamic_basis(self, dp, part_out=None):
         M = C.c_int32()

@@ -356,6 +356,104 @@ __global__ void __launch_bounds__(CT) k_res_restrict(StencilT S, LevelView L,
   if (first) warp_partial(r * r, partials);
 }
 
+// ---------------------------------------------------------------- NEXT-2: red-black ILU(0)
+// ILU(0) of A in red-black ordering (red: i + j + k even; reading B12; oracle/ilu.py).
+// With the 7-point stencil red cells couple only to black cells, so the factors keep A's
+// off-diagonal entries: L = [I 0; A_br D_r^-1 I], U = [D_r A_rb; 0 D~_b] with
+// D~_b = a_bb - sum_r a_br a_rb / a_rr over the red neighbours (the fill between black
+// cells is dropped), and one smoothing step x += (LU)^{-1} r is three parallel passes:
+// r = b - A x (k_residual), then black cells e_b = (r_b - sum a_br r_r / a_rr) / D~_b,
+// then red cells e_r = (r_r - sum a_rb e_b) / a_rr.  Sums in ascending neighbour index
+// (-z, -y, -x, +x, +y, +z), the order of the oracle's row-wise elimination and solves.
+__device__ __forceinline__ double diag_at(const StencilT& S, int c, int i, int j, int k) {
+  const int nx = S.g.nx, sxy = S.g.nxy;
+  const double txp = S.Tx[c], typ = S.Ty[c], tzp = S.Tz[c];
+  const double txm = i > 0 ? S.Tx[c - 1] : 0.0;
+  const double tym = j > 0 ? S.Ty[c - nx] : 0.0;
+  const double tzm = k > 0 ? S.Tz[c - sxy] : 0.0;
+  const double D = txp + txm + typ + tym + tzp + tzm;
+  return c == 0 ? 2.0 * D : D;
+}
+
+// face transmissibilities of cell c in ascending neighbour order and the neighbours
+__device__ __forceinline__ void faces_at(const StencilT& S, int c, int i, int j, int k,
+                                         double t[6], int nb[6]) {
+  const int nx = S.g.nx, ny = S.g.ny, nz = S.g.nz, sxy = S.g.nxy;
+  t[0] = k > 0 ? S.Tz[c - sxy] : 0.0;      nb[0] = c - sxy;
+  t[1] = j > 0 ? S.Ty[c - nx] : 0.0;       nb[1] = c - nx;
+  t[2] = i > 0 ? S.Tx[c - 1] : 0.0;        nb[2] = c - 1;
+  t[3] = i < nx - 1 ? S.Tx[c] : 0.0;       nb[3] = c + 1;
+  t[4] = j < ny - 1 ? S.Ty[c] : 0.0;       nb[4] = c + nx;
+  t[5] = k < nz - 1 ? S.Tz[c] : 0.0;       nb[5] = c + sxy;
+}
+
+__global__ void __launch_bounds__(CT) k_ilu_diag(StencilT S, double* __restrict__ d) {
+  const int N = S.g.nxy * S.g.nz;
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= N) return;
+  int i, j, k;
+  g3_coords(S.g, c, i, j, k);
+  double a = diag_at(S, c, i, j, k);
+  if ((i + j + k) & 1) {  // black: subtract l_bk u_kb = (a_bk / a_kk) a_kb over red neighbours
+    double t[6];
+    int nb[6];
+    faces_at(S, c, i, j, k, t, nb);
+#pragma unroll
+    for (int f = 0; f < 6; ++f) {
+      if (t[f] == 0.0) continue;
+      int ii, jj, kk;
+      g3_coords(S.g, nb[f], ii, jj, kk);
+      const double l = -t[f] / diag_at(S, nb[f], ii, jj, kk);
+      a = a - l * -t[f];
+    }
+  }
+  d[c] = a;
+}
+
+// black cells: e_b = (r_b - sum_k l_bk r_k) / D~_b, stored over r_b; x_b += e_b
+__global__ void __launch_bounds__(CT) k_ilu_black(StencilT S, const double* __restrict__ d,
+                                                  double* __restrict__ r, double* __restrict__ x,
+                                                  const IterState* st) {
+  if (is_done(st)) return;
+  const int N = S.g.nxy * S.g.nz;
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= N) return;
+  int i, j, k;
+  g3_coords(S.g, c, i, j, k);
+  if (!((i + j + k) & 1)) return;
+  double t[6];
+  int nb[6];
+  faces_at(S, c, i, j, k, t, nb);
+  double y = r[c];
+#pragma unroll
+  for (int f = 0; f < 6; ++f)
+    if (t[f] != 0.0) y = y - (-t[f] / d[nb[f]]) * r[nb[f]];
+  const double e = y / d[c];
+  r[c] = e;
+  x[c] += e;
+}
+
+// red cells: e_r = (r_r - sum_b a_rb e_b) / a_rr; x_r += e_r
+__global__ void __launch_bounds__(CT) k_ilu_red(StencilT S, const double* __restrict__ d,
+                                                const double* __restrict__ r,
+                                                double* __restrict__ x, const IterState* st) {
+  if (is_done(st)) return;
+  const int N = S.g.nxy * S.g.nz;
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= N) return;
+  int i, j, k;
+  g3_coords(S.g, c, i, j, k);
+  if ((i + j + k) & 1) return;
+  double t[6];
+  int nb[6];
+  faces_at(S, c, i, j, k, t, nb);
+  double y = r[c];
+#pragma unroll
+  for (int f = 0; f < 6; ++f)
+    if (t[f] != 0.0) y = y - (-t[f]) * r[nb[f]];
+  x[c] += y / d[c];
+}
+
 // a6 + a8 for explicit levels with few columns (M <= RRS_MAX_M: well, indicator and
 // dynamic partitions): the warp-segmented sums go to a per-CTA shared-memory copy of r_c
 // and each CTA adds its nonzero entries to global memory once, instead of one global
@@ -1143,6 +1241,7 @@ static msb_status enqueue_stage(msb_ctx ctx, msb_solver s, msb_level L, const do
   // the rest of the iteration and is joined before the next iteration's first kernel
   // (kernels that have not yet seen `done` then do harmless work).
   const bool side = s->levels.size() == 1 && s->nu == 1 && !s->post && L->kind == 0 &&
+                    s->smoother == 0 &&
                     !getenv("MSB_SERIAL_FINALIZE");
   auto fin = [&](unsigned np) -> msb_status {  // np = blocks of the kernel that wrote partials
     if (side) {
@@ -1170,7 +1269,7 @@ static msb_status enqueue_stage(msb_ctx ctx, msb_solver s, msb_level L, const do
   // fused Jacobi + residual (opt-in, MSB_JACRES=1): measured 57 us against 15.7 + 16.8 us
   // for the two passes it replaces — the 3D halo (4.5 x loads and 2.4 Jacobi updates
   // per cell) and 2 CTAs/SM by registers cost more than the second pass over x, b, T
-  const bool jr = L->kind == 0 && !s->post && s->nu == 1 && getenv("MSB_JACRES");
+  const bool jr = L->kind == 0 && !s->post && s->nu == 1 && s->smoother == 0 && getenv("MSB_JACRES");
   auto jacres = [&]() -> msb_status {
     const dim3 gr((unsigned)((op->nx + JR_X - 1) / JR_X), (unsigned)((op->ny + JR_Y - 1) / JR_Y),
                   (unsigned)((op->nz + JR_Z - 1) / JR_Z));
@@ -1188,7 +1287,7 @@ static msb_status enqueue_stage(msb_ctx ctx, msb_solver s, msb_level L, const do
   // fused Jacobi + residual, TMA z-marching (jacres_tma.cu, opt-in MSB_JQ=1): Cartesian
   // level, pre-smoothing, ν = 1, grid and b TMA-compatible (even nx, 16-byte aligned b)
   bool jq = false;
-  if (!jr && L->kind == 0 && !s->post && s->nu == 1 && s->no_fuse) {
+  if (!jr && L->kind == 0 && !s->post && s->nu == 1 && s->no_fuse && s->smoother == 0) {
     if (!s->jq) s->jq = new JQPlan();
     if (!s->jq->ok || s->jq->b != b || s->jq->x[0] != s->xbuf[0] || s->jq->x[1] != s->xbuf[1])
       jacres_tma_plan(ctx, op, s->xbuf[0], s->xbuf[1], b, s->jq);
@@ -1203,7 +1302,24 @@ static msb_status enqueue_stage(msb_ctx ctx, msb_solver s, msb_level L, const do
     cur ^= 1;
     return MSB_OK;
   };
+  auto ilu = [&]() -> msb_status {  // ν red-black ILU(0) steps on x in place (NEXT-2)
+    for (int v = 0; v < s->nu; ++v) {
+      k_residual<<<g4, CT, 0, st>>>(S, s->xbuf[cur], b, s->r, first ? 1 : 0, s->partials, s->st);
+      MSB_LAUNCH_CHECK(ctx);
+      if (first) {
+        msb_status rc = fin(g4);
+        if (rc) return rc;
+      }
+      first = false;
+      k_ilu_black<<<g, CT, 0, st>>>(S, s->ilu_d, s->r, s->xbuf[cur], s->st);
+      MSB_LAUNCH_CHECK(ctx);
+      k_ilu_red<<<g, CT, 0, st>>>(S, s->ilu_d, s->r, s->xbuf[cur], s->st);
+      MSB_LAUNCH_CHECK(ctx);
+    }
+    return MSB_OK;
+  };
   auto jac = [&]() -> msb_status {
+    if (s->smoother == 1) return ilu();
     for (int v = 0; v < s->nu; ++v) {
       k_jacobi<<<g4, CT, 0, st>>>(S, s->xbuf[cur], s->xbuf[cur ^ 1], b, s->omega_s, first ? 1 : 0,
                                  s->partials, s->st);
@@ -1391,6 +1507,13 @@ static msb_status chunk_graph(msb_ctx ctx, msb_solver s, const double* db, int c
   return MSB_OK;
 }
 
+msb_status msb_solver_set_smoother(msb_ctx ctx, msb_solver s, int32_t kind) {
+  if (!ctx || !s || kind < 0 || kind > 1) return set_error(ctx, MSB_EINVAL, "msb_solver_set_smoother");
+  if (kind != s->smoother) drop_graphs(s);
+  s->smoother = kind;
+  return MSB_OK;
+}
+
 msb_status msb_partition_indicator(msb_ctx ctx, msb_op op, const double* ind, const double* edges,
                                    int32_t n_edges, int32_t max_blocks, int32_t* part,
                                    int32_t* M_out) {
@@ -1483,13 +1606,15 @@ msb_status msb_ms_iterate(msb_ctx ctx, msb_solver s, const double* b, double* x,
   h.tol = tol;
   h.bscale = 1.0;
   MSB_CUDA_TRY(ctx, cudaMemcpyAsync(s->st, &h, sizeof(h), cudaMemcpyHostToDevice, st));
+  msb_status rc = solver_smoother_setup(ctx, s);  // pivots from the operator's current T
+  if (rc) return rc;
   l2_begin(ctx, s);
   struct L2Guard {
     msb_ctx ctx;
     msb_solver s;
     ~L2Guard() { l2_end(ctx, s); }
   } l2_guard{ctx, s};
-  msb_status rc = enqueue_norm(ctx, s, s->xbuf[0], db, 1);
+  rc = enqueue_norm(ctx, s, s->xbuf[0], db, 1);
   if (rc) return rc;
   int cur = 0;
   int target = fixed_iters > 0 ? fixed_iters : max_iter;
@@ -1498,7 +1623,8 @@ msb_status msb_ms_iterate(msb_ctx ctx, msb_solver s, const double* b, double* x,
   std::vector<int32_t> dynM;
   IterState hs{};
   const bool persist = !s->dyn && s->levels.size() == 1 && s->levels[0]->kind == 0 && !s->post &&
-                       s->nu == 1 && s->levels[0]->co.Xp && op->nx <= 512 && getenv("MSB_PERSIST");
+                       s->nu == 1 && s->smoother == 0 && s->levels[0]->co.Xp && op->nx <= 512 &&
+                       getenv("MSB_PERSIST");
   if (persist) {
     msb_level L = s->levels[0];
     const size_t smem = restrict_rows_smem(op->nx);
@@ -1541,7 +1667,8 @@ msb_status msb_ms_iterate(msb_ctx ctx, msb_solver s, const double* b, double* x,
   }
   if (!s->dyn) {
     const int chunk = 16;
-    const int flips = s->nu * (int)s->levels.size();  // x-buffer swaps per iteration
+    // x-buffer swaps per iteration (Jacobi writes out of place; ILU(0) updates in place)
+    const int flips = s->smoother == 0 ? s->nu * (int)s->levels.size() : 0;
     int issued = 0;
     while (true) {
       int n = std::min(chunk, target - issued);
@@ -1636,6 +1763,7 @@ msb_status msb_solver_destroy(msb_solver s) {
   dfree(ctx, s->bins);
   dfree(ctx, s->scratch_i);
   if (s->dyn_level) level_free(s->dyn_level);
+  dfree(ctx, s->ilu_d);
   delete s->jq;
   drop_graphs(s);
   if (s->cap_stream) cudaStreamDestroy(s->cap_stream);
@@ -1651,6 +1779,14 @@ msb_status msb_solver_destroy(msb_solver s) {
 // z = M^{-1} v for FGMRES (fgmres.cu): one iteration of Eq. (8) over the solver's static
 // levels from x = 0 with right-hand side v (no stop test, no dynamic stage).
 namespace msb {
+msb_status solver_smoother_setup(msb_ctx ctx, msb_solver s) {
+  if (s->smoother != 1) return MSB_OK;
+  if (!s->ilu_d) MSB_ALLOC(ctx, s->ilu_d, double, s->op->N);
+  k_ilu_diag<<<grid_for(s->op->N, CT), CT, 0, ctx->stream>>>(stencil(s->op), s->ilu_d);
+  MSB_LAUNCH_CHECK(ctx);
+  return MSB_OK;
+}
+
 void solver_l2_begin(msb_ctx ctx, msb_solver s) { l2_begin(ctx, s); }
 void solver_l2_end(msb_ctx ctx, msb_solver s) { l2_end(ctx, s); }
 

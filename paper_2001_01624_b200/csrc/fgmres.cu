@@ -97,6 +97,10 @@ extern "C" msb_status msb_fgmres(msb_ctx ctx, msb_solver s, const double* b, dou
   void* ob = nullptr;
   const double* db = b ? (const double*)stage_in(ctx, b, N * sizeof(double), &ob) : op->q;
   if (!db) return set_error(ctx, MSB_ENOMEM, "rhs staging");
+  {
+    msb_status r0 = solver_smoother_setup(ctx, s);
+    if (r0) return r0;
+  }
   solver_l2_begin(ctx, s);
   struct L2Guard {
     msb_ctx ctx;

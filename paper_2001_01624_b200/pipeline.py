@@ -66,7 +66,7 @@ def static_partition(ctx: Context, op: Operator, prob, spec):
 def make_solver(ctx: Context, op: Operator, levels, prob):
     return Solver(ctx, op, levels, omega_s=prob.omega_s, nu=prob.nu,
                   post_smooth=prob.post_smooth, dynamic=prob.dynamic, edges=prob.dyn_edges,
-                  max_blocks=prob.dyn_max_blocks)
+                  max_blocks=prob.dyn_max_blocks, smoother=prob.smoother)
 
 
 def run(ctx: Context, prob, sweeps=None, fixed_sweeps=None, fixed_iters=None, max_iter=None,

@@ -53,6 +53,7 @@ class Problem:
     # NEXT-3 static levels after the general ones, e.g. ({"kind": "wells", "radius": 2,
     # "halo": 2}, {"kind": "indicator", "edges": (1.0,), "halo": 1, "max_blocks": 512})
     static_levels: tuple = ()
+    smoother: str = "jacobi"              # "jacobi" (A9) or "ilu0" (NEXT-2, the paper's)
 
     @property
     def N(self) -> int:
