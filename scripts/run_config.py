@@ -79,14 +79,17 @@ def config_single(cfg, args):
 
 def config_static(cfg, args):
     """Config `cfg` solved with and without the NEXT-3 static levels (wells, MsRSB halo 2;
-    log-permeability indicator, constant basis): iterations and solve time."""
+    log-permeability indicator, constant basis) and with the Jacobi or the NEXT-2 ILU(0)
+    smoother: iterations and solve time."""
     ctx = Context(0)
     st = torch.cuda.current_stream()
     W = {"kind": "wells", "radius": 2, "halo": 2}
     I = {"kind": "indicator", "edges": (1.0, 2.5), "halo": 0, "max_blocks": 1024}
     recs = []
-    for name, sl in (("cartesian", ()), ("cartesian+wells+logk", (W, I))):
-        prob = make_problem(cfg, static_levels=sl)
+    for name, sl, sm in (("cartesian", (), "jacobi"), ("cartesian+wells+logk", (W, I), "jacobi"),
+                         ("cartesian / ilu0", (), "ilu0"),
+                         ("cartesian+wells+logk / ilu0", (W, I), "ilu0")):
+        prob = make_problem(cfg, static_levels=sl, smoother=sm)
         e0 = ev(st)
         op = gp.build_operator(ctx, prob)
         levels, info = gp.build_levels(ctx, op, prob)
