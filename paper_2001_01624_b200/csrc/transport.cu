@@ -6,7 +6,9 @@
 // fw_max' is the largest forward-difference slope of f_w on the grid S = k/1000
 // (the same rule in the oracle), so both sides pick the same sub-step count.
 #include <algorithm>
+#include <climits>
 #include <cmath>
+#include <cstdlib>
 
 #include "internal.cuh"
 
@@ -83,6 +85,57 @@ __global__ void k_transport_step(FluxView F, const double* __restrict__ p,
   So[c] = sc + h / (phi[c] * vol) * net;
 }
 
+// Face fluxes of the step, once per msb_transport_upwind call (p is fixed during the
+// sub-steps): Fx[c] = Tx[c] (p_c - p_{c+1}) etc., cell-padded like T (0 past the last
+// column / row / plane).  The sub-step kernel below reads them with the orientation
+// sign instead of re-forming T (p_c - p_l) every sub-step; T (a - b) and T (b - a) are
+// exact negatives, so the arithmetic is bit-for-bit that of k_transport_step.
+__global__ void k_face_fluxes(FluxView F, Grid3 g, const double* __restrict__ p,
+                              double* __restrict__ Fx, double* __restrict__ Fy,
+                              double* __restrict__ Fz) {
+  const int N = g.nxy * g.nz;
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= N) return;
+  int i, j, k;
+  g3_coords(g, c, i, j, k);
+  const double pc = p[c];
+  Fx[c] = i < F.nx - 1 ? F.Tx[c] * (pc - p[c + 1]) : 0.0;
+  Fy[c] = j < F.ny - 1 ? F.Ty[c] * (pc - p[c + F.nx]) : 0.0;
+  Fz[c] = k < F.nz - 1 ? F.Tz[c] * (pc - p[c + g.nxy]) : 0.0;
+}
+
+// One explicit upwind sub-step from precomputed face fluxes (same order of terms as
+// k_transport_step: -z, -y, -x, +x, +y, +z, then the source), 32-bit cell indexing.
+__global__ void __launch_bounds__(256) k_transport_flux_step(
+    Grid3 g, const double* __restrict__ Fx, const double* __restrict__ Fy,
+    const double* __restrict__ Fz, const double* __restrict__ q, const double* __restrict__ phi,
+    double vol, double muw, double muo, double h, const double* __restrict__ S,
+    double* __restrict__ So) {
+  const int N = g.nxy * g.nz;
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= N) return;
+  int i, j, k;
+  g3_coords(g, c, i, j, k);
+  const int nx = g.nx, sxy = g.nxy;
+  const double sc = S[c];
+  const double fc = fw(sc, muw, muo);
+  double net = 0.0;
+  auto face = [&](double Fl, int l) {  // Fl: flux leaving c through the face
+    if (Fl > 0.0) net -= Fl * fc;
+    else net -= Fl * fw(S[l], muw, muo);
+  };
+  if (k > 0) face(-Fz[c - sxy], c - sxy);
+  if (j > 0) face(-Fy[c - nx], c - nx);
+  if (i > 0) face(-Fx[c - 1], c - 1);
+  if (i < g.nx - 1) face(Fx[c], c + 1);
+  if (j < g.ny - 1) face(Fy[c], c + nx);
+  if (k < g.nz - 1) face(Fz[c], c + sxy);
+  const double qc = q[c];
+  if (qc > 0.0) net += qc;
+  else net += qc * fc;
+  So[c] = sc + h / (phi[c] * vol) * net;
+}
+
 // Upstream total mobility per face (compact face layout); ties (F = 0) -> lower cell.
 __global__ void k_upstream_mob(FluxView F, const double* __restrict__ p, const double* __restrict__ S,
                                double muw, double muo, double* __restrict__ mob) {
@@ -147,14 +200,30 @@ extern "C" msb_status msb_transport_upwind(msb_ctx ctx, msb_op op, const double*
     nsub = std::max(1, (int)std::ceil(dt / dt_cfl));
   }
   double h = dt / nsub;
-  double* tmp = dalloc_n<double>(ctx, N);
+  double* tmp = dalloc_n<double>(ctx, 4 * N);  // S ping-pong + the three face-flux planes
   if (!tmp) return set_error(ctx, MSB_ENOMEM, "transport scratch");
   double* a = S;
   double* b = tmp;
-  for (int t = 0; t < nsub; ++t) {
-    k_transport_step<<<grid_for(N, 256), 256, 0, st>>>(F, p, op->q, phi, vol, mu_w, mu_o, h, a, b);
+  static const bool legacy = getenv("MSB_TRANSPORT_LEGACY") != nullptr;
+  if (legacy || N > INT32_MAX / 2) {
+    for (int t = 0; t < nsub; ++t) {
+      k_transport_step<<<grid_for(N, 256), 256, 0, st>>>(F, p, op->q, phi, vol, mu_w, mu_o, h, a, b);
+      MSB_LAUNCH_CHECK(ctx);
+      std::swap(a, b);
+    }
+  } else {
+    const Grid3 g = make_grid3(op->nx, op->ny, op->nz);
+    double* Fx = tmp + N;
+    double* Fy = tmp + 2 * N;
+    double* Fz = tmp + 3 * N;
+    k_face_fluxes<<<grid_for(N, 256), 256, 0, st>>>(F, g, p, Fx, Fy, Fz);
     MSB_LAUNCH_CHECK(ctx);
-    std::swap(a, b);
+    for (int t = 0; t < nsub; ++t) {
+      k_transport_flux_step<<<grid_for(N, 256), 256, 0, st>>>(g, Fx, Fy, Fz, op->q, phi, vol, mu_w,
+                                                               mu_o, h, a, b);
+      MSB_LAUNCH_CHECK(ctx);
+      std::swap(a, b);
+    }
   }
   if (a != S) MSB_CUDA_TRY(ctx, cudaMemcpyAsync(S, a, N * sizeof(double), cudaMemcpyDeviceToDevice, st));
   if (mob_out) {
