@@ -364,7 +364,9 @@ __global__ void __launch_bounds__(CT) k_res_restrict(StencilT S, LevelView L,
 // cells is dropped), and one smoothing step x += (LU)^{-1} r is three parallel passes:
 // r = b - A x (k_residual), then black cells e_b = (r_b - sum a_br r_r / a_rr) / D~_b,
 // then red cells e_r = (r_r - sum a_rb e_b) / a_rr.  Sums in ascending neighbour index
-// (-z, -y, -x, +x, +y, +z), the order of the oracle's row-wise elimination and solves.
+// (-z, -y, -x, +x, +y, +z), the order of the oracle's row-wise elimination and solves;
+// the solves multiply by stored reciprocal pivots (one division per cell per solve
+// instead of seven per step) and each colour pass runs one thread per cell of its colour.
 __device__ __forceinline__ double diag_at(const StencilT& S, int c, int i, int j, int k) {
   const int nx = S.g.nx, sxy = S.g.nxy;
   const double txp = S.Tx[c], typ = S.Ty[c], tzp = S.Tz[c];
@@ -387,7 +389,8 @@ __device__ __forceinline__ void faces_at(const StencilT& S, int c, int i, int j,
   t[5] = k < nz - 1 ? S.Tz[c] : 0.0;       nb[5] = c + sxy;
 }
 
-__global__ void __launch_bounds__(CT) k_ilu_diag(StencilT S, double* __restrict__ d) {
+// dinv[c] = 1 / pivot: 1 / a_rr on red cells, 1 / D~_b on black cells
+__global__ void __launch_bounds__(CT) k_ilu_diag(StencilT S, double* __restrict__ dinv) {
   const int N = S.g.nxy * S.g.nz;
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= N) return;
@@ -407,51 +410,58 @@ __global__ void __launch_bounds__(CT) k_ilu_diag(StencilT S, double* __restrict_
       a = a - l * -t[f];
     }
   }
-  d[c] = a;
+  dinv[c] = 1.0 / a;
 }
 
-// black cells: e_b = (r_b - sum_k l_bk r_k) / D~_b, stored over r_b; x_b += e_b
-__global__ void __launch_bounds__(CT) k_ilu_black(StencilT S, const double* __restrict__ d,
+// colour-compact thread map: thread t -> the q-th cell of colour `col` in grid row
+// rho = t / hx (hx = ceil(nx / 2)), i = 2 q + ((j + k + col) & 1); false past the row end
+__device__ __forceinline__ bool colour_cell(const Grid3& g, int t, int col, int& c, int& i,
+                                            int& j, int& k) {
+  const int hx = (g.nx + 1) >> 1;
+  const int rho = t / hx, q = t - rho * hx;
+  k = rho / g.ny;
+  j = rho - k * g.ny;
+  if (k >= g.nz) return false;
+  i = 2 * q + ((j + k + col) & 1);
+  if (i >= g.nx) return false;
+  c = i + g.nx * j + g.nxy * k;
+  return true;
+}
+
+// black cells: e_b = (r_b + sum_k T_bk r_k / a_kk) / D~_b, stored over r_b; x_b += e_b
+__global__ void __launch_bounds__(CT) k_ilu_black(StencilT S, const double* __restrict__ dinv,
                                                   double* __restrict__ r, double* __restrict__ x,
                                                   const IterState* st) {
   if (is_done(st)) return;
-  const int N = S.g.nxy * S.g.nz;
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= N) return;
-  int i, j, k;
-  g3_coords(S.g, c, i, j, k);
-  if (!((i + j + k) & 1)) return;
+  int c, i, j, k;
+  if (!colour_cell(S.g, blockIdx.x * blockDim.x + threadIdx.x, 1, c, i, j, k)) return;
   double t[6];
   int nb[6];
   faces_at(S, c, i, j, k, t, nb);
   double y = r[c];
 #pragma unroll
   for (int f = 0; f < 6; ++f)
-    if (t[f] != 0.0) y = y - (-t[f] / d[nb[f]]) * r[nb[f]];
-  const double e = y / d[c];
+    if (t[f] != 0.0) y += t[f] * (r[nb[f]] * dinv[nb[f]]);
+  const double e = y * dinv[c];
   r[c] = e;
   x[c] += e;
 }
 
-// red cells: e_r = (r_r - sum_b a_rb e_b) / a_rr; x_r += e_r
-__global__ void __launch_bounds__(CT) k_ilu_red(StencilT S, const double* __restrict__ d,
+// red cells: e_r = (r_r + sum_b T_rb e_b) / a_rr; x_r += e_r
+__global__ void __launch_bounds__(CT) k_ilu_red(StencilT S, const double* __restrict__ dinv,
                                                 const double* __restrict__ r,
                                                 double* __restrict__ x, const IterState* st) {
   if (is_done(st)) return;
-  const int N = S.g.nxy * S.g.nz;
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= N) return;
-  int i, j, k;
-  g3_coords(S.g, c, i, j, k);
-  if ((i + j + k) & 1) return;
+  int c, i, j, k;
+  if (!colour_cell(S.g, blockIdx.x * blockDim.x + threadIdx.x, 0, c, i, j, k)) return;
   double t[6];
   int nb[6];
   faces_at(S, c, i, j, k, t, nb);
   double y = r[c];
 #pragma unroll
   for (int f = 0; f < 6; ++f)
-    if (t[f] != 0.0) y = y - (-t[f]) * r[nb[f]];
-  x[c] += y / d[c];
+    if (t[f] != 0.0) y += t[f] * r[nb[f]];
+  x[c] += y * dinv[c];
 }
 
 // a6 + a8 for explicit levels with few columns (M <= RRS_MAX_M: well, indicator and
@@ -1311,9 +1321,10 @@ static msb_status enqueue_stage(msb_ctx ctx, msb_solver s, msb_level L, const do
         if (rc) return rc;
       }
       first = false;
-      k_ilu_black<<<g, CT, 0, st>>>(S, s->ilu_d, s->r, s->xbuf[cur], s->st);
+      const unsigned gc = grid_for((int64_t)((op->nx + 1) / 2) * op->ny * op->nz, CT);
+      k_ilu_black<<<gc, CT, 0, st>>>(S, s->ilu_d, s->r, s->xbuf[cur], s->st);
       MSB_LAUNCH_CHECK(ctx);
-      k_ilu_red<<<g, CT, 0, st>>>(S, s->ilu_d, s->r, s->xbuf[cur], s->st);
+      k_ilu_red<<<gc, CT, 0, st>>>(S, s->ilu_d, s->r, s->xbuf[cur], s->st);
       MSB_LAUNCH_CHECK(ctx);
     }
     return MSB_OK;
