@@ -101,7 +101,8 @@ int64_t msb_launch_count(void);
  * mob    host|dev or NULL: same layout, face mobility λ_f (config 4).
  * src    host array of n_src sources; q_i = Σ rates of sources in cell i.
  * out    new operator; owns T face arrays (cell-padded), q and a face-open mask
- *        (mult == 1) used by the fault-split partition. */
+ *        (mult == 1) used by the fault-split partition.
+ * Errors: MSB_EINVAL as above; MSB_EDIM when 3N >= 2^31 (cells are int32-indexed). */
 msb_status msb_build_tpfa(msb_ctx ctx, const msb_grid* grid, const double* K, const double* mult,
                           const double* mob, const msb_source* src, int32_t n_src, msb_op* out);
 /* Replace the face mobility (host|dev, compact face layout) and rebuild T. */

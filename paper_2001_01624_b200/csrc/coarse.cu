@@ -55,7 +55,12 @@ __global__ void k_rap(const msb_level_s L, const double* __restrict__ P, const d
   if (c >= N) return;
   const int M = L.M;
   int64_t sxy = (int64_t)L.nx * L.ny;
-  int i = (int)(c % L.nx), j = (int)((c / L.nx) % L.ny), k = (int)(c / sxy);
+  // 32-bit coordinates (msb_build_tpfa bounds 3N < 2^31): 64-bit division is an
+  // emulated ~100-instruction sequence and dominated this kernel (362 us per dynamic-stage
+  // assembly on config 3)
+  const int c32 = (int)c, nxy32 = L.nx * L.ny;
+  const int k = c32 / nxy32, rem = c32 - k * nxy32;
+  const int j = rem / L.nx, i = rem - j * L.nx;
   int cc[RMAX];
   double cv[RMAX];
   int nc = row_entries(L, P, c, cc, cv);

@@ -929,9 +929,20 @@ __global__ void k_bins(const double* __restrict__ dp, int64_t N, const unsigned 
   bins[c] = (a >= e0 * m) + (a >= e1 * m);
 }
 
+// component sizes: runs of equal labels in consecutive lanes are counted with one atomic
+// (a large component would otherwise send every cell's increment to one address)
 __global__ void k_sizes(const int32_t* __restrict__ lab, int64_t N, int32_t* __restrict__ cnt) {
-  int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (c < N) atomicAdd(cnt + lab[c], 1);
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const unsigned full = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  const int key = c < N ? lab[c] : -1;
+  const int prev = __shfl_up_sync(full, key, 1);
+  const unsigned heads = __ballot_sync(full, lane == 0 || prev != key);
+  const int next = __shfl_down_sync(full, key, 1);
+  if (key >= 0 && (lane == 31 || next != key)) {  // run tail: run length = lane - head + 1
+    const int head = 31 - __clz(heads & ((2u << lane) - 1u));
+    atomicAdd(cnt + key, lane - head + 1);
+  }
 }
 
 // counts[0] = #roots with size >= smin; counts[1..3] = bin b has a small component

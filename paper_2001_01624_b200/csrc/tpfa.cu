@@ -5,6 +5,8 @@
 // Storage: cell-padded face arrays Tx[c] (face c|c+1), Ty[c] (c|c+nx), Tz[c]
 // (c|c+nx*ny), zero where the face does not exist; 24 B/cell, read with
 // coalesced fp64 loads by every stencil kernel.
+#include <climits>
+
 #include "internal.cuh"
 
 namespace msb {
@@ -159,6 +161,11 @@ msb_status msb_build_tpfa(msb_ctx ctx, const msb_grid* g, const double* K, const
     return set_error(ctx, MSB_EINVAL, "msb_build_tpfa: bad grid");
   *out = nullptr;
   int64_t N = (int64_t)g->nx * g->ny * g->nz;
+  // cells are indexed with int32 on the device (config 5: 10^7), and the
+  // 8-slot planes of P with size_t: 3N (the T block) must stay addressable as int32 offsets
+  if (3 * N >= (int64_t)INT32_MAX)
+    return set_error(ctx, MSB_EDIM, "msb_build_tpfa: %lld cells exceed the int32 cell indexing",
+                     (long long)N);
   int64_t nf = (int64_t)(g->nx - 1) * g->ny * g->nz + (int64_t)g->nx * (g->ny - 1) * g->nz +
                (int64_t)g->nx * g->ny * (g->nz - 1);
   msb_op op = new msb_op_s();

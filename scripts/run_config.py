@@ -4,6 +4,8 @@ is config 2); this is the config-5 / config-4 measurement harness.
 
 usage: python scripts/run_config.py 5 [--iters 20] [--sweeps 300]
        python scripts/run_config.py 4 [--steps 100]
+       python scripts/run_config.py 1|3          (full pipeline incl. split/dynamic stages)
+       python scripts/run_config.py 2 --static   (NEXT-2/-3 variants)
 """
 import argparse
 import json
@@ -110,6 +112,35 @@ def config_static(cfg, args):
     print(json.dumps(dict(config=cfg, static_levels=recs)), flush=True)
 
 
+def config_pipeline(cfg, args):
+    """Configs 1 and 3 (and any config) through the full pipeline: all of the config's
+    levels (config 3: Cartesian + fault-split, dynamic stage, post-smoothing), phases timed
+    with CUDA events; the solve is timed after a warm-up solve."""
+    prob = make_problem(cfg)
+    ctx = Context(0)
+    st = torch.cuda.current_stream()
+    e0 = ev(st)
+    op = gp.build_operator(ctx, prob)
+    levels, info = gp.build_levels(ctx, op, prob)
+    e1 = ev(st)
+    s = gp.make_solver(ctx, op, levels, prob)
+    x = torch.zeros(prob.N, dtype=torch.float64, device="cuda")
+    s.iterate(x, None, prob.cycle_tol, prob.max_iter, prob.fixed_iters)
+    x.zero_()
+    e2 = ev(st)
+    out = s.iterate(x, None, prob.cycle_tol, prob.max_iter, prob.fixed_iters)
+    e3 = ev(st)
+    torch.cuda.synchronize()
+    dyn = out.get("dyn_M")
+    rec = dict(config=cfg, N=prob.N, M=[lv.info()["M"] for lv in levels],
+               sweeps=[i[0] for i in info], iters=out["iters"], converged=out["converged"],
+               final_res=float(out["res"][-1]), setup_levels_ms=e0.elapsed_time(e1),
+               solve_ms=e2.elapsed_time(e3),
+               ms_per_iteration=e2.elapsed_time(e3) / max(1, out["iters"]),
+               dyn_M_median=float(np.median(dyn[dyn > 0])) if dyn is not None and np.any(dyn > 0) else 0)
+    print(json.dumps(rec), flush=True)
+
+
 def config4(args):
     prob = make_problem(4)
     ctx = Context(0)
@@ -134,6 +165,8 @@ if __name__ == "__main__":
     a = ap.parse_args()
     if a.static:
         config_static(a.config, a)
+    elif a.config in (1, 3):
+        config_pipeline(a.config, a)
     elif a.config == 4:
         config4(a)
     else:
