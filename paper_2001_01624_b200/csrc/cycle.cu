@@ -469,7 +469,7 @@ __global__ void __launch_bounds__(CT) k_ilu_red(StencilT S, const double* __rest
 // and each CTA adds its nonzero entries to global memory once, instead of one global
 // atomic per warp segment — with M = 6 (the well level) those ~70k atomics all hit six
 // addresses.  Grid-stride over cells with a fixed grid (rrs_grid()).
-constexpr int RRS_MAX_M = 4096;
+constexpr int RRS_MAX_M = 6000;  // shared r_c within the 48 KB default (static smem included)
 __global__ void __launch_bounds__(CT) k_res_restrict_small(StencilT S, LevelView L, int M,
                                                            const double* __restrict__ x,
                                                            const double* __restrict__ b,
