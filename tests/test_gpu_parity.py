@@ -922,3 +922,57 @@ def test_ilu_smoother_fgmres(ctx):
     x = torch.zeros(prob.N, dtype=torch.float64, device="cuda")
     out = s.fgmres(x, None, tol=1e-6, restart=20, max_iter=500)
     assert out["converged"] and abs(out["iters"] - free["iters"]) <= 1, (out["iters"], free["iters"])
+
+
+# ---------------------------------------------------------------- degenerate shapes and arguments
+DEGENERATE = {
+    "two_cells_two_blocks": lambda: random_problem(21, 2, 1, 1, (1, 1, 1), max_sweeps=20),
+    "one_block_whole_grid": lambda: random_problem(22, 6, 5, 3, (6, 5, 3), max_sweeps=20),
+    "nx1_column": lambda: random_problem(23, 1, 9, 7, (1, 3, 2), max_sweeps=20),
+    "chain_1d": lambda: random_problem(24, 11, 1, 1, (3, 1, 1), max_sweeps=20),
+    "blocks_larger_than_grid": lambda: random_problem(25, 5, 4, 3, (8, 8, 8), max_sweeps=20),
+}
+
+
+@pytest.mark.parametrize("name", list(DEGENERATE))
+def test_degenerate_shapes_pipeline(ctx, name):
+    """Whole path on degenerate grids (2 cells, M = 1, nx = 1, 1D, blocks larger than the
+    grid): basis after fixed sweeps and the iterate after fixed cycles against the oracle."""
+    from paper_2001_01624_b200 import pipeline as gp
+    prob = DEGENERATE[name]()
+    orc = _oracle_full(prob, sweeps=7, fixed_sweeps=True, fixed_iters=4)
+    g = gp.run(ctx, prob, sweeps=7, fixed_sweeps=True, fixed_iters=4)
+    rowptr, cols, vals, _ = g["levels"][0].export()
+    _assert_P(rowptr, cols, vals, orc["levels_info"][0]["P"])
+    xo = orc["sol"]["x"]
+    x = g["x"].cpu().numpy()
+    assert np.linalg.norm(x - xo) <= 1e-10 * max(1.0, np.linalg.norm(xo))
+
+
+def test_degenerate_arguments(ctx):
+    """max_iter = 0, FGMRES restart = 1, out-of-range restart/kind, smoothing with 0 sweeps."""
+    import torch
+    from paper_2001_01624_b200 import pipeline as gp
+    from paper_2001_01624_b200.api import MsbError
+    prob = random_problem(26, 8, 6, 4, (4, 3, 2), max_sweeps=10)
+    op = gp.build_operator(ctx, prob)
+    levels, _ = gp.build_levels(ctx, op, prob)
+    s = gp.make_solver(ctx, op, levels, prob)
+    x = torch.zeros(prob.N, dtype=torch.float64, device="cuda")
+    out = s.iterate(x, None, 1e-6, 0)
+    assert out["iters"] == 0 and not out["converged"]
+    assert float(x.abs().max()) == 0.0
+    out = s.fgmres(x, None, tol=1e-6, restart=1, max_iter=400)
+    orc = _oracle_full(prob, fixed_iters=1)
+    from oracle import fgmres as og
+    ref = og.fgmres(orc["A"], orc["q"], np.zeros(prob.N), orc["levels"], omega_s=prob.omega_s,
+                    nu=prob.nu, post=prob.post_smooth, tol=1e-6, restart=1, max_iter=400)
+    assert out["converged"] == ref["converged"] and abs(out["iters"] - ref["iters"]) <= 1
+    with pytest.raises(MsbError):
+        s.fgmres(x, None, restart=0)
+    with pytest.raises(MsbError):
+        s.fgmres(x, None, restart=65)
+    with pytest.raises(KeyError):
+        s.set_smoother("gauss-seidel")
+    n, last, deltas, st = levels[0].smooth(op, 0, prob.omega, 1e-3)
+    assert n == 0 and len(deltas) == 0
