@@ -11,6 +11,8 @@
 #include <algorithm>
 #include <cstdlib>
 
+#include <climits>
+
 #include "internal.cuh"
 #include "symv.cuh"
 
@@ -47,9 +49,85 @@ __device__ __forceinline__ int row_entries(const msb_level_s& L, const double* _
 
 constexpr int RMAX = 32;
 
+// ---------------------------------------------------------------- deterministic constant-basis RAP
+// For a constant basis (explicit level, one slot: the dynamic, indicator-halo-0 and
+// constant levels) A_c = sum over faces between blocks J != K of T (e_J - e_K)(e_J - e_K)^T
+// (+ the gauge term).  The entries are accumulated EXACTLY in 128-bit fixed point with
+// 64-bit integer atomics (carry into the high word), so the result does not depend on the
+// order in which the atomics land: the same inputs give the same A_c bits on every run
+// (the dynamic stage is rebuilt every iteration and its Δp bins amplify any run-to-run
+// rounding noise).  Scale 2^F with F = 90 - ilogb(max T): every entry sum stays below
+// 2^126, contributions are exact down to 2^-50 relative to max T.
+__global__ void k_absmax_t(const double* __restrict__ T, int64_t n, unsigned long long* out) {
+  double m = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    m = fmax(m, fabs(T[i]));
+  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(out, (unsigned long long)__double_as_longlong(m));
+}
+
+__device__ __forceinline__ void fx_add(unsigned long long* e, double v, int F) {
+  const bool neg = v < 0.0;
+  const double t = ldexp(fabs(v), F);  // < 2^92, exact power-of-two scaling
+  unsigned long long hi = (unsigned long long)floor(ldexp(t, -64));
+  unsigned long long lo = (unsigned long long)(t - ldexp((double)hi, 64));
+  if (neg) {  // two's complement of (hi, lo)
+    lo = ~lo + 1ull;
+    hi = ~hi + (lo == 0ull ? 1ull : 0ull);
+  }
+  const unsigned long long old = atomicAdd(e, lo);
+  atomicAdd(e + 1, hi + (old + lo < old ? 1ull : 0ull));
+}
+
+__global__ void k_rap_const_det(const int32_t* __restrict__ col, Grid3 g, int M,
+                                const double* __restrict__ Tx, const double* __restrict__ Ty,
+                                const double* __restrict__ Tz,
+                                const unsigned long long* __restrict__ tmax_bits,
+                                unsigned long long* __restrict__ acc) {
+  const int N = g.nxy * g.nz;
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= N) return;
+  int i, j, k;
+  g3_coords(g, c, i, j, k);
+  const int F = 90 - ilogb(__longlong_as_double((long long)*tmax_bits));
+  const int J = col[c];
+  const double Tf[3] = {i < g.nx - 1 ? Tx[c] : 0.0, j < g.ny - 1 ? Ty[c] : 0.0,
+                        k < g.nz - 1 ? Tz[c] : 0.0};
+  const int nb[3] = {c + 1, c + g.nx, c + g.nxy};
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    if (!(Tf[d] != 0.0)) continue;
+    const int K = col[nb[d]];
+    if (K == J) continue;
+    fx_add(acc + 2 * ((size_t)J * M + J), Tf[d], F);
+    fx_add(acc + 2 * ((size_t)K * M + K), Tf[d], F);
+    fx_add(acc + 2 * ((size_t)J * M + K), -Tf[d], F);
+    fx_add(acc + 2 * ((size_t)K * M + J), -Tf[d], F);
+  }
+  if (c == 0) fx_add(acc + 2 * ((size_t)J * M + J), Tf[0] + 0.0 + Tf[1] + 0.0 + Tf[2] + 0.0, F);
+}
+
+__global__ void k_fx_to_double(const unsigned long long* __restrict__ acc, int64_t n,
+                               const unsigned long long* __restrict__ tmax_bits,
+                               double* __restrict__ Ac) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= n) return;
+  const int F = 90 - ilogb(__longlong_as_double((long long)*tmax_bits));
+  const long long hi = (long long)acc[2 * e + 1];
+  const unsigned long long lo = acc[2 * e];
+  // the 128-bit integer hi 2^64 + lo, rounded to double (deterministic), scaled back
+  Ac[e] = ldexp(ldexp((double)hi, 64) + (double)lo, -F);
+}
+
+// FX: accumulate into the 128-bit fixed-point buffer (deterministic, see above) instead of
+// fp64 atomics; |T g_a g_b| <= max T because P entries lie in [0, 1]
+template <bool FX>
 __global__ void k_rap(const msb_level_s L, const double* __restrict__ P, const double* __restrict__ Tx,
                       const double* __restrict__ Ty, const double* __restrict__ Tz,
-                      double* __restrict__ Ac) {
+                      double* __restrict__ Ac, unsigned long long* __restrict__ acc,
+                      const unsigned long long* __restrict__ tmax_bits) {
+  const int F = FX ? 90 - ilogb(__longlong_as_double((long long)*tmax_bits)) : 0;
   int64_t N = L.N;
   int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= N) return;
@@ -96,14 +174,18 @@ __global__ void k_rap(const msb_level_s L, const double* __restrict__ P, const d
       double ta = T * gv[a];
       for (int b = 0; b < ng; ++b) {
         if (gv[b] == 0.0) continue;
-        atomicAdd(Ac + (int64_t)gc[a] * M + gc[b], ta * gv[b]);
+        if (FX) fx_add(acc + 2 * ((int64_t)gc[a] * M + gc[b]), ta * gv[b], F);
+        else atomicAdd(Ac + (int64_t)gc[a] * M + gc[b], ta * gv[b]);
       }
     }
   }
   if (c == 0) {  // gauge: A_00 doubled adds A^T_00 (P_0.)^T P_0.
     double d0 = Tf[0] + 0.0 + Tf[1] + 0.0 + Tf[2] + 0.0;
     for (int a = 0; a < nc; ++a)
-      for (int b = 0; b < nc; ++b) atomicAdd(Ac + (int64_t)cc[a] * M + cc[b], d0 * cv[a] * cv[b]);
+      for (int b = 0; b < nc; ++b) {
+        if (FX) fx_add(acc + 2 * ((int64_t)cc[a] * M + cc[b]), d0 * cv[a] * cv[b], F);
+        else atomicAdd(Ac + (int64_t)cc[a] * M + cc[b], d0 * cv[a] * cv[b]);
+      }
   }
 }
 
@@ -283,9 +365,39 @@ msb_status coarse_assemble_dense(msb_ctx ctx, msb_level L, msb_op op) {
     co.cap = cap;
   }
   co.M = M;
-  MSB_CUDA_TRY(ctx, cudaMemsetAsync(co.Ac, 0, (size_t)M * M * sizeof(double), ctx->stream));
-  k_rap<<<grid_for(L->N, 128), 128, 0, ctx->stream>>>(*L, L->P[L->cur], op->Tx, op->Ty, op->Tz,
-                                                      co.Ac);
+  // deterministic exact accumulation (128-bit fixed point) whenever its 16 B per entry fit
+  // comfortably (M <= 8192: 1 GiB); config 5 (M = 20,000) keeps fp64 atomics
+  static const bool det_off = getenv("MSB_RAP_ATOMIC") != nullptr;
+  cudaStream_t st = ctx->stream;
+  if (!det_off && M <= 8192) {
+    const size_t n = (size_t)M * M;
+    if (co.acc_cap < n) {
+      dfree(ctx, co.acc);
+      co.acc = nullptr;
+      co.acc_cap = 0;
+      MSB_ALLOC(ctx, co.acc, unsigned long long, 2 * n + 1);
+      co.acc_cap = n;
+    }
+    unsigned long long* tmax = co.acc + 2 * n;
+    MSB_CUDA_TRY(ctx, cudaMemsetAsync(co.acc, 0, (2 * n + 1) * sizeof(unsigned long long), st));
+    k_absmax_t<<<std::min<int64_t>(grid_for(3 * op->N, 256), 4 * ctx->sm_count), 256, 0, st>>>(
+        op->Tx, 3 * op->N, tmax);
+    MSB_LAUNCH_CHECK(ctx);
+    if (L->kind == 1 && L->W == 1) {  // constant basis: only the faces between blocks
+      k_rap_const_det<<<grid_for(op->N, 256), 256, 0, st>>>(
+          L->col, make_grid3(op->nx, op->ny, op->nz), M, op->Tx, op->Ty, op->Tz, tmax, co.acc);
+    } else {
+      k_rap<true><<<grid_for(L->N, 128), 128, 0, st>>>(*L, L->P[L->cur], op->Tx, op->Ty, op->Tz,
+                                                       co.Ac, co.acc, tmax);
+    }
+    MSB_LAUNCH_CHECK(ctx);
+    k_fx_to_double<<<grid_for((int64_t)n, 256), 256, 0, st>>>(co.acc, (int64_t)n, tmax, co.Ac);
+    MSB_LAUNCH_CHECK(ctx);
+    return coarse_factor_dense(ctx, co);
+  }
+  MSB_CUDA_TRY(ctx, cudaMemsetAsync(co.Ac, 0, (size_t)M * M * sizeof(double), st));
+  k_rap<false><<<grid_for(L->N, 128), 128, 0, st>>>(*L, L->P[L->cur], op->Tx, op->Ty, op->Tz,
+                                                    co.Ac, nullptr, nullptr);
   MSB_LAUNCH_CHECK(ctx);
   return coarse_factor_dense(ctx, co);
 }
@@ -296,6 +408,9 @@ void coarse_free(msb_ctx ctx, Coarse& co) {
   dfree(ctx, co.L);
   dfree(ctx, co.Xp);
   dfree(ctx, co.part);
+  dfree(ctx, co.acc);
+  co.acc = nullptr;
+  co.acc_cap = 0;
   co.Xp = co.part = nullptr;
   co.xp_cap = 0;
   co.Ac = co.Ainv = co.L = nullptr;

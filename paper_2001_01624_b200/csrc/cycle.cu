@@ -507,7 +507,84 @@ __global__ void __launch_bounds__(CT) k_res_restrict_small(StencilT S, LevelView
   if (first) warp_partial(v2, partials);
 }
 
-// a9: x += P xc (row gather).
+// Deterministic form for M <= RRD_MAX_M (the dynamic, well and indicator levels): no
+// atomics anywhere.  Each warp reduces runs of equal columns with shuffles and its run
+// tails add into the warp's own shared row one lane at a time (ascending lane), the CTA
+// sums its eight rows in order into rc_part[cta][.], and k_rc_combine sums the CTAs in
+// order.  The same inputs give the same r_c bits on every run, so the chaotic
+// dynamic-stage iteration (its Δp bins) cannot drift with atomics order.
+constexpr int RRD_MAX_M = 1536;
+constexpr int RRD_WARPS = CT / 32;
+__global__ void __launch_bounds__(CT) k_res_restrict_det(StencilT S, LevelView L, int M,
+                                                         const double* __restrict__ x,
+                                                         const double* __restrict__ b,
+                                                         double* __restrict__ rc_part, int first,
+                                                         double* __restrict__ partials,
+                                                         const IterState* st) {
+  if (is_done(st)) return;
+  extern __shared__ double acc[];  // [RRD_WARPS][M]
+  for (int m = threadIdx.x; m < RRD_WARPS * M; m += blockDim.x) acc[m] = 0.0;
+  __syncthreads();
+  const unsigned full = 0xffffffffu;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double* row = acc + warp * M;
+  const int N = S.g.nxy * S.g.nz;
+  const int stride = gridDim.x * blockDim.x;
+  double v2 = 0.0;
+  for (int base = blockIdx.x * blockDim.x; base < N; base += stride) {  // warp-uniform
+    const int c = base + threadIdx.x;
+    const bool in = c < N;
+    const int cc = in ? c : N - 1;
+    int i, j, k;
+    g3_coords(S.g, cc, i, j, k);
+    double r = 0.0;
+    if (in) {
+      double dA;
+      r = residual_at(S, x, b, c, i, j, k, &dA);
+    }
+    v2 += r * r;
+    for (int s2 = 0; s2 < L.W; ++s2) {
+      const int key = in ? L.col[(size_t)s2 * N + c] : -1;
+      double v = key >= 0 ? L.P[(size_t)s2 * N + c] * r : 0.0;
+      // inclusive segmented scan over runs of equal keys (fixed shuffle order)
+      const int prev = __shfl_up_sync(full, key, 1);
+      const unsigned heads = __ballot_sync(full, lane == 0 || prev != key);
+      const int start = 31 - __clz(heads & ((2u << lane) - 1u));
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const double y = __shfl_up_sync(full, v, o);
+        if (lane - o >= start) v += y;
+      }
+      const int next = __shfl_down_sync(full, key, 1);
+      unsigned tails = __ballot_sync(full, key >= 0 && (lane == 31 || next != key));
+      while (tails) {  // one run tail at a time, ascending lane
+        const int t = __ffs(tails) - 1;
+        if (lane == t) row[key] += v;
+        __syncwarp();
+        tails &= tails - 1;
+      }
+    }
+  }
+  __syncthreads();
+  for (int m = threadIdx.x; m < M; m += blockDim.x) {
+    double t = 0.0;
+    for (int w = 0; w < RRD_WARPS; ++w) t += acc[w * M + m];
+    rc_part[(size_t)blockIdx.x * M + m] = t;
+  }
+  if (first) warp_partial(v2, partials);
+}
+
+__global__ void k_rc_combine(const double* __restrict__ rc_part, int G, int M,
+                             double* __restrict__ rc, const IterState* st) {
+  if (is_done(st)) return;
+  const int m = blockIdx.x * blockDim.x + threadIdx.x;
+  if (m >= M) return;
+  double t = 0.0;
+  for (int g = 0; g < G; ++g) t += rc_part[(size_t)g * M + m];
+  rc[m] = t;
+}
+
+// a9: x += P xc (row gather).// a9: x += P xc (row gather).
 __global__ void __launch_bounds__(CT) k_prolong(LevelView L, double* __restrict__ x,
                                                 const double* __restrict__ xc,
                                                 const IterState* st) {
@@ -1396,7 +1473,28 @@ static msb_status enqueue_stage(msb_ctx ctx, msb_solver s, msb_level L, const do
     MSB_LAUNCH_CHECK(ctx);
     unsigned gpart = g;  // blocks that write stop-test partials
     static const bool no_small = getenv("MSB_NO_RRS") != nullptr;
-    if (L->kind == 1 && L->M <= RRS_MAX_M && !no_small) {
+    if (L->kind == 1 && L->M <= RRD_MAX_M && !no_small) {
+      gpart = (unsigned)std::min<int64_t>(g, 4 * ctx->sm_count);
+      const size_t need = (size_t)gpart * L->M;
+      if (s->rc_part_cap < need) {
+        dfree(ctx, s->rc_part);
+        s->rc_part = dalloc_n<double>(ctx, need);
+        if (!s->rc_part) return set_error(ctx, MSB_ENOMEM, "restriction partials");
+        s->rc_part_cap = need;
+      }
+      const size_t smem = (size_t)RRD_WARPS * L->M * sizeof(double);
+      static bool attr = false;
+      if (!attr) {
+        MSB_CUDA_TRY(ctx, cudaFuncSetAttribute(k_res_restrict_det,
+                                               cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               (int)(RRD_WARPS * RRD_MAX_M * sizeof(double))));
+        attr = true;
+      }
+      k_res_restrict_det<<<gpart, CT, smem, st>>>(S, V, L->M, s->xbuf[cur], b, s->rc_part,
+                                                  first ? 1 : 0, s->partials, s->st);
+      MSB_LAUNCH_CHECK(ctx);
+      k_rc_combine<<<grid_for(L->M, 256), 256, 0, st>>>(s->rc_part, (int)gpart, L->M, s->rc, s->st);
+    } else if (L->kind == 1 && L->M <= RRS_MAX_M && !no_small) {
       gpart = (unsigned)std::min<int64_t>(g, 4 * ctx->sm_count);
       k_res_restrict_small<<<gpart, CT, (size_t)L->M * sizeof(double), st>>>(
           S, V, L->M, s->xbuf[cur], b, s->rc, first ? 1 : 0, s->partials, s->st);
@@ -1777,6 +1875,7 @@ msb_status msb_solver_destroy(msb_solver s) {
   dfree(ctx, s->rc);
   dfree(ctx, s->xc);
   dfree(ctx, s->partials);
+  dfree(ctx, s->rc_part);
   dfree(ctx, s->st);
   dfree(ctx, s->res_dev);
   dfree(ctx, s->lab);

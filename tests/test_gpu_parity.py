@@ -976,3 +976,21 @@ def test_degenerate_arguments(ctx):
         s.set_smoother("gauss-seidel")
     n, last, deltas, st = levels[0].smooth(op, 0, prob.omega, 1e-3)
     assert n == 0 and len(deltas) == 0
+
+
+@pytest.mark.parametrize("name", ["config1_dynamic", "config3_recipe"])
+def test_run_to_run_bitwise_reproducible(ctx, name):
+    """The whole path is deterministic for M <= 8192: two runs give identical bits
+    (pressure, residual history, dynamic-stage sizes).  Every reduction is fixed-order,
+    the coarse assembly accumulates exactly in 128-bit fixed point, the sweep's δ is an
+    order-free maximum."""
+    prob = {"config1_dynamic": lambda: make_problem(1, dynamic=True),
+            "config3_recipe": lambda: make_problem(3, shape=(18, 33, 10), max_sweeps=60,
+                                                   max_iter=20000)}[name]()
+    from paper_2001_01624_b200 import pipeline as gp
+    a = gp.run(ctx, prob)
+    b = gp.run(ctx, prob)
+    assert a["sol"]["iters"] == b["sol"]["iters"]
+    assert np.array_equal(a["x"].cpu().numpy(), b["x"].cpu().numpy())
+    assert np.array_equal(a["sol"]["res"], b["sol"]["res"])
+    assert np.array_equal(a["sol"]["dyn_M"], b["sol"]["dyn_M"])
