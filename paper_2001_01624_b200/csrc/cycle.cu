@@ -574,14 +574,23 @@ __global__ void __launch_bounds__(CT) k_res_restrict_det(StencilT S, LevelView L
   if (first) warp_partial(v2, partials);
 }
 
-__global__ void k_rc_combine(const double* __restrict__ rc_part, int G, int M,
-                             double* __restrict__ rc, const IterState* st) {
+// one CTA per column: strided partial sums then a shuffle/shared tree, all fixed-order
+__global__ void __launch_bounds__(256) k_rc_combine(const double* __restrict__ rc_part, int G,
+                                                    int M, double* __restrict__ rc,
+                                                    const IterState* st) {
   if (is_done(st)) return;
-  const int m = blockIdx.x * blockDim.x + threadIdx.x;
-  if (m >= M) return;
+  const int m = blockIdx.x;
   double t = 0.0;
-  for (int g = 0; g < G; ++g) t += rc_part[(size_t)g * M + m];
-  rc[m] = t;
+  for (int g = threadIdx.x; g < G; g += blockDim.x) t += rc_part[(size_t)g * M + m];
+  __shared__ double sh[8];
+  for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = t;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double u = 0.0;
+    for (int w = 0; w < 8; ++w) u += sh[w];
+    rc[m] = u;
+  }
 }
 
 // a9: x += P xc (row gather).// a9: x += P xc (row gather).
@@ -1493,7 +1502,7 @@ static msb_status enqueue_stage(msb_ctx ctx, msb_solver s, msb_level L, const do
       k_res_restrict_det<<<gpart, CT, smem, st>>>(S, V, L->M, s->xbuf[cur], b, s->rc_part,
                                                   first ? 1 : 0, s->partials, s->st);
       MSB_LAUNCH_CHECK(ctx);
-      k_rc_combine<<<grid_for(L->M, 256), 256, 0, st>>>(s->rc_part, (int)gpart, L->M, s->rc, s->st);
+      k_rc_combine<<<L->M, 256, 0, st>>>(s->rc_part, (int)gpart, L->M, s->rc, s->st);
     } else if (L->kind == 1 && L->M <= RRS_MAX_M && !no_small) {
       gpart = (unsigned)std::min<int64_t>(g, 4 * ctx->sm_count);
       k_res_restrict_small<<<gpart, CT, (size_t)L->M * sizeof(double), st>>>(

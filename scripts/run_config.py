@@ -104,11 +104,21 @@ def config_static(cfg, args):
         out = s.iterate(x, None, prob.cycle_tol, prob.max_iter, 0)
         e3 = ev(st)
         torch.cuda.synchronize()
+        x.zero_()
+        s.fgmres(x, None, tol=prob.cycle_tol, restart=20, max_iter=2000)  # warm-up
+        x.zero_()
+        e4 = ev(st)
+        fg = s.fgmres(x, None, tol=prob.cycle_tol, restart=20, max_iter=2000)
+        e5 = ev(st)
+        torch.cuda.synchronize()
         recs.append(dict(levels=name, M=[lv.info()["M"] for lv in levels],
                          sweeps=[i[0] for i in info], iters=out["iters"],
                          converged=out["converged"], setup_ms=e0.elapsed_time(e1),
                          solve_ms=e2.elapsed_time(e3),
-                         ms_per_iteration=e2.elapsed_time(e3) / max(1, out["iters"])))
+                         ms_per_iteration=e2.elapsed_time(e3) / max(1, out["iters"]),
+                         fgmres_steps=fg["iters"], fgmres_converged=fg["converged"],
+                         fgmres_ms=e4.elapsed_time(e5),
+                         fgmres_ms_per_step=e4.elapsed_time(e5) / max(1, fg["iters"])))
     print(json.dumps(dict(config=cfg, static_levels=recs)), flush=True)
 
 
