@@ -1923,10 +1923,9 @@ void solver_l2_end(msb_ctx ctx, msb_solver s) { l2_end(ctx, s); }
 msb_status solver_precondition(msb_ctx ctx, msb_solver s, const double* v, double* z) {
   cudaStream_t st = ctx->stream;
   const int64_t N = s->op->N;
-  IterState h{};
-  h.bscale = 1.0;
-  h.max_iter = 1;
-  MSB_CUDA_TRY(ctx, cudaMemcpyAsync(s->st, &h, sizeof(h), cudaMemcpyHostToDevice, st));
+  // no stop test runs inside the preconditioner (first = false): only `done` is read,
+  // and it must be 0 — a memset, not a pageable host copy, so nothing waits on the host
+  MSB_CUDA_TRY(ctx, cudaMemsetAsync(s->st, 0, sizeof(IterState), st));
   MSB_CUDA_TRY(ctx, cudaMemsetAsync(s->xbuf[0], 0, N * sizeof(double), st));
   int cur = 0;
   bool first = false;

@@ -66,6 +66,24 @@ __global__ void __launch_bounds__(FG_T) k_multiaxpy(const double* __restrict__ V
   w[c] += alpha * acc;
 }
 
+// Arnoldi column on the device: h_i = (0 + d1_i) + d2_i (the two CGS passes, in the order
+// the host accumulated them before), h_{j+1} = sqrt(w.w)
+__global__ void k_hcol(const double* __restrict__ d1, const double* __restrict__ d2,
+                       const double* __restrict__ ww, int j, double* __restrict__ h) {
+  const int i = threadIdx.x;
+  if (i <= j) h[i] = (0.0 + d1[i]) + d2[i];
+  if (i == 0) h[j + 1] = sqrt(*ww);
+}
+
+// v_{j+1} = w / h_{j+1} (as (1 / h) w), or 0 on breakdown (h = 0), h read on the device
+__global__ void k_scale_by(const double* __restrict__ h, const double* __restrict__ w,
+                           double* __restrict__ v, int64_t N) {
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= N) return;
+  const double hn = *h;
+  v[c] = hn != 0.0 ? (1.0 / hn) * w[c] : 0.0;
+}
+
 // y = x - y  (r = b - A x with y = A x on entry)
 __global__ void k_xmy(const double* __restrict__ x, double* __restrict__ y, int64_t N) {
   const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -114,7 +132,12 @@ extern "C" msb_status msb_fgmres(msb_ctx ctx, msb_solver s, const double* b, dou
   MSB_ALLOC(ctx, xd, double, N);
   const int nb = 4 * ctx->sm_count;
   MSB_ALLOC(ctx, part, double, (size_t)(m + 1) * nb);
-  MSB_ALLOC(ctx, dots, double, m + 2);
+  MSB_ALLOC(ctx, dots, double, 3 * (m + 2) + 1);  // pass-1 dots | pass-2 dots | H column | w.w
+  double* dots2 = dots + (m + 2);
+  double* hcol = dots + 2 * (m + 2);
+  double* wwd = dots + 3 * (m + 2);
+  double* hpin = static_cast<double*>(pinned_scratch(ctx, (m + 2) * sizeof(double)));
+  if (!hpin) return set_error(ctx, MSB_ENOMEM, "pinned readback buffer");
   MSB_CUDA_TRY(ctx, cudaMemcpyAsync(xd, x, N * sizeof(double), cudaMemcpyDefault, st));
   const unsigned ge = grid_for(N, FG_T);
   msb_status rc = MSB_OK;
@@ -173,22 +196,29 @@ extern "C" msb_status msb_fgmres(msb_ctx ctx, msb_solver s, const double* b, dou
       double* zj = Z + (size_t)j * N;
       if ((rc = solver_precondition(ctx, s, vj, zj))) return rc;
       if ((rc = msb_op_apply(ctx, op, zj, w))) return rc;
-      // CGS2: h = V^T w; w -= V h; twice
+      // CGS2: h = V^T w; w -= V h; twice — all on the device, then ||w||, the Arnoldi
+      // column and v_{j+1}; one host round trip per step reads the column for the rotations
       for (int pass = 0; pass < 2; ++pass) {
-        if ((rc = multidot(V, j + 1, w))) return rc;
-        for (int i = 0; i <= j; ++i) Hij(i, j) += hd[i];
-        k_multiaxpy<<<ge, FG_T, 0, st>>>(V, j + 1, N, dots, -1.0, w);
+        double* dd = pass ? dots2 : dots;
+        k_multidot<<<nb, FG_T, 0, st>>>(V, j + 1, N, w, part);
+        MSB_LAUNCH_CHECK(ctx);
+        k_reduce_parts<<<j + 1, FG_T, 0, st>>>(part, nb, dd);
+        MSB_LAUNCH_CHECK(ctx);
+        k_multiaxpy<<<ge, FG_T, 0, st>>>(V, j + 1, N, dd, -1.0, w);
         MSB_LAUNCH_CHECK(ctx);
       }
-      double hn;
-      if ((rc = nrm2(w, &hn))) return rc;
-      Hij(j + 1, j) = hn;
-      if (hn != 0.0) {
-        k_scale<<<ge, FG_T, 0, st>>>(1.0 / hn, w, V + (size_t)(j + 1) * N, N);
-        MSB_LAUNCH_CHECK(ctx);
-      } else {  // breakdown: v_{j+1} = 0, as in the oracle
-        MSB_CUDA_TRY(ctx, cudaMemsetAsync(V + (size_t)(j + 1) * N, 0, N * sizeof(double), st));
-      }
+      k_multidot<<<nb, FG_T, 0, st>>>(w, 1, N, w, part);
+      MSB_LAUNCH_CHECK(ctx);
+      k_reduce_parts<<<1, FG_T, 0, st>>>(part, nb, wwd);
+      MSB_LAUNCH_CHECK(ctx);
+      k_hcol<<<1, 64, 0, st>>>(dots, dots2, wwd, j, hcol);
+      MSB_LAUNCH_CHECK(ctx);
+      k_scale_by<<<ge, FG_T, 0, st>>>(hcol + j + 1, w, V + (size_t)(j + 1) * N, N);
+      MSB_LAUNCH_CHECK(ctx);
+      MSB_CUDA_TRY(ctx, cudaMemcpyAsync(hpin, hcol, (j + 2) * sizeof(double),
+                                        cudaMemcpyDeviceToHost, st));
+      MSB_CUDA_TRY(ctx, cudaStreamSynchronize(st));
+      for (int i = 0; i <= j + 1; ++i) Hij(i, j) = hpin[i];
       for (int i = 0; i < j; ++i) {
         const double t = cs[i] * Hij(i, j) + sn[i] * Hij(i + 1, j);
         Hij(i + 1, j) = -sn[i] * Hij(i, j) + cs[i] * Hij(i + 1, j);
