@@ -265,7 +265,7 @@ __global__ void __launch_bounds__(SYMV_T) k_symv_tiles(const double* __restrict_
   symv_tile_body<false>(Xp, M, rc, part, blockIdx.x);
 }
 
-__global__ void __launch_bounds__(4 * ST) k_symv_reduce(const double* __restrict__ part, int M,
+__global__ void __launch_bounds__(16 * ST) k_symv_reduce(const double* __restrict__ part, int M,
                                                         int ntb, double* __restrict__ xc,
                                                         const int* done) {
   const bool skip = done && *(volatile const int*)done;
@@ -344,7 +344,7 @@ void coarse_solve_dense(msb_ctx ctx, const Coarse& co, const double* rc, double*
   if (co.Xp && !getenv("MSB_DENSE_GEMV")) {
     const int64_t nt = (int64_t)co.ntb * (co.ntb + 1) / 2;
     k_symv_tiles<<<(unsigned)nt, SYMV_T, 0, ctx->stream>>>(co.Xp, co.M, rc, co.part);
-    k_symv_reduce<<<co.ntb, 4 * ST, 0, ctx->stream>>>(co.part, co.M, co.ntb, xc, done);
+    k_symv_reduce<<<co.ntb, 16 * ST, 0, ctx->stream>>>(co.part, co.M, co.ntb, xc, done);
     count_launch();
     count_launch();
     return;

@@ -74,24 +74,26 @@ __device__ __forceinline__ void symv_tile_body(const double* __restrict__ Xp, in
 }
 
 // output block b: xc[b] = sum_{j <= b} row part of (b, j) + sum_{k > b} column part of (k, b),
-// four thread groups of 64 taking every fourth contribution, then a fixed-order combine
+// G = blockDim / 64 thread groups of 64 taking every G-th contribution (the persistent
+// kernel runs 4 groups, k_symv_reduce 16: a 4-deep instead of 14-deep chain of dependent
+// L2 loads per thread at M = 3,400), then a fixed-order combine of the groups
 template <bool CG>
 __device__ __forceinline__ void symv_reduce_body(const double* part, int M, int ntb,
                                                  double* __restrict__ xc, int b, bool skip) {
-  const int i = threadIdx.x & (ST - 1), g = threadIdx.x / ST;
+  const int i = threadIdx.x & (ST - 1), g = threadIdx.x / ST, G = blockDim.x / ST;
   const int64_t rowbase = (int64_t)b * (b + 1) / 2;
   double v = 0.0;
-  if (g < 4)
-    for (int e = g; e < ntb; e += 4) {
-      const int64_t off = e <= b ? (rowbase + e) * 2 * ST + i
-                                 : ((int64_t)e * (e + 1) / 2 + b) * 2 * ST + ST + i;
-      v += ld_mut<CG>(part + off);
-    }
-  __shared__ double sh[4][ST];
-  if (g < 4) sh[g][i] = v;
+  for (int e = g; e < ntb; e += G) {
+    const int64_t off = e <= b ? (rowbase + e) * 2 * ST + i
+                               : ((int64_t)e * (e + 1) / 2 + b) * 2 * ST + ST + i;
+    v += ld_mut<CG>(part + off);
+  }
+  __shared__ double sh[16][ST];
+  sh[g][i] = v;
   __syncthreads();
   if (g == 0) {
-    const double tot = (sh[0][i] + sh[1][i]) + (sh[2][i] + sh[3][i]);
+    double tot = 0.0;
+    for (int q = 0; q < G; ++q) tot += sh[q][i];
     const int row = b * ST + i;
     if (row < M && !skip) xc[row] = tot;
   }
