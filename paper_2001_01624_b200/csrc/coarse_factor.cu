@@ -150,6 +150,7 @@ struct BlasApi {
   decltype(&cublasSetStream_v2) set_stream = nullptr;
   decltype(&cublasDgemm_v2) dgemm = nullptr;
   decltype(&cublasDsyrk_v2) dsyrk = nullptr;
+  decltype(&cublasDtrmm_v2) dtrmm = nullptr;
 };
 
 static BlasApi* blas(msb_ctx ctx) {
@@ -169,6 +170,7 @@ static BlasApi* blas(msb_ctx ctx) {
     a.set_stream = reinterpret_cast<decltype(&cublasSetStream_v2)>(dlsym(lib, "cublasSetStream_v2"));
     a.dgemm = reinterpret_cast<decltype(&cublasDgemm_v2)>(dlsym(lib, "cublasDgemm_v2"));
     a.dsyrk = reinterpret_cast<decltype(&cublasDsyrk_v2)>(dlsym(lib, "cublasDsyrk_v2"));
+    a.dtrmm = reinterpret_cast<decltype(&cublasDtrmm_v2)>(dlsym(lib, "cublasDtrmm_v2"));
     auto set_mode =
         reinterpret_cast<decltype(&cublasSetMathMode)>(dlsym(lib, "cublasSetMathMode"));
     if (!create || !a.set_stream || !a.dgemm || !a.dsyrk) return nullptr;
@@ -205,6 +207,19 @@ static bool blas_syrk(msb_ctx ctx, bool at, int n, int k, double alpha, const do
   if (!b || b->set_stream(b->h, ctx->stream) != CUBLAS_STATUS_SUCCESS) return false;
   return b->dsyrk(b->h, CUBLAS_FILL_MODE_UPPER, at ? CUBLAS_OP_N : CUBLAS_OP_T, n, k, &alpha, A,
                   (int)lda, &beta, C, (int)ldc) == CUBLAS_STATUS_SUCCESS;
+}
+
+// Row-major C (m x n, ldc) = W22^T W21 for W22 lower triangular (n x n, lda) and W21
+// (n rows x m cols, ldb): in column-major terms C_cm = W21_cm W22_cm^T with W22_cm upper
+// triangular — cuBLAS DTRMM, side right, out of place.
+static bool blas_trmm_lt(msb_ctx ctx, int m, int n, const double* W22, int64_t lda,
+                         const double* W21, int64_t ldb, double* C, int64_t ldc) {
+  BlasApi* b = blas(ctx);
+  if (!b || !b->dtrmm || b->set_stream(b->h, ctx->stream) != CUBLAS_STATUS_SUCCESS) return false;
+  const double one = 1.0;
+  return b->dtrmm(b->h, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_T,
+                  CUBLAS_DIAG_NON_UNIT, m, n, &one, W22, (int)lda, W21, (int)ldb, C,
+                  (int)ldc) == CUBLAS_STATUS_SUCCESS;
 }
 
 constexpr size_t GEMM_SMEM = 2 * 2 * GK * (GB + GPAD) * sizeof(double);
@@ -388,6 +403,23 @@ __global__ void k_absmax2(const double* __restrict__ A, int64_t n, unsigned long
   if ((threadIdx.x & 31) == 0) atomicMax(out, (unsigned long long)__double_as_longlong(m));
 }
 
+// Lower triangle of F = W^T W for lower-triangular W (LAPACK dlauum, recursive):
+//   [W11 0; W21 W22]: F11 = W11^T W11 + W21^T W21, F21 = W22^T W21, F22 = W22^T W22
+// — M^3/3 flops instead of the M^3 of one DSYRK over the full (half-zero) W.  Leaves
+// (n <= 512) are one DSYRK.  Returns false when cuBLAS is not available.
+static bool lauum(msb_ctx ctx, const double* W, double* F, int n, int64_t ld) {
+  if (n <= 512) return blas_syrk(ctx, true, n, n, 1.0, W, ld, 0.0, F, ld);
+  const int n1 = split1(n), n2 = n - n1;
+  const double* W21 = W + (int64_t)n1 * ld;
+  const double* W22 = W21 + n1;
+  double* F21 = F + (int64_t)n1 * ld;
+  double* F22 = F21 + n1;
+  if (!lauum(ctx, W, F, n1, ld)) return false;
+  if (!blas_syrk(ctx, true, n1, n2, 1.0, W21, ld, 1.0, F, ld)) return false;
+  if (!blas_trmm_lt(ctx, n1, n2, W22, ld, W21, ld, F21, ld)) return false;
+  return lauum(ctx, W22, F22, n2, ld);
+}
+
 msb_status coarse_factor_dense(msb_ctx ctx, Coarse& co) {
   const int M = co.M;
   cudaStream_t s = ctx->stream;
@@ -418,7 +450,10 @@ msb_status coarse_factor_dense(msb_ctx ctx, Coarse& co) {
   // A_c^{-1} = W^T W: lower tiles with the K range restricted to the nonzeros of W,
   // written over the factor buffer (L is no longer needed), then mirrored; swap so
   // that co.Ainv holds the inverse and co.L the inverse factor W.
-  if (blas_syrk(ctx, true, M, M, 1.0, Wb, M, 0.0, F, M))
+  static const bool full_syrk = getenv("MSB_FULL_SYRK") != nullptr;
+  if (!full_syrk && lauum(ctx, Wb, F, M, M))
+    count_launch();
+  else if (blas_syrk(ctx, true, M, M, 1.0, Wb, M, 0.0, F, M))
     count_launch();
   else if ((rc = gemm<true, false>(ctx, M, M, M, 1.0, Wb, M, Wb, M, 0.0, F, M, true, true)))
     return rc;
