@@ -50,7 +50,8 @@ enum {
   MSB_EDIM = -2,           /* dimension mismatch                                       */
   MSB_EZERO_DIAG = -3,     /* zero diagonal in A_T                       */
   MSB_ESINGULAR = -4,      /* coarse pivot <= 1e-14 * max|A_c|            */
-  MSB_EINCONSISTENT = -5,  /* pure Neumann problem with sum(q) != 0                    */
+  MSB_EINCONSISTENT = -5,  /* reserved, never returned: the A_00 gauge (reading A7)
+                              makes every right-hand side solvable                      */
   MSB_EDIVERGED = -6,      /* residual > 1e6 * initial residual           */
   MSB_ENOMEM = -7,         /* allocator returned NULL                                  */
   MSB_ECUDA = -8           /* CUDA runtime error / no device                           */

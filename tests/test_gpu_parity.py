@@ -994,3 +994,47 @@ def test_run_to_run_bitwise_reproducible(ctx, name):
     assert np.array_equal(a["x"].cpu().numpy(), b["x"].cpu().numpy())
     assert np.array_equal(a["sol"]["res"], b["sol"]["res"])
     assert np.array_equal(a["sol"]["dyn_M"], b["sol"]["dyn_M"])
+
+
+def test_error_paths_fail_loudly(ctx):
+    """Documented error codes (include/msb.h) surface as MsbError with the code name."""
+    import torch
+    from paper_2001_01624_b200 import Level, Operator, Solver
+    from paper_2001_01624_b200.api import MsbError, partition_indicator, partition_wells
+    from paper_2001_01624_b200 import pipeline as gp
+    prob = random_problem(31, 8, 6, 4, (4, 3, 2), max_sweeps=10)
+    K = gp.problem_K(prob)
+    with pytest.raises(MsbError, match="EINVAL"):  # K <= 0
+        Operator(ctx, prob.nx, prob.ny, prob.nz, np.where(np.arange(len(K)) == 5, -1.0, K),
+                 prob.src_cells, prob.src_rates)
+    with pytest.raises(MsbError, match="EDIM"):  # 3N >= 2^31: int32 cell indexing
+        Operator(ctx, 2048, 2048, 256, np.ones(3), [], [])
+    op = gp.build_operator(ctx, prob)
+    other = gp.build_operator(ctx, random_problem(32, 5, 5, 5, (5, 5, 5)))
+    lev = Level.cartesian(ctx, op, prob.block)
+    lev.smooth(op, 5, prob.omega, -1.0)
+    lev.assemble(op)
+    with pytest.raises(MsbError, match="EDIM"):  # level built on another grid
+        Solver(ctx, other, [lev])
+    # a block without cells: A_c has a zero row and column -> singular pivot
+    part = np.zeros(prob.N, dtype=np.int32)
+    part[prob.N // 2:] = 2
+    empty = Level.constant(ctx, op, part, 3)
+    with pytest.raises(MsbError, match="ESINGULAR"):
+        empty.assemble(op)
+    with pytest.raises(MsbError, match="EINVAL"):  # partition value out of range
+        Level.general(ctx, op, np.full(prob.N, 5, dtype=np.int32), 3, 1)
+    with pytest.raises(MsbError, match="EINVAL"):  # more than 16 supports per cell
+        Level.general(ctx, op, np.arange(prob.N, dtype=np.int32), prob.N, 4)
+    with pytest.raises(MsbError, match="EINVAL"):
+        partition_wells(ctx, prob.nx, prob.ny, prob.nz, [np.array([0])], -1)
+    with pytest.raises(MsbError, match="EINVAL"):
+        partition_wells(ctx, prob.nx, prob.ny, prob.nz, [np.array([prob.N])], 1)
+    with pytest.raises(MsbError, match="EINVAL"):
+        partition_indicator(ctx, op, np.zeros(prob.N), (2.0, 1.0))
+    s = Solver(ctx, op, [lev])
+    with pytest.raises(MsbError, match="EINVAL"):
+        ctx.check(ctx.lib.msb_solver_set_smoother(ctx.h, s.h, 7), "msb_solver_set_smoother")
+    x = torch.zeros(prob.N, dtype=torch.float64, device="cuda")
+    out = s.iterate(x, None, 1e-300, 3)  # unreachable tolerance: MSB_NOT_CONVERGED, not an error
+    assert out["iters"] == 3 and not out["converged"]
