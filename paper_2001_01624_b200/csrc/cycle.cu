@@ -18,6 +18,7 @@
 
 #include <cooperative_groups.h>
 
+#include <chrono>
 #include <cstdio>
 
 #include "internal.cuh"
@@ -1100,6 +1101,21 @@ static msb_status build_dynamic(msb_ctx ctx, msb_solver s, const double* dp, int
   msb_op op = s->op;
   int64_t N = op->N;
   cudaStream_t st = ctx->stream;
+  static const bool tdbg = getenv("MSB_DYN_TIMING") != nullptr;
+  static double tt[6] = {0, 0, 0, 0, 0, 0};
+  static int calls = 0;
+  auto now = [&]() {
+    cudaStreamSynchronize(st);
+    return std::chrono::duration<double, std::micro>(
+               std::chrono::steady_clock::now().time_since_epoch()).count();
+  };
+  double tq = tdbg ? now() : 0;
+  auto lap = [&](int i) {
+    if (!tdbg) return;
+    const double t = now();
+    tt[i] += t - tq;
+    tq = t;
+  };
   unsigned long long* mx = reinterpret_cast<unsigned long long*>(s->scratch_i);
   int32_t* counts = s->scratch_i + 2;
   int32_t* rep = s->scratch_i + 8;
@@ -1115,10 +1131,12 @@ static msb_status build_dynamic(msb_ctx ctx, msb_solver s, const double* dp, int
     *M_out = 0;
     return MSB_OK;
   }
+  lap(0);
   k_bins<<<grid_for(N, 256), 256, 0, st>>>(dp, N, mx, s->edge0, s->edge1, s->bins);
   MSB_LAUNCH_CHECK(ctx);
   msb_status rc = cc_label(ctx, op, s->bins, s->lab, false, nullptr);
   if (rc) return rc;
+  lap(1);
   MSB_CUDA_TRY(ctx, cudaMemsetAsync(s->cnt, 0, N * sizeof(int32_t), st));
   k_sizes<<<grid_for(N, 256), 256, 0, st>>>(s->lab, N, s->cnt);
   MSB_LAUNCH_CHECK(ctx);
@@ -1140,6 +1158,7 @@ static msb_status build_dynamic(msb_ctx ctx, msb_solver s, const double* dp, int
   MSB_LAUNCH_CHECK(ctx);
   k_merge_label<<<grid_for(N, 256), 256, 0, st>>>(s->lab, s->cnt, s->bins, N, smin, rep, s->ids);
   MSB_LAUNCH_CHECK(ctx);
+  lap(2);
   int32_t M = 0;
   // canonical numbering: labels are minimum cells of their blocks
   rc = canonical_number(ctx, N, s->ids, s->lab, s->cnt /* 2N scratch: cnt|bins reused */, &M);
@@ -1151,8 +1170,13 @@ static msb_status build_dynamic(msb_ctx ctx, msb_solver s, const double* dp, int
   D->cur = 0;
   D->M = M;
   if (part_out) MSB_CUDA_TRY(ctx, copy_out(ctx, part_out, D->part, N * sizeof(int32_t)));
+  lap(3);
   rc = coarse_assemble_dense(ctx, D, op);
   if (rc) return rc;
+  lap(4);
+  if (tdbg && ++calls % 50 == 0)
+    fprintf(stderr, "build_dynamic (us/call over %d): absmax %.0f cc %.0f merge %.0f canon %.0f assemble %.0f\n",
+            calls, tt[0] / calls, tt[1] / calls, tt[2] / calls, tt[3] / calls, tt[4] / calls);
   *M_out = M;
   return MSB_OK;
 }
@@ -1831,18 +1855,30 @@ msb_status msb_ms_iterate(msb_ctx ctx, msb_solver s, const double* b, double* x,
     }
   } else {
     // dynamic stage: host-synchronous per iteration (M_dyn is data dependent)
+    static const bool tdbg = getenv("MSB_DYN_TIMING") != nullptr;
+    double t_norm = 0, t_build = 0, t_stages = 0;
+    auto now = [&]() {
+      cudaStreamSynchronize(st);
+      return std::chrono::duration<double, std::micro>(
+                 std::chrono::steady_clock::now().time_since_epoch()).count();
+    };
     while (true) {
+      double t0 = tdbg ? now() : 0;
       if ((rc = enqueue_norm(ctx, s, s->xbuf[cur], db, 0))) return rc;
       MSB_CUDA_TRY(ctx, cudaMemcpyAsync(&hs, s->st, sizeof(hs), cudaMemcpyDeviceToHost, st));
       MSB_CUDA_TRY(ctx, cudaStreamSynchronize(st));
+      if (tdbg) t_norm += now() - t0;
       if (hs.done) break;
       int k = hs.k;  // iteration about to run (1-based)
       int32_t M = 0;
+      double t1 = tdbg ? now() : 0;
       if (k >= 2) {
         k_dp<<<grid_for(N, 256), 256, 0, st>>>(s->xbuf[cur], s->xprev, N, s->dpbuf);
         MSB_LAUNCH_CHECK(ctx);
         if ((rc = build_dynamic(ctx, s, s->dpbuf, &M, nullptr))) return rc;
       }
+      if (tdbg) t_build += now() - t1;
+      if (tdbg) t1 = now();
       dynM.push_back(M);
       MSB_CUDA_TRY(ctx, cudaMemcpyAsync(s->xprev, s->xbuf[cur], N * sizeof(double),
                                         cudaMemcpyDeviceToDevice, st));
@@ -1851,8 +1887,12 @@ msb_status msb_ms_iterate(msb_ctx ctx, msb_solver s, const double* b, double* x,
         if ((rc = enqueue_stage(ctx, s, L, db, cur, first))) return rc;
       if (M > 0)
         if ((rc = enqueue_stage(ctx, s, s->dyn_level, db, cur, first))) return rc;
+      if (tdbg) t_stages += now() - t1;
       cur_after.push_back(cur);
     }
+    if (tdbg)
+      fprintf(stderr, "dyn timing (us, %d its): norm+sync %.0f build %.0f stages %.0f\n", hs.k,
+              t_norm, t_build, t_stages);
   }
 finish:
   int k = hs.k;
