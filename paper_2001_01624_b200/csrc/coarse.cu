@@ -80,32 +80,120 @@ __device__ __forceinline__ void fx_add(unsigned long long* e, double v, int F) {
   atomicAdd(e + 1, hi + (old + lo < old ? 1ull : 0ull));
 }
 
-__global__ void k_rap_const_det(const int32_t* __restrict__ col, Grid3 g, int M,
-                                const double* __restrict__ Tx, const double* __restrict__ Ty,
-                                const double* __restrict__ Tz,
-                                const unsigned long long* __restrict__ tmax_bits,
-                                unsigned long long* __restrict__ acc) {
+// Unsigned 128-bit fixed point (lo, hi) of t = v 2^F for v >= 0 (fx_add's conversion).
+__device__ __forceinline__ void fx_split(double v, int F, unsigned long long& lo,
+                                         unsigned long long& hi) {
+  const double t = ldexp(v, F);
+  hi = (unsigned long long)floor(ldexp(t, -64));
+  lo = (unsigned long long)(t - ldexp((double)hi, 64));
+}
+
+__device__ __forceinline__ void add128(unsigned long long& lo, unsigned long long& hi,
+                                       unsigned long long ylo, unsigned long long yhi) {
+  const unsigned long long s = lo + ylo;
+  hi += yhi + (s < lo ? 1ull : 0ull);
+  lo = s;
+}
+
+__device__ __forceinline__ double fx_value(unsigned long long lo, unsigned long long hi, int F) {
+  return ldexp(ldexp((double)(long long)hi, 64) + (double)lo, -F);
+}
+
+// Constant basis (W = 1): A_c = P^T A P has (A_c)_JK = -sum of T_f over the faces between
+// blocks J != K, and (A_c)_JJ = sum over J's outer faces (+ the gauge term of cell 0).
+// Only the magnitude sum of each unordered pair {J, K} is accumulated, into the lower entry
+// (max, min); the conversion (k_fx_const_to_double) negates it into both off-diagonal
+// entries and forms each diagonal as its row's pair sums — exact integer sums, so the
+// result is the same as accumulating all four entries per face, and order-independent.
+// Faces along a block boundary hit the same pair from consecutive lanes: runs of equal
+// pairs within a warp are summed first (segmented shuffle scan, exact 128-bit adds) and the
+// run's last lane issues the two atomics.  The gauge term goes to the diagonal slot.
+__global__ void __launch_bounds__(256) k_rap_const_det(const int32_t* __restrict__ col, Grid3 g, int M,
+                                                       const double* __restrict__ Tx,
+                                                       const double* __restrict__ Ty,
+                                                       const double* __restrict__ Tz,
+                                                       const unsigned long long* __restrict__ tmax_bits,
+                                                       unsigned long long* __restrict__ acc) {
+  const unsigned FULL = 0xffffffffu, NONE = 0xffffffffu;
   const int N = g.nxy * g.nz;
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= N) return;
-  int i, j, k;
-  g3_coords(g, c, i, j, k);
+  const int lane = threadIdx.x & 31;
+  const bool in = c < N;
+  int i = 0, j = 0, k = 0;
+  if (in) g3_coords(g, c, i, j, k);
   const int F = 90 - ilogb(__longlong_as_double((long long)*tmax_bits));
-  const int J = col[c];
-  const double Tf[3] = {i < g.nx - 1 ? Tx[c] : 0.0, j < g.ny - 1 ? Ty[c] : 0.0,
-                        k < g.nz - 1 ? Tz[c] : 0.0};
+  const int J = in ? col[c] : -1;
+  double Tf[3] = {0.0, 0.0, 0.0};
+  if (in) {
+    Tf[0] = i < g.nx - 1 ? Tx[c] : 0.0;
+    Tf[1] = j < g.ny - 1 ? Ty[c] : 0.0;
+    Tf[2] = k < g.nz - 1 ? Tz[c] : 0.0;
+  }
   const int nb[3] = {c + 1, c + g.nx, c + g.nxy};
 #pragma unroll
   for (int d = 0; d < 3; ++d) {
-    if (!(Tf[d] != 0.0)) continue;
-    const int K = col[nb[d]];
-    if (K == J) continue;
-    fx_add(acc + 2 * ((size_t)J * M + J), Tf[d], F);
-    fx_add(acc + 2 * ((size_t)K * M + K), Tf[d], F);
-    fx_add(acc + 2 * ((size_t)J * M + K), -Tf[d], F);
-    fx_add(acc + 2 * ((size_t)K * M + J), -Tf[d], F);
+    unsigned key = NONE;
+    unsigned long long lo = 0, hi = 0;
+    if (in && Tf[d] != 0.0) {
+      const int K = col[nb[d]];
+      if (K != J) {
+        key = (unsigned)(J > K ? J * M + K : K * M + J);
+        fx_split(Tf[d], F, lo, hi);
+      }
+    }
+    const unsigned prev = __shfl_up_sync(FULL, key, 1);
+    const unsigned next = __shfl_down_sync(FULL, key, 1);
+    const unsigned heads = __ballot_sync(FULL, lane == 0 || prev != key);
+    const int start = 31 - __clz(heads & (FULL >> (31 - lane)));
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned long long ylo = __shfl_up_sync(FULL, lo, o);
+      const unsigned long long yhi = __shfl_up_sync(FULL, hi, o);
+      if (lane - o >= start) add128(lo, hi, ylo, yhi);
+    }
+    if (key != NONE && (lane == 31 || next != key)) {
+      unsigned long long* e = acc + 2 * (size_t)key;
+      const unsigned long long old = atomicAdd(e, lo);
+      atomicAdd(e + 1, hi + (old + lo < old ? 1ull : 0ull));
+    }
   }
   if (c == 0) fx_add(acc + 2 * ((size_t)J * M + J), Tf[0] + 0.0 + Tf[1] + 0.0 + Tf[2] + 0.0, F);
+}
+
+// One CTA per row a of the constant-basis A_c: off-diagonal entries from the pair sums,
+// the diagonal as their exact 128-bit total plus the gauge slot.
+__global__ void __launch_bounds__(256) k_fx_const_to_double(const unsigned long long* __restrict__ acc,
+                                                            int M,
+                                                            const unsigned long long* __restrict__ tmax_bits,
+                                                            double* __restrict__ Ac) {
+  const int a = blockIdx.x;
+  const int F = 90 - ilogb(__longlong_as_double((long long)*tmax_bits));
+  unsigned long long slo = 0, shi = 0;
+  for (int b = threadIdx.x; b < M; b += blockDim.x) {
+    if (b == a) continue;
+    const size_t e = a > b ? (size_t)a * M + b : (size_t)b * M + a;
+    const unsigned long long lo = acc[2 * e], hi = acc[2 * e + 1];
+    Ac[(size_t)a * M + b] = -fx_value(lo, hi, F);
+    add128(slo, shi, lo, hi);
+  }
+  if (threadIdx.x == 0) add128(slo, shi, acc[2 * ((size_t)a * M + a)], acc[2 * ((size_t)a * M + a) + 1]);
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long ylo = __shfl_xor_sync(0xffffffffu, slo, o);
+    const unsigned long long yhi = __shfl_xor_sync(0xffffffffu, shi, o);
+    add128(slo, shi, ylo, yhi);
+  }
+  __shared__ unsigned long long wl[8], wh[8];
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) {
+    wl[w] = slo;
+    wh[w] = shi;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long lo = wl[0], hi = wh[0];
+    for (int v = 1; v < (int)(blockDim.x >> 5); ++v) add128(lo, hi, wl[v], wh[v]);
+    Ac[(size_t)a * M + a] = fx_value(lo, hi, F);
+  }
 }
 
 __global__ void k_fx_to_double(const unsigned long long* __restrict__ acc, int64_t n,
@@ -114,10 +202,8 @@ __global__ void k_fx_to_double(const unsigned long long* __restrict__ acc, int64
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= n) return;
   const int F = 90 - ilogb(__longlong_as_double((long long)*tmax_bits));
-  const long long hi = (long long)acc[2 * e + 1];
-  const unsigned long long lo = acc[2 * e];
   // the 128-bit integer hi 2^64 + lo, rounded to double (deterministic), scaled back
-  Ac[e] = ldexp(ldexp((double)hi, 64) + (double)lo, -F);
+  Ac[e] = fx_value(acc[2 * e], acc[2 * e + 1], F);
 }
 
 // FX: accumulate into the 128-bit fixed-point buffer (deterministic, see above) instead of
@@ -371,12 +457,13 @@ msb_status coarse_assemble_dense(msb_ctx ctx, msb_level L, msb_op op) {
   cudaStream_t st = ctx->stream;
   if (!det_off && M <= 8192) {
     const size_t n = (size_t)M * M;
-    if (co.acc_cap < n) {
+    if (co.acc_cap < n) {  // sized for the buffers' capacity: a growing M_dyn reallocates once
+      const size_t ncap = std::max(n, (size_t)co.cap * co.cap);
       dfree(ctx, co.acc);
       co.acc = nullptr;
       co.acc_cap = 0;
-      MSB_ALLOC(ctx, co.acc, unsigned long long, 2 * n + 1);
-      co.acc_cap = n;
+      MSB_ALLOC(ctx, co.acc, unsigned long long, 2 * ncap + 1);
+      co.acc_cap = ncap;
     }
     unsigned long long* tmax = co.acc + 2 * n;
     MSB_CUDA_TRY(ctx, cudaMemsetAsync(co.acc, 0, (2 * n + 1) * sizeof(unsigned long long), st));
@@ -391,7 +478,10 @@ msb_status coarse_assemble_dense(msb_ctx ctx, msb_level L, msb_op op) {
                                                        co.Ac, co.acc, tmax);
     }
     MSB_LAUNCH_CHECK(ctx);
-    k_fx_to_double<<<grid_for((int64_t)n, 256), 256, 0, st>>>(co.acc, (int64_t)n, tmax, co.Ac);
+    if (L->kind == 1 && L->W == 1)
+      k_fx_const_to_double<<<M, 256, 0, st>>>(co.acc, M, tmax, co.Ac);
+    else
+      k_fx_to_double<<<grid_for((int64_t)n, 256), 256, 0, st>>>(co.acc, (int64_t)n, tmax, co.Ac);
     MSB_LAUNCH_CHECK(ctx);
     return coarse_factor_dense(ctx, co);
   }
@@ -409,6 +499,8 @@ void coarse_free(msb_ctx ctx, Coarse& co) {
   dfree(ctx, co.Xp);
   dfree(ctx, co.part);
   dfree(ctx, co.acc);
+  dfree(ctx, co.flags);
+  co.flags = nullptr;
   co.acc = nullptr;
   co.acc_cap = 0;
   co.Xp = co.part = nullptr;

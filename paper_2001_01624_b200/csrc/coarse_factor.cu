@@ -423,16 +423,16 @@ static bool lauum(msb_ctx ctx, const double* W, double* F, int n, int64_t ld) {
 msb_status coarse_factor_dense(msb_ctx ctx, Coarse& co) {
   const int M = co.M;
   cudaStream_t s = ctx->stream;
+  if (!co.flags) MSB_ALLOC(ctx, co.flags, unsigned long long, 2);
+  unsigned long long* amax = co.flags;
+  int* sing = reinterpret_cast<int*>(co.flags + 1);
   if (!co.L) MSB_ALLOC(ctx, co.L, double, (int64_t)M * M);
   if (!co.Ainv) MSB_ALLOC(ctx, co.Ainv, double, (int64_t)M * M);
   double* F = co.L;
   double* Wb = co.Ainv;
   MSB_CUDA_TRY(ctx, cudaMemcpyAsync(F, co.Ac, (size_t)M * M * sizeof(double), cudaMemcpyDeviceToDevice, s));
   MSB_CUDA_TRY(ctx, cudaMemsetAsync(Wb, 0, (size_t)M * M * sizeof(double), s));
-  unsigned long long* amax = dalloc_n<unsigned long long>(ctx, 1);
-  int* sing = dalloc_n<int>(ctx, 1);
-  MSB_CUDA_TRY(ctx, cudaMemsetAsync(amax, 0, 8, s));
-  MSB_CUDA_TRY(ctx, cudaMemsetAsync(sing, 0, 4, s));
+  MSB_CUDA_TRY(ctx, cudaMemsetAsync(co.flags, 0, 16, s));
   k_absmax2<<<std::min<int64_t>(grid_for((int64_t)M * M, 256), 4 * ctx->sm_count), 256, 0, s>>>(
       F, (int64_t)M * M, amax);
   MSB_LAUNCH_CHECK(ctx);
@@ -441,8 +441,6 @@ msb_status coarse_factor_dense(msb_ctx ctx, Coarse& co) {
   int hs = 0;
   MSB_CUDA_TRY(ctx, cudaMemcpyAsync(&hs, sing, 4, cudaMemcpyDeviceToHost, s));
   MSB_CUDA_TRY(ctx, cudaStreamSynchronize(s));
-  dfree(ctx, amax);
-  dfree(ctx, sing);
   if (hs) {
     co.ready = false;
     return set_error(ctx, MSB_ESINGULAR, "singular coarse matrix: pivot <= 1e-14 max|A_c| (M=%d)", M);

@@ -134,36 +134,61 @@ __global__ void k_scan_add(int32_t* __restrict__ out, const int32_t* __restrict_
   if (i < n) out[i] += offs[blockIdx.x];
 }
 
-msb_status scan_exclusive(msb_ctx ctx, const int32_t* in, int32_t* out, int64_t n,
-                          int32_t* total) {
-  int64_t nb = (n + SCAN_BLOCK - 1) / SCAN_BLOCK;
-  if (nb == 0) {
-    if (total) *total = 0;
-    return MSB_OK;
-  }
-  int32_t* sums = dalloc_n<int32_t>(ctx, nb + 1);
-  int32_t* offs = dalloc_n<int32_t>(ctx, nb + 1);
-  if (!sums || !offs) return set_error(ctx, MSB_ENOMEM, "scan scratch");
+// One level: block scans of `in`, their sums scanned recursively into offs, added back.
+static msb_status scan_level(msb_ctx ctx, const int32_t* in, int32_t* out, int64_t n, int32_t* scr) {
+  const int64_t nb = (n + SCAN_BLOCK - 1) / SCAN_BLOCK;
+  int32_t* sums = scr;
+  int32_t* offs = scr + nb + 1;
   k_scan_block<<<(unsigned)nb, SCAN_BLOCK, 0, ctx->stream>>>(in, out, sums, n);
   MSB_LAUNCH_CHECK(ctx);
-  msb_status st = MSB_OK;
   if (nb > 1) {
-    int32_t t = 0;
-    st = scan_exclusive(ctx, sums, offs, nb, &t);
+    msb_status st = scan_level(ctx, sums, offs, nb, scr + 2 * (nb + 1));
     if (st != MSB_OK) return st;
     k_scan_add<<<(unsigned)nb, SCAN_BLOCK, 0, ctx->stream>>>(out, offs, n);
     MSB_LAUNCH_CHECK(ctx);
   }
-  if (total) {
-    int32_t last_out = 0, last_in = 0;
-    MSB_CUDA_TRY(ctx, cudaMemcpyAsync(&last_out, out + n - 1, 4, cudaMemcpyDeviceToHost, ctx->stream));
-    MSB_CUDA_TRY(ctx, cudaMemcpyAsync(&last_in, in + n - 1, 4, cudaMemcpyDeviceToHost, ctx->stream));
-    MSB_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
-    *total = last_out + last_in;
+  return MSB_OK;
+}
+
+__global__ void k_scan_total(const int32_t* __restrict__ in, const int32_t* __restrict__ out,
+                             int64_t n, int32_t* __restrict__ total) {
+  *total = out[n - 1] + in[n - 1];
+}
+
+// Exclusive prefix sum of n int32 (device); *total (host, optional) = sum of all, read
+// back with one synchronisation.  Scratch is the context's, reused across calls.
+msb_status scan_exclusive(msb_ctx ctx, const int32_t* in, int32_t* out, int64_t n,
+                          int32_t* total) {
+  if (n <= 0) {
+    if (total) *total = 0;
+    return MSB_OK;
   }
-  dfree(ctx, sums);
-  dfree(ctx, offs);
-  return st;
+  int64_t need = 1;  // the total word, then sums|offs of every level scan_level visits
+  for (int64_t m = n;;) {
+    const int64_t nb = (m + SCAN_BLOCK - 1) / SCAN_BLOCK;
+    need += 2 * (nb + 1);
+    if (nb <= 1) break;
+    m = nb;
+  }
+  if (ctx->scan_cap < need) {
+    dfree(ctx, ctx->scan_scr);
+    ctx->scan_scr = nullptr;
+    ctx->scan_cap = 0;
+    MSB_ALLOC(ctx, ctx->scan_scr, int32_t, need);
+    ctx->scan_cap = need;
+  }
+  int32_t* tot = ctx->scan_scr;
+  msb_status st = scan_level(ctx, in, out, n, ctx->scan_scr + 1);
+  if (st != MSB_OK) return st;
+  if (total) {
+    k_scan_total<<<1, 1, 0, ctx->stream>>>(in, out, n, tot);
+    MSB_LAUNCH_CHECK(ctx);
+    int32_t h = 0;
+    MSB_CUDA_TRY(ctx, cudaMemcpyAsync(&h, tot, 4, cudaMemcpyDeviceToHost, ctx->stream));
+    MSB_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    *total = h;
+  }
+  return MSB_OK;
 }
 
 }  // namespace msb
@@ -196,6 +221,7 @@ msb_status msb_ctx_create(msb_ctx* out, int device, void* cuda_stream, msb_alloc
 msb_status msb_ctx_destroy(msb_ctx ctx) {
   if (!ctx) return MSB_EINVAL;
   if (ctx->pinned) cudaFreeHost(ctx->pinned);
+  msb::dfree(ctx, ctx->scan_scr);
   delete ctx;
   return MSB_OK;
 }

@@ -17,6 +17,7 @@
 #include <cmath>
 
 #include <cooperative_groups.h>
+#include <cub/device/device_radix_sort.cuh>
 
 #include <chrono>
 #include <cstdio>
@@ -592,6 +593,48 @@ __global__ void __launch_bounds__(256) k_rc_combine(const double* __restrict__ r
     for (int w = 0; w < 8; ++w) u += sh[w];
     rc[m] = u;
   }
+}
+
+// a8 for explicit levels with many columns (M > RRD_MAX_M: the fault-split level): one warp
+// per column gathers its entries from the column-major index (positions ascending) —
+// r_c[J] = sum_k P[pos_k] r[cell_k], lane-strided then a fixed shuffle tree: no atomics,
+// so r_c is the same bits on every run (the atomic scatter it replaces spent ~100 us per
+// config-3 iteration in contended fp64 atomics and made the dynamic stage's bins drift).
+__global__ void __launch_bounds__(256) k_restrict_csc(const int32_t* __restrict__ ptr,
+                                                      const int32_t* __restrict__ pos,
+                                                      const double* __restrict__ P,
+                                                      const double* __restrict__ r, int N, int M,
+                                                      double* __restrict__ rc, const IterState* st) {
+  if (is_done(st)) return;
+  const int w = (int)((blockIdx.x * (unsigned)blockDim.x + threadIdx.x) >> 5);
+  const int lane = threadIdx.x & 31;
+  if (w >= M) return;  // warp-uniform
+  const int k1 = ptr[w + 1];
+  double t = 0.0;
+  for (int k = ptr[w] + lane; k < k1; k += 32) {
+    const int p = pos[k];
+    t += P[p] * r[p - (p / N) * N];
+  }
+  for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+  if (lane == 0) rc[w] = t;
+}
+
+// Column-major index build: keys (column << 32 | position) of the valid entries, radix
+// sorted (CUB), column counts scanned into csc_ptr.
+__global__ void k_csc_keys(const int32_t* __restrict__ col, int64_t n, int32_t* __restrict__ cnt,
+                           unsigned long long* __restrict__ keys, int* __restrict__ fill) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= n) return;
+  const int J = col[e];
+  if (J < 0) return;
+  atomicAdd(cnt + J, 1);
+  keys[atomicAdd(fill, 1)] = ((unsigned long long)J << 32) | (unsigned)e;
+}
+
+__global__ void k_csc_pos(const unsigned long long* __restrict__ keys, int64_t n,
+                          int32_t* __restrict__ pos) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e < n) pos[e] = (int32_t)(unsigned)(keys[e] & 0xffffffffull);
 }
 
 // a9: x += P xc (row gather).// a9: x += P xc (row gather).
@@ -1257,6 +1300,81 @@ static void l2_end(msb_ctx ctx, msb_solver s) {
   s->l2_bytes = 0;
 }
 
+namespace msb {
+// Column-major index of an explicit level's pattern for the gather restriction
+// (k_restrict_csc); built once per level, before any graph capture.
+static msb_status level_csc_build(msb_ctx ctx, msb_level L) {
+  if (L->csc_ptr) return MSB_OK;
+  const int64_t n = (int64_t)L->W * L->N;
+  if (n >= INT32_MAX) return set_error(ctx, MSB_EDIM, "explicit pattern too large for int32 positions");
+  cudaStream_t st = ctx->stream;
+  const int M = L->M;
+  int32_t* cnt = nullptr;
+  unsigned long long *keys = nullptr, *sorted = nullptr;
+  int* fill = nullptr;
+  void* tmp = nullptr;
+  size_t tmp_bytes = 0;
+  msb_status rc = MSB_OK;
+  int32_t total = 0;
+  int end_bit = 32;
+  while ((1ll << (end_bit - 32)) < (long long)M + 1) ++end_bit;
+  MSB_ALLOC(ctx, L->csc_ptr, int32_t, M + 1);
+  cnt = dalloc_n<int32_t>(ctx, M + 1);
+  keys = dalloc_n<unsigned long long>(ctx, (size_t)L->nnz + 1);
+  sorted = dalloc_n<unsigned long long>(ctx, (size_t)L->nnz + 1);
+  fill = dalloc_n<int>(ctx, 1);
+  L->csc_pos = dalloc_n<int32_t>(ctx, (size_t)L->nnz + 1);
+  if (!cnt || !keys || !sorted || !fill || !L->csc_pos) {
+    rc = set_error(ctx, MSB_ENOMEM, "restriction index");
+    goto out;
+  }
+  if (cudaMemsetAsync(cnt, 0, (M + 1) * sizeof(int32_t), st) != cudaSuccess ||
+      cudaMemsetAsync(fill, 0, sizeof(int), st) != cudaSuccess) {
+    rc = set_error(ctx, MSB_ECUDA, "restriction index memset");
+    goto out;
+  }
+  k_csc_keys<<<grid_for(n, 256), 256, 0, st>>>(L->col, n, cnt, keys, fill);
+  count_launch();
+  cub::DeviceRadixSort::SortKeys(nullptr, tmp_bytes, keys, sorted, (int)L->nnz, 0, end_bit, st);
+  tmp = dalloc(ctx, tmp_bytes + 16);
+  if (!tmp) {
+    rc = set_error(ctx, MSB_ENOMEM, "restriction index sort");
+    goto out;
+  }
+  if (cub::DeviceRadixSort::SortKeys(tmp, tmp_bytes, keys, sorted, (int)L->nnz, 0, end_bit, st) !=
+      cudaSuccess) {
+    rc = set_error(ctx, MSB_ECUDA, "restriction index sort");
+    goto out;
+  }
+  count_launch();
+  k_csc_pos<<<grid_for(L->nnz, 256), 256, 0, st>>>(sorted, L->nnz, L->csc_pos);
+  count_launch();
+  rc = scan_exclusive(ctx, cnt, L->csc_ptr, M + 1, &total);
+  if (!rc && total != L->nnz)
+    rc = set_error(ctx, MSB_EINVAL, "restriction index: %d entries, level has %lld", total,
+                   (long long)L->nnz);
+out:
+  if (cudaGetLastError() != cudaSuccess && !rc) rc = set_error(ctx, MSB_ECUDA, "restriction index build");
+  cudaStreamSynchronize(st);
+  dfree(ctx, cnt);
+  dfree(ctx, keys);
+  dfree(ctx, sorted);
+  dfree(ctx, fill);
+  dfree(ctx, tmp);
+  if (rc) {
+    dfree(ctx, L->csc_ptr);
+    dfree(ctx, L->csc_pos);
+    L->csc_ptr = L->csc_pos = nullptr;
+  }
+  return rc;
+}
+
+static bool use_csc(msb_solver s, msb_level L) {
+  static const bool off = getenv("MSB_NO_CSC") != nullptr;
+  return !off && L->kind == 1 && L->M > RRD_MAX_M && L != s->dyn_level && L->csc_ptr;
+}
+}  // namespace msb
+
 extern "C" {
 
 msb_status msb_solver_create(msb_ctx ctx, msb_op op, const msb_level* levels, int32_t n_levels,
@@ -1285,6 +1403,10 @@ msb_status msb_solver_create(msb_ctx ctx, msb_op op, const msb_level* levels, in
     msb_level L = levels[l];
     if (!L || L->N != op->N) return set_error(ctx, MSB_EDIM, "level %d size mismatch", l);
     if (!L->co.ready) return set_error(ctx, MSB_EINVAL, "level %d not assembled", l);
+    if (L->kind == 1 && L->M > RRD_MAX_M && !getenv("MSB_NO_CSC")) {
+      msb_status rc = level_csc_build(ctx, L);
+      if (rc) return rc;
+    }
     s->levels.push_back(L);
     maxM = std::max(maxM, L->M);
   }
@@ -1499,6 +1621,22 @@ static msb_status enqueue_stage(msb_ctx ctx, msb_solver s, msb_level L, const do
       MSB_LAUNCH_CHECK(ctx);
       coarse_solve_dense(ctx, L->co, s->rc, s->xc, &s->st->done);
       k_prolong_cart<<<g, CT, 0, st>>>(V, s->xbuf[cur], s->xc, s->st);
+      MSB_LAUNCH_CHECK(ctx);
+      return MSB_OK;
+    }
+    if (use_csc(s, L)) {
+      k_residual<<<g4, CT, 0, st>>>(S, s->xbuf[cur], b, s->r, first ? 1 : 0, s->partials, s->st);
+      MSB_LAUNCH_CHECK(ctx);
+      if (first) {
+        msb_status rc = fin(g4);
+        if (rc) return rc;
+      }
+      first = false;
+      k_restrict_csc<<<(unsigned)((L->M + 7) / 8), 256, 0, st>>>(L->csc_ptr, L->csc_pos, L->P[L->cur],
+                                                              s->r, (int)L->N, L->M, s->rc, s->st);
+      MSB_LAUNCH_CHECK(ctx);
+      coarse_solve_dense(ctx, L->co, s->rc, s->xc, &s->st->done);
+      k_prolong<<<g, CT, 0, st>>>(V, s->xbuf[cur], s->xc, s->st);
       MSB_LAUNCH_CHECK(ctx);
       return MSB_OK;
     }

@@ -248,6 +248,8 @@ void level_free(msb_level L) {
   dfree(ctx, L->amask);
   dfree(ctx, L->col);
   dfree(ctx, L->nbs);
+  dfree(ctx, L->csc_ptr);
+  dfree(ctx, L->csc_pos);
   coarse_free(ctx, L->co);
   delete L;
 }

@@ -1,0 +1,61 @@
+// fp64 latency / throughput and CTA-barrier cost on one SM (what bounds the 64x64
+// Cholesky leaf): nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o fp64_probe fp64_probe.cu
+#include <cstdio>
+#include <cuda_runtime.h>
+
+__global__ void k_dfma_chain(double* out, int n, double a) {  // dependent DFMA chain
+  double x = threadIdx.x;
+  for (int i = 0; i < n; ++i) x = fma(x, a, 1e-3);
+  if (x == 12345.0) out[0] = x;
+}
+__global__ void k_dfma_tput(double* out, int n, double a) {  // 8 independent chains
+  double x[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) x[k] = threadIdx.x + k;
+  for (int i = 0; i < n; ++i)
+#pragma unroll
+    for (int k = 0; k < 8; ++k) x[k] = fma(x[k], a, 1e-3);
+  double s = 0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) s += x[k];
+  if (s == 12345.0) out[0] = s;
+}
+__global__ void k_sqrt_rcp_chain(double* out, int n) {
+  double x = 2.0 + threadIdx.x;
+  for (int i = 0; i < n; ++i) x = 1.0 / sqrt(x) + 2.0;
+  if (x == 12345.0) out[0] = x;
+}
+__global__ void k_bar(double* out, int n) {
+  for (int i = 0; i < n; ++i) __syncthreads();
+  if (threadIdx.x == 9999) out[0] = 1;
+}
+
+int main() {
+  double* d;
+  cudaMalloc(&d, 8);
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  const int n = 4096;
+  auto run = [&](const char* name, auto launch, double per) {
+    launch();
+    cudaDeviceSynchronize();
+    cudaEventRecord(a);
+    launch();
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+    float ms;
+    cudaEventElapsedTime(&ms, a, b);
+    printf("%-34s %9.3f us  %8.2f ns/op  %7.1f cycles/op @1.965GHz\n", name, ms * 1e3, ms * 1e6 / per,
+           ms * 1e6 / per * 1.965);
+  };
+  run("dfma chain, 1 warp", [&] { k_dfma_chain<<<1, 32>>>(d, n, 0.999); }, n);
+  run("dfma chain, 32 warps (1 SM)", [&] { k_dfma_chain<<<1, 1024>>>(d, n, 0.999); }, n);
+  run("dfma 8 chains, 1 warp", [&] { k_dfma_tput<<<1, 32>>>(d, n, 0.999); }, n);
+  run("dfma 8 chains, 32 warps (1 SM)", [&] { k_dfma_tput<<<1, 1024>>>(d, n, 0.999); }, n);
+  run("1/sqrt chain, 1 warp", [&] { k_sqrt_rcp_chain<<<1, 32>>>(d, n); }, n);
+  run("1/sqrt chain, 32 warps", [&] { k_sqrt_rcp_chain<<<1, 1024>>>(d, n); }, n);
+  run("__syncthreads, 1024 threads", [&] { k_bar<<<1, 1024>>>(d, n); }, n);
+  run("__syncthreads, 256 threads", [&] { k_bar<<<1, 256>>>(d, n); }, n);
+  return 0;
+}
