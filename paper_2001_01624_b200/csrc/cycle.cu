@@ -1043,11 +1043,22 @@ __global__ void k_dp(const double* __restrict__ x, const double* __restrict__ xp
   if (c < N) dp[c] = x[c] - xp[c];
 }
 
-__global__ void k_absmax_vec(const double* __restrict__ dp, int64_t N, unsigned long long* mx) {
-  int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  double a = c < N ? fabs(dp[c]) : 0.0;
+// max|dp| (bit pattern of a non-negative double orders like the value): grid-stride,
+// block reduction, one atomic per CTA (one per warp contended on the single word: 27 us)
+__global__ void __launch_bounds__(256) k_absmax_vec(const double* __restrict__ dp, int64_t N,
+                                                    unsigned long long* mx) {
+  double a = 0.0;
+  for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < N;
+       c += (int64_t)gridDim.x * blockDim.x)
+    a = fmax(a, fabs(dp[c]));
   for (int o = 16; o > 0; o >>= 1) a = fmax(a, __shfl_xor_sync(0xffffffffu, a, o));
-  if ((threadIdx.x & 31) == 0) atomicMax(mx, (unsigned long long)__double_as_longlong(a));
+  __shared__ double wm[8];
+  if ((threadIdx.x & 31) == 0) wm[threadIdx.x >> 5] = a;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) a = fmax(a, wm[w]);
+    atomicMax(mx, (unsigned long long)__double_as_longlong(a));
+  }
 }
 
 __global__ void k_bins(const double* __restrict__ dp, int64_t N, const unsigned long long* mx,
@@ -1163,18 +1174,11 @@ static msb_status build_dynamic(msb_ctx ctx, msb_solver s, const double* dp, int
   int32_t* counts = s->scratch_i + 2;
   int32_t* rep = s->scratch_i + 8;
   MSB_CUDA_TRY(ctx, cudaMemsetAsync(mx, 0, 8, st));
-  k_absmax_vec<<<grid_for(N, 256), 256, 0, st>>>(dp, N, mx);
+  k_absmax_vec<<<(unsigned)std::min<int64_t>(grid_for(N, 256), 2 * ctx->sm_count), 256, 0, st>>>(dp, N, mx);
   MSB_LAUNCH_CHECK(ctx);
-  unsigned long long hm = 0;
-  MSB_CUDA_TRY(ctx, cudaMemcpyAsync(&hm, mx, 8, cudaMemcpyDeviceToHost, st));
-  MSB_CUDA_TRY(ctx, cudaStreamSynchronize(st));
-  double m;
-  memcpy(&m, &hm, 8);
-  if (!(m > 0.0)) {  // max|Δp| = 0: stage skipped
-    *M_out = 0;
-    return MSB_OK;
-  }
   lap(0);
+  // max|Δp| is read back with the first merge count (no synchronisation of its own); when
+  // it is 0 the stage is skipped there
   k_bins<<<grid_for(N, 256), 256, 0, st>>>(dp, N, mx, s->edge0, s->edge1, s->bins);
   MSB_LAUNCH_CHECK(ctx);
   msb_status rc = cc_label(ctx, op, s->bins, s->lab, false, nullptr);
@@ -1188,9 +1192,18 @@ static msb_status build_dynamic(msb_ctx ctx, msb_solver s, const double* dp, int
     MSB_CUDA_TRY(ctx, cudaMemsetAsync(counts, 0, 4 * sizeof(int32_t), st));
     k_merge_count<<<grid_for(N, 256), 256, 0, st>>>(s->lab, s->cnt, s->bins, N, smin, counts);
     MSB_LAUNCH_CHECK(ctx);
-    int32_t hc[4];
-    MSB_CUDA_TRY(ctx, cudaMemcpyAsync(hc, counts, sizeof(hc), cudaMemcpyDeviceToHost, st));
+    int32_t hb[6];  // scratch_i[0..1] = max|Δp| bits, [2..5] = counts: one readback
+    MSB_CUDA_TRY(ctx, cudaMemcpyAsync(hb, s->scratch_i, sizeof(hb), cudaMemcpyDeviceToHost, st));
     MSB_CUDA_TRY(ctx, cudaStreamSynchronize(st));
+    if (smin == 1) {
+      double m;
+      memcpy(&m, hb, 8);
+      if (!(m > 0.0)) {  // max|Δp| = 0: stage skipped
+        *M_out = 0;
+        return MSB_OK;
+      }
+    }
+    const int32_t* hc = hb + 2;
     int nb = hc[0] + hc[1] + hc[2] + hc[3];
     if (nb <= s->dyn_max || (int64_t)smin > N) break;
     smin *= 2;
