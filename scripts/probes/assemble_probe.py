@@ -12,7 +12,8 @@ prob = make_problem(3)
 ctx = Context(0)
 op = gp.build_operator(ctx, prob)
 N = prob.N
-for M in (40, 165, 168, 200, 400):
+Ms = [int(a) for a in sys.argv[1:]] or [40, 165, 168, 200, 400]
+for M in Ms:
     part = (np.arange(N, dtype=np.int64) * M // N).astype(np.int32)  # M contiguous slabs
     lev = Level.constant(ctx, op, part, M)
     for _ in range(3):

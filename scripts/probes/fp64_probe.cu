@@ -30,6 +30,29 @@ __global__ void k_bar(double* out, int n) {
   if (threadIdx.x == 9999) out[0] = 1;
 }
 
+
+// one 64-step pivot chain through shared memory: read d, rsqrt, write the next, barrier
+__global__ void k_pivot_chain(double* out, int steps, int rs) {
+  __shared__ double sd[128];
+  if (threadIdx.x < 128) sd[threadIdx.x] = 2.0 + threadIdx.x;
+  __syncthreads();
+  double acc = 0;
+  for (int j = 0; j < steps; ++j) {
+    const double d = sd[j & 63];
+    const double inv = rs ? rsqrt(d) : 1.0 / sqrt(d);
+    acc += inv;
+    if (threadIdx.x == (j & 127)) sd[(j + 1) & 63] = fma(d, 1e-9, 2.0 + inv * 1e-12);
+    __syncthreads();
+  }
+  if (acc == 12345.0) out[0] = acc;
+}
+__global__ void k_ldg_loop(const double* in, double* out, int per) {  // per sequential loads
+  __shared__ double sm[4096];
+  for (int e = threadIdx.x; e < per * blockDim.x; e += blockDim.x) sm[e & 4095] = in[e];
+  __syncthreads();
+  if (sm[threadIdx.x] == 12345.0) out[0] = 1;
+}
+
 int main() {
   double* d;
   cudaMalloc(&d, 8);
@@ -57,5 +80,14 @@ int main() {
   run("1/sqrt chain, 32 warps", [&] { k_sqrt_rcp_chain<<<1, 1024>>>(d, n); }, n);
   run("__syncthreads, 1024 threads", [&] { k_bar<<<1, 1024>>>(d, n); }, n);
   run("__syncthreads, 256 threads", [&] { k_bar<<<1, 256>>>(d, n); }, n);
+  run("pivot chain rsqrt, 128 thr, 64 steps", [&] { k_pivot_chain<<<1, 128>>>(d, 64, 1); }, 64);
+  run("pivot chain 1/sqrt, 128 thr, 64 steps", [&] { k_pivot_chain<<<1, 128>>>(d, 64, 0); }, 64);
+  run("pivot chain rsqrt, 1024 thr, 64 steps", [&] { k_pivot_chain<<<1, 1024>>>(d, 64, 1); }, 64);
+  double* big;
+  cudaMalloc(&big, 8 << 20);
+  cudaMemset(big, 0, 8 << 20);
+  run("32 sequential LDG per thread, 128 thr", [&] { k_ldg_loop<<<1, 128>>>(big, d, 32); }, 32);
+  run("4 sequential LDG per thread, 1024 thr", [&] { k_ldg_loop<<<1, 1024>>>(big, d, 4); }, 4);
+  run("empty launch", [&] { k_bar<<<1, 32>>>(d, 0); }, 1);
   return 0;
 }
