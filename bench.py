@@ -183,10 +183,28 @@ class Clocks:
         try:
             self.f = open(self.path, "w")
             self.p = subprocess.Popen(["nvidia-smi", f"--id={self.idx}", f"--query-gpu={q}",
-                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                       "--format=csv,noheader,nounits", "-lms", "100"],
                                       stdout=self.f, stderr=subprocess.DEVNULL)
         except Exception:
             self.p = None
+            return
+        # nvidia-smi takes a while to produce its first sample: wait for it, so that the
+        # (short) timed region is sampled; only lines written after mark() count
+        t0 = time.time()
+        while time.time() - t0 < 10 and self.p.poll() is None:
+            self.f.flush()
+            if os.path.getsize(self.path) > 0:
+                break
+            time.sleep(0.05)
+        self.skip = 0
+
+    def mark(self):
+        """Start of the timed region: samples written so far are not counted."""
+        try:
+            with open(self.path) as f:
+                self.skip = sum(1 for _ in f)
+        except OSError:
+            self.skip = 0
 
     def stop(self):
         if self.p is None:
@@ -199,7 +217,7 @@ class Clocks:
         self.f.close()
         sm, mx, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for line in open(self.path):
+        for line in list(open(self.path))[getattr(self, "skip", 0):]:
             parts = [s.strip() for s in line.split(",")]
             if len(parts) < 9:
                 continue
@@ -266,12 +284,13 @@ def run_gpu(args):
     for _ in range(args.warmup):
         step(K_dev)
     clocks = Clocks(local)
+    clocks.start()
     flush.zero_()
     torch.cuda.synchronize()
     if dist:
         dist.barrier()
+    clocks.mark()
     launches0 = ctx.launch_count()
-    clocks.start()
     infos = []
     for _ in range(args.steps):
         flush.zero_()  # L2 flush between steps (256 MB write)
