@@ -610,11 +610,25 @@ __global__ void __launch_bounds__(256) k_restrict_csc(const int32_t* __restrict_
   const int lane = threadIdx.x & 31;
   if (w >= M) return;  // warp-uniform
   const int k1 = ptr[w + 1];
-  double t = 0.0;
-  for (int k = ptr[w] + lane; k < k1; k += 32) {
-    const int p = pos[k];
-    t += P[p] * r[p - (p / N) * N];
+  // four independent chains per lane (positions k, k+32, k+64, k+96): the dependent
+  // index -> value loads of one column overlap; partial sums combined in a fixed order
+  double t0 = 0.0, t1 = 0.0, t2 = 0.0, t3 = 0.0;
+  int k = ptr[w] + lane;
+  for (; k + 96 < k1; k += 128) {
+    const int p0 = pos[k], p1 = pos[k + 32], p2 = pos[k + 64], p3 = pos[k + 96];
+    const double a0 = P[p0], a1 = P[p1], a2 = P[p2], a3 = P[p3];
+    const double b0 = r[p0 - (p0 / N) * N], b1 = r[p1 - (p1 / N) * N], b2 = r[p2 - (p2 / N) * N],
+                 b3 = r[p3 - (p3 / N) * N];
+    t0 = fma(a0, b0, t0);
+    t1 = fma(a1, b1, t1);
+    t2 = fma(a2, b2, t2);
+    t3 = fma(a3, b3, t3);
   }
+  for (; k < k1; k += 32) {
+    const int p = pos[k];
+    t0 = fma(P[p], r[p - (p / N) * N], t0);
+  }
+  double t = (t0 + t1) + (t2 + t3);
   for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
   if (lane == 0) rc[w] = t;
 }
