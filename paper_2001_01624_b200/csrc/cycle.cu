@@ -669,7 +669,24 @@ __global__ void __launch_bounds__(CT) k_prolong(LevelView L, double* __restrict_
       if (key >= 0) acc += L.P[(size_t)s * N + c] * xc[key];
     }
   } else {
-    for (int s = 0; s < L.W; ++s) {
+    // four slots at a time: their column and value loads, then the x_c gathers, are
+    // independent and overlap; the sum is still taken in slot order
+    int s = 0;
+    for (; s + 4 <= L.W; s += 4) {
+      int key[4];
+      double p[4], v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        key[u] = L.col[(size_t)(s + u) * N + c];
+        p[u] = L.P[(size_t)(s + u) * N + c];
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) v[u] = key[u] >= 0 ? p[u] * xc[key[u]] : 0.0;
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (key[u] >= 0) acc += v[u];
+    }
+    for (; s < L.W; ++s) {
       int key = L.col[(size_t)s * N + c];
       if (key >= 0) acc += L.P[(size_t)s * N + c] * xc[key];
     }
