@@ -67,17 +67,28 @@ __global__ void k_absmax_t(const double* __restrict__ T, int64_t n, unsigned lon
   if ((threadIdx.x & 31) == 0) atomicMax(out, (unsigned long long)__double_as_longlong(m));
 }
 
-__device__ __forceinline__ void fx_add(unsigned long long* e, double v, int F) {
+// v 2^F as a 128-bit two's-complement integer (lo, hi), truncated toward zero
+__device__ __forceinline__ void fx_of(double v, int F, unsigned long long& lo, unsigned long long& hi) {
   const bool neg = v < 0.0;
   const double t = ldexp(fabs(v), F);  // < 2^92, exact power-of-two scaling
-  unsigned long long hi = (unsigned long long)floor(ldexp(t, -64));
-  unsigned long long lo = (unsigned long long)(t - ldexp((double)hi, 64));
+  hi = (unsigned long long)floor(ldexp(t, -64));
+  lo = (unsigned long long)(t - ldexp((double)hi, 64));
   if (neg) {  // two's complement of (hi, lo)
     lo = ~lo + 1ull;
     hi = ~hi + (lo == 0ull ? 1ull : 0ull);
   }
+}
+
+__device__ __forceinline__ void fx_add_raw(unsigned long long* e, unsigned long long lo,
+                                           unsigned long long hi) {
   const unsigned long long old = atomicAdd(e, lo);
   atomicAdd(e + 1, hi + (old + lo < old ? 1ull : 0ull));
+}
+
+__device__ __forceinline__ void fx_add(unsigned long long* e, double v, int F) {
+  unsigned long long lo, hi;
+  fx_of(v, F, lo, hi);
+  fx_add_raw(e, lo, hi);
 }
 
 // Unsigned 128-bit fixed point (lo, hi) of t = v 2^F for v >= 0 (fx_add's conversion).
@@ -206,9 +217,51 @@ __global__ void k_fx_to_double(const unsigned long long* __restrict__ acc, int64
   Ac[e] = fx_value(acc[2 * e], acc[2 * e + 1], F);
 }
 
+// Rows of P summing to one (MsRSB's partition of unity) make sum_b (A_c)_ab over the face
+// terms vanish, so k_rap<true, true> accumulates only the lower off-diagonal entries (half
+// the atomics, and none on the diagonal — the entries every face of a support hits) and
+// the diagonal is minus the row's off-diagonal total plus the diagonal slot (the gauge
+// term's correction).  Equal to the direct sum up to the rounding of P's row sums.
+__global__ void __launch_bounds__(256) k_fx_sym_to_double(const unsigned long long* __restrict__ acc,
+                                                          int M,
+                                                          const unsigned long long* __restrict__ tmax_bits,
+                                                          double* __restrict__ Ac) {
+  const int a = blockIdx.x;
+  const int F = 90 - ilogb(__longlong_as_double((long long)*tmax_bits));
+  unsigned long long slo = 0, shi = 0;
+  for (int b = threadIdx.x; b < M; b += blockDim.x) {
+    if (b == a) continue;
+    const size_t e = a > b ? (size_t)a * M + b : (size_t)b * M + a;
+    const unsigned long long lo = acc[2 * e], hi = acc[2 * e + 1];
+    Ac[(size_t)a * M + b] = fx_value(lo, hi, F);
+    add128(slo, shi, lo, hi);
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long ylo = __shfl_xor_sync(0xffffffffu, slo, o);
+    const unsigned long long yhi = __shfl_xor_sync(0xffffffffu, shi, o);
+    add128(slo, shi, ylo, yhi);
+  }
+  __shared__ unsigned long long wl[8], wh[8];
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) {
+    wl[w] = slo;
+    wh[w] = shi;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long lo = wl[0], hi = wh[0];
+    for (int v = 1; v < (int)(blockDim.x >> 5); ++v) add128(lo, hi, wl[v], wh[v]);
+    // diagonal = slot(a, a) - row total (two's complement)
+    const unsigned long long nlo = ~lo + 1ull, nhi = ~hi + (nlo == 0ull ? 1ull : 0ull);
+    unsigned long long dlo = acc[2 * ((size_t)a * M + a)], dhi = acc[2 * ((size_t)a * M + a) + 1];
+    add128(dlo, dhi, nlo, nhi);
+    Ac[(size_t)a * M + a] = fx_value(dlo, dhi, F);
+  }
+}
+
 // FX: accumulate into the 128-bit fixed-point buffer (deterministic, see above) instead of
 // fp64 atomics; |T g_a g_b| <= max T because P entries lie in [0, 1]
-template <bool FX>
+template <bool FX, bool SYM>
 __global__ void k_rap(const msb_level_s L, const double* __restrict__ P, const double* __restrict__ Tx,
                       const double* __restrict__ Ty, const double* __restrict__ Tz,
                       double* __restrict__ Ac, unsigned long long* __restrict__ acc,
@@ -260,18 +313,44 @@ __global__ void k_rap(const msb_level_s L, const double* __restrict__ P, const d
       double ta = T * gv[a];
       for (int b = 0; b < ng; ++b) {
         if (gv[b] == 0.0) continue;
-        if (FX) fx_add(acc + 2 * ((int64_t)gc[a] * M + gc[b]), ta * gv[b], F);
-        else atomicAdd(Ac + (int64_t)gc[a] * M + gc[b], ta * gv[b]);
+        if (FX && SYM) {
+          // symmetric and row-sum-free: one add per unordered pair into its lower entry;
+          // the diagonal is formed from the row in k_fx_sym_to_double
+          if (gc[a] > gc[b]) fx_add(acc + 2 * ((int64_t)gc[a] * M + gc[b]), ta * gv[b], F);
+        } else if (FX) {
+          fx_add(acc + 2 * ((int64_t)gc[a] * M + gc[b]), ta * gv[b], F);
+        } else {
+          atomicAdd(Ac + (int64_t)gc[a] * M + gc[b], ta * gv[b]);
+        }
       }
     }
   }
   if (c == 0) {  // gauge: A_00 doubled adds A^T_00 (P_0.)^T P_0.
     double d0 = Tf[0] + 0.0 + Tf[1] + 0.0 + Tf[2] + 0.0;
-    for (int a = 0; a < nc; ++a)
-      for (int b = 0; b < nc; ++b) {
-        if (FX) fx_add(acc + 2 * ((int64_t)cc[a] * M + cc[b]), d0 * cv[a] * cv[b], F);
-        else atomicAdd(Ac + (int64_t)cc[a] * M + cc[b], d0 * cv[a] * cv[b]);
+    for (int a = 0; a < nc; ++a) {
+      if (FX && SYM) {
+        // off-diagonal gauge terms join the pair sums; the diagonal slot takes the gauge
+        // diagonal plus the row's gauge off-diagonals (same integers), which the
+        // conversion's row sum removes again
+        unsigned long long dlo, dhi;
+        fx_of(d0 * cv[a] * cv[a], F, dlo, dhi);
+        for (int b = 0; b < nc; ++b) {
+          if (b == a) continue;
+          unsigned long long lo, hi;
+          fx_of(d0 * cv[a] * cv[b], F, lo, hi);
+          const unsigned long long s2 = dlo + lo;
+          dhi += hi + (s2 < dlo ? 1ull : 0ull);
+          dlo = s2;
+          if (cc[a] > cc[b]) fx_add_raw(acc + 2 * ((int64_t)cc[a] * M + cc[b]), lo, hi);
+        }
+        fx_add_raw(acc + 2 * ((int64_t)cc[a] * M + cc[a]), dlo, dhi);
+      } else {
+        for (int b = 0; b < nc; ++b) {
+          if (FX) fx_add(acc + 2 * ((int64_t)cc[a] * M + cc[b]), d0 * cv[a] * cv[b], F);
+          else atomicAdd(Ac + (int64_t)cc[a] * M + cc[b], d0 * cv[a] * cv[b]);
+        }
       }
+    }
   }
 }
 
@@ -474,19 +553,25 @@ msb_status coarse_assemble_dense(msb_ctx ctx, msb_level L, msb_op op) {
       k_rap_const_det<<<grid_for(op->N, 256), 256, 0, st>>>(
           L->col, make_grid3(op->nx, op->ny, op->nz), M, op->Tx, op->Ty, op->Tz, tmax, co.acc);
     } else {
-      k_rap<true><<<grid_for(L->N, 128), 128, 0, st>>>(*L, L->P[L->cur], op->Tx, op->Ty, op->Tz,
-                                                       co.Ac, co.acc, tmax);
+      if (L->unity && !getenv("MSB_RAP_FULL"))
+        k_rap<true, true><<<grid_for(L->N, 128), 128, 0, st>>>(*L, L->P[L->cur], op->Tx, op->Ty,
+                                                              op->Tz, co.Ac, co.acc, tmax);
+      else
+        k_rap<true, false><<<grid_for(L->N, 128), 128, 0, st>>>(*L, L->P[L->cur], op->Tx, op->Ty,
+                                                               op->Tz, co.Ac, co.acc, tmax);
     }
     MSB_LAUNCH_CHECK(ctx);
     if (L->kind == 1 && L->W == 1)
       k_fx_const_to_double<<<M, 256, 0, st>>>(co.acc, M, tmax, co.Ac);
+    else if (L->unity && !getenv("MSB_RAP_FULL"))
+      k_fx_sym_to_double<<<M, 256, 0, st>>>(co.acc, M, tmax, co.Ac);
     else
       k_fx_to_double<<<grid_for((int64_t)n, 256), 256, 0, st>>>(co.acc, (int64_t)n, tmax, co.Ac);
     MSB_LAUNCH_CHECK(ctx);
     return coarse_factor_dense(ctx, co);
   }
   MSB_CUDA_TRY(ctx, cudaMemsetAsync(co.Ac, 0, (size_t)M * M * sizeof(double), st));
-  k_rap<false><<<grid_for(L->N, 128), 128, 0, st>>>(*L, L->P[L->cur], op->Tx, op->Ty, op->Tz,
+  k_rap<false, false><<<grid_for(L->N, 128), 128, 0, st>>>(*L, L->P[L->cur], op->Tx, op->Ty, op->Tz,
                                                     co.Ac, nullptr, nullptr);
   MSB_LAUNCH_CHECK(ctx);
   return coarse_factor_dense(ctx, co);

@@ -406,6 +406,7 @@ msb_status msb_level_import_values(msb_ctx ctx, msb_level L, const double* vals)
   const double* d = (const double*)stage_in(ctx, vals, (size_t)total * sizeof(double), &o);
   k_import_csr<<<grid_for(N, 128), 128, 0, ctx->stream>>>(*L, L->P[L->cur], start, d);
   MSB_LAUNCH_CHECK(ctx);
+  L->unity = false;  // arbitrary values: the coarse assembly accumulates every entry
   MSB_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
   if (o) dfree(ctx, o);
   dfree(ctx, cnt);

@@ -901,6 +901,7 @@ extern "C" msb_status msb_smooth_basis(msb_ctx ctx, msb_level L, msb_op op, int3
       return set_error(ctx, MSB_EZERO_DIAG, "zero diagonal in A_T (a cell with no open face)");
     }
   }
+  L->unity = true;  // every sweep renormalises the rows of P to sum to one
   if (L->kind == 0 && !L->amask) {
     int tot = op->nx + op->ny + op->nz;
     MSB_ALLOC(ctx, L->amask, uint8_t, tot);

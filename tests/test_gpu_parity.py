@@ -139,6 +139,36 @@ def test_rap_parity_lockstep(ctx, shape):
     assert np.max(np.abs(Ac - ref)) <= 1e-12 * np.abs(ref).max()
 
 
+@pytest.mark.parametrize("shape", [(24, 44, 20), (23, 17, 7)])
+def test_rap_symmetric_row_sum_path(ctx, shape, monkeypatch):
+    """Smoothed (partition-of-unity) levels assemble only the lower off-diagonal pair sums
+    and form the diagonal from the row: against the full accumulation (MSB_RAP_FULL=1)
+    and against scipy P^T A P of the exported P."""
+    import scipy.sparse as sp
+    from oracle import coarse, tpfa
+    from paper_2001_01624_b200 import Level
+    from paper_2001_01624_b200.pipeline import build_operator
+    prob = make_problem(2, shape=shape) if shape[0] == 24 else random_problem(
+        5, *shape, (5, 4, 3), sigma=2.0)
+    A_T, A, q, _ = tpfa.build(prob)
+    op = build_operator(ctx, prob)
+    lev = Level.cartesian(ctx, op, prob.block)
+    lev.smooth(op, 30, prob.omega, -1.0)
+    lev.assemble(op)
+    rowptr, cols, vals, Ac_sym = lev.export(with_Ac=True)
+    monkeypatch.setenv("MSB_RAP_FULL", "1")
+    lev.assemble(op)
+    _, _, _, Ac_full = lev.export(with_Ac=True)
+    monkeypatch.delenv("MSB_RAP_FULL")
+    scale = np.abs(Ac_full).max()
+    assert np.max(np.abs(Ac_sym - Ac_full)) <= 1e-13 * scale
+    assert np.array_equal(Ac_sym, Ac_sym.T)
+    P = sp.csr_matrix((vals, cols, rowptr), shape=(prob.N, Ac_sym.shape[0]))
+    ref = coarse.galerkin(P, A)
+    ref = ref.toarray() if hasattr(ref, "toarray") else np.asarray(ref)
+    assert np.max(np.abs(Ac_sym - ref)) <= 1e-12 * np.abs(ref).max()
+
+
 @pytest.mark.parametrize("M", [1, 7, 160, 1100])
 def test_rap_constant_basis_parity(ctx, M):
     """Constant-basis A_c (dynamic / halo-0 levels: pair sums with warp-aggregated exact
