@@ -173,7 +173,9 @@ msb_status msb_level_info(msb_ctx ctx, msb_level lev, int32_t* M, int64_t* nnz, 
  * (host|dev, NULL skips; requires a dense coarse operator). */
 msb_status msb_level_export(msb_ctx ctx, msb_level lev, int64_t* rowptr, int32_t* cols,
                             double* vals, double* Ac_dense);
-/* Overwrite P from CSR (same pattern as exported; host|dev) — lockstep tests. */
+/* Overwrite P from CSR (same pattern as exported; host|dev) — lockstep tests.  Imported
+ * rows need not sum to one: the level's next msb_coarse_assemble accumulates every entry
+ * of A_c (until a msb_smooth_basis call renormalises the rows again). */
 msb_status msb_level_import_values(msb_ctx ctx, msb_level lev, const double* vals);
 msb_status msb_level_destroy(msb_level lev);
 
@@ -194,7 +196,11 @@ msb_status msb_smooth_basis(msb_ctx ctx, msb_level lev, msb_op op, int32_t max_s
  *   A_c = Σ_f T_f (P_i. - P_l.)^T (P_i. - P_l.) + A_00^T (P_0.)^T P_0.  (gauge term),
  * then factorised on the device (SPD Cholesky = LU without pivoting for SPD A_c,
  * PAPER.md:410) and, for dense A_c, inverted so that each coarse solve is one GEMV.
- * Returns MSB_ESINGULAR if a pivot is <= 1e-14 * max|A_c|. */
+ * For M <= 8192 the sum is exact in 128-bit fixed point (run-to-run identical); when the
+ * rows of P sum to one (created or smoothed levels: MsRSB's partition of unity) each face
+ * adds only the lower off-diagonal products and the diagonal is minus the row's
+ * off-diagonal total plus the gauge term — the same matrix up to the rounding of P's row
+ * sums.  Returns MSB_ESINGULAR if a pivot is <= 1e-14 * max|A_c|. */
 msb_status msb_coarse_assemble(msb_ctx ctx, msb_level lev, msb_op op);
 
 /* ---------------------------------------------------------------- solver (rows a6–a11)
