@@ -158,7 +158,8 @@ __global__ void k_scan_total(const int32_t* __restrict__ in, const int32_t* __re
 // Exclusive prefix sum of n int32 (device); *total (host, optional) = sum of all, read
 // back with one synchronisation.  Scratch is the context's, reused across calls.
 msb_status scan_exclusive(msb_ctx ctx, const int32_t* in, int32_t* out, int64_t n,
-                          int32_t* total) {
+                          int32_t* total, const void* extra_dev, void* extra_host,
+                          size_t extra_bytes) {
   if (n <= 0) {
     if (total) *total = 0;
     return MSB_OK;
@@ -185,6 +186,9 @@ msb_status scan_exclusive(msb_ctx ctx, const int32_t* in, int32_t* out, int64_t 
     MSB_LAUNCH_CHECK(ctx);
     int32_t h = 0;
     MSB_CUDA_TRY(ctx, cudaMemcpyAsync(&h, tot, 4, cudaMemcpyDeviceToHost, ctx->stream));
+    if (extra_bytes)  // a caller's value read back under the same synchronisation
+      MSB_CUDA_TRY(ctx, cudaMemcpyAsync(extra_host, extra_dev, extra_bytes, cudaMemcpyDeviceToHost,
+                                        ctx->stream));
     MSB_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
     *total = h;
   }

@@ -1128,21 +1128,57 @@ __global__ void k_merge_count(const int32_t* __restrict__ lab, const int32_t* __
   else atomicExch(counts + 1 + bins[c], 1);
 }
 
+// smin_dev (if set) overrides smin: the threshold chosen on the device (k_pick_smin)
 __global__ void k_merge_rep(const int32_t* __restrict__ lab, const int32_t* __restrict__ cnt,
                             const int32_t* __restrict__ bins, int64_t N, int smin,
-                            int32_t* __restrict__ rep) {
+                            int32_t* __restrict__ rep, const int32_t* smin_dev = nullptr) {
   int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= N) return;
+  if (smin_dev) smin = *smin_dev;
   if (cnt[lab[c]] < smin) atomicMin(rep + bins[c], (int32_t)c);
 }
 
 __global__ void k_merge_label(int32_t* __restrict__ lab, const int32_t* __restrict__ cnt,
                               const int32_t* __restrict__ bins, int64_t N, int smin,
-                              const int32_t* __restrict__ rep, int32_t* __restrict__ out) {
+                              const int32_t* __restrict__ rep, int32_t* __restrict__ out,
+                              const int32_t* smin_dev = nullptr) {
   int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= N) return;
+  if (smin_dev) smin = *smin_dev;
   int32_t r = lab[c];
   out[c] = cnt[r] < smin ? rep[bins[c]] : r;
+}
+
+// The A15 merge threshold without a host round trip: one pass histograms the component
+// sizes by floor(log2) — over all roots and per bin — and k_pick_smin replays the host
+// rule on the histograms: s_min = 1, 2, 4, ... until (#roots with size >= s_min) + (#bins
+// with a component smaller than s_min) <= max_blocks or s_min > N.  For s_min = 2^s,
+// "size >= s_min" is exactly "floor(log2 size) >= s".  hist[0..31] all roots, hist[32 +
+// 32 b + k] bin b; hist[128] = s_min; hist[129..131] = the per-bin representatives.
+__global__ void k_size_hist(const int32_t* __restrict__ lab, const int32_t* __restrict__ cnt,
+                            const int32_t* __restrict__ bins, int64_t N, int32_t* __restrict__ hist) {
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= N || lab[c] != (int32_t)c) return;
+  const int k = 31 - __clz(max(cnt[c], 1));
+  atomicAdd(hist + k, 1);
+  atomicAdd(hist + 32 + 32 * bins[c] + k, 1);
+}
+
+__global__ void k_pick_smin(int32_t* __restrict__ hist, int max_blocks, int64_t N) {
+  if (threadIdx.x != 0) return;
+  int64_t smin = 1;
+  for (int s = 0;; ++s, smin *= 2) {
+    long long nb = 0;
+    for (int k = s; k < 32; ++k) nb += hist[k];
+    for (int b = 0; b < 3; ++b) {
+      int small = 0;
+      for (int k = 0; k < s && k < 32; ++k) small += hist[32 + 32 * b + k];
+      nb += small > 0;
+    }
+    if (nb <= max_blocks || smin > N || s >= 31) break;
+  }
+  hist[128] = (int32_t)smin;
+  hist[129] = hist[130] = hist[131] = INT32_MAX;
 }
 
 // NEXT-3 indicator partition: bin = #{e : edges[e] <= |ind|} (absolute edges)
@@ -1202,14 +1238,12 @@ static msb_status build_dynamic(msb_ctx ctx, msb_solver s, const double* dp, int
     tq = t;
   };
   unsigned long long* mx = reinterpret_cast<unsigned long long*>(s->scratch_i);
-  int32_t* counts = s->scratch_i + 2;
-  int32_t* rep = s->scratch_i + 8;
   MSB_CUDA_TRY(ctx, cudaMemsetAsync(mx, 0, 8, st));
   k_absmax_vec<<<(unsigned)std::min<int64_t>(grid_for(N, 256), 2 * ctx->sm_count), 256, 0, st>>>(dp, N, mx);
   MSB_LAUNCH_CHECK(ctx);
   lap(0);
-  // max|Δp| is read back with the first merge count (no synchronisation of its own); when
-  // it is 0 the stage is skipped there
+  // max|Δp| is read back with the block count (no synchronisation of its own); when it is
+  // 0 the stage is skipped there
   k_bins<<<grid_for(N, 256), 256, 0, st>>>(dp, N, mx, s->edge0, s->edge1, s->bins);
   MSB_LAUNCH_CHECK(ctx);
   msb_status rc = cc_label(ctx, op, s->bins, s->lab, false, nullptr);
@@ -1218,38 +1252,34 @@ static msb_status build_dynamic(msb_ctx ctx, msb_solver s, const double* dp, int
   MSB_CUDA_TRY(ctx, cudaMemsetAsync(s->cnt, 0, N * sizeof(int32_t), st));
   k_sizes<<<grid_for(N, 256), 256, 0, st>>>(s->lab, N, s->cnt);
   MSB_LAUNCH_CHECK(ctx);
-  int smin = 1;
-  while (true) {
-    MSB_CUDA_TRY(ctx, cudaMemsetAsync(counts, 0, 4 * sizeof(int32_t), st));
-    k_merge_count<<<grid_for(N, 256), 256, 0, st>>>(s->lab, s->cnt, s->bins, N, smin, counts);
-    MSB_LAUNCH_CHECK(ctx);
-    int32_t hb[6];  // scratch_i[0..1] = max|Δp| bits, [2..5] = counts: one readback
-    MSB_CUDA_TRY(ctx, cudaMemcpyAsync(hb, s->scratch_i, sizeof(hb), cudaMemcpyDeviceToHost, st));
-    MSB_CUDA_TRY(ctx, cudaStreamSynchronize(st));
-    if (smin == 1) {
-      double m;
-      memcpy(&m, hb, 8);
-      if (!(m > 0.0)) {  // max|Δp| = 0: stage skipped
-        *M_out = 0;
-        return MSB_OK;
-      }
-    }
-    const int32_t* hc = hb + 2;
-    int nb = hc[0] + hc[1] + hc[2] + hc[3];
-    if (nb <= s->dyn_max || (int64_t)smin > N) break;
-    smin *= 2;
-  }
-  int32_t big[3] = {INT32_MAX, INT32_MAX, INT32_MAX};
-  MSB_CUDA_TRY(ctx, cudaMemcpyAsync(rep, big, sizeof(big), cudaMemcpyHostToDevice, st));
-  k_merge_rep<<<grid_for(N, 256), 256, 0, st>>>(s->lab, s->cnt, s->bins, N, smin, rep);
+  // merge threshold on the device (k_size_hist + k_pick_smin): no readback here
+  MSB_CUDA_TRY(ctx, cudaMemsetAsync(s->mhist, 0, 132 * sizeof(int32_t), st));
+  k_size_hist<<<grid_for(N, 256), 256, 0, st>>>(s->lab, s->cnt, s->bins, N, s->mhist);
   MSB_LAUNCH_CHECK(ctx);
-  k_merge_label<<<grid_for(N, 256), 256, 0, st>>>(s->lab, s->cnt, s->bins, N, smin, rep, s->ids);
+  k_pick_smin<<<1, 32, 0, st>>>(s->mhist, s->dyn_max, N);
+  MSB_LAUNCH_CHECK(ctx);
+  k_merge_rep<<<grid_for(N, 256), 256, 0, st>>>(s->lab, s->cnt, s->bins, N, 1, s->mhist + 129,
+                                                s->mhist + 128);
+  MSB_LAUNCH_CHECK(ctx);
+  k_merge_label<<<grid_for(N, 256), 256, 0, st>>>(s->lab, s->cnt, s->bins, N, 1, s->mhist + 129,
+                                                  s->ids, s->mhist + 128);
   MSB_LAUNCH_CHECK(ctx);
   lap(2);
   int32_t M = 0;
-  // canonical numbering: labels are minimum cells of their blocks
-  rc = canonical_number(ctx, N, s->ids, s->lab, s->cnt /* 2N scratch: cnt|bins reused */, &M);
+  // canonical numbering: labels are minimum cells of their blocks; max|Δp| comes back with
+  // its count (one synchronisation for both)
+  unsigned long long hm = 0;
+  rc = canonical_number(ctx, N, s->ids, s->lab, s->cnt /* 2N scratch: cnt|bins reused */, &M, mx,
+                        &hm, sizeof(hm));
   if (rc) return rc;
+  {
+    double m;
+    memcpy(&m, &hm, 8);
+    if (!(m > 0.0)) {  // max|Δp| = 0: stage skipped
+      *M_out = 0;
+      return MSB_OK;
+    }
+  }
   msb_level D = s->dyn_level;
   k_refill_const<<<grid_for(N, 256), 256, 0, st>>>(s->lab, N, D->col, D->P[0]);
   MSB_LAUNCH_CHECK(ctx);
@@ -1474,6 +1504,7 @@ msb_status msb_solver_create(msb_ctx ctx, msb_op op, const msb_level* levels, in
     MSB_ALLOC(ctx, s->cnt, int32_t, 2 * N);
     s->bins = s->cnt + N;  // bins live in the second half of the cnt scratch
     MSB_ALLOC(ctx, s->scratch_i, int32_t, 64);
+    MSB_ALLOC(ctx, s->mhist, int32_t, 132);
     // constant-basis level reused across iterations
     msb_level D = new msb_level_s();
     D->ctx = ctx;
@@ -2114,6 +2145,7 @@ msb_status msb_solver_destroy(msb_solver s) {
   dfree(ctx, s->cnt);
   dfree(ctx, s->bins);
   dfree(ctx, s->scratch_i);
+  dfree(ctx, s->mhist);
   if (s->dyn_level) level_free(s->dyn_level);
   dfree(ctx, s->ilu_d);
   delete s->jq;

@@ -172,13 +172,14 @@ __global__ void k_gather_ids(const int32_t* __restrict__ lab, const int32_t* __r
 
 // lab[i] must be a cell index that is its own label for the representative cell.
 msb_status canonical_number(msb_ctx ctx, int64_t N, const int32_t* lab, int32_t* out,
-                            int32_t* scratch, int32_t* M_out) {
+                            int32_t* scratch, int32_t* M_out, const void* extra_dev,
+                            void* extra_host, size_t extra_bytes) {
   int32_t* flags = scratch;
   int32_t* ids = scratch + N;
   k_root_flags<<<grid_for(N, 256), 256, 0, ctx->stream>>>(lab, N, flags);
   MSB_LAUNCH_CHECK(ctx);
   int32_t M = 0;
-  msb_status st = scan_exclusive(ctx, flags, ids, N, &M);
+  msb_status st = scan_exclusive(ctx, flags, ids, N, &M, extra_dev, extra_host, extra_bytes);
   if (st != MSB_OK) return st;
   k_gather_ids<<<grid_for(N, 256), 256, 0, ctx->stream>>>(lab, ids, N, out);
   MSB_LAUNCH_CHECK(ctx);
