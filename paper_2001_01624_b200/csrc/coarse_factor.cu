@@ -439,8 +439,10 @@ msb_status coarse_factor_dense(msb_ctx ctx, Coarse& co) {
   msb_status rc = chol_inv(ctx, F, Wb, M, M, amax, sing);
   if (rc) return rc;
   int hs = 0;
-  MSB_CUDA_TRY(ctx, cudaMemcpyAsync(&hs, sing, 4, cudaMemcpyDeviceToHost, s));
-  MSB_CUDA_TRY(ctx, cudaStreamSynchronize(s));
+  if (!co.defer_check) {  // the dynamic stage reads the flag with its next stop-test readback
+    MSB_CUDA_TRY(ctx, cudaMemcpyAsync(&hs, sing, 4, cudaMemcpyDeviceToHost, s));
+    MSB_CUDA_TRY(ctx, cudaStreamSynchronize(s));
+  }
   if (hs) {
     co.ready = false;
     return set_error(ctx, MSB_ESINGULAR, "singular coarse matrix: pivot <= 1e-14 max|A_c| (M=%d)", M);

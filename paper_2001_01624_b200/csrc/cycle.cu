@@ -2075,12 +2075,22 @@ msb_status msb_ms_iterate(msb_ctx ctx, msb_solver s, const double* b, double* x,
       return std::chrono::duration<double, std::micro>(
                  std::chrono::steady_clock::now().time_since_epoch()).count();
     };
+    // the rebuilt level's singular-pivot flag is read with the stop-test state (one
+    // synchronisation per iteration for both); a singular rebuild fails the call there
+    msb_level D = s->dyn_level;
+    int hsing = 0;
     while (true) {
       double t0 = tdbg ? now() : 0;
       if ((rc = enqueue_norm(ctx, s, s->xbuf[cur], db, 0))) return rc;
       MSB_CUDA_TRY(ctx, cudaMemcpyAsync(&hs, s->st, sizeof(hs), cudaMemcpyDeviceToHost, st));
+      if (D->co.flags)
+        MSB_CUDA_TRY(ctx, cudaMemcpyAsync(&hsing, D->co.flags + 1, sizeof(int), cudaMemcpyDeviceToHost, st));
       MSB_CUDA_TRY(ctx, cudaStreamSynchronize(st));
       if (tdbg) t_norm += now() - t0;
+      if (hsing) {
+        D->co.ready = false;
+        return set_error(ctx, MSB_ESINGULAR, "dynamic stage: singular coarse matrix (M=%d)", D->M);
+      }
       if (hs.done) break;
       int k = hs.k;  // iteration about to run (1-based)
       int32_t M = 0;
@@ -2088,7 +2098,10 @@ msb_status msb_ms_iterate(msb_ctx ctx, msb_solver s, const double* b, double* x,
       if (k >= 2) {
         k_dp<<<grid_for(N, 256), 256, 0, st>>>(s->xbuf[cur], s->xprev, N, s->dpbuf);
         MSB_LAUNCH_CHECK(ctx);
-        if ((rc = build_dynamic(ctx, s, s->dpbuf, &M, nullptr))) return rc;
+        D->co.defer_check = true;
+        rc = build_dynamic(ctx, s, s->dpbuf, &M, nullptr);
+        D->co.defer_check = false;
+        if (rc) return rc;
       }
       if (tdbg) t_build += now() - t1;
       if (tdbg) t1 = now();
