@@ -1103,7 +1103,18 @@ __global__ void k_bins(const double* __restrict__ dp, int64_t N, const unsigned 
 
 // component sizes: runs of equal labels in consecutive lanes are counted with one atomic
 // (a large component would otherwise send every cell's increment to one address)
-__global__ void k_sizes(const int32_t* __restrict__ lab, int64_t N, int32_t* __restrict__ cnt) {
+// Component sizes.  Run lengths of equal labels within a warp, then a 16-slot shared table
+// per CTA (a CTA's 256 consecutive cells carry few labels), one global atomic per distinct
+// label per CTA: the large components' counters were hit by every warp (25 us).  Integer
+// sums, so the result does not depend on the order.
+__global__ void __launch_bounds__(256) k_sizes(const int32_t* __restrict__ lab, int64_t N,
+                                               int32_t* __restrict__ cnt) {
+  __shared__ int tkey[16], tval[16];
+  if (threadIdx.x < 16) {
+    tkey[threadIdx.x] = -1;
+    tval[threadIdx.x] = 0;
+  }
+  __syncthreads();
   const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const unsigned full = 0xffffffffu;
   const int lane = threadIdx.x & 31;
@@ -1113,8 +1124,20 @@ __global__ void k_sizes(const int32_t* __restrict__ lab, int64_t N, int32_t* __r
   const int next = __shfl_down_sync(full, key, 1);
   if (key >= 0 && (lane == 31 || next != key)) {  // run tail: run length = lane - head + 1
     const int head = 31 - __clz(heads & ((2u << lane) - 1u));
-    atomicAdd(cnt + key, lane - head + 1);
+    const int len = lane - head + 1;
+    bool put = false;
+    for (int p = 0; p < 16 && !put; ++p) {
+      const int sl = (int)(((unsigned)key * 2654435761u >> 28) + p) & 15;
+      const int old = atomicCAS(tkey + sl, -1, key);
+      if (old == -1 || old == key) {
+        atomicAdd(tval + sl, len);
+        put = true;
+      }
+    }
+    if (!put) atomicAdd(cnt + key, len);
   }
+  __syncthreads();
+  if (threadIdx.x < 16 && tkey[threadIdx.x] >= 0) atomicAdd(cnt + tkey[threadIdx.x], tval[threadIdx.x]);
 }
 
 // counts[0] = #roots with size >= smin; counts[1..3] = bin b has a small component
