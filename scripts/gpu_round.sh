@@ -11,7 +11,8 @@ timeout 1500 python -m pytest tests -m gpu -q > $OUT/pytest_gpu.log 2>&1; echo "
 timeout 900 python bench.py > $OUT/bench.log 2>&1; echo "bench rc=$?" >> $OUT/bench.log
 timeout 600 python scripts/run_config.py 5 > $OUT/config5.json 2>&1
 timeout 900 python scripts/run_config.py 4 --steps 100 > $OUT/config4.json 2>&1
-MSB_DYN_TIMING=1 timeout 300 python scripts/run_config.py 3 > $OUT/config3.json 2>&1
+timeout 300 python scripts/run_config.py 3 > $OUT/config3.json 2>&1
+MSB_DYN_TIMING=1 timeout 300 python scripts/run_config.py 3 > $OUT/config3_timing.json 2>&1
 # launch list of the bench command itself (one step, shares comparable with the bench's phases)
 timeout 300 python bench.py --steps 1 --warmup 0 --no-cpu-baseline --no-e2e > $OUT/bench_plain.log 2>&1 &&
 timeout 1500 ncu --metrics gpu__time_duration.sum --clock-control none -c 12000 --csv \
