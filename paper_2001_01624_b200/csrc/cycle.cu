@@ -292,6 +292,7 @@ struct LevelView {
   const int32_t* tab;
   const int32_t* col;
   const double* P;
+  int unit;  // W = 1 with rows summing to one: every P entry is exactly 1, not read
 };
 
 __device__ __forceinline__ int lv_col(const LevelView& L, int c, int i, int j, int k, int s) {
@@ -499,7 +500,7 @@ __global__ void __launch_bounds__(CT) k_res_restrict_small(StencilT S, LevelView
     v2 += r * r;
     for (int s2 = 0; s2 < L.W; ++s2) {
       const int key = in ? L.col[(size_t)s2 * N + c] : -1;
-      const double v = key >= 0 ? L.P[(size_t)s2 * N + c] * r : 0.0;
+      const double v = key >= 0 ? (L.unit ? r : L.P[(size_t)s2 * N + c] * r) : 0.0;
       warp_segmented_add(key, v, rsm);
     }
   }
@@ -547,7 +548,7 @@ __global__ void __launch_bounds__(CT) k_res_restrict_det(StencilT S, LevelView L
     v2 += r * r;
     for (int s2 = 0; s2 < L.W; ++s2) {
       const int key = in ? L.col[(size_t)s2 * N + c] : -1;
-      double v = key >= 0 ? L.P[(size_t)s2 * N + c] * r : 0.0;
+      double v = key >= 0 ? (L.unit ? r : L.P[(size_t)s2 * N + c] * r) : 0.0;
       // inclusive segmented scan over runs of equal keys (fixed shuffle order)
       const int prev = __shfl_up_sync(full, key, 1);
       const unsigned heads = __ballot_sync(full, lane == 0 || prev != key);
@@ -688,7 +689,7 @@ __global__ void __launch_bounds__(CT) k_prolong(LevelView L, double* __restrict_
     }
     for (; s < L.W; ++s) {
       int key = L.col[(size_t)s * N + c];
-      if (key >= 0) acc += L.P[(size_t)s * N + c] * xc[key];
+      if (key >= 0) acc += L.unit ? xc[key] : L.P[(size_t)s * N + c] * xc[key];
     }
   }
   x[c] += acc;
@@ -1237,7 +1238,8 @@ static StencilT stencil(msb_op op) {
 
 static LevelView view(msb_level L) {
   return LevelView{L->kind, L->W, L->nb[0], L->nb[1], L->nb[2], L->bs[0], L->bs[1], L->bs[2],
-                   make_grid3(L->nx, L->ny, L->nz), L->tab, L->col, L->P[L->cur]};
+                   make_grid3(L->nx, L->ny, L->nz), L->tab, L->col, L->P[L->cur],
+                   (L->kind == 1 && L->W == 1 && L->unity) ? 1 : 0};
 }
 // Build the dynamic constant-basis stage from dp (device, length N) into s->dyn_level.
 static msb_status build_dynamic(msb_ctx ctx, msb_solver s, const double* dp, int32_t* M_out,
