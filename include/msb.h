@@ -50,8 +50,9 @@ enum {
   MSB_EDIM = -2,           /* dimension mismatch                                       */
   MSB_EZERO_DIAG = -3,     /* zero diagonal in A_T                       */
   MSB_ESINGULAR = -4,      /* coarse pivot <= 1e-14 * max|A_c|            */
-  MSB_EINCONSISTENT = -5,  /* reserved, never returned: the A_00 gauge (reading A7)
-                              makes every right-hand side solvable                      */
+  MSB_EINCONSISTENT = -5,  /* A singular: sealing faces (T = 0) cut off a compartment
+                              without the gauge cell 0, so the A_00 gauge (reading A7)
+                              does not fix its pure-Neumann null space      */
   MSB_EDIVERGED = -6,      /* residual > 1e6 * initial residual           */
   MSB_ENOMEM = -7,         /* allocator returned NULL                                  */
   MSB_ECUDA = -8           /* CUDA runtime error / no device                           */
@@ -212,7 +213,10 @@ msb_status msb_coarse_assemble(msb_ctx ctx, msb_level lev, msb_op op);
  * iteration k >= 2, Δp = x_start(k) - x_start(k-1) is binned at dyn_edge{0,1}*max|Δp|,
  * split into connected components (canonical numbering by minimum cell), small
  * components merged per bin until at most dyn_max_blocks blocks, and appended as a
- * constant-basis stage.  Levels must have been assembled (msb_coarse_assemble). */
+ * constant-basis stage.  Levels must have been assembled (msb_coarse_assemble).
+ * Errors: MSB_EINCONSISTENT when the faces with T > 0 do not connect every cell to the
+ * gauge cell 0 (A is then singular: "pre: A nonsingular"); MSB_EDIM for a level
+ * of another grid; MSB_EINVAL for an unassembled level. */
 msb_status msb_solver_create(msb_ctx ctx, msb_op op, const msb_level* levels, int32_t n_levels,
                              double omega_s, int32_t nu, int32_t post_smooth, int32_t dyn_enable,
                              double dyn_edge0, double dyn_edge1, int32_t dyn_max_blocks,
@@ -271,6 +275,17 @@ msb_status msb_fgmres(msb_ctx ctx, msb_solver s, const double* b, double* x, dou
 msb_status msb_transport_upwind(msb_ctx ctx, msb_op op, const double* p, double* S,
                                 const double* phi, double mu_w, double mu_o, double dt,
                                 double* mob_out, int32_t* substeps_out);
+/* Per-face upstream total mobility λ_t(S_up) = S^2/μ_w + (1-S)^2/μ_o, upstream by the
+ * sign of p_i - p_l (ties to the left/lower cell; reading A17).
+ * p, S: host|dev N doubles, or NULL for zero (step 1: S = 0 gives λ_t = 1/μ_o on every
+ * face).  mob_out: host|dev, compact face layout.  Synchronises. */
+msb_status msb_upstream_mobility(msb_ctx ctx, msb_op op, const double* p, const double* S,
+                                 double mu_w, double mu_o, double* mob_out);
+/* Config-4 pressure step length (reading A18): dt = pv_per_step * Σ_i φ_i |Ω_i| / Σ_i q_i^+
+ * (0 without injection), summed on the device in a fixed order.  phi host|dev N doubles;
+ * dt_out host.  Synchronises. */
+msb_status msb_transport_step_size(msb_ctx ctx, msb_op op, const double* phi,
+                                   double pv_per_step, double* dt_out);
 
 #ifdef __cplusplus
 }

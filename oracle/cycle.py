@@ -27,11 +27,14 @@ from .partition import dynamic_partition
 
 
 class Level:
-    def __init__(self, P, A):
+    """One (P, R = P^T, A_c) stage.  coarse / assoc select an alternate exact coarse
+    solver / summation order (oracle.coarse; floor measurement only)."""
+
+    def __init__(self, P, A, coarse="lu", assoc="right"):
         self.P = sp.csr_matrix(P)
         self.PT = self.P.T.tocsr()
-        self.Ac = galerkin(self.P, A)
-        self.solver = CoarseSolver(self.Ac)
+        self.Ac = galerkin(self.P, A, assoc)
+        self.solver = CoarseSolver(self.Ac, coarse)
 
     @property
     def M(self):
@@ -80,10 +83,15 @@ def stage(A, DA, b, x, level, omega_s, nu, post, smoother=None):
 
 
 def iterate(A, b, x0, levels, omega_s=2.0 / 3.0, nu=1, post=False, tol=1e-6,
-            max_iter=1000, fixed_iters=0, dynamic=None, record_dynamic=False, smoother=None):
+            max_iter=1000, fixed_iters=0, dynamic=None, record_dynamic=False, smoother=None,
+            coarse="lu", assoc="right"):
     """Run the multibasis Richardson iteration.
 
     dynamic: None or dict(nx=, ny=, nz=, edges=(0.1, 0.5), max_blocks=1024).
+    record_dynamic: True keeps every (k, part, M) in out["dyn"]; a callable is called
+    with (k, part, M) instead.
+    coarse / assoc: alternate coarse solver / A_c summation order for the dynamic
+    stage's levels (oracle.coarse; floor measurement only).
     Returns dict(x, iters, res (ρ_0..ρ_k), converged, diverged, dyn=[(k, part, M)])."""
     A = sp.csr_matrix(A)
     DA = A.diagonal()
@@ -110,8 +118,10 @@ def iterate(A, b, x0, levels, omega_s=2.0 / 3.0, nu=1, post=False, tol=1e-6,
                                         dynamic.get("max_blocks", 1024))
             out["dyn_M"].append(M)
             if part is not None:
-                stages.append(Level(constant_basis(part, M), A))
-                if record_dynamic:
+                stages.append(Level(constant_basis(part, M), A, coarse, assoc))
+                if callable(record_dynamic):
+                    record_dynamic(k, part, M)
+                elif record_dynamic:
                     out["dyn"].append((k, part, M))
         x_prev_start = x_start
         for lev in stages:

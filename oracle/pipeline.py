@@ -59,8 +59,14 @@ def static_partition(prob, spec):
 
 
 def run(prob, sweeps=None, fixed_sweeps=None, fixed_iters=None, max_iter=None,
-        record_dynamic=False, x0=None):
+        record_dynamic=False, x0=None, coarse="lu", assoc="right", levels_info=None):
+    """coarse / assoc: alternate exact coarse solver / A_c summation order (oracle.coarse,
+    floor measurement only).  levels_info: reuse the smoothed levels of an earlier run
+    (the alternates differ only after smoothing)."""
     A_T, A, q, trans = _tpfa.build(prob)
+    if levels_info is not None:
+        return _solve(prob, A_T, A, q, trans, levels_info, fixed_iters, max_iter,
+                      record_dynamic, x0, coarse, assoc)
     cart = cartesian_level(prob, A_T, sweeps, fixed_sweeps)
     levels_info = [cart]
     if prob.split_level:
@@ -68,7 +74,13 @@ def run(prob, sweeps=None, fixed_sweeps=None, fixed_iters=None, max_iter=None,
     for spec in prob.static_levels:  # NEXT-3 (reading B11: after the general levels)
         part, M = static_partition(prob, spec)
         levels_info.append(general_level(prob, A_T, part, M, spec["halo"], sweeps, fixed_sweeps))
-    levels = [Level(li["P"].matrix(), A) for li in levels_info]
+    return _solve(prob, A_T, A, q, trans, levels_info, fixed_iters, max_iter, record_dynamic,
+                  x0, coarse, assoc)
+
+
+def _solve(prob, A_T, A, q, trans, levels_info, fixed_iters, max_iter, record_dynamic, x0,
+           coarse, assoc):
+    levels = [Level(li["P"].matrix(), A, coarse, assoc) for li in levels_info]
     dyn = None
     if prob.dynamic:
         dyn = dict(nx=prob.nx, ny=prob.ny, nz=prob.nz, edges=prob.dyn_edges,
@@ -78,7 +90,7 @@ def run(prob, sweeps=None, fixed_sweeps=None, fixed_iters=None, max_iter=None,
     x0 = np.zeros(prob.N) if x0 is None else x0
     smoother = make_smoother(prob, A)
     sol = iterate(A, q, x0, levels, prob.omega_s, prob.nu, prob.post_smooth,
-                  prob.cycle_tol, mi, fi, dyn, record_dynamic, smoother)
+                  prob.cycle_tol, mi, fi, dyn, record_dynamic, smoother, coarse, assoc)
     return dict(A_T=A_T, A=A, q=q, trans=trans, levels_info=levels_info, levels=levels,
                 sol=sol, smoother=smoother)
 

@@ -106,9 +106,10 @@ def step_size(prob, q, phi, pv_per_step=0.005):
 
 
 def run(prob, steps=100, k_adapt=5, mu_w=1.0, mu_o=5.0, pv_per_step=0.005,
-        init_sweeps=None, init_fixed=None, fixed_iters=None, max_iter=None):
+        init_sweeps=None, init_fixed=None, fixed_iters=None, max_iter=None, coarse="lu"):
     """Config-4 outer loop.  fixed_iters: None, or a per-step list of iteration counts
-    (lockstep mode, SURVEY.md §8.c protocol 5).  Returns per-step records."""
+    (lockstep mode, SURVEY.md §8.c protocol 5).  coarse: alternate exact coarse solver
+    (oracle.coarse; floor measurement only).  Returns per-step records."""
     N = prob.N
     vol = prob.dx * prob.dy * prob.dz
     phi = np.full(N, prob.phi)
@@ -126,7 +127,7 @@ def run(prob, steps=100, k_adapt=5, mu_w=1.0, mu_o=5.0, pv_per_step=0.005,
     for n in range(steps):
         A_T, A, _, trans = _tpfa.build(prob, mob)
         P, _, _ = _basis.smooth(P, A_T, prob.omega, k_adapt, 0.0, fixed=True)
-        lev = Level(P.matrix(), A)
+        lev = Level(P.matrix(), A, coarse)
         fi = fixed_iters[n] if fixed_iters is not None else 0
         sol = iterate(A, q, x, [lev], prob.omega_s, prob.nu, prob.post_smooth,
                       prob.cycle_tol, mi, fi)

@@ -63,6 +63,8 @@ SIGNATURES = {
     "msb_solver_destroy": (i32, [p]),
     "msb_fgmres": (i32, [p, p, p, p, f64, i32, i32, i32, pi32, p]),
     "msb_transport_upwind": (i32, [p, p, p, p, p, f64, f64, f64, p, pi32]),
+    "msb_upstream_mobility": (i32, [p, p, p, p, f64, f64, p]),
+    "msb_transport_step_size": (i32, [p, p, p, f64, pf64]),
 }
 
 _lib = None

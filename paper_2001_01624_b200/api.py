@@ -167,6 +167,22 @@ class Operator:
                        "msb_transport_upwind")
         return n.value
 
+    def upstream_mobility(self, p, S, mu_w, mu_o, mob_out):
+        """Per-face upstream λ_t (msb_upstream_mobility); p / S None = zero vectors."""
+        self.ctx.check(self.ctx.lib.msb_upstream_mobility(self.ctx.h, self.h, _ptr(p), _ptr(S),
+                                                          float(mu_w), float(mu_o),
+                                                          _ptr(mob_out)),
+                       "msb_upstream_mobility")
+        return mob_out
+
+    def step_size(self, phi, pv_per_step):
+        """Config-4 step length dt (msb_transport_step_size)."""
+        dt = C.c_double()
+        self.ctx.check(self.ctx.lib.msb_transport_step_size(self.ctx.h, self.h, _ptr(phi),
+                                                            float(pv_per_step), C.byref(dt)),
+                       "msb_transport_step_size")
+        return dt.value
+
     def close(self):
         if getattr(self, "h", None):
             self.ctx.lib.msb_op_destroy(self.h)

@@ -354,51 +354,6 @@ __global__ void k_rap(const msb_level_s L, const double* __restrict__ P, const d
   }
 }
 
-// ---------------------------------------------------------------- GEMV solve
-// xc = X rc, one CTA per row: 256 threads each issue all of their (<= 8 at M <= 4096)
-// 16-byte loads of the row at once, so a row costs one memory round trip and ~8 rows
-// per SM are in flight; fixed-order per-thread sums + shuffle/smem tree: deterministic.
-// The done flag is read at entry and tested before the store.
-template <bool kStream>
-__global__ void __launch_bounds__(256) k_gemv(const double* __restrict__ X, int M,
-                                              const double* __restrict__ rc,
-                                              double* __restrict__ xc, const int* done) {
-  const bool skip = done && *(volatile const int*)done;
-  const int64_t row = blockIdx.x;
-  const double* a = X + row * M;
-  double s = 0.0;
-  if ((M & 1) == 0) {
-    const double2* a2 = reinterpret_cast<const double2*>(a);
-    const double2* r2 = reinterpret_cast<const double2*>(rc);
-    const int h = M >> 1;
-    for (int t0 = threadIdx.x; t0 < h; t0 += 8 * 256) {
-      double2 av[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int t = t0 + 256 * u;
-        av[u] = t < h ? (kStream ? __ldcs(a2 + t) : a2[t]) : make_double2(0.0, 0.0);
-      }
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int t = t0 + 256 * u;
-        const double2 b = t < h ? r2[t] : make_double2(0.0, 0.0);
-        s += av[u].x * b.x + av[u].y * b.y;
-      }
-    }
-  } else {
-    for (int t = threadIdx.x; t < M; t += 256) s += (kStream ? __ldcs(a + t) : a[t]) * rc[t];
-  }
-  __shared__ double sh[8];
-  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = s;
-  __syncthreads();
-  if (threadIdx.x == 0 && !skip) {
-    double t = 0.0;
-    for (int w = 0; w < 8; ++w) t += sh[w];
-    xc[row] = t;
-  }
-}
-
 // ---------------------------------------------------------------- symmetric GEMV (SYMV)
 // A_c^{-1} is symmetric, so the coarse solve reads only its lower triangle: 64 x 64
 // tiles (bi >= bj) packed contiguously, tile t = bi(bi+1)/2 + bj, zero-padded at the
@@ -454,67 +409,12 @@ msb_status coarse_pack_symmetric(msb_ctx ctx, Coarse& co) {
   return MSB_OK;
 }
 
-// L2 residency of the dense inverse (B200: 126 MB L2).  The inverse is the only operand
-// of the cycle that is read unchanged every stage, so when the device allows a
-// persisting carve-out the GEMV is launched with an access-policy window over it:
-// after the first solve its lines stay in L2 and the per-stage M^2 HBM stream becomes
-// an L2 read.  Opt-in (MSB_L2_PERSIST=1): measured on config 2 the carve-out cost the
-// sweep 2x (its working set loses L2) for a 0.7 % cycle gain (profiles/r01_v1/).
-static size_t persist_bytes(msb_ctx ctx, size_t want) {
-  static int state = -1;  // -1 unknown, 0 off, 1 on
-  static size_t max_win = 0, max_persist = 0;
-  if (state < 0) {
-    const char* e = getenv("MSB_L2_PERSIST");
-    state = (e && e[0] == '1') ? 1 : 0;
-    int v = 0;
-    if (state && cudaDeviceGetAttribute(&v, cudaDevAttrMaxAccessPolicyWindowSize, ctx->device) == cudaSuccess)
-      max_win = (size_t)v;
-    if (state && cudaDeviceGetAttribute(&v, cudaDevAttrMaxPersistingL2CacheSize, ctx->device) == cudaSuccess)
-      max_persist = (size_t)v;
-    if (!max_win || !max_persist) state = 0;
-    if (state && cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, max_persist) != cudaSuccess) state = 0;
-    cudaGetLastError();
-  }
-  if (!state) return 0;
-  return std::min(want, std::min(max_win, max_persist));
-}
-
-void coarse_persist_init(msb_ctx ctx) { persist_bytes(ctx, 0); }
-
 void coarse_solve_dense(msb_ctx ctx, const Coarse& co, const double* rc, double* xc,
                         const int* done) {
-  const size_t bytes = (size_t)co.M * co.M * sizeof(double);
-  const size_t win = persist_bytes(ctx, bytes);
-  if (win) {
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(co.M);
-    cfg.blockDim = dim3(256);
-    cfg.stream = ctx->stream;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeAccessPolicyWindow;
-    at[0].val.accessPolicyWindow.base_ptr = co.Ainv;
-    at[0].val.accessPolicyWindow.num_bytes = win;
-    at[0].val.accessPolicyWindow.hitRatio = 1.0f;
-    at[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-    at[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
-    if (cudaLaunchKernelEx(&cfg, k_gemv<false>, (const double*)co.Ainv, co.M, rc, xc, done) ==
-        cudaSuccess) {
-      count_launch();
-      return;
-    }
-    cudaGetLastError();
-  }
-  if (co.Xp && !getenv("MSB_DENSE_GEMV")) {
-    const int64_t nt = (int64_t)co.ntb * (co.ntb + 1) / 2;
-    k_symv_tiles<<<(unsigned)nt, SYMV_T, 0, ctx->stream>>>(co.Xp, co.M, rc, co.part);
-    k_symv_reduce<<<co.ntb, 16 * ST, 0, ctx->stream>>>(co.part, co.M, co.ntb, xc, done);
-    count_launch();
-    count_launch();
-    return;
-  }
-  k_gemv<true><<<co.M, 256, 0, ctx->stream>>>(co.Ainv, co.M, rc, xc, done);
+  const int64_t nt = (int64_t)co.ntb * (co.ntb + 1) / 2;
+  k_symv_tiles<<<(unsigned)nt, SYMV_T, 0, ctx->stream>>>(co.Xp, co.M, rc, co.part);
+  k_symv_reduce<<<co.ntb, 16 * ST, 0, ctx->stream>>>(co.part, co.M, co.ntb, xc, done);
+  count_launch();
   count_launch();
 }
 
@@ -532,9 +432,11 @@ msb_status coarse_assemble_dense(msb_ctx ctx, msb_level L, msb_op op) {
   co.M = M;
   // deterministic exact accumulation (128-bit fixed point) whenever its 16 B per entry fit
   // comfortably (M <= 8192: 1 GiB); config 5 (M = 20,000) keeps fp64 atomics
-  static const bool det_off = getenv("MSB_RAP_ATOMIC") != nullptr;
   cudaStream_t st = ctx->stream;
-  if (!det_off && M <= 8192) {
+  // constant basis (W = 1, every P entry exactly 1): only the faces between blocks; an
+  // imported W = 1 level (rows no longer known to sum to one) takes the general path
+  const bool constant = L->kind == 1 && L->W == 1 && L->unity;
+  if (M <= 8192) {
     const size_t n = (size_t)M * M;
     if (co.acc_cap < n) {  // sized for the buffers' capacity: a growing M_dyn reallocates once
       const size_t ncap = std::max(n, (size_t)co.cap * co.cap);
@@ -549,11 +451,11 @@ msb_status coarse_assemble_dense(msb_ctx ctx, msb_level L, msb_op op) {
     k_absmax_t<<<std::min<int64_t>(grid_for(3 * op->N, 256), 4 * ctx->sm_count), 256, 0, st>>>(
         op->Tx, 3 * op->N, tmax);
     MSB_LAUNCH_CHECK(ctx);
-    if (L->kind == 1 && L->W == 1) {  // constant basis: only the faces between blocks
+    if (constant) {
       k_rap_const_det<<<grid_for(op->N, 256), 256, 0, st>>>(
           L->col, make_grid3(op->nx, op->ny, op->nz), M, op->Tx, op->Ty, op->Tz, tmax, co.acc);
     } else {
-      if (L->unity && !getenv("MSB_RAP_FULL"))
+      if (L->unity)
         k_rap<true, true><<<grid_for(L->N, 128), 128, 0, st>>>(*L, L->P[L->cur], op->Tx, op->Ty,
                                                               op->Tz, co.Ac, co.acc, tmax);
       else
@@ -561,9 +463,9 @@ msb_status coarse_assemble_dense(msb_ctx ctx, msb_level L, msb_op op) {
                                                                op->Tz, co.Ac, co.acc, tmax);
     }
     MSB_LAUNCH_CHECK(ctx);
-    if (L->kind == 1 && L->W == 1)
+    if (constant)
       k_fx_const_to_double<<<M, 256, 0, st>>>(co.acc, M, tmax, co.Ac);
-    else if (L->unity && !getenv("MSB_RAP_FULL"))
+    else if (L->unity)
       k_fx_sym_to_double<<<M, 256, 0, st>>>(co.acc, M, tmax, co.Ac);
     else
       k_fx_to_double<<<grid_for((int64_t)n, 256), 256, 0, st>>>(co.acc, (int64_t)n, tmax, co.Ac);

@@ -35,7 +35,6 @@ struct IterState {
   double tol;
   double bscale;  // ||b|| (1 if b = 0)
   double r0;
-  int cur;        // x buffer holding x_k (persistent cycle kernel)
 };
 
 namespace msb {
@@ -189,101 +188,6 @@ __global__ void __launch_bounds__(CT) k_jacobi(StencilT S, const double* __restr
     }
   }
   if (first) warp_partial(v, partials);
-}
-
-// a7 + a6 fused (one pre-smoothing Jacobi sweep, then the residual of its result):
-// x1 = x0 + ω D_A^{-1}(b - A x0) and r1 = b - A x1 in one pass.  A CTA owns a 32x4x4
-// block; it stages x0 on the block plus a 2-cell halo in shared memory (coalesced
-// 36-wide rows), evaluates the Jacobi update on the block plus a 1-cell halo (the halo
-// recompute: 1224 updates for 512 cells, T and b from L1/L2) into shared memory, and
-// then the residual of x1 on the block.  x0, b and T cross HBM once instead of twice
-// and r never round-trips between the two passes.  Same operations, in the same order,
-// as k_jacobi followed by k_residual (bit-identical x1 and r1).
-constexpr int JR_X = 32, JR_Y = 4, JR_Z = 4;
-__global__ void __launch_bounds__(JR_X * JR_Y * JR_Z) k_jacres(
-    StencilT S, const double* __restrict__ x, double* __restrict__ xo,
-    const double* __restrict__ b, double* __restrict__ r, double omega, int first,
-    double* __restrict__ partials, const IterState* st) {
-  const bool done = is_done(st);
-  __shared__ double xs[JR_Z + 4][JR_Y + 4][JR_X + 4];
-  __shared__ double x1s[JR_Z + 2][JR_Y + 2][JR_X + 2];
-  const int nx = S.g.nx, ny = S.g.ny, nz = S.g.nz, sxy = S.g.nxy;
-  const int X0 = blockIdx.x * JR_X, Y0 = blockIdx.y * JR_Y, Z0 = blockIdx.z * JR_Z;
-  const int tid = threadIdx.x + JR_X * (threadIdx.y + JR_Y * threadIdx.z);
-  constexpr int NT = JR_X * JR_Y * JR_Z;
-  constexpr int AX = JR_X + 4, AY = JR_Y + 4, AZ = JR_Z + 4;
-  for (int e = tid; e < AX * AY * AZ; e += NT) {
-    const int zz = e / (AX * AY), rem = e - zz * AX * AY, yy = rem / AX, xx = rem - yy * AX;
-    const int gx = X0 - 2 + xx, gy = Y0 - 2 + yy, gz = Z0 - 2 + zz;
-    const bool in = gx >= 0 && gx < nx && gy >= 0 && gy < ny && gz >= 0 && gz < nz;
-    (&xs[0][0][0])[e] = in ? x[gx + nx * gy + sxy * gz] : 0.0;
-  }
-  __syncthreads();
-  constexpr int BX = JR_X + 2, BY = JR_Y + 2, BZ = JR_Z + 2;
-  double nrm = 0.0;
-  for (int e = tid; e < BX * BY * BZ; e += NT) {
-    const int zz = e / (BX * BY), rem = e - zz * BX * BY, yy = rem / BX, xx = rem - yy * BX;
-    const int gx = X0 - 1 + xx, gy = Y0 - 1 + yy, gz = Z0 - 1 + zz;
-    double v = 0.0;
-    if (gx >= 0 && gx < nx && gy >= 0 && gy < ny && gz >= 0 && gz < nz) {
-      const int c = gx + nx * gy + sxy * gz;
-      const double txp = S.Tx[c], typ = S.Ty[c], tzp = S.Tz[c];
-      const double txm = gx > 0 ? S.Tx[c - 1] : 0.0;
-      const double tym = gy > 0 ? S.Ty[c - nx] : 0.0;
-      const double tzm = gz > 0 ? S.Tz[c - sxy] : 0.0;
-      const double D = txp + txm + typ + tym + tzp + tzm;
-      double off = 0.0;
-      if (gz > 0) off += tzm * xs[zz][yy + 1][xx + 1];
-      if (gy > 0) off += tym * xs[zz + 1][yy][xx + 1];
-      if (gx > 0) off += txm * xs[zz + 1][yy + 1][xx];
-      if (gx < nx - 1) off += txp * xs[zz + 1][yy + 1][xx + 2];
-      if (gy < ny - 1) off += typ * xs[zz + 1][yy + 2][xx + 1];
-      if (gz < nz - 1) off += tzp * xs[zz + 2][yy + 1][xx + 1];
-      const double dA = (c == 0) ? 2.0 * D : D;
-      const double x0c = xs[zz + 1][yy + 1][xx + 1];
-      const double r0 = b[c] - (dA * x0c - off);
-      v = x0c + omega * (r0 / dA);
-      if (xx >= 1 && xx <= JR_X && yy >= 1 && yy <= JR_Y && zz >= 1 && zz <= JR_Z) nrm += r0 * r0;
-    }
-    (&x1s[0][0][0])[e] = v;
-  }
-  __syncthreads();
-  const int tx = threadIdx.x, ty = threadIdx.y, tz = threadIdx.z;
-  const int gx = X0 + tx, gy = Y0 + ty, gz = Z0 + tz;
-  if (gx < nx && gy < ny && gz < nz) {
-    const int c = gx + nx * gy + sxy * gz;
-    const double txp = S.Tx[c], typ = S.Ty[c], tzp = S.Tz[c];
-    const double txm = gx > 0 ? S.Tx[c - 1] : 0.0;
-    const double tym = gy > 0 ? S.Ty[c - nx] : 0.0;
-    const double tzm = gz > 0 ? S.Tz[c - sxy] : 0.0;
-    const double D = txp + txm + typ + tym + tzp + tzm;
-    double off = 0.0;
-    if (gz > 0) off += tzm * x1s[tz][ty + 1][tx + 1];
-    if (gy > 0) off += tym * x1s[tz + 1][ty][tx + 1];
-    if (gx > 0) off += txm * x1s[tz + 1][ty + 1][tx];
-    if (gx < nx - 1) off += txp * x1s[tz + 1][ty + 1][tx + 2];
-    if (gy < ny - 1) off += typ * x1s[tz + 1][ty + 2][tx + 1];
-    if (gz < nz - 1) off += tzp * x1s[tz + 2][ty + 1][tx + 1];
-    const double dA = (c == 0) ? 2.0 * D : D;
-    const double x1c = x1s[tz + 1][ty + 1][tx + 1];
-    const double r1 = b[c] - (dA * x1c - off);
-    if (!done) {
-      xo[c] = x1c;
-      r[c] = r1;
-    }
-  }
-  if (first) {
-    __shared__ double sh[32];
-    for (int o = 16; o > 0; o >>= 1) nrm += __shfl_xor_sync(0xffffffffu, nrm, o);
-    if ((tid & 31) == 0) sh[tid >> 5] = nrm;
-    __syncthreads();
-    if (tid < 32) {
-      double w = tid < NT / 32 ? sh[tid] : 0.0;
-      for (int o = 16; o > 0; o >>= 1) w += __shfl_xor_sync(0xffffffffu, w, o);
-      if (tid == 0)
-        partials[blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z)] = w;
-    }
-  }
 }
 
 struct LevelView {
@@ -465,49 +369,6 @@ __global__ void __launch_bounds__(CT) k_ilu_red(StencilT S, const double* __rest
   for (int f = 0; f < 6; ++f)
     if (t[f] != 0.0) y += t[f] * r[nb[f]];
   x[c] += y * dinv[c];
-}
-
-// a6 + a8 for explicit levels with few columns (M <= RRS_MAX_M: well, indicator and
-// dynamic partitions): the warp-segmented sums go to a per-CTA shared-memory copy of r_c
-// and each CTA adds its nonzero entries to global memory once, instead of one global
-// atomic per warp segment — with M = 6 (the well level) those ~70k atomics all hit six
-// addresses.  Grid-stride over cells with a fixed grid (rrs_grid()).
-constexpr int RRS_MAX_M = 6000;  // shared r_c within the 48 KB default (static smem included)
-__global__ void __launch_bounds__(CT) k_res_restrict_small(StencilT S, LevelView L, int M,
-                                                           const double* __restrict__ x,
-                                                           const double* __restrict__ b,
-                                                           double* __restrict__ rc, int first,
-                                                           double* __restrict__ partials,
-                                                           const IterState* st) {
-  if (is_done(st)) return;
-  extern __shared__ double rsm[];
-  for (int m = threadIdx.x; m < M; m += blockDim.x) rsm[m] = 0.0;
-  __syncthreads();
-  const int N = S.g.nxy * S.g.nz;
-  const int stride = gridDim.x * blockDim.x;
-  double v2 = 0.0;
-  for (int base = blockIdx.x * blockDim.x; base < N; base += stride) {  // warp-uniform
-    const int c = base + threadIdx.x;
-    const bool in = c < N;
-    const int cc = in ? c : N - 1;
-    int i, j, k;
-    g3_coords(S.g, cc, i, j, k);
-    double r = 0.0;
-    if (in) {
-      double dA;
-      r = residual_at(S, x, b, c, i, j, k, &dA);
-    }
-    v2 += r * r;
-    for (int s2 = 0; s2 < L.W; ++s2) {
-      const int key = in ? L.col[(size_t)s2 * N + c] : -1;
-      const double v = key >= 0 ? (L.unit ? r : L.P[(size_t)s2 * N + c] * r) : 0.0;
-      warp_segmented_add(key, v, rsm);
-    }
-  }
-  __syncthreads();
-  for (int m = threadIdx.x; m < M; m += blockDim.x)
-    if (rsm[m] != 0.0) atomicAdd(rc + m, rsm[m]);
-  if (first) warp_partial(v2, partials);
 }
 
 // Deterministic form for M <= RRD_MAX_M (the dynamic, well and indicator levels): no
@@ -826,7 +687,6 @@ __device__ __forceinline__ void restrict_row_body(const LevelView& L, const doub
     for (int x = x0; x < x1; ++x) v += tp[x < 256 ? x : XL + (x - 256)];
     if (!done) rc[Jx + L.nb0 * (Jy + L.nb1 * Jz)] = v;
   }
-  __syncthreads();  // rsh is reused by the next unit of a persistent CTA
 }
 
 __global__ void __launch_bounds__(RR2_THREADS) k_restrict_cart(LevelView L,
@@ -875,191 +735,6 @@ __global__ void __launch_bounds__(CT) k_prolong_cart(LevelView L, double* __rest
   for (int s = 0; s < 8; ++s) acc += v[s] * xv[s];
   const double xn = x[c] + acc;
   if (!done) x[c] = xn;
-}
-
-// ---------------------------------------------------------------- persistent cycle (rows a6–a11)
-// Opt-in (MSB_PERSIST=1).  Measured slower than the CUDA-graph chain of kernels:
-// 114 us vs 71.7 us per config-2 iteration, 1.21 vs 0.76 ms on config 5
-// (profiles/r01_v8) — six grid barriers per iteration, one register budget for all
-// phases and L2-only (cg) loads of the stencil inputs cost more than the launch ramps
-// they remove.
-// The whole Richardson solve for one pre-smoothed Cartesian level (ν = 1) as ONE
-// cooperative launch: phases Jacobi → stop test → residual → restriction → SYMV tiles →
-// SYMV reduce → prolongation, separated by grid-wide barriers, looping on the device
-// until the stop test fires.  At config-2 size every pass is ~50–70 MB, where a kernel
-// launch's ramp-up and drain cost ~6 µs (a plain 54 MB 5-read/1-write pass reaches only
-// 3.3 TB/s, scripts/probes/stream_probe.cu); resident CTAs start each phase's loads the
-// moment the barrier opens.  The stop test is evaluated redundantly by every CTA from
-// the per-CTA partials in one fixed order, so all CTAs take the same decision without
-// another barrier.  Data rewritten inside the launch (x, r, r_c, partials, x_c) is read
-// with ld.global.cg: no kernel boundary invalidates L1 between phases.
-struct PersistArgs {
-  StencilT S;
-  LevelView V;
-  const double* b;
-  double* xb0;
-  double* xb1;
-  double* r;
-  double* rc;
-  double* xc;
-  double* partials;
-  const double* Xp;
-  double* part;
-  int M, ntb;
-  long long nt;
-  double omega;
-  IterState* st;
-  double* res;
-  int cur0;
-};
-
-__device__ __forceinline__ double block_sum256(double v, double* sh32) {
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  if ((threadIdx.x & 31) == 0) sh32[threadIdx.x >> 5] = v;
-  __syncthreads();
-  double w = 0.0;
-  if (threadIdx.x < 32) {
-    w = threadIdx.x < (blockDim.x >> 5) ? sh32[threadIdx.x] : 0.0;
-    for (int o = 16; o > 0; o >>= 1) w += __shfl_xor_sync(0xffffffffu, w, o);
-  }
-  __syncthreads();
-  return w;  // valid in warp 0
-}
-
-// r = b - A x at cell c with coherent loads of x (same order as residual_at)
-__device__ __forceinline__ double residual_cg(const StencilT& S, const double* x,
-                                              const double* __restrict__ b, int c, double* dAo,
-                                              double* xco) {
-  int i, j, k;
-  g3_coords(S.g, c, i, j, k);
-  const int nx = S.g.nx, sxy = S.g.nxy;
-  const double txp = S.Tx[c], typ = S.Ty[c], tzp = S.Tz[c];
-  const double txm = i > 0 ? S.Tx[c - 1] : 0.0;
-  const double tym = j > 0 ? S.Ty[c - nx] : 0.0;
-  const double tzm = k > 0 ? S.Tz[c - sxy] : 0.0;
-  const double D = txp + txm + typ + tym + tzp + tzm;
-  double off = 0.0;
-  if (k > 0) off += tzm * __ldcg(x + c - sxy);
-  if (j > 0) off += tym * __ldcg(x + c - nx);
-  if (i > 0) off += txm * __ldcg(x + c - 1);
-  if (i < nx - 1) off += txp * __ldcg(x + c + 1);
-  if (j < S.g.ny - 1) off += typ * __ldcg(x + c + nx);
-  if (k < S.g.nz - 1) off += tzp * __ldcg(x + c + sxy);
-  const double dA = (c == 0) ? 2.0 * D : D;
-  const double xc = __ldcg(x + c);
-  *dAo = dA;
-  *xco = xc;
-  return b[c] - (dA * xc - off);
-}
-
-__global__ void __launch_bounds__(256) k_cycle_persistent(PersistArgs A) {
-  namespace cgr = cooperative_groups;
-  cgr::grid_group grid = cgr::this_grid();
-  extern __shared__ double dsm[];  // restriction scratch
-  __shared__ double sh32[32];
-  __shared__ double wsh;
-  const StencilT& S = A.S;
-  const int N = S.g.nxy * S.g.nz;
-  const int gtid = blockIdx.x * blockDim.x + threadIdx.x, gsz = gridDim.x * blockDim.x;
-  IterState ls = *A.st;  // the stop-test state, identical in every CTA
-  int cur = A.cur0;
-  const bool writer = blockIdx.x == 0 && threadIdx.x == 0;
-  for (;;) {
-    const double* x0 = cur ? A.xb1 : A.xb0;
-    double* x1 = cur ? A.xb0 : A.xb1;
-    // a7: Jacobi, with the ||r||^2 partial of the stop test
-    double v = 0.0;
-    for (int c = gtid; c < N; c += gsz) {
-      double dA, xc;
-      const double r0 = residual_cg(S, x0, A.b, c, &dA, &xc);
-      x1[c] = xc + A.omega * (r0 / dA);
-      v += r0 * r0;
-    }
-    v = block_sum256(v, sh32);
-    if (threadIdx.x == 0) A.partials[blockIdx.x] = v;
-    grid.sync();
-    // a11: stop test — every CTA sums the partials in the same order
-    double w = 0.0;
-    for (int t = threadIdx.x; t < (int)gridDim.x; t += blockDim.x) w += __ldcg(A.partials + t);
-    w = block_sum256(w, sh32);
-    if (threadIdx.x == 0) wsh = w;
-    __syncthreads();
-    w = wsh;
-    {
-      const double nrm = sqrt(w);
-      const int k = ls.k;
-      const double rho = nrm / ls.bscale;
-      if (writer) A.res[k] = rho;
-      if (k == 0) ls.r0 = nrm;
-      int done = 0;
-      if (ls.fixed > 0) {
-        if (k >= ls.fixed) {
-          done = 1;
-          ls.converged = rho <= ls.tol;
-        }
-      } else if (rho <= ls.tol) {
-        done = 1;
-        ls.converged = 1;
-      } else if (k >= ls.max_iter) {
-        done = 1;
-      }
-      if (!(nrm <= 1e6 * ls.r0) && ls.r0 > 0.0) {
-        done = 1;
-        ls.diverged = 1;
-      }
-      if (done) {
-        ls.done = 1;
-        break;
-      }
-      ls.k = k + 1;
-    }
-    // a6: residual of the smoothed iterate
-    for (int c = gtid; c < N; c += gsz) {
-      double dA, xc;
-      A.r[c] = residual_cg(S, x1, A.b, c, &dA, &xc);
-    }
-    grid.sync();
-    // a8: restriction, one (Jy, Jz) row of coarse blocks per unit
-    for (int u = blockIdx.x; u < A.V.nb1 * A.V.nb2; u += gridDim.x)
-      restrict_row_body<true>(A.V, A.r, A.rc, u, dsm, false);
-    grid.sync();
-    // a5: x_c = A_c^{-1} r_c (symmetric GEMV)
-    for (long long t = blockIdx.x; t < A.nt; t += gridDim.x) symv_tile_body<true>(A.Xp, A.M, A.rc, A.part, t);
-    grid.sync();
-    for (int bb = blockIdx.x; bb < A.ntb; bb += gridDim.x)
-      symv_reduce_body<true>(A.part, A.M, A.ntb, A.xc, bb, false);
-    grid.sync();
-    // a9: prolongation
-    for (int c = gtid; c < N; c += gsz) {
-      int i, j, k;
-      g3_coords(A.V.g, c, i, j, k);
-      const int2 tx = reinterpret_cast<const int2*>(A.V.tab)[i];
-      const int2 ty = reinterpret_cast<const int2*>(A.V.tab)[A.V.g.nx + j];
-      const int2 tz = reinterpret_cast<const int2*>(A.V.tab)[A.V.g.nx + A.V.g.ny + k];
-      const double* __restrict__ base = A.V.P + c;
-      double acc = 0.0;
-#pragma unroll
-      for (int s = 0; s < 8; ++s) {
-        const int jx = (s & 1) ? tx.y : tx.x, jy = (s & 2) ? ty.y : ty.x, jz = (s & 4) ? tz.y : tz.x;
-        const bool act = (jx | jy | jz) >= 0;
-        const int col = jx + A.V.nb0 * (jy + A.V.nb1 * jz);
-        const double pv = act ? base[(size_t)s * N] : 0.0;
-        const double xv = act ? __ldcg(A.xc + col) : 0.0;
-        acc += pv * xv;
-      }
-      x1[c] = __ldcg(x1 + c) + acc;
-    }
-    cur ^= 1;
-    grid.sync();
-  }
-  if (writer) {
-    A.st->k = ls.k;
-    A.st->done = ls.done;
-    A.st->converged = ls.converged;
-    A.st->diverged = ls.diverged;
-    A.st->r0 = ls.r0;
-    A.st->cur = cur;
-  }
 }
 
 __global__ void k_zero_if(double* __restrict__ p, int n, const IterState* st) {
@@ -1247,33 +922,16 @@ static msb_status build_dynamic(msb_ctx ctx, msb_solver s, const double* dp, int
   msb_op op = s->op;
   int64_t N = op->N;
   cudaStream_t st = ctx->stream;
-  static const bool tdbg = getenv("MSB_DYN_TIMING") != nullptr;
-  static double tt[6] = {0, 0, 0, 0, 0, 0};
-  static int calls = 0;
-  auto now = [&]() {
-    cudaStreamSynchronize(st);
-    return std::chrono::duration<double, std::micro>(
-               std::chrono::steady_clock::now().time_since_epoch()).count();
-  };
-  double tq = tdbg ? now() : 0;
-  auto lap = [&](int i) {
-    if (!tdbg) return;
-    const double t = now();
-    tt[i] += t - tq;
-    tq = t;
-  };
   unsigned long long* mx = reinterpret_cast<unsigned long long*>(s->scratch_i);
   MSB_CUDA_TRY(ctx, cudaMemsetAsync(mx, 0, 8, st));
   k_absmax_vec<<<(unsigned)std::min<int64_t>(grid_for(N, 256), 2 * ctx->sm_count), 256, 0, st>>>(dp, N, mx);
   MSB_LAUNCH_CHECK(ctx);
-  lap(0);
   // max|Δp| is read back with the block count (no synchronisation of its own); when it is
   // 0 the stage is skipped there
   k_bins<<<grid_for(N, 256), 256, 0, st>>>(dp, N, mx, s->edge0, s->edge1, s->bins);
   MSB_LAUNCH_CHECK(ctx);
-  msb_status rc = cc_label(ctx, op, s->bins, s->lab, false, nullptr);
+  msb_status rc = cc_label(ctx, op, s->bins, s->lab, nullptr);
   if (rc) return rc;
-  lap(1);
   MSB_CUDA_TRY(ctx, cudaMemsetAsync(s->cnt, 0, N * sizeof(int32_t), st));
   k_sizes<<<grid_for(N, 256), 256, 0, st>>>(s->lab, N, s->cnt);
   MSB_LAUNCH_CHECK(ctx);
@@ -1289,7 +947,6 @@ static msb_status build_dynamic(msb_ctx ctx, msb_solver s, const double* dp, int
   k_merge_label<<<grid_for(N, 256), 256, 0, st>>>(s->lab, s->cnt, s->bins, N, 1, s->mhist + 129,
                                                   s->ids, s->mhist + 128);
   MSB_LAUNCH_CHECK(ctx);
-  lap(2);
   int32_t M = 0;
   // canonical numbering: labels are minimum cells of their blocks; max|Δp| comes back with
   // its count (one synchronisation for both)
@@ -1312,91 +969,10 @@ static msb_status build_dynamic(msb_ctx ctx, msb_solver s, const double* dp, int
   D->cur = 0;
   D->M = M;
   if (part_out) MSB_CUDA_TRY(ctx, copy_out(ctx, part_out, D->part, N * sizeof(int32_t)));
-  lap(3);
   rc = coarse_assemble_dense(ctx, D, op);
   if (rc) return rc;
-  lap(4);
-  if (tdbg && ++calls % 50 == 0)
-    fprintf(stderr, "build_dynamic (us/call over %d): absmax %.0f cc %.0f merge %.0f canon %.0f assemble %.0f\n",
-            calls, tt[0] / calls, tt[1] / calls, tt[2] / calls, tt[3] / calls, tt[4] / calls);
   *M_out = M;
   return MSB_OK;
-}
-
-// ---------------------------------------------------------------- L2 residency of P
-// P is read twice per iteration (restriction, prolongation) and, on the 1.1M-cell grid,
-// fits the device's persisting-L2 carve-out (8N doubles = 71.8 MB <= 82.9 MB on B200).
-// While a solve runs the carve-out is set to P's size and the library stream (and the
-// graph-capture stream) carry an access-policy window over P, so after the first
-// iteration P is served from L2 (ncu, direct launches: restriction DRAM reads 53 -> 0.3 MB).
-// The window covers only P's addresses, so the other kernels' accesses are unaffected.
-// When the solve returns, the streams' previous windows are restored, persisting lines
-// are reset and the carve-out is released, so the basis sweeps keep the whole L2.
-// Opt-in (MSB_L2_P=1) and skipped when P does not fit (config 5: 640 MB): measured on
-// config 2 the restriction's DRAM reads drop as intended, but the 74.6 MB set-aside
-// leaves the stencil passes 58 MB of normal L2 and the iteration runs 72.0 -> 74.4 us
-// (profiles/r01_v10).  A per-launch access-policy attribute had no effect at all; the
-// window has to be a stream attribute (and, for captured graphs, a kernel-node attribute).
-static void set_window(cudaStream_t st, const cudaAccessPolicyWindow& w) {
-  if (!st) return;
-  cudaStreamAttrValue sv{};
-  sv.accessPolicyWindow = w;
-  cudaStreamSetAttribute(st, cudaStreamAttributeAccessPolicyWindow, &sv);
-}
-
-static cudaAccessPolicyWindow p_window(msb_solver s) {
-  cudaAccessPolicyWindow w{};
-  w.base_ptr = const_cast<void*>(s->l2_base);
-  w.num_bytes = s->l2_bytes;
-  w.hitRatio = 1.0f;
-  w.hitProp = cudaAccessPropertyPersisting;
-  w.missProp = cudaAccessPropertyStreaming;
-  return w;
-}
-
-static void l2_begin(msb_ctx ctx, msb_solver s) {
-  s->l2_base = nullptr;
-  s->l2_bytes = 0;
-  const char* e = getenv("MSB_L2_P");
-  if (!(e && e[0] == '1') || s->levels.size() != 1 || s->levels[0]->kind != 0) return;
-  static size_t max_persist = (size_t)-1, max_win = 0;
-  if (max_persist == (size_t)-1) {
-    int v = 0, w = 0;
-    max_persist = cudaDeviceGetAttribute(&v, cudaDevAttrMaxPersistingL2CacheSize, ctx->device) ==
-                          cudaSuccess ? (size_t)v : 0;
-    max_win = cudaDeviceGetAttribute(&w, cudaDevAttrMaxAccessPolicyWindowSize, ctx->device) ==
-                      cudaSuccess ? (size_t)w : 0;
-    cudaGetLastError();
-  }
-  msb_level L = s->levels[0];
-  const size_t bytes = (size_t)8 * L->N * sizeof(double);
-  if (bytes > max_persist || bytes > max_win) return;
-  if (cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, bytes) != cudaSuccess) {
-    cudaGetLastError();
-    return;
-  }
-  cudaStreamAttrValue prev{};
-  if (ctx->stream &&
-      cudaStreamGetAttribute(ctx->stream, cudaStreamAttributeAccessPolicyWindow, &prev) == cudaSuccess)
-    s->l2_prev = prev.accessPolicyWindow;
-  else
-    s->l2_prev = cudaAccessPolicyWindow{};
-  cudaGetLastError();
-  s->l2_base = L->P[L->cur];
-  s->l2_bytes = bytes;
-  set_window(ctx->stream, p_window(s));
-  set_window(s->cap_stream, p_window(s));
-}
-
-static void l2_end(msb_ctx ctx, msb_solver s) {
-  if (!s->l2_bytes) return;
-  set_window(ctx->stream, s->l2_prev);
-  set_window(s->cap_stream, cudaAccessPolicyWindow{});
-  cudaCtxResetPersistingL2Cache();
-  cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, 0);
-  cudaGetLastError();
-  s->l2_base = nullptr;
-  s->l2_bytes = 0;
 }
 
 namespace msb {
@@ -1469,8 +1045,7 @@ out:
 }
 
 static bool use_csc(msb_solver s, msb_level L) {
-  static const bool off = getenv("MSB_NO_CSC") != nullptr;
-  return !off && L->kind == 1 && L->M > RRD_MAX_M && L != s->dyn_level && L->csc_ptr;
+  return L->kind == 1 && L->M > RRD_MAX_M && L != s->dyn_level && L->csc_ptr;
 }
 }  // namespace msb
 
@@ -1483,6 +1058,15 @@ msb_status msb_solver_create(msb_ctx ctx, msb_op op, const msb_level* levels, in
   if (!ctx || !op || !out || n_levels < 0 || (n_levels > 0 && !levels) || nu < 0)
     return set_error(ctx, MSB_EINVAL, "msb_solver_create args");
   if (n_levels == 0 && !dyn_enable) return set_error(ctx, MSB_EINVAL, "solver needs a level");
+  {  // A must be nonsingular: every cell connected to the gauge cell (reading A7)
+    bool conn = false;
+    msb_status rc = op_connected(ctx, op, &conn);
+    if (rc) return rc;
+    if (!conn)
+      return set_error(ctx, MSB_EINCONSISTENT,
+                       "the faces with T > 0 split the grid into several compartments: A is "
+                       "singular on every compartment without the gauge cell 0");
+  }
   msb_solver s = new msb_solver_s();
   s->ctx = ctx;
   s->op = op;
@@ -1493,16 +1077,12 @@ msb_status msb_solver_create(msb_ctx ctx, msb_op op, const msb_level* levels, in
   s->edge0 = dyn_edge0;
   s->edge1 = dyn_edge1;
   s->dyn_max = dyn_max_blocks > 0 ? dyn_max_blocks : 1024;
-  // fused TMA residual+restriction (cycle_tma.cu) is opt-in: on config 2 it measured
-  // 46 us against 16 + 27 us for the residual and gather passes it replaces, but the
-  // cycle as a whole ran 103 vs 90 us (profiles/r01_v3) — TMA box-row throughput bound
-  s->no_fuse = getenv("MSB_FUSE_RR") == nullptr;
   int maxM = 1;
   for (int l = 0; l < n_levels; ++l) {
     msb_level L = levels[l];
     if (!L || L->N != op->N) return set_error(ctx, MSB_EDIM, "level %d size mismatch", l);
     if (!L->co.ready) return set_error(ctx, MSB_EINVAL, "level %d not assembled", l);
-    if (L->kind == 1 && L->M > RRD_MAX_M && !getenv("MSB_NO_CSC")) {
+    if (L->kind == 1 && L->M > RRD_MAX_M) {
       msb_status rc = level_csc_build(ctx, L);
       if (rc) return rc;
     }
@@ -1510,7 +1090,6 @@ msb_status msb_solver_create(msb_ctx ctx, msb_op op, const msb_level* levels, in
     maxM = std::max(maxM, L->M);
   }
   int64_t N = op->N;
-  coarse_persist_init(ctx);  // device-wide L2 carve-out, never inside a graph capture
   if (s->dyn) maxM = std::max(maxM, s->dyn_max + 3);
   s->maxM = maxM;
   MSB_ALLOC(ctx, s->xbuf[0], double, N);
@@ -1594,8 +1173,7 @@ static msb_status enqueue_stage(msb_ctx ctx, msb_solver s, msb_level L, const do
   // the rest of the iteration and is joined before the next iteration's first kernel
   // (kernels that have not yet seen `done` then do harmless work).
   const bool side = s->levels.size() == 1 && s->nu == 1 && !s->post && L->kind == 0 &&
-                    s->smoother == 0 &&
-                    !getenv("MSB_SERIAL_FINALIZE");
+                    s->smoother == 0;
   auto fin = [&](unsigned np) -> msb_status {  // np = blocks of the kernel that wrote partials
     if (side) {
       if (!s->side_stream) {
@@ -1619,42 +1197,6 @@ static msb_status enqueue_stage(msb_ctx ctx, msb_solver s, msb_level L, const do
     MSB_CUDA_TRY(ctx, cudaStreamWaitEvent(st, s->ev_join, 0));
     s->pending_join = false;
   }
-  // fused Jacobi + residual (opt-in, MSB_JACRES=1): measured 57 us against 15.7 + 16.8 us
-  // for the two passes it replaces — the 3D halo (4.5 x loads and 2.4 Jacobi updates
-  // per cell) and 2 CTAs/SM by registers cost more than the second pass over x, b, T
-  const bool jr = L->kind == 0 && !s->post && s->nu == 1 && s->smoother == 0 && getenv("MSB_JACRES");
-  auto jacres = [&]() -> msb_status {
-    const dim3 gr((unsigned)((op->nx + JR_X - 1) / JR_X), (unsigned)((op->ny + JR_Y - 1) / JR_Y),
-                  (unsigned)((op->nz + JR_Z - 1) / JR_Z));
-    k_jacres<<<gr, dim3(JR_X, JR_Y, JR_Z), 0, st>>>(S, s->xbuf[cur], s->xbuf[cur ^ 1], b, s->r,
-                                                   s->omega_s, first ? 1 : 0, s->partials, s->st);
-    MSB_LAUNCH_CHECK(ctx);
-    if (first) {
-      msb_status rc = fin(gr.x * gr.y * gr.z);
-      if (rc) return rc;
-    }
-    first = false;
-    cur ^= 1;
-    return MSB_OK;
-  };
-  // fused Jacobi + residual, TMA z-marching (jacres_tma.cu, opt-in MSB_JQ=1): Cartesian
-  // level, pre-smoothing, ν = 1, grid and b TMA-compatible (even nx, 16-byte aligned b)
-  bool jq = false;
-  if (!jr && L->kind == 0 && !s->post && s->nu == 1 && s->no_fuse && s->smoother == 0) {
-    if (!s->jq) s->jq = new JQPlan();
-    if (!s->jq->ok || s->jq->b != b || s->jq->x[0] != s->xbuf[0] || s->jq->x[1] != s->xbuf[1])
-      jacres_tma_plan(ctx, op, s->xbuf[0], s->xbuf[1], b, s->jq);
-    jq = s->jq->ok;
-  }
-  auto jqres = [&]() -> msb_status {
-    msb_status rc = jacres_tma_launch(ctx, op, *s->jq, cur, s->xbuf[cur ^ 1], s->r, s->omega_s,
-                                      first ? 1 : 0, s->partials, &s->st->done);
-    if (rc) return rc;
-    if (first && (rc = fin(s->jq->grid))) return rc;
-    first = false;
-    cur ^= 1;
-    return MSB_OK;
-  };
   auto ilu = [&]() -> msb_status {  // ν red-black ILU(0) steps on x in place (NEXT-2)
     for (int v = 0; v < s->nu; ++v) {
       k_residual<<<g4, CT, 0, st>>>(S, s->xbuf[cur], b, s->r, first ? 1 : 0, s->partials, s->st);
@@ -1688,32 +1230,14 @@ static msb_status enqueue_stage(msb_ctx ctx, msb_solver s, msb_level L, const do
     return MSB_OK;
   };
   auto corr = [&]() -> msb_status {
-    RRLaunch rr;
-    if (L->kind == 0 && !s->no_fuse && resrestrict_plan(ctx, op, L, s->xbuf[cur], b, &rr)) {
-      k_zero_if<<<grid_for(L->M, 256), 256, 0, st>>>(s->rc, L->M, s->st);
+    if (L->kind == 0) {
+      k_residual<<<g4, CT, 0, st>>>(S, s->xbuf[cur], b, s->r, first ? 1 : 0, s->partials, s->st);
       MSB_LAUNCH_CHECK(ctx);
-      msb_status rc = resrestrict_launch(ctx, op, L, rr, s->rc, first ? 1 : 0, s->partials,
-                                         &s->st->done);
-      if (rc) return rc;
       if (first) {
-        if ((rc = fin(rr.grid))) return rc;
+        msb_status rc = fin(g4);
+        if (rc) return rc;
       }
       first = false;
-      coarse_solve_dense(ctx, L->co, s->rc, s->xc, &s->st->done);
-      k_prolong_cart<<<g, CT, 0, st>>>(V, s->xbuf[cur], s->xc, s->st);
-      MSB_LAUNCH_CHECK(ctx);
-      return MSB_OK;
-    }
-    if (L->kind == 0) {
-      if (!jr && !jq) {
-        k_residual<<<g4, CT, 0, st>>>(S, s->xbuf[cur], b, s->r, first ? 1 : 0, s->partials, s->st);
-        MSB_LAUNCH_CHECK(ctx);
-        if (first) {
-          msb_status rc = fin(g4);
-          if (rc) return rc;
-        }
-        first = false;
-      }
       if (op->nx > 512)
         return set_error(ctx, MSB_EINVAL, "Cartesian restriction supports nx <= 512 (nx=%d)", op->nx);
       k_restrict_cart<<<L->nb[1] * L->nb[2], RR2_THREADS, restrict_rows_smem(op->nx), st>>>(
@@ -1743,8 +1267,7 @@ static msb_status enqueue_stage(msb_ctx ctx, msb_solver s, msb_level L, const do
     k_zero_if<<<grid_for(L->M, 256), 256, 0, st>>>(s->rc, L->M, s->st);
     MSB_LAUNCH_CHECK(ctx);
     unsigned gpart = g;  // blocks that write stop-test partials
-    static const bool no_small = getenv("MSB_NO_RRS") != nullptr;
-    if (L->kind == 1 && L->M <= RRD_MAX_M && !no_small) {
+    if (L->kind == 1 && L->M <= RRD_MAX_M) {
       gpart = (unsigned)std::min<int64_t>(g, 4 * ctx->sm_count);
       const size_t need = (size_t)gpart * L->M;
       if (s->rc_part_cap < need) {
@@ -1765,10 +1288,6 @@ static msb_status enqueue_stage(msb_ctx ctx, msb_solver s, msb_level L, const do
                                                   first ? 1 : 0, s->partials, s->st);
       MSB_LAUNCH_CHECK(ctx);
       k_rc_combine<<<L->M, 256, 0, st>>>(s->rc_part, (int)gpart, L->M, s->rc, s->st);
-    } else if (L->kind == 1 && L->M <= RRS_MAX_M && !no_small) {
-      gpart = (unsigned)std::min<int64_t>(g, 4 * ctx->sm_count);
-      k_res_restrict_small<<<gpart, CT, (size_t)L->M * sizeof(double), st>>>(
-          S, V, L->M, s->xbuf[cur], b, s->rc, first ? 1 : 0, s->partials, s->st);
     } else {
       k_res_restrict<<<g, CT, 0, st>>>(S, V, s->xbuf[cur], b, s->rc, first ? 1 : 0, s->partials,
                                        s->st);
@@ -1789,7 +1308,7 @@ static msb_status enqueue_stage(msb_ctx ctx, msb_solver s, msb_level L, const do
     if ((rc = corr())) return rc;
     if ((rc = jac())) return rc;
   } else {
-    if ((rc = jr ? jacres() : (jq ? jqres() : jac()))) return rc;
+    if ((rc = jac())) return rc;
     if ((rc = corr())) return rc;
   }
   return MSB_OK;
@@ -1829,7 +1348,7 @@ static void drop_graphs(msb_solver s) {
 static msb_status chunk_graph(msb_ctx ctx, msb_solver s, const double* db, int cur0, int n,
                               cudaGraphExec_t* out) {
   *out = nullptr;
-  std::vector<const void*> key = {db, s->res_dev, (const void*)(intptr_t)n, s->l2_base};
+  std::vector<const void*> key = {db, s->res_dev, (const void*)(intptr_t)n};
   for (msb_level L : s->levels) {
     key.push_back(L->P[L->cur]);
     key.push_back(L->co.Ainv);
@@ -1845,7 +1364,6 @@ static msb_status chunk_graph(msb_ctx ctx, msb_solver s, const double* db, int c
   }
   if (!s->cap_stream) {
     MSB_CUDA_TRY(ctx, cudaStreamCreateWithFlags(&s->cap_stream, cudaStreamNonBlocking));
-    if (s->l2_bytes) set_window(s->cap_stream, p_window(s));
   }
   cudaStream_t user = ctx->stream;
   ctx->stream = s->cap_stream;
@@ -1863,21 +1381,6 @@ static msb_status chunk_graph(msb_ctx ctx, msb_solver s, const double* db, int c
     s->pending_join = false;
     cudaGraph_t graph = nullptr;
     cudaError_t e2 = cudaStreamEndCapture(s->cap_stream, &graph);
-    if (!rc && e2 == cudaSuccess && s->l2_bytes) {
-      // stream attributes are not captured: put the P window on every kernel node
-      size_t nn = 0;
-      cudaGraphGetNodes(graph, nullptr, &nn);
-      std::vector<cudaGraphNode_t> nodes(nn);
-      if (nn) cudaGraphGetNodes(graph, nodes.data(), &nn);
-      cudaKernelNodeAttrValue kv{};
-      kv.accessPolicyWindow = p_window(s);
-      for (cudaGraphNode_t nd : nodes) {
-        cudaGraphNodeType ty;
-        if (cudaGraphNodeGetType(nd, &ty) == cudaSuccess && ty == cudaGraphNodeTypeKernel)
-          cudaGraphKernelNodeSetAttribute(nd, cudaKernelNodeAttributeAccessPolicyWindow, &kv);
-      }
-      cudaGetLastError();
-    }
     if (!rc && e2 == cudaSuccess) {
       e = cudaGraphInstantiate(&s->gexec[cur0], graph, 0);
     } else if (e2 != cudaSuccess) {
@@ -1934,7 +1437,7 @@ msb_status msb_partition_indicator(msb_ctx ctx, msb_op op, const double* ind, co
   int32_t* rep = scr + nbin + 1;  // per bin: minimum cell of its small components
   k_bins_abs<<<grid_for(N, 256), 256, 0, st>>>(d, N, E, bins);
   MSB_LAUNCH_CHECK(ctx);
-  msb_status rc = cc_label(ctx, op, bins, lab, false, nullptr);
+  msb_status rc = cc_label(ctx, op, bins, lab, nullptr);
   if (rc) return rc;
   MSB_CUDA_TRY(ctx, cudaMemsetAsync(cnt, 0, N * sizeof(int32_t), st));
   k_sizes<<<grid_for(N, 256), 256, 0, st>>>(lab, N, cnt);
@@ -1999,12 +1502,6 @@ msb_status msb_ms_iterate(msb_ctx ctx, msb_solver s, const double* b, double* x,
   MSB_CUDA_TRY(ctx, cudaMemcpyAsync(s->st, &h, sizeof(h), cudaMemcpyHostToDevice, st));
   msb_status rc = solver_smoother_setup(ctx, s);  // pivots from the operator's current T
   if (rc) return rc;
-  l2_begin(ctx, s);
-  struct L2Guard {
-    msb_ctx ctx;
-    msb_solver s;
-    ~L2Guard() { l2_end(ctx, s); }
-  } l2_guard{ctx, s};
   rc = enqueue_norm(ctx, s, s->xbuf[0], db, 1);
   if (rc) return rc;
   int cur = 0;
@@ -2013,49 +1510,6 @@ msb_status msb_ms_iterate(msb_ctx ctx, msb_solver s, const double* b, double* x,
   cur_after.push_back(0);
   std::vector<int32_t> dynM;
   IterState hs{};
-  const bool persist = !s->dyn && s->levels.size() == 1 && s->levels[0]->kind == 0 && !s->post &&
-                       s->nu == 1 && s->smoother == 0 && s->levels[0]->co.Xp && op->nx <= 512 &&
-                       getenv("MSB_PERSIST");
-  if (persist) {
-    msb_level L = s->levels[0];
-    const size_t smem = restrict_rows_smem(op->nx);
-    int dev_coop = 0, occ = 0;
-    cudaDeviceGetAttribute(&dev_coop, cudaDevAttrCooperativeLaunch, ctx->device);
-    MSB_CUDA_TRY(ctx, cudaFuncSetAttribute(k_cycle_persistent,
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    MSB_CUDA_TRY(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_cycle_persistent, 256,
-                                                                   smem));
-    if (dev_coop && occ > 0) {
-      PersistArgs A;
-      A.S = stencil(op);
-      A.V = view(L);
-      A.b = db;
-      A.xb0 = s->xbuf[0];
-      A.xb1 = s->xbuf[1];
-      A.r = s->r;
-      A.rc = s->rc;
-      A.xc = s->xc;
-      A.partials = s->partials;
-      A.Xp = L->co.Xp;
-      A.part = L->co.part;
-      A.M = L->M;
-      A.ntb = L->co.ntb;
-      A.nt = (long long)L->co.ntb * (L->co.ntb + 1) / 2;
-      A.omega = s->omega_s;
-      A.st = s->st;
-      A.res = s->res_dev;
-      A.cur0 = 0;
-      const unsigned grid = (unsigned)(occ * ctx->sm_count);
-      void* args[] = {&A};
-      MSB_CUDA_TRY(ctx, cudaLaunchCooperativeKernel((void*)k_cycle_persistent, grid, 256, args,
-                                                    smem, st));
-      count_launch();
-      MSB_CUDA_TRY(ctx, cudaMemcpyAsync(&hs, s->st, sizeof(hs), cudaMemcpyDeviceToHost, st));
-      MSB_CUDA_TRY(ctx, cudaStreamSynchronize(st));
-      cur_after.assign((size_t)hs.k + 1, hs.cur);
-      goto finish;
-    }
-  }
   if (!s->dyn) {
     const int chunk = 16;
     // x-buffer swaps per iteration (Jacobi writes out of place; ILU(0) updates in place)
@@ -2093,25 +1547,19 @@ msb_status msb_ms_iterate(msb_ctx ctx, msb_solver s, const double* b, double* x,
     }
   } else {
     // dynamic stage: host-synchronous per iteration (M_dyn is data dependent)
-    static const bool tdbg = getenv("MSB_DYN_TIMING") != nullptr;
-    double t_norm = 0, t_build = 0, t_stages = 0;
-    auto now = [&]() {
-      cudaStreamSynchronize(st);
-      return std::chrono::duration<double, std::micro>(
-                 std::chrono::steady_clock::now().time_since_epoch()).count();
-    };
     // the rebuilt level's singular-pivot flag is read with the stop-test state (one
     // synchronisation per iteration for both); a singular rebuild fails the call there
     msb_level D = s->dyn_level;
     int hsing = 0;
+    // a singular flag left by an earlier call (a failed rebuild) must not fail this one
+    // before it has rebuilt anything: only this call's rebuilds may set it
+    if (D->co.flags) MSB_CUDA_TRY(ctx, cudaMemsetAsync(D->co.flags + 1, 0, sizeof(int), st));
     while (true) {
-      double t0 = tdbg ? now() : 0;
       if ((rc = enqueue_norm(ctx, s, s->xbuf[cur], db, 0))) return rc;
       MSB_CUDA_TRY(ctx, cudaMemcpyAsync(&hs, s->st, sizeof(hs), cudaMemcpyDeviceToHost, st));
       if (D->co.flags)
         MSB_CUDA_TRY(ctx, cudaMemcpyAsync(&hsing, D->co.flags + 1, sizeof(int), cudaMemcpyDeviceToHost, st));
       MSB_CUDA_TRY(ctx, cudaStreamSynchronize(st));
-      if (tdbg) t_norm += now() - t0;
       if (hsing) {
         D->co.ready = false;
         return set_error(ctx, MSB_ESINGULAR, "dynamic stage: singular coarse matrix (M=%d)", D->M);
@@ -2119,7 +1567,6 @@ msb_status msb_ms_iterate(msb_ctx ctx, msb_solver s, const double* b, double* x,
       if (hs.done) break;
       int k = hs.k;  // iteration about to run (1-based)
       int32_t M = 0;
-      double t1 = tdbg ? now() : 0;
       if (k >= 2) {
         k_dp<<<grid_for(N, 256), 256, 0, st>>>(s->xbuf[cur], s->xprev, N, s->dpbuf);
         MSB_LAUNCH_CHECK(ctx);
@@ -2128,8 +1575,6 @@ msb_status msb_ms_iterate(msb_ctx ctx, msb_solver s, const double* b, double* x,
         D->co.defer_check = false;
         if (rc) return rc;
       }
-      if (tdbg) t_build += now() - t1;
-      if (tdbg) t1 = now();
       dynM.push_back(M);
       MSB_CUDA_TRY(ctx, cudaMemcpyAsync(s->xprev, s->xbuf[cur], N * sizeof(double),
                                         cudaMemcpyDeviceToDevice, st));
@@ -2138,14 +1583,9 @@ msb_status msb_ms_iterate(msb_ctx ctx, msb_solver s, const double* b, double* x,
         if ((rc = enqueue_stage(ctx, s, L, db, cur, first))) return rc;
       if (M > 0)
         if ((rc = enqueue_stage(ctx, s, s->dyn_level, db, cur, first))) return rc;
-      if (tdbg) t_stages += now() - t1;
       cur_after.push_back(cur);
     }
-    if (tdbg)
-      fprintf(stderr, "dyn timing (us, %d its): norm+sync %.0f build %.0f stages %.0f\n", hs.k,
-              t_norm, t_build, t_stages);
   }
-finish:
   int k = hs.k;
   int xb = cur_after[std::min<size_t>(k, cur_after.size() - 1)];
   MSB_CUDA_TRY(ctx, cudaMemcpyAsync(x, s->xbuf[xb], N * sizeof(double), cudaMemcpyDefault, st));
@@ -2186,7 +1626,6 @@ msb_status msb_solver_destroy(msb_solver s) {
   dfree(ctx, s->mhist);
   if (s->dyn_level) level_free(s->dyn_level);
   dfree(ctx, s->ilu_d);
-  delete s->jq;
   drop_graphs(s);
   if (s->cap_stream) cudaStreamDestroy(s->cap_stream);
   if (s->side_stream) cudaStreamDestroy(s->side_stream);
@@ -2209,8 +1648,6 @@ msb_status solver_smoother_setup(msb_ctx ctx, msb_solver s) {
   return MSB_OK;
 }
 
-void solver_l2_begin(msb_ctx ctx, msb_solver s) { l2_begin(ctx, s); }
-void solver_l2_end(msb_ctx ctx, msb_solver s) { l2_end(ctx, s); }
 
 msb_status solver_precondition(msb_ctx ctx, msb_solver s, const double* v, double* z) {
   cudaStream_t st = ctx->stream;

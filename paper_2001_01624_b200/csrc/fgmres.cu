@@ -112,20 +112,26 @@ extern "C" msb_status msb_fgmres(msb_ctx ctx, msb_solver s, const double* b, dou
   const int64_t N = op->N;
   cudaStream_t st = ctx->stream;
   const int m = restart;
-  void* ob = nullptr;
-  const double* db = b ? (const double*)stage_in(ctx, b, N * sizeof(double), &ob) : op->q;
+  // the Krylov workspace (and the staged rhs) is released on every return path: the
+  // stream is drained first, so no enqueued kernel still reads a freed buffer
+  struct Workspace {
+    msb_ctx ctx;
+    void* ob = nullptr;
+    double *V = nullptr, *Z = nullptr, *w = nullptr, *xd = nullptr, *part = nullptr,
+           *dots = nullptr;
+    ~Workspace() {
+      cudaStreamSynchronize(ctx->stream);
+      for (void* p : {(void*)V, (void*)Z, (void*)w, (void*)xd, (void*)part, (void*)dots, ob})
+        dfree(ctx, p);
+    }
+  } ws{ctx};
+  const double* db = b ? (const double*)stage_in(ctx, b, N * sizeof(double), &ws.ob) : op->q;
   if (!db) return set_error(ctx, MSB_ENOMEM, "rhs staging");
   {
     msb_status r0 = solver_smoother_setup(ctx, s);
     if (r0) return r0;
   }
-  solver_l2_begin(ctx, s);
-  struct L2Guard {
-    msb_ctx ctx;
-    msb_solver s;
-    ~L2Guard() { solver_l2_end(ctx, s); }
-  } l2_guard{ctx, s};
-  double *V, *Z, *w, *xd, *part, *dots;
+  double *&V = ws.V, *&Z = ws.Z, *&w = ws.w, *&xd = ws.xd, *&part = ws.part, *&dots = ws.dots;
   MSB_ALLOC(ctx, V, double, (size_t)(m + 1) * N);
   MSB_ALLOC(ctx, Z, double, (size_t)m * N);
   MSB_ALLOC(ctx, w, double, N);
@@ -255,13 +261,6 @@ extern "C" msb_status msb_fgmres(msb_ctx ctx, msb_solver s, const double* b, dou
   if (res_hist)
     for (size_t t = 0; t < res.size(); ++t) res_hist[t] = res[t];
   if (iters_out) *iters_out = k;
-  dfree(ctx, V);
-  dfree(ctx, Z);
-  dfree(ctx, w);
-  dfree(ctx, xd);
-  dfree(ctx, part);
-  dfree(ctx, dots);
-  if (ob) dfree(ctx, ob);
   if (fixed_iters > 0) return MSB_OK;
   return converged ? MSB_OK : MSB_NOT_CONVERGED;
 }

@@ -58,22 +58,6 @@ __global__ void k_compress(int32_t* __restrict__ par, int64_t n) {
   par[i] = x;
 }
 
-// Cells joined across +x/+y/+z faces when klass matches and (optionally) the face
-// is open (multiplier == 1).
-__global__ void k_cc_cells(const int32_t* __restrict__ klass, const uint8_t* __restrict__ open,
-                           int nx, int ny, int nz, int32_t* __restrict__ par) {
-  int64_t N = (int64_t)nx * ny * nz;
-  int64_t sxy = (int64_t)nx * ny;
-  int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= N) return;
-  int i = (int)(c % nx), j = (int)((c / nx) % ny), k = (int)(c / sxy);
-  uint8_t o = open ? open[c] : 7;
-  int32_t kc = klass[c];
-  if (i < nx - 1 && (o & 1) && klass[c + 1] == kc) uf_union(par, (int32_t)c, (int32_t)(c + 1));
-  if (j < ny - 1 && (o & 2) && klass[c + nx] == kc) uf_union(par, (int32_t)c, (int32_t)(c + nx));
-  if (k < nz - 1 && (o & 4) && klass[c + sxy] == kc) uf_union(par, (int32_t)c, (int32_t)(c + sxy));
-}
-
 // Two-phase labelling (same roots as unioning every face globally: roots are component
 // minima either way).  Phase 1: each CTA labels a 16x4x4 tile in shared memory (local
 // union-find over the tile's interior faces; local and global index orders agree inside a
@@ -187,24 +171,71 @@ msb_status canonical_number(msb_ctx ctx, int64_t N, const int32_t* lab, int32_t*
   return MSB_OK;
 }
 
-msb_status cc_label(msb_ctx ctx, msb_op op, const int32_t* klass, int32_t* lab, bool use_open,
-                    int32_t*) {
+// bit a of m[c]: the face (c, c + e_a) has base transmissibility T > 0
+__global__ void k_tpos_mask(const double* __restrict__ Tb, Grid3 g, uint8_t* __restrict__ m) {
+  const int N = g.nxy * g.nz;
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= N) return;
+  int i, j, k;
+  g3_coords(g, c, i, j, k);
+  m[c] = (uint8_t)((i < g.nx - 1 && Tb[c] > 0.0 ? 1 : 0) | (j < g.ny - 1 && Tb[N + c] > 0.0 ? 2 : 0) |
+                   (k < g.nz - 1 && Tb[2 * N + c] > 0.0 ? 4 : 0));
+}
+
+__global__ void k_count_ne0(const int32_t* __restrict__ lab, int64_t N, int* __restrict__ flag) {
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c < N && lab[c] != 0) atomicOr(flag, 1);
+}
+
+msb_status op_connected(msb_ctx ctx, msb_op op, bool* connected) {
+  if (op->connected >= 0) {
+    *connected = op->connected == 1;
+    return MSB_OK;
+  }
+  const int64_t N = op->N;
+  cudaStream_t st = ctx->stream;
+  int32_t* klass = dalloc_n<int32_t>(ctx, 2 * N);
+  uint8_t* m = dalloc_n<uint8_t>(ctx, N);
+  int* flag = dalloc_n<int>(ctx, 1);
+  msb_status rc = MSB_OK;
+  int h = 0;
+  if (!klass || !m || !flag) rc = set_error(ctx, MSB_ENOMEM, "connectivity scratch");
+  if (!rc && (cudaMemsetAsync(klass, 0, N * sizeof(int32_t), st) != cudaSuccess ||
+              cudaMemsetAsync(flag, 0, sizeof(int), st) != cudaSuccess))
+    rc = set_error(ctx, MSB_ECUDA, "connectivity memset");
+  if (!rc) {
+    k_tpos_mask<<<grid_for(N, 256), 256, 0, st>>>(op->Tb, make_grid3(op->nx, op->ny, op->nz), m);
+    count_launch();
+    rc = cc_label(ctx, op, klass, klass + N, m);
+  }
+  if (!rc) {
+    k_count_ne0<<<grid_for(N, 256), 256, 0, st>>>(klass + N, N, flag);
+    count_launch();
+    if (cudaMemcpyAsync(&h, flag, sizeof(int), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+        cudaStreamSynchronize(st) != cudaSuccess)
+      rc = set_error(ctx, MSB_ECUDA, "connectivity readback");
+  }
+  cudaStreamSynchronize(st);
+  dfree(ctx, klass);
+  dfree(ctx, m);
+  dfree(ctx, flag);
+  if (rc) return rc;
+  op->connected = h ? 0 : 1;
+  *connected = op->connected == 1;
+  return MSB_OK;
+}
+
+msb_status cc_label(msb_ctx ctx, msb_op op, const int32_t* klass, int32_t* lab,
+                    const uint8_t* open) {
   int64_t N = op->N;
-  static const bool one_phase = getenv("MSB_CC_GLOBAL") != nullptr;
-  if (one_phase) {
-    k_iota<<<grid_for(N, 256), 256, 0, ctx->stream>>>(lab, N);
-    MSB_LAUNCH_CHECK(ctx);
-    k_cc_cells<<<grid_for(N, 256), 256, 0, ctx->stream>>>(klass, use_open ? op->open : nullptr,
-                                                          op->nx, op->ny, op->nz, lab);
-    MSB_LAUNCH_CHECK(ctx);
-  } else {
+  {
     const int tx = (op->nx + CCT_X - 1) / CCT_X, ty = (op->ny + CCT_Y - 1) / CCT_Y,
               tz = (op->nz + CCT_Z - 1) / CCT_Z;
     k_cc_tile<<<(unsigned)((int64_t)tx * ty * tz), 256, 0, ctx->stream>>>(
-        klass, use_open ? op->open : nullptr, op->nx, op->ny, op->nz, tx, ty, lab);
+        klass, open, op->nx, op->ny, op->nz, tx, ty, lab);
     MSB_LAUNCH_CHECK(ctx);
-    k_cc_cross<<<grid_for(N, 256), 256, 0, ctx->stream>>>(klass, use_open ? op->open : nullptr,
-                                                          op->nx, op->ny, op->nz, lab);
+    k_cc_cross<<<grid_for(N, 256), 256, 0, ctx->stream>>>(klass, open, op->nx, op->ny, op->nz,
+                                                          lab);
     MSB_LAUNCH_CHECK(ctx);
   }
   k_compress<<<grid_for(N, 256), 256, 0, ctx->stream>>>(lab, N);
@@ -367,7 +398,7 @@ extern "C" msb_status msb_level_create_split(msb_ctx ctx, msb_op op, msb_level p
   MSB_ALLOC(ctx, lab, int32_t, N);
   MSB_ALLOC(ctx, spart, int32_t, N);
   MSB_ALLOC(ctx, scratch, int32_t, 2 * N);
-  msb_status st = cc_label(ctx, op, parent->part, lab, true, nullptr);
+  msb_status st = cc_label(ctx, op, parent->part, lab, op->open);
   if (st) return st;
   int32_t Ms = 0;
   st = canonical_number(ctx, N, lab, spart, scratch, &Ms);

@@ -165,15 +165,6 @@ __global__ void __launch_bounds__(SWEEP_BLOCK, 4) k_sweep_cart(
 // TMA requires the innermost box start to be 16-byte aligned, so the x halo is two
 // cells wide on each side (box x range [x0-2, x0+34), x0 a multiple of 32).
 constexpr int TT_X = 32, TT_Y = 4;
-constexpr int TT_STAGES_DEFAULT = 4;  // ring depth TT_S (MSB_SW_STAGES=4|5|6 to A/B)
-constexpr int SW8_TY_DEFAULT = 4, SW8_STAGES_DEFAULT = 3;  // k_sweep_tma8 tile rows, ring depth
-constexpr int TB_X = TT_X + 4, TB_Y = TT_Y + 2, TQ_Y = TT_Y + 1;
-constexpr int TP_DBL = 8 * TB_Y * TB_X;  // P box (doubles): rows y0-1 .. y0+TT_Y
-constexpr int TQ_DBL = 3 * TQ_Y * TB_X;  // T box: rows y0-1 .. y0+TT_Y-1
-constexpr int TSTAGE_DBL = ((TP_DBL + TQ_DBL) * 8 + 127) / 128 * 128 / 8;
-constexpr uint32_t TSTAGE_TX = (uint32_t)(TP_DBL + TQ_DBL) * 8u;
-constexpr size_t tsweep_smem(int S) { return (size_t)S * TSTAGE_DBL * 8 + 64; }
-constexpr int TSWEEP_THREADS = 2 * TT_X * TT_Y;
 
 struct SweepTiles {
   int ntx, nty, kz, items;
@@ -202,158 +193,11 @@ __device__ __forceinline__ double div_rn(double a, double b, double rb) {
   return fma(e, rb, q);
 }
 
-template <int TT_S>
-__global__ void __launch_bounds__(TSWEEP_THREADS) k_sweep_tma(
-    const __grid_constant__ CUtensorMap mP0, const __grid_constant__ CUtensorMap mP1,
-    const __grid_constant__ CUtensorMap mT, double* __restrict__ P0, double* __restrict__ P1,
-    const uint8_t* __restrict__ amask, Grid3 g, SweepTiles tl, double omega, int n, double tol,
-    unsigned long long* __restrict__ dslots) {
-  if (sweep_skip(dslots, n, tol)) return;
-  // dynamic shared memory declared 128-byte aligned (TMA destination requirement) and
-  // indexed directly, so every stage read compiles to LDS (a pointer laundered through
-  // integer alignment arithmetic would fall back to generic LD).
-  extern __shared__ __align__(128) double sm[];
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + TT_S * TSTAGE_DBL);
-  const CUtensorMap* mIn = (n & 1) ? &mP1 : &mP0;
-  double* __restrict__ Pout = (n & 1) ? P0 : P1;
-  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, h = lane >> 4;
-  const int ty = w >> 1, tx = ((w & 1) << 4) + (lane & 15);
-  const int nx = g.nx, ny = g.ny, nz = g.nz, N = g.nxy * g.nz;
-  if (tid == 0) {
-    if (smem_u32(sm) & 127u) __trap();  // TMA destinations must be 128-byte aligned
-    for (int t = 0; t < TT_S; ++t) mbar_init(&bars[t], 1);
-    mbar_fence_init();
-  }
-  __syncthreads();
-  const double om1 = 1.0 - omega;
-  const int loc = (ty + 1) * TB_X + (tx + 2);  // same offset in the P and T boxes' row grid
-  uint32_t seq = 0;  // plane sequence number over this CTA's lifetime (ring slot / phase)
-  double dloc = 0.0;
-  for (int item = blockIdx.x; item < tl.items; item += gridDim.x) {
-    const int xt = item % tl.ntx, rest = item / tl.ntx;
-    const int yt = rest % tl.nty, zc = rest / tl.nty;
-    const int x0 = xt * TT_X, y0 = yt * TT_Y, k0 = zc * tl.kz, k1 = min(k0 + tl.kz, nz);
-    const int np = k1 - k0 + 2;  // planes k0-1 .. k1
-    auto issue = [&](int p) {    // plane p of this item (z = k0 - 1 + p)
-      const uint32_t sq = seq + p;
-      const int slot = sq % TT_S;
-      double* st = sm + slot * TSTAGE_DBL;
-      mbar_expect_tx(&bars[slot], TSTAGE_TX);
-      tma_load_4d(st, mIn, &bars[slot], x0 - 2, y0 - 1, k0 - 1 + p, 0);
-      tma_load_4d(st + TP_DBL, &mT, &bars[slot], x0 - 2, y0 - 1, k0 - 1 + p, 0);
-    };
-    auto wait = [&](int p) {
-      const uint32_t sq = seq + p;
-      mbar_wait(&bars[sq % TT_S], (sq / TT_S) & 1u);
-    };
-    // The ring holds planes pc..pc+TT_S-1 during step pc: the cell's own minus-z
-    // values (P at k-1 for its 4 slots, Tz at k-1) are carried in registers from the
-    // previous step, so only planes k and k+1 are read; plane pc's slot is refilled
-    // (with plane pc+TT_S) right after step pc, TT_S-2 steps before that plane is needed.
-    if (tid == 0)
-      for (int p = 0; p < min(TT_S, np); ++p) issue(p);
-    const int x = x0 + tx, y = y0 + ty;
-    const bool inxy = x < nx && y < ny;
-    const unsigned mx = inxy ? amask[x] : 0u, my = inxy ? amask[nx + y] : 0u;
-    unsigned mz_next = amask[nx + ny + k0];
-    const int ob = 4 * h * TB_Y * TB_X + loc;
-    double pzm[4], tzm;
-    // one thread waits on the ring's mbarriers and the CTA barrier publishes the data:
-    // planes 0..2 before the first step, plane pc+2 at the end of step pc
-    if (tid == 0) {
-      wait(0);
-      wait(1);
-      if (np > 2) wait(2);
-    }
-    __syncthreads();
-    {
-      const double* s0 = sm + (seq % TT_S) * TSTAGE_DBL;
-#pragma unroll
-      for (int q = 0; q < 4; ++q) pzm[q] = s0[ob + q * TB_Y * TB_X];
-      tzm = s0[TP_DBL + 2 * TQ_Y * TB_X + loc];
-    }
-    __syncthreads();  // plane 0 is consumed: refill its slot with plane TT_S
-    if (tid == 0) {
-      fence_proxy_async_smem();
-      if (TT_S < np) issue(TT_S);
-    }
-    for (int k = k0; k < k1; ++k) {
-      const int pc = k - k0 + 1;
-      const unsigned mz = mz_next;
-      if (k + 1 < k1) mz_next = amask[nx + ny + k + 1];
-      const double* __restrict__ sC = sm + ((seq + pc) % TT_S) * TSTAGE_DBL;
-      const double* __restrict__ sP = sm + ((seq + pc + 1) % TT_S) * TSTAGE_DBL;
-      const double* __restrict__ tC = sC + TP_DBL;
-      const double txp = tC[loc], txm = tC[loc - 1];
-      const double typ = tC[TQ_Y * TB_X + loc], tym = tC[TQ_Y * TB_X + loc - TB_X];
-      const double tzp = tC[2 * TQ_Y * TB_X + loc];
-      const double D = txp + txm + typ + tym + tzp + tzm;
-      // out-of-domain tile cells see zero-filled T (D = 0): give them wD = 0 so their
-      // (unused) values stay finite
-      const double wD = inxy ? omega * rcp_fast(D) : 0.0;
-      const unsigned zb = (mz >> h) & 1u;
-      const double wzm = mask_d(tzm, (mz >> (2 + h)) & 1u), wzp = mask_d(tzp, (mz >> (4 + h)) & 1u);
-      const double wxm0 = mask_d(txm, (mx >> 2) & 1u), wxm1 = mask_d(txm, (mx >> 3) & 1u);
-      const double wxp0 = mask_d(txp, (mx >> 4) & 1u), wxp1 = mask_d(txp, (mx >> 5) & 1u);
-      const double wym0 = mask_d(tym, (my >> 2) & 1u), wym1 = mask_d(tym, (my >> 3) & 1u);
-      const double wyp0 = mask_d(typ, (my >> 4) & 1u), wyp1 = mask_d(typ, (my >> 5) & 1u);
-      // No activity select is needed: an inactive (cell, slot) holds 0, its neighbours
-      // along the inactive axis are masked, and its neighbours along the other axes
-      // share that coordinate and so hold 0 too — hence ph = 0 exactly.
-      double ph[4], po[4];
-      double sum = 0.0;
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int px = q & 1, py = q >> 1;
-        const int o = ob + q * TB_Y * TB_X;
-        double acc = wzm * pzm[q];
-        acc += (py ? wym1 : wym0) * sC[o - TB_X];
-        acc += (px ? wxm1 : wxm0) * sC[o - 1];
-        acc += (px ? wxp1 : wxp0) * sC[o + 1];
-        acc += (py ? wyp1 : wyp0) * sC[o + TB_X];
-        acc += wzp * sP[o];
-        po[q] = sC[o];
-        ph[q] = om1 * po[q] + wD * acc;
-        sum += ph[q];
-      }
-      sum += __shfl_xor_sync(0xffffffffu, sum, 16);
-      const unsigned act = zb & (unsigned)inxy;
-      if (act) {
-        const double rs = rcp_fast(sum);
-        const int c = x + nx * (y + ny * k);
-        double* __restrict__ ob_out = Pout + (size_t)(4 * h) * N + c;
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int px = q & 1, py = q >> 1;
-          if ((mx >> px) & (my >> py) & 1u) {
-            const double pn = div_rn(ph[q], sum, rs);
-            ob_out[(size_t)q * N] = pn;
-            dloc = fmax(dloc, fabs(pn - po[q]));
-          }
-        }
-      }
-#pragma unroll
-      for (int q = 0; q < 4; ++q) pzm[q] = po[q];
-      tzm = tzp;
-      if (tid == 0 && pc + 2 < np) wait(pc + 2);
-      __syncthreads();  // plane pc+2 is published; plane pc (read last in this step) is free
-      if (tid == 0) {
-        fence_proxy_async_smem();
-        if (pc + TT_S < np) issue(pc + TT_S);  // TT_S-2 steps before its wait
-      }
-    }
-    seq += np;
-  }
-  sweep_fold(dloc, dslots, n);
-}
-
-// ---------------------------------------------------------------- G2'': one thread per cell
-// Same TMA ring and arithmetic as k_sweep_tma, but each thread owns a cell and all 8
-// slots: the per-cell work (five T reads, D, 1/D, the twelve masked weights, the row
-// sum, 1/sum, the store address) is done once instead of twice, which cuts the issued
-// instructions per cell ~2x (the two-thread kernel is issue-bound: profiles/r01_v9).
-// The TMA issue cursor runs ahead across items, so the next item's first planes load
-// during the current item's last steps (no ring drain at item boundaries).
+// One thread per cell owns all 8 slots: the per-cell work (five T reads, D, 1/D, the
+// twelve masked weights, the row sum, 1/sum, the store address) is done once (a
+// two-threads-per-cell variant was issue-bound: profiles/r01_v9).  The TMA issue cursor
+// runs ahead across items, so the next item's first planes load during the current
+// item's last steps (no ring drain at item boundaries).
 template <int TY>
 struct SweepBox {
   static constexpr int BX = TT_X + 4;           // 2-cell x halo (16-byte TMA start)
@@ -375,162 +219,6 @@ __device__ __forceinline__ double and_mask(double v, unsigned long long m) {
   return __longlong_as_double((long long)((unsigned long long)__double_as_longlong(v) & m));
 }
 
-template <int TY, int S>
-__global__ void __launch_bounds__(32 * TY) k_sweep_tma8(
-    const __grid_constant__ CUtensorMap mP0, const __grid_constant__ CUtensorMap mP1,
-    const __grid_constant__ CUtensorMap mT, double* __restrict__ P0, double* __restrict__ P1,
-    const uint8_t* __restrict__ amask, Grid3 g, SweepTiles tl, double omega, int n, double tol,
-    unsigned long long* __restrict__ dslots) {
-  using B = SweepBox<TY>;
-  if (sweep_skip(dslots, n, tol)) return;
-  extern __shared__ __align__(128) double sm[];
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + S * B::STAGE);
-  const CUtensorMap* mIn = (n & 1) ? &mP1 : &mP0;
-  double* __restrict__ Pout = (n & 1) ? P0 : P1;
-  const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;
-  const int nx = g.nx, ny = g.ny, nz = g.nz, nxy = g.nxy, N = g.nxy * g.nz;
-  if (tid == 0) {
-    if (smem_u32(sm) & 127u) __trap();  // TMA destinations must be 128-byte aligned
-    for (int t = 0; t < S; ++t) mbar_init(&bars[t], 1);
-    mbar_fence_init();
-  }
-  __syncthreads();
-  // issue cursor (thread 0): item ci, plane cp of its cnp planes, ring sequence iss
-  const int tiles = tl.ntx * tl.nty;
-  int ci = blockIdx.x, cp = 0, cnp = 0;
-  uint32_t iss = 0;
-  auto planes_of = [&](int it) {
-    const int k0 = (it / tiles) * tl.kz;
-    return min(k0 + tl.kz, nz) - k0 + 2;
-  };
-  if (ci < tl.items) cnp = planes_of(ci);
-  auto issue_one = [&]() {
-    if (ci >= tl.items) return;
-    const int xt = ci % tl.ntx, yt = (ci / tl.ntx) % tl.nty, zc = ci / tiles;
-    const int slot = iss % S;
-    double* st = sm + slot * B::STAGE;
-    const int z = zc * tl.kz - 1 + cp;
-    mbar_expect_tx(&bars[slot], B::TX);
-    tma_load_4d(st, mIn, &bars[slot], xt * TT_X - 2, yt * TY - 1, z, 0);
-    tma_load_4d(st + B::P_DBL, &mT, &bars[slot], xt * TT_X - 2, yt * TY - 1, z, 0);
-    ++iss;
-    if (++cp == cnp) {
-      ci += gridDim.x;
-      cp = 0;
-      cnp = ci < tl.items ? planes_of(ci) : 0;
-    }
-  };
-  if (tid == 0)
-    for (int p = 0; p < S; ++p) issue_one();
-  const double om1 = 1.0 - omega;
-  const int loc = (ty + 1) * B::BX + (tx + 2);  // same offset in the P and T boxes' row grid
-  uint32_t seq = 0;  // ring sequence number of the current item's plane 0
-  double dloc = 0.0;
-  for (int item = blockIdx.x; item < tl.items; item += gridDim.x) {
-    const int xt = item % tl.ntx, yt = (item / tl.ntx) % tl.nty, zc = item / tiles;
-    const int x0 = xt * TT_X, y0 = yt * TY, k0 = zc * tl.kz, k1 = min(k0 + tl.kz, nz);
-    const int np = k1 - k0 + 2;  // planes k0-1 .. k1 (>= 3)
-    auto wait = [&](int p) {
-      const uint32_t sq = seq + p;
-      mbar_wait(&bars[sq % S], (sq / S) & 1u);
-    };
-    const int x = x0 + tx, y = y0 + ty;
-    const bool inxy = x < nx && y < ny;
-    const unsigned mx = inxy ? amask[x] : 0u, my = inxy ? amask[nx + y] : 0u;
-    // loop-invariant x/y neighbour masks (all-ones or zero)
-    const unsigned long long mxm0 = 0ull - ((mx >> 2) & 1u), mxm1 = 0ull - ((mx >> 3) & 1u);
-    const unsigned long long mxp0 = 0ull - ((mx >> 4) & 1u), mxp1 = 0ull - ((mx >> 5) & 1u);
-    const unsigned long long mym0 = 0ull - ((my >> 2) & 1u), mym1 = 0ull - ((my >> 3) & 1u);
-    const unsigned long long myp0 = 0ull - ((my >> 4) & 1u), myp1 = 0ull - ((my >> 5) & 1u);
-    unsigned mz_next = amask[nx + ny + k0];
-    double pzm[8], tzm;
-    if (tid == 0) {
-      wait(0);
-      wait(1);
-      wait(2);
-    }
-    __syncthreads();
-    {
-      const double* s0 = sm + (seq % S) * B::STAGE;
-#pragma unroll
-      for (int s = 0; s < 8; ++s) pzm[s] = s0[loc + s * B::PPL];
-      tzm = s0[B::P_DBL + 2 * B::TPL + loc];
-    }
-    __syncthreads();  // plane 0 is consumed
-    if (tid == 0) {
-      fence_proxy_async_smem();
-      issue_one();
-    }
-    double* __restrict__ pout = Pout + (size_t)(x + nx * y) + (size_t)k0 * nxy;
-    for (int k = k0; k < k1; ++k) {
-      const int pc = k - k0 + 1;
-      const unsigned mz = mz_next;
-      if (k + 1 < k1) mz_next = amask[nx + ny + k + 1];
-      const double* __restrict__ sC = sm + ((seq + pc) % S) * B::STAGE;
-      const double* __restrict__ sP = sm + ((seq + pc + 1) % S) * B::STAGE;
-      const double* __restrict__ tC = sC + B::P_DBL;
-      const double txp = tC[loc], txm = tC[loc - 1];
-      const double typ = tC[B::TPL + loc], tym = tC[B::TPL + loc - B::BX];
-      const double tzp = tC[2 * B::TPL + loc];
-      const double D = txp + txm + typ + tym + tzp + tzm;
-      const double wD = inxy ? omega * rcp_fast(D) : 0.0;
-      const double wxm0 = and_mask(txm, mxm0), wxm1 = and_mask(txm, mxm1);
-      const double wxp0 = and_mask(txp, mxp0), wxp1 = and_mask(txp, mxp1);
-      const double wym0 = and_mask(tym, mym0), wym1 = and_mask(tym, mym1);
-      const double wyp0 = and_mask(typ, myp0), wyp1 = and_mask(typ, myp1);
-      const double wzm0 = mask_d(tzm, (mz >> 2) & 1u), wzm1 = mask_d(tzm, (mz >> 3) & 1u);
-      const double wzp0 = mask_d(tzp, (mz >> 4) & 1u), wzp1 = mask_d(tzp, (mz >> 5) & 1u);
-      double ph[8], po[8];
-#pragma unroll
-      for (int s = 0; s < 8; ++s) {
-        const int px = s & 1, py = (s >> 1) & 1, pz = s >> 2;
-        const int o = loc + s * B::PPL;
-        double acc = (pz ? wzm1 : wzm0) * pzm[s];
-        acc += (py ? wym1 : wym0) * sC[o - B::BX];
-        acc += (px ? wxm1 : wxm0) * sC[o - 1];
-        acc += (px ? wxp1 : wxp0) * sC[o + 1];
-        acc += (py ? wyp1 : wyp0) * sC[o + B::BX];
-        acc += (pz ? wzp1 : wzp0) * sP[o];
-        po[s] = sC[o];
-        ph[s] = om1 * po[s] + wD * acc;
-      }
-      // row sum in the two-thread kernel's order: (z-parity-0 half) + (z-parity-1 half)
-      double slo = 0.0, shi = 0.0;
-#pragma unroll
-      for (int s = 0; s < 4; ++s) {
-        slo += ph[s];
-        shi += ph[4 + s];
-      }
-      const double sum = slo + shi;
-      if (inxy) {
-        const double rs = rcp_fast(sum);
-#pragma unroll
-        for (int s = 0; s < 8; ++s) {
-          const int px = s & 1, py = (s >> 1) & 1, pz = s >> 2;
-          if ((mx >> px) & (my >> py) & (mz >> pz) & 1u) {
-            const double pn = div_rn(ph[s], sum, rs);
-            pout[(size_t)s * N] = pn;
-            const double d = fabs(pn - po[s]);
-            dloc = d > dloc ? d : dloc;
-          }
-        }
-      }
-#pragma unroll
-      for (int s = 0; s < 8; ++s) pzm[s] = po[s];
-      tzm = tzp;
-      pout += nxy;
-      if (tid == 0 && pc + 2 < np) wait(pc + 2);
-      __syncthreads();  // plane pc+2 is published; plane pc (and after the last step, np-1) is free
-      if (tid == 0) {
-        fence_proxy_async_smem();
-        issue_one();
-        if (pc == np - 2) issue_one();
-      }
-    }
-    seq += np;
-  }
-  sweep_fold(dloc, dslots, n);
-}
 
 // Grid-wide barrier for the persistent multi-sweep launch (all CTAs co-resident: the
 // launch is cooperative).  The fences order this CTA's generic-proxy stores before the
@@ -793,14 +481,10 @@ __global__ void __launch_bounds__(SWEEP_BLOCK) k_sweep_ell(
   sweep_fold(dloc, dslots, n);
 }
 
-using SweepKern = void (*)(const CUtensorMap, const CUtensorMap, const CUtensorMap, double*,
-                           double*, const uint8_t*, Grid3, SweepTiles, double, int, double,
-                           unsigned long long*);
 using SweepKernMulti = void (*)(const CUtensorMap, const CUtensorMap, const CUtensorMap, double*,
                                 double*, const uint8_t*, Grid3, SweepTiles, double, int, int,
                                 double, unsigned long long*, unsigned*);
 struct SweepLaunch {
-  SweepKern kern = nullptr;        // one sweep per launch
   SweepKernMulti multi = nullptr;  // a chunk of sweeps per (cooperative) launch
   int threads = 0, ty = 0, occ = 0;
   size_t smem = 0;
@@ -818,48 +502,16 @@ static cudaError_t sweep_setup_common(SweepLaunch* out, K kern, int threads, int
   out->smem = smem;
   return cudaSuccess;
 }
-static cudaError_t sweep_setup(SweepLaunch* out, SweepKern kern, int threads, int ty, size_t smem) {
-  out->kern = kern;
-  return sweep_setup_common(out, kern, threads, ty, smem);
-}
 static cudaError_t sweep_setup(SweepLaunch* out, SweepKernMulti kern, int threads, int ty,
                                size_t smem) {
   out->multi = kern;
   return sweep_setup_common(out, kern, threads, ty, smem);
 }
 
-// Kernel choice (A/B knobs, read once per process): MSB_SW_KERNEL=1 two threads per cell
-// (MSB_SW_STAGES=4|5|6), =2 one thread per cell with CTA barriers (MSB_SW_TY=4|8,
-// MSB_SW_STAGES=3|4), default: warp-specialised persistent multi-sweep
-// (MSB_SW_TY=4|8, MSB_SW_STAGES=3|4|5).
+// The sweep kernel: warp-specialised TMA ring, persistent over a chunk of sweeps
+// (4 consumer warps, 3 ring stages; DESIGN.md §4.1 lists the variants measured).
 static cudaError_t sweep_variant(SweepLaunch* out) {
-  const char* ek = getenv("MSB_SW_KERNEL");
-  const char* es = getenv("MSB_SW_STAGES");
-  const char* ey = getenv("MSB_SW_TY");
-  const int kind = ek ? atoi(ek) : 3;
-  if (kind == 1) {
-    const int S = es ? atoi(es) : TT_STAGES_DEFAULT;
-    if (S == 5) return sweep_setup(out, k_sweep_tma<5>, TSWEEP_THREADS, TT_Y, tsweep_smem(5));
-    if (S == 6) return sweep_setup(out, k_sweep_tma<6>, TSWEEP_THREADS, TT_Y, tsweep_smem(6));
-    return sweep_setup(out, k_sweep_tma<4>, TSWEEP_THREADS, TT_Y, tsweep_smem(4));
-  }
-  const int S = es ? atoi(es) : SW8_STAGES_DEFAULT;
-  const int TY = ey ? atoi(ey) : SW8_TY_DEFAULT;
-  if (kind == 2) {
-    if (TY == 8) {
-      if (S == 4) return sweep_setup(out, k_sweep_tma8<8, 4>, 256, 8, SweepBox<8>::smem(4));
-      return sweep_setup(out, k_sweep_tma8<8, 3>, 256, 8, SweepBox<8>::smem(3));
-    }
-    if (S == 3) return sweep_setup(out, k_sweep_tma8<4, 3>, 128, 4, SweepBox<4>::smem(3));
-    return sweep_setup(out, k_sweep_tma8<4, 4>, 128, 4, SweepBox<4>::smem(4));
-  }
-  if (TY == 8) {
-    if (S == 3) return sweep_setup(out, k_sweep_ws<8, 3>, 288, 8, SweepBox<8>::smem(3) + 64);
-    return sweep_setup(out, k_sweep_ws<8, 4>, 288, 8, SweepBox<8>::smem(4) + 64);
-  }
-  if (S == 3) return sweep_setup(out, k_sweep_ws<4, 3>, 160, 4, SweepBox<4>::smem(3) + 64);
-  if (S == 5) return sweep_setup(out, k_sweep_ws<4, 5>, 160, 4, SweepBox<4>::smem(5) + 64);
-  return sweep_setup(out, k_sweep_ws<4, 4>, 160, 4, SweepBox<4>::smem(4) + 64);
+  return sweep_setup(out, k_sweep_ws<4, 3>, 160, 4, SweepBox<4>::smem(3) + 64);
 }
 
 }  // namespace msb
@@ -916,17 +568,14 @@ extern "C" msb_status msb_smooth_basis(msb_ctx ctx, msb_level L, msb_op op, int3
   double* Pa = L->P[L->cur];
   double* Pb = L->P[L->cur ^ 1];
   // TMA path: tensor maps over both P buffers and the 3N transmissibility block.
-  // Variants (A/B knobs): MSB_SW_KERNEL=1 selects the two-thread-per-cell kernel
-  // (MSB_SW_STAGES=4|5|6); the default one-thread-per-cell kernel takes
-  // MSB_SW_TY=4|8 tile rows and MSB_SW_STAGES=3|4 ring stages.
   bool use_tma = false;
   CUtensorMap mP[2], mT;
   SweepTiles tl{};
   unsigned tgrid = 0;
   SweepLaunch sl{};
-  if (L->kind == 0 && (op->nx % 2) == 0 && !getenv("MSB_NO_TMA")) {
+  if (L->kind == 0 && (op->nx % 2) == 0) {
     static SweepLaunch cached{};
-    if (!cached.kern) MSB_CUDA_TRY(ctx, sweep_variant(&cached));
+    if (!cached.multi) MSB_CUDA_TRY(ctx, sweep_variant(&cached));
     sl = cached;
     const uint64_t dP[4] = {(uint64_t)op->nx, (uint64_t)op->ny, (uint64_t)op->nz, 8};
     const uint64_t dT[4] = {(uint64_t)op->nx, (uint64_t)op->ny, (uint64_t)op->nz, 3};
@@ -995,10 +644,7 @@ extern "C" msb_status msb_smooth_basis(msb_ctx ctx, msb_level L, msb_op op, int3
     } else {
       for (int t = 0; t < nl; ++t) {
         const int idx = issued + t;
-        if (use_tma)
-          sl.kern<<<tgrid, sl.threads, sl.smem, st>>>(mP[0], mP[1], mT, Pa, Pb, L->amask, g, tl,
-                                                      omega, idx, tol, dslots);
-        else if (L->kind == 0)
+        if (L->kind == 0)
           k_sweep_cart<<<grid, SWEEP_BLOCK, 0, st>>>(Pa, Pb, op->Tx, op->Ty, op->Tz, L->amask, g,
                                                      omega, idx, tol, dslots);
         else

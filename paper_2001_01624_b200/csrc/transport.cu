@@ -165,9 +165,122 @@ __global__ void k_upstream_mob(FluxView F, const double* __restrict__ p, const d
   }
 }
 
+// Σ φ_i and Σ max(q_i, 0): per-CTA partials in a fixed order, then one CTA sums them
+// in a fixed order (deterministic).
+__global__ void __launch_bounds__(256) k_pv_parts(const double* __restrict__ phi,
+                                                  const double* __restrict__ q, int64_t N,
+                                                  double* __restrict__ part) {
+  double a = 0.0, b = 0.0;
+  for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < N;
+       c += (int64_t)gridDim.x * blockDim.x) {
+    a += phi[c];
+    b += fmax(q[c], 0.0);
+  }
+  __shared__ double sa[8], sb[8];
+  for (int o = 16; o > 0; o >>= 1) {
+    a += __shfl_xor_sync(0xffffffffu, a, o);
+    b += __shfl_xor_sync(0xffffffffu, b, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    sa[threadIdx.x >> 5] = a;
+    sb[threadIdx.x >> 5] = b;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double ta = 0.0, tb = 0.0;
+    for (int w = 0; w < 8; ++w) {
+      ta += sa[w];
+      tb += sb[w];
+    }
+    part[2 * blockIdx.x] = ta;
+    part[2 * blockIdx.x + 1] = tb;
+  }
+}
+
+__global__ void k_pv_final(const double* __restrict__ part, int n, double vol, double pv,
+                           double* __restrict__ dt) {
+  if (threadIdx.x != 0) return;
+  double a = 0.0, b = 0.0;
+  for (int t = 0; t < n; ++t) {
+    a += part[2 * t];
+    b += part[2 * t + 1];
+  }
+  *dt = b > 0.0 ? pv * (a * vol) / b : 0.0;
+}
+
 }  // namespace msb
 
 using namespace msb;
+
+extern "C" msb_status msb_upstream_mobility(msb_ctx ctx, msb_op op, const double* p,
+                                            const double* S, double mu_w, double mu_o,
+                                            double* mob_out) {
+  if (!ctx || !op || !mob_out) return set_error(ctx, MSB_EINVAL, "msb_upstream_mobility: null");
+  if (!(mu_w > 0) || !(mu_o > 0)) return set_error(ctx, MSB_EINVAL, "msb_upstream_mobility: bad viscosity");
+  const int64_t N = op->N;
+  cudaStream_t st = ctx->stream;
+  // NULL p (no previous flux) and NULL S (dry reservoir) read as zero vectors
+  double* z = nullptr;
+  if (!p || !S) {
+    z = dalloc_n<double>(ctx, N);
+    if (!z) return set_error(ctx, MSB_ENOMEM, "mobility scratch");
+    MSB_CUDA_TRY(ctx, cudaMemsetAsync(z, 0, N * sizeof(double), st));
+  }
+  void *op_, *os_;
+  const double* dp = p ? (const double*)stage_in(ctx, p, N * sizeof(double), &op_) : z;
+  if (!p) op_ = nullptr;
+  const double* ds = S ? (const double*)stage_in(ctx, S, N * sizeof(double), &os_) : z;
+  if (!S) os_ = nullptr;
+  const int64_t nf = (int64_t)(op->nx - 1) * op->ny * op->nz +
+                     (int64_t)op->nx * (op->ny - 1) * op->nz + (int64_t)op->nx * op->ny * (op->nz - 1);
+  const bool dev = is_device_ptr(mob_out);
+  double* d = dev ? mob_out : dalloc_n<double>(ctx, nf + 1);
+  msb_status rc = MSB_OK;
+  if (!dp || !ds || !d) rc = set_error(ctx, MSB_ENOMEM, "mobility staging");
+  if (!rc) {
+    FluxView F{op->Tx, op->Ty, op->Tz, op->nx, op->ny, op->nz};
+    k_upstream_mob<<<grid_for(N, 256), 256, 0, st>>>(F, dp, ds, mu_w, mu_o, d);
+    count_launch();
+    if (cudaGetLastError() != cudaSuccess) rc = set_error(ctx, MSB_ECUDA, "k_upstream_mob launch");
+  }
+  if (!rc && !dev && copy_out(ctx, mob_out, d, nf * sizeof(double)) != cudaSuccess)
+    rc = set_error(ctx, MSB_ECUDA, "mobility copy-out");
+  cudaStreamSynchronize(st);
+  if (!dev) dfree(ctx, d);
+  dfree(ctx, z);
+  dfree(ctx, op_);
+  dfree(ctx, os_);
+  return rc;
+}
+
+extern "C" msb_status msb_transport_step_size(msb_ctx ctx, msb_op op, const double* phi,
+                                              double pv_per_step, double* dt_out) {
+  if (!ctx || !op || !phi || !dt_out || !(pv_per_step >= 0))
+    return set_error(ctx, MSB_EINVAL, "msb_transport_step_size: args");
+  const int64_t N = op->N;
+  cudaStream_t st = ctx->stream;
+  void* o = nullptr;
+  const double* dphi = (const double*)stage_in(ctx, phi, N * sizeof(double), &o);
+  const int nb = 2 * ctx->sm_count;
+  double* part = dalloc_n<double>(ctx, 2 * (size_t)nb + 1);
+  msb_status rc = MSB_OK;
+  if (!dphi || !part) rc = set_error(ctx, MSB_ENOMEM, "step-size scratch");
+  double h = 0.0;
+  if (!rc) {
+    k_pv_parts<<<nb, 256, 0, st>>>(dphi, op->q, N, part);
+    k_pv_final<<<1, 32, 0, st>>>(part, nb, op->dx * op->dy * op->dz, pv_per_step, part + 2 * nb);
+    count_launch();
+    count_launch();
+    if (cudaGetLastError() != cudaSuccess ||
+        cudaMemcpyAsync(&h, part + 2 * nb, 8, cudaMemcpyDeviceToHost, st) != cudaSuccess)
+      rc = set_error(ctx, MSB_ECUDA, "step-size reduction");
+  }
+  cudaStreamSynchronize(st);
+  dfree(ctx, part);
+  dfree(ctx, o);
+  if (!rc) *dt_out = h;
+  return rc;
+}
 
 extern "C" msb_status msb_transport_upwind(msb_ctx ctx, msb_op op, const double* p, double* S,
                                            const double* phi, double mu_w, double mu_o, double dt,
@@ -204,8 +317,7 @@ extern "C" msb_status msb_transport_upwind(msb_ctx ctx, msb_op op, const double*
   if (!tmp) return set_error(ctx, MSB_ENOMEM, "transport scratch");
   double* a = S;
   double* b = tmp;
-  static const bool legacy = getenv("MSB_TRANSPORT_LEGACY") != nullptr;
-  if (legacy || N > INT32_MAX / 2) {
+  if (N > INT32_MAX / 2) {  // the per-face kernel (64-bit indices) beyond int32 cell ids
     for (int t = 0; t < nsub; ++t) {
       k_transport_step<<<grid_for(N, 256), 256, 0, st>>>(F, p, op->q, phi, vol, mu_w, mu_o, h, a, b);
       MSB_LAUNCH_CHECK(ctx);

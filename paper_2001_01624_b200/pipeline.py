@@ -86,11 +86,6 @@ def run(ctx: Context, prob, sweeps=None, fixed_sweeps=None, fixed_iters=None, ma
     return dict(op=op, levels=levels, sweep_info=sweep_info, solver=solver, x=x, sol=sol)
 
 
-def initial_mobility(prob, mu_w=1.0, mu_o=5.0):
-    """Step-1 face mobility λ_t(S = 0) = 1/μ_o on every face (reading A17)."""
-    return np.full(prob.n_faces, (1.0 - 0.0) ** 2 / mu_o)
-
-
 def run_sequential(ctx: Context, prob, steps=100, k_adapt=5, mu_w=1.0, mu_o=5.0,
                    pv_per_step=0.005, init_sweeps=None, init_fixed=None, fixed_iters=None,
                    max_iter=None, keep_states=False):
@@ -102,14 +97,14 @@ def run_sequential(ctx: Context, prob, steps=100, k_adapt=5, mu_w=1.0, mu_o=5.0,
 
     dev = f"cuda:{ctx.device}"
     N = prob.N
-    q = prob.rhs()
-    vol = prob.dx * prob.dy * prob.dz
-    dt = pv_per_step * prob.phi * N * vol / float(q[q > 0].sum())
     phi = torch.full((N,), float(prob.phi), dtype=torch.float64, device=dev)
-    mob = torch.as_tensor(initial_mobility(prob, mu_w, mu_o), device=dev)
     # the initial basis is config 2's (λ = 1); a uniform λ scales A_T and leaves the
     # smoothing update unchanged, so smoothing before or after the first λ is equivalent
     op = build_operator(ctx, prob)
+    dt = op.step_size(phi, pv_per_step)
+    # step 1: S = 0 everywhere, λ_t(0) = 1/μ_o on every face (reading A17)
+    mob = op.upstream_mobility(None, None, mu_w, mu_o,
+                               torch.empty(prob.n_faces, dtype=torch.float64, device=dev))
     cart = Level.cartesian(ctx, op, prob.block)
     ms = prob.max_sweeps if init_sweeps is None else init_sweeps
     fx = prob.fixed_sweeps if init_fixed is None else init_fixed

@@ -22,3 +22,34 @@ def gpu_available():
         return torch.cuda.is_available()
     except Exception:
         return False
+
+
+# ---------------------------------------------------------------- parity log
+# Every GPU parity comparison records (case, k_gpu, k_oracle, err, floor, tol) so the
+# distances behind each green test are visible, not just pass/fail.  Written at the end of
+# the session to $PARITY_LOG (default gpurun_out/parity_r02.json when a GPU ran).
+PARITY_RECORDS = []
+
+
+def record_parity(case, **kw):
+    rec = {"case": case}
+    for k, v in kw.items():
+        try:
+            import numpy as np
+            if isinstance(v, (np.generic,)):
+                v = v.item()
+        except Exception:
+            pass
+        rec[k] = v
+    PARITY_RECORDS.append(rec)
+    return rec
+
+
+def pytest_sessionfinish(session, exitstatus):
+    if not PARITY_RECORDS:
+        return
+    import json
+    path = os.environ.get("PARITY_LOG", os.path.join(ROOT, "gpurun_out", "parity_r02.json"))
+    os.makedirs(os.path.dirname(path), exist_ok=True)
+    with open(path, "w") as f:
+        json.dump({"records": PARITY_RECORDS, "exitstatus": int(exitstatus)}, f, indent=1)
