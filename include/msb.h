@@ -178,6 +178,14 @@ msb_status msb_level_export(msb_ctx ctx, msb_level lev, int64_t* rowptr, int32_t
  * rows need not sum to one: the level's next msb_coarse_assemble accumulates every entry
  * of A_c (until a msb_smooth_basis call renormalises the rows again). */
 msb_status msb_level_import_values(msb_ctx ctx, msb_level lev, const double* vals);
+/* Parity dump of a Cartesian level's assembled A_c in its box-stencil storage, as COO in
+ * row-major order (every in-range slot (a, b), |b - a| <= 2 blocks per axis, zeros
+ * included): nnz_out host; rows, cols int32[nnz] and vals double[nnz] (host|dev, each may
+ * be NULL: call once with NULLs for nnz).  Available for every Cartesian level (the dense
+ * dump of msb_level_export only where the dense solver is used, M <= 4096).
+ * Errors: MSB_EINVAL for an explicit level or before msb_coarse_assemble. */
+msb_status msb_level_export_coarse(msb_ctx ctx, msb_level lev, int64_t* nnz_out, int32_t* rows,
+                                   int32_t* cols, double* vals);
 msb_status msb_level_destroy(msb_level lev);
 
 /* ---------------------------------------------------------------- basis smoothing (row a3)

@@ -59,11 +59,13 @@ def static_partition(prob, spec):
 
 
 def run(prob, sweeps=None, fixed_sweeps=None, fixed_iters=None, max_iter=None,
-        record_dynamic=False, x0=None, coarse="lu", assoc="right", levels_info=None):
-    """coarse / assoc: alternate exact coarse solver / A_c summation order (oracle.coarse,
-    floor measurement only).  levels_info: reuse the smoothed levels of an earlier run
-    (the alternates differ only after smoothing)."""
-    A_T, A, q, trans = _tpfa.build(prob)
+        record_dynamic=False, x0=None, coarse="lu", assoc="right", levels_info=None,
+        diag_order="assembly"):
+    """coarse / assoc / diag_order: alternate exact coarse solver / A_c summation order /
+    diagonal summation order of A (oracle.coarse, oracle.tpfa; floor measurement only).
+    levels_info: reuse the smoothed levels of an earlier run (the alternates differ only
+    after smoothing)."""
+    A_T, A, q, trans = _tpfa.build(prob, diag_order=diag_order)
     if levels_info is not None:
         return _solve(prob, A_T, A, q, trans, levels_info, fixed_iters, max_iter,
                       record_dynamic, x0, coarse, assoc)

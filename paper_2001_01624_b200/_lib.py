@@ -53,6 +53,7 @@ SIGNATURES = {
     "msb_level_info": (i32, [p, p, pi32, pi64, pi32, p]),
     "msb_level_export": (i32, [p, p, p, p, p, p]),
     "msb_level_import_values": (i32, [p, p, p]),
+    "msb_level_export_coarse": (i32, [p, p, pi64, p, p, p]),
     "msb_level_destroy": (i32, [p]),
     "msb_smooth_basis": (i32, [p, p, p, i32, f64, f64, pi32, pf64, p]),
     "msb_coarse_assemble": (i32, [p, p, p]),

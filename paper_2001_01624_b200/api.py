@@ -321,6 +321,21 @@ class Level:
                        "msb_level_export")
         return rowptr, cols, vals, Ac
 
+    def export_coarse(self):
+        """A_c of a Cartesian level as COO (rows, cols, vals) from its box-stencil storage."""
+        nnz = C.c_int64()
+        self.ctx.check(self.ctx.lib.msb_level_export_coarse(self.ctx.h, self.h, C.byref(nnz),
+                                                            None, None, None),
+                       "msb_level_export_coarse")
+        r = np.empty(nnz.value, dtype=np.int32)
+        c = np.empty(nnz.value, dtype=np.int32)
+        v = np.empty(nnz.value)
+        self.ctx.check(self.ctx.lib.msb_level_export_coarse(self.ctx.h, self.h, C.byref(nnz),
+                                                            _ptr(r, np.int32), _ptr(c, np.int32),
+                                                            _ptr(v)),
+                       "msb_level_export_coarse")
+        return r, c, v
+
     def import_values(self, vals):
         self.ctx.check(self.ctx.lib.msb_level_import_values(self.ctx.h, self.h, _ptr(vals)),
                        "msb_level_import_values")

@@ -12,6 +12,7 @@
 #include <cstdlib>
 
 #include <climits>
+#include <vector>
 
 #include "internal.cuh"
 #include "symv.cuh"
@@ -261,11 +262,97 @@ __global__ void __launch_bounds__(256) k_fx_sym_to_double(const unsigned long lo
 
 // FX: accumulate into the 128-bit fixed-point buffer (deterministic, see above) instead of
 // fp64 atomics; |T g_a g_b| <= max T because P entries lie in [0, 1]
-template <bool FX, bool SYM>
+constexpr int ELLW = 125, ELLC = 62;  // box-stencil slots per row, centre slot
+
+// ELL conversions, one warp per row a of the box stencil (Cartesian levels).  The
+// neighbour b of slot d is a + offset(d) when its block coordinates stay in range.
+__device__ __forceinline__ int ell_nb(int a, int d, int n0, int n1, int n2) {
+  const int ax = a % n0, ay = (a / n0) % n1, az = a / (n0 * n1);
+  const int bx = ax + d % 5 - 2, by = ay + (d / 5) % 5 - 2, bz = az + d / 25 - 2;
+  if (bx < 0 || bx >= n0 || by < 0 || by >= n1 || bz < 0 || bz >= n2) return -1;
+  return bx + n0 * (by + n1 * bz);
+}
+
+// SYM (partition-of-unity rows): off-diagonal (a, b) lives in the lower entry — row
+// max(a, b) at the slot of min(a, b) — and the diagonal is the centre slot minus the row's
+// exact off-diagonal total (as k_fx_sym_to_double).
+__global__ void __launch_bounds__(256) k_fx_ell_sym(const unsigned long long* __restrict__ acc,
+                                                    int M, int n0, int n1, int n2,
+                                                    const unsigned long long* __restrict__ tmax_bits,
+                                                    double* __restrict__ Aell) {
+  const int a = (int)((blockIdx.x * (unsigned)blockDim.x + threadIdx.x) >> 5);
+  const int lane = threadIdx.x & 31;
+  if (a >= M) return;  // warp-uniform
+  const int F = 90 - ilogb(__longlong_as_double((long long)*tmax_bits));
+  unsigned long long slo = 0, shi = 0;
+  for (int d = lane; d < ELLW; d += 32) {
+    double v = 0.0;
+    const int b = d == ELLC ? -1 : ell_nb(a, d, n0, n1, n2);
+    if (b >= 0) {
+      const size_t e = b < a ? (size_t)a * ELLW + d : (size_t)b * ELLW + (ELLW - 1 - d);
+      const unsigned long long lo = acc[2 * e], hi = acc[2 * e + 1];
+      v = fx_value(lo, hi, F);
+      add128(slo, shi, lo, hi);
+    }
+    if (d != ELLC) Aell[(size_t)a * ELLW + d] = v;
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long ylo = __shfl_xor_sync(0xffffffffu, slo, o);
+    const unsigned long long yhi = __shfl_xor_sync(0xffffffffu, shi, o);
+    add128(slo, shi, ylo, yhi);
+  }
+  if (lane == 0) {
+    const unsigned long long nlo = ~slo + 1ull, nhi = ~shi + (nlo == 0ull ? 1ull : 0ull);
+    unsigned long long dlo = acc[2 * ((size_t)a * ELLW + ELLC)],
+                       dhi = acc[2 * ((size_t)a * ELLW + ELLC) + 1];
+    add128(dlo, dhi, nlo, nhi);
+    Aell[(size_t)a * ELLW + ELLC] = fx_value(dlo, dhi, F);
+  }
+}
+
+// full accumulation (imported P): every entry (a, b) was summed at row a
+__global__ void k_fx_ell_full(const unsigned long long* __restrict__ acc, int M, int n0, int n1,
+                              int n2, const unsigned long long* __restrict__ tmax_bits,
+                              double* __restrict__ Aell) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (int64_t)M * ELLW) return;
+  const int a = (int)(e / ELLW), d = (int)(e - (int64_t)a * ELLW);
+  const int F = 90 - ilogb(__longlong_as_double((long long)*tmax_bits));
+  const bool ok = d == ELLC || ell_nb(a, d, n0, n1, n2) >= 0;
+  Aell[e] = ok ? fx_value(acc[2 * e], acc[2 * e + 1], F) : 0.0;
+}
+
+// dense row-major A_c (M x M, zero-filled beforehand) from the box stencil
+__global__ void k_ell_to_dense(const double* __restrict__ Aell, int M, int n0, int n1, int n2,
+                               double* __restrict__ Ac) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (int64_t)M * ELLW) return;
+  const int a = (int)(e / ELLW), d = (int)(e - (int64_t)a * ELLW);
+  const int b = d == ELLC ? a : ell_nb(a, d, n0, n1, n2);
+  if (b >= 0) Ac[(int64_t)a * M + b] = Aell[e];
+}
+
+// ELL (Cartesian levels): the accumulator is the 125-slot box stencil of each row,
+// entry (a, b) at acc[a * 125 + ell_slot(a, b)] (|b_x - a_x|, |b_y - a_y|, |b_z - a_z| <= 2:
+// open-box supports reach at most the second neighbour block, coarse.cu header); an entry
+// outside the box sets bad[0] (never expected).
+__device__ __forceinline__ int64_t ell_at(const msb_level_s& L, int a, int b, int* bad) {
+  const int n0 = L.nb[0], n1 = L.nb[1];
+  const int ax = a % n0, ay = (a / n0) % n1, az = a / (n0 * n1);
+  const int bx = b % n0, by = (b / n0) % n1, bz = b / (n0 * n1);
+  const int dx = bx - ax + 2, dy = by - ay + 2, dz = bz - az + 2;
+  if ((unsigned)dx > 4u || (unsigned)dy > 4u || (unsigned)dz > 4u) {
+    atomicOr(bad, 1);
+    return (int64_t)a * ELLW + ELLC;
+  }
+  return (int64_t)a * ELLW + dx + 5 * dy + 25 * dz;
+}
+
+template <bool FX, bool SYM, bool ELL = false>
 __global__ void k_rap(const msb_level_s L, const double* __restrict__ P, const double* __restrict__ Tx,
                       const double* __restrict__ Ty, const double* __restrict__ Tz,
                       double* __restrict__ Ac, unsigned long long* __restrict__ acc,
-                      const unsigned long long* __restrict__ tmax_bits) {
+                      const unsigned long long* __restrict__ tmax_bits, int* bad = nullptr) {
   const int F = FX ? 90 - ilogb(__longlong_as_double((long long)*tmax_bits)) : 0;
   int64_t N = L.N;
   int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -316,9 +403,12 @@ __global__ void k_rap(const msb_level_s L, const double* __restrict__ P, const d
         if (FX && SYM) {
           // symmetric and row-sum-free: one add per unordered pair into its lower entry;
           // the diagonal is formed from the row in k_fx_sym_to_double
-          if (gc[a] > gc[b]) fx_add(acc + 2 * ((int64_t)gc[a] * M + gc[b]), ta * gv[b], F);
+          if (gc[a] > gc[b])
+            fx_add(acc + 2 * (ELL ? ell_at(L, gc[a], gc[b], bad) : (int64_t)gc[a] * M + gc[b]),
+                   ta * gv[b], F);
         } else if (FX) {
-          fx_add(acc + 2 * ((int64_t)gc[a] * M + gc[b]), ta * gv[b], F);
+          fx_add(acc + 2 * (ELL ? ell_at(L, gc[a], gc[b], bad) : (int64_t)gc[a] * M + gc[b]),
+                 ta * gv[b], F);
         } else {
           atomicAdd(Ac + (int64_t)gc[a] * M + gc[b], ta * gv[b]);
         }
@@ -341,12 +431,17 @@ __global__ void k_rap(const msb_level_s L, const double* __restrict__ P, const d
           const unsigned long long s2 = dlo + lo;
           dhi += hi + (s2 < dlo ? 1ull : 0ull);
           dlo = s2;
-          if (cc[a] > cc[b]) fx_add_raw(acc + 2 * ((int64_t)cc[a] * M + cc[b]), lo, hi);
+          if (cc[a] > cc[b])
+            fx_add_raw(acc + 2 * (ELL ? ell_at(L, cc[a], cc[b], bad) : (int64_t)cc[a] * M + cc[b]),
+                       lo, hi);
         }
-        fx_add_raw(acc + 2 * ((int64_t)cc[a] * M + cc[a]), dlo, dhi);
+        fx_add_raw(acc + 2 * (ELL ? (int64_t)cc[a] * ELLW + ELLC : (int64_t)cc[a] * M + cc[a]), dlo,
+                   dhi);
       } else {
         for (int b = 0; b < nc; ++b) {
-          if (FX) fx_add(acc + 2 * ((int64_t)cc[a] * M + cc[b]), d0 * cv[a] * cv[b], F);
+          if (FX)
+            fx_add(acc + 2 * (ELL ? ell_at(L, cc[a], cc[b], bad) : (int64_t)cc[a] * M + cc[b]),
+                   d0 * cv[a] * cv[b], F);
           else atomicAdd(Ac + (int64_t)cc[a] * M + cc[b], d0 * cv[a] * cv[b]);
         }
       }
@@ -392,6 +487,45 @@ __global__ void __launch_bounds__(16 * ST) k_symv_reduce(const double* __restric
   symv_reduce_body<false>(part, M, ntb, xc, blockIdx.x, skip);
 }
 
+// batched form (several packed matrices, vector rows through an optional index map):
+// one CTA per tile descriptor, one CTA per output-block descriptor
+__global__ void __launch_bounds__(SYMV_T) k_symv_tiles_b(const SymvTile* __restrict__ td,
+                                                         const double* __restrict__ Xp,
+                                                         const double* __restrict__ vec,
+                                                         const int32_t* __restrict__ map,
+                                                         double* __restrict__ part) {
+  const SymvTile d = td[blockIdx.x];
+  symv_tile_body<false>(Xp + d.tile_base * ST * ST, d.M, vec, part + d.tile_base * 2 * ST, d.t,
+                        map, d.roff);
+}
+
+__global__ void __launch_bounds__(16 * ST) k_symv_reduce_b(const SymvRow* __restrict__ rd,
+                                                          const double* __restrict__ part,
+                                                          double* __restrict__ out,
+                                                          const int32_t* __restrict__ omap,
+                                                          const int* done) {
+  const bool skip = done && *(volatile const int*)done;
+  const SymvRow d = rd[blockIdx.x];
+  symv_reduce_body<false>(part + d.tile_base * 2 * ST, d.M, d.ntb, out, d.b, skip, omap, d.roff);
+}
+
+void symv_batched(msb_ctx ctx, const SymvTile* td, int ntile, const SymvRow* rd, int nrow,
+                  const double* Xp, const double* vec, const int32_t* map, double* part,
+                  double* out, const int32_t* omap, const int* done) {
+  k_symv_tiles_b<<<ntile, SYMV_T, 0, ctx->stream>>>(td, Xp, vec, map, part);
+  k_symv_reduce_b<<<nrow, 16 * ST, 0, ctx->stream>>>(rd, part, out, omap, done);
+  count_launch();
+  count_launch();
+}
+
+void coarse_solve(msb_ctx ctx, const Coarse& co, const double* rc, double* xc, const int* done) {
+  if (co.kind == 1) {
+    coarse_schur_solve(ctx, co, rc, xc, done);
+    return;
+  }
+  coarse_solve_dense(ctx, co, rc, xc, done);
+}
+
 msb_status coarse_pack_symmetric(msb_ctx ctx, Coarse& co) {
   const int M = co.M;
   const int ntb = (M + ST - 1) / ST;
@@ -418,20 +552,110 @@ void coarse_solve_dense(msb_ctx ctx, const Coarse& co, const double* rc, double*
   count_launch();
 }
 
+// Cartesian levels: exact 128-bit fixed-point accumulation into the box stencil (16 B x 125
+// per row: 40 MB at M = 20,000), converted to co.Aell; then the dense explicit inverse for
+// M <= SCHUR_MIN_M, else the Schur-complement solver (coarse_schur.cu).
+constexpr int SCHUR_MIN_M = 4096;
+
+static msb_status ensure_dense(msb_ctx ctx, Coarse& co, int M) {
+  if (co.cap >= M) return MSB_OK;
+  dfree(ctx, co.Ac);
+  dfree(ctx, co.L);
+  dfree(ctx, co.Ainv);
+  co.Ac = co.L = co.Ainv = nullptr;
+  co.cap = 0;
+  MSB_ALLOC(ctx, co.Ac, double, (int64_t)M * M);
+  MSB_ALLOC(ctx, co.L, double, (int64_t)M * M);
+  MSB_ALLOC(ctx, co.Ainv, double, (int64_t)M * M);
+  co.cap = M;
+  return MSB_OK;
+}
+
+static msb_status coarse_assemble_cart(msb_ctx ctx, msb_level L, msb_op op) {
+  const int M = L->M;
+  Coarse& co = L->co;
+  cudaStream_t st = ctx->stream;
+  co.M = M;
+  co.ready = false;
+  for (int a = 0; a < 3; ++a) co.nb[a] = L->nb[a];
+  const size_t n = (size_t)M * ELLW;
+  if (co.acc_cap < n) {
+    dfree(ctx, co.acc);
+    co.acc = nullptr;
+    co.acc_cap = 0;
+    MSB_ALLOC(ctx, co.acc, unsigned long long, 2 * n + 2);
+    co.acc_cap = n;
+  }
+  if (co.ell_cap < M) {
+    dfree(ctx, co.Aell);
+    co.Aell = nullptr;
+    co.ell_cap = 0;
+    MSB_ALLOC(ctx, co.Aell, double, n);
+    co.ell_cap = M;
+  }
+  unsigned long long* tmax = co.acc + 2 * n;
+  int* bad = reinterpret_cast<int*>(co.acc + 2 * n + 1);
+  MSB_CUDA_TRY(ctx, cudaMemsetAsync(co.acc, 0, (2 * n + 2) * sizeof(unsigned long long), st));
+  k_absmax_t<<<std::min<int64_t>(grid_for(3 * op->N, 256), 4 * ctx->sm_count), 256, 0, st>>>(
+      op->Tx, 3 * op->N, tmax);
+  MSB_LAUNCH_CHECK(ctx);
+  if (L->unity)
+    k_rap<true, true, true><<<grid_for(L->N, 128), 128, 0, st>>>(*L, L->P[L->cur], op->Tx, op->Ty,
+                                                                op->Tz, nullptr, co.acc, tmax, bad);
+  else
+    k_rap<true, false, true><<<grid_for(L->N, 128), 128, 0, st>>>(*L, L->P[L->cur], op->Tx, op->Ty,
+                                                                 op->Tz, nullptr, co.acc, tmax, bad);
+  MSB_LAUNCH_CHECK(ctx);
+  if (L->unity)
+    k_fx_ell_sym<<<grid_for((int64_t)M * 32, 256), 256, 0, st>>>(co.acc, M, L->nb[0], L->nb[1],
+                                                                 L->nb[2], tmax, co.Aell);
+  else
+    k_fx_ell_full<<<grid_for((int64_t)n, 256), 256, 0, st>>>(co.acc, M, L->nb[0], L->nb[1],
+                                                             L->nb[2], tmax, co.Aell);
+  MSB_LAUNCH_CHECK(ctx);
+  int hbad = 0;
+  MSB_CUDA_TRY(ctx, cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, st));
+  MSB_CUDA_TRY(ctx, cudaStreamSynchronize(st));
+  if (hbad)
+    return set_error(ctx, MSB_EINVAL, "coarse coupling beyond the second neighbour block");
+  if (M > SCHUR_MIN_M) {
+    coarse_schur_free(ctx, co);
+    msb_status rc = coarse_schur_setup(ctx, co, *L);
+    if (rc == MSB_OK) {
+      co.kind = 1;
+      co.ready = true;
+      return MSB_OK;
+    }
+    if (rc != MSB_EINVAL) return rc;  // EINVAL: no useful split of this coarse grid
+    ctx->err[0] = 0;
+  }
+  co.kind = 0;
+  msb_status rc = ensure_dense(ctx, co, M);
+  if (rc) return rc;
+  MSB_CUDA_TRY(ctx, cudaMemsetAsync(co.Ac, 0, (size_t)M * M * sizeof(double), st));
+  k_ell_to_dense<<<grid_for((int64_t)n, 256), 256, 0, st>>>(co.Aell, M, L->nb[0], L->nb[1],
+                                                           L->nb[2], co.Ac);
+  MSB_LAUNCH_CHECK(ctx);
+  return coarse_factor_dense(ctx, co);
+}
+
+msb_status coarse_assemble(msb_ctx ctx, msb_level L, msb_op op) {
+  if (L->kind == 0) return coarse_assemble_cart(ctx, L, op);
+  return coarse_assemble_dense(ctx, L, op);
+}
+
 msb_status coarse_assemble_dense(msb_ctx ctx, msb_level L, msb_op op) {
   int M = L->M;
   Coarse& co = L->co;
   if (co.cap < M) {
     coarse_free(ctx, co);
-    int cap = M;
-    MSB_ALLOC(ctx, co.Ac, double, (int64_t)cap * cap);
-    MSB_ALLOC(ctx, co.L, double, (int64_t)cap * cap);
-    MSB_ALLOC(ctx, co.Ainv, double, (int64_t)cap * cap);
-    co.cap = cap;
+    msb_status rc = ensure_dense(ctx, co, M);
+    if (rc) return rc;
   }
   co.M = M;
-  // deterministic exact accumulation (128-bit fixed point) whenever its 16 B per entry fit
-  // comfortably (M <= 8192: 1 GiB); config 5 (M = 20,000) keeps fp64 atomics
+  co.kind = 0;
+  // explicit levels: deterministic exact accumulation (128-bit fixed point) whenever its
+  // 16 B per entry fit comfortably (M <= 8192: 1 GiB); beyond, fp64 atomics
   cudaStream_t st = ctx->stream;
   // constant basis (W = 1, every P entry exactly 1): only the faces between blocks; an
   // imported W = 1 level (rows no longer known to sum to one) takes the general path
@@ -480,6 +704,11 @@ msb_status coarse_assemble_dense(msb_ctx ctx, msb_level L, msb_op op) {
 }
 
 void coarse_free(msb_ctx ctx, Coarse& co) {
+  coarse_schur_free(ctx, co);
+  dfree(ctx, co.Aell);
+  co.Aell = nullptr;
+  co.ell_cap = 0;
+  co.kind = 0;
   dfree(ctx, co.Ac);
   dfree(ctx, co.Ainv);
   dfree(ctx, co.L);
@@ -504,7 +733,74 @@ using namespace msb;
 extern "C" msb_status msb_coarse_assemble(msb_ctx ctx, msb_level L, msb_op op) {
   if (!ctx || !L || !op) return set_error(ctx, MSB_EINVAL, "msb_coarse_assemble: null");
   if (L->N != op->N) return set_error(ctx, MSB_EDIM, "level/operator size mismatch");
-  if ((int64_t)L->M * L->M > (int64_t)1 << 31)
+  if (L->kind != 0 && (int64_t)L->M * L->M > (int64_t)1 << 31)
     return set_error(ctx, MSB_EINVAL, "dense coarse operator too large (M=%d)", L->M);
-  return coarse_assemble_dense(ctx, L, op);
+  return coarse_assemble(ctx, L, op);
+}
+
+// COO dump of a Cartesian level's assembled A_c (every in-range box-stencil slot, zeros
+// included): nnz_out host; rows/cols int32, vals double (host|dev, each may be NULL).
+__global__ void k_ell_coo(const double* __restrict__ Aell, int M, int n0, int n1, int n2,
+                          const int64_t* __restrict__ pos, int32_t* __restrict__ r,
+                          int32_t* __restrict__ c, double* __restrict__ v) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (int64_t)M * ELLW) return;
+  const int a = (int)(e / ELLW), d = (int)(e - (int64_t)a * ELLW);
+  const int b = d == ELLC ? a : ell_nb(a, d, n0, n1, n2);
+  if (b < 0) return;
+  const int64_t k = pos[e];
+  r[k] = a;
+  c[k] = b;
+  v[k] = Aell[e];
+}
+
+__global__ void k_ell_valid(int M, int n0, int n1, int n2, int64_t* __restrict__ flag) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (int64_t)M * ELLW) return;
+  const int a = (int)(e / ELLW), d = (int)(e - (int64_t)a * ELLW);
+  flag[e] = (d == ELLC || ell_nb(a, d, n0, n1, n2) >= 0) ? 1 : 0;
+}
+
+extern "C" msb_status msb_level_export_coarse(msb_ctx ctx, msb_level L, int64_t* nnz_out,
+                                              int32_t* rows, int32_t* cols, double* vals) {
+  if (!ctx || !L || !nnz_out) return set_error(ctx, MSB_EINVAL, "msb_level_export_coarse: null");
+  const Coarse& co = L->co;
+  if (L->kind != 0 || !co.Aell || !co.ready)
+    return set_error(ctx, MSB_EINVAL, "no assembled Cartesian coarse operator");
+  const int M = L->M;
+  const int64_t n = (int64_t)M * ELLW;
+  cudaStream_t st = ctx->stream;
+  std::vector<int64_t> flag(n);
+  int64_t* dflag = dalloc_n<int64_t>(ctx, n);
+  if (!dflag) return set_error(ctx, MSB_ENOMEM, "export scratch");
+  k_ell_valid<<<grid_for(n, 256), 256, 0, st>>>(M, co.nb[0], co.nb[1], co.nb[2], dflag);
+  count_launch();
+  MSB_CUDA_TRY(ctx, cudaMemcpyAsync(flag.data(), dflag, n * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  MSB_CUDA_TRY(ctx, cudaStreamSynchronize(st));
+  int64_t nnz = 0;
+  for (int64_t e = 0; e < n; ++e) {  // exclusive positions (row-major, slot order)
+    const int64_t f = flag[e];
+    flag[e] = nnz;
+    nnz += f;
+  }
+  *nnz_out = nnz;
+  if (rows || cols || vals) {
+    MSB_CUDA_TRY(ctx, cudaMemcpyAsync(dflag, flag.data(), n * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+    int32_t* dr = dalloc_n<int32_t>(ctx, nnz);
+    int32_t* dc = dalloc_n<int32_t>(ctx, nnz);
+    double* dv = dalloc_n<double>(ctx, nnz);
+    if (!dr || !dc || !dv) return set_error(ctx, MSB_ENOMEM, "export scratch");
+    k_ell_coo<<<grid_for(n, 256), 256, 0, st>>>(co.Aell, M, co.nb[0], co.nb[1], co.nb[2], dflag, dr,
+                                                dc, dv);
+    count_launch();
+    if (rows) MSB_CUDA_TRY(ctx, copy_out(ctx, rows, dr, nnz * sizeof(int32_t)));
+    if (cols) MSB_CUDA_TRY(ctx, copy_out(ctx, cols, dc, nnz * sizeof(int32_t)));
+    if (vals) MSB_CUDA_TRY(ctx, copy_out(ctx, vals, dv, nnz * sizeof(double)));
+    MSB_CUDA_TRY(ctx, cudaStreamSynchronize(st));
+    dfree(ctx, dr);
+    dfree(ctx, dc);
+    dfree(ctx, dv);
+  }
+  dfree(ctx, dflag);
+  return MSB_OK;
 }

@@ -15,236 +15,183 @@
 //   A_c^{-1} = W^T W                             (GEMM over the nonzero K range, lower
 //                                                 tiles, then mirrored)
 //
-// so all O(M^3) work is in plain GEMM / SYRK products and the leaves (n <= 64) are
-// one-CTA kernels.  The products go to cuBLAS (DGEMM/DSYRK: 33-36 TFLOP/s fp64 on B200
-// at these sizes, scripts/probes/dgemm_probe.py) — plain library GEMMs — resolved at run
-// time with dlopen so the library has no link dependency; without it (or with
-// MSB_OWN_DGEMM=1) they run on k_dgemm below, a register-blocked fp64 GEMM (128x128
-// tiles, 8x8 per thread, double-buffered shared memory; lower-tile and triangular-K
-// variants for the symmetric products).  Either way every step runs on the GPU.
-// Flops: M^3/3 (chol) + M^3/3 (inverse of L) + M^3/3 (W^T W, triangular K range on
-// k_dgemm; the DSYRK form does not skip W's zero upper triangle: M^3) ~ M^3 .. 5M^3/3.
+// so all O(M^3) work is in plain GEMM / SYRK / TRMM products on the library's own fp64
+// tensor-core GEMM (k_dgemm below, DMMA) and the leaves (n <= 64) are one-CTA kernels.
+// Flops: M^3/3 (chol) + M^3/3 (inverse of L) + M^3/3 (W^T W, triangular K range) ~ M^3.
 // Pivot test: d_jj <= 1e-14 max|A_c| -> MSB_ESINGULAR.
-#include <dlfcn.h>
-
 #include <algorithm>
 #include <cstdlib>
-
-#include <cublas_v2.h>
 
 #include "internal.cuh"
 
 namespace msb {
 
-constexpr int GB = 128;   // GEMM tile (rows and columns)
-constexpr int GK = 16;    // GEMM k step
-constexpr int GPAD = 4;   // smem row padding (doubles)
 constexpr int LEAF = 64;  // recursion leaf
 
-// C (m x n, ldc) = alpha * op(A) op(B) + beta * C,
-//   op(A)(i,t) = TA ? A[t*lda + i] : A[i*lda + t],   op(B)(t,j) = TB ? B[j*ldb + t] : B[t*ldb + j].
-// lower: skip tiles strictly above the diagonal (row tile < col tile).
-// tri_k: op(A)(i,t) = 0 for t < i and op(B)(t,j) = 0 for t < j (A = B = W^T W case):
-//        the K loop of tile (bi, bj) starts at max(bi, bj) * GB.
+// ---------------------------------------------------------------- fp64 tensor-core GEMM
+// C (m x n, ldc) = alpha * op(A) op(B) + beta * C, row-major,
+//   op(A)(i,t) = TA ? A[t*lda + i] : A[i*lda + t],   op(B)(t,j) = TB ? B[j*ldb + t] : B[t*ldb + j],
+// on the fp64 tensor cores (DMMA, mma.sync m8n8k4 f64: the only fp64 MMA of sm_100a —
+// tcgen05 has no f64 kind).  128 x 128 output tile per CTA, 8 warps as 2 (m) x 4 (n), each
+// 64 x 32 = 8 x 4 fragments of 8 x 8; K in steps of 16 through a 3-stage cp.async ring
+// (8-byte copies: leading dimensions may be odd; out-of-range elements zero-filled).
+//   lower: skip tiles strictly above the diagonal (row tile < col tile): SYRK.
+//   kmode 1: op(A)(i,t) = 0 for t < i (A^T of a lower-triangular A): TRMM, K from i0;
+//   kmode 2: additionally op(B)(t,j) = 0 for t < j (W^T W): K from max(i0, j0).
+// fp64 FMA throughout (DMMA rounds each product-sum exactly like an fp64 FMA chain, in a
+// fixed order per output element), so results are deterministic run to run.
+constexpr int DG_T = 128, DG_K = 16, DG_S = 3;
+constexpr int DG_PAD = 4;
+constexpr int DG_A_MK = DG_T * (DG_K + DG_PAD);  // [m][k] layout (TA = false)
+constexpr int DG_A_KM = DG_K * (DG_T + DG_PAD);  // [k][m] layout (TA = true)
+constexpr int DG_STAGE = (DG_A_MK > DG_A_KM ? DG_A_MK : DG_A_KM);
+constexpr size_t DG_SMEM = (size_t)2 * DG_S * DG_STAGE * sizeof(double);
+
+__device__ __forceinline__ void cp_async8(double* dst, const double* src, bool ok) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  const int sz = ok ? 8 : 0;
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(d), "l"(src), "r"(sz) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+__device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
+}
+
 template <bool TA, bool TB>
 __global__ void __launch_bounds__(256) k_dgemm(int m, int n, int K, double alpha,
                                                const double* __restrict__ A, int64_t lda,
                                                const double* __restrict__ B, int64_t ldb,
                                                double beta, double* __restrict__ C, int64_t ldc,
-                                               int lower, int tri_k) {
+                                               int lower, int kmode) {
   const int bi = blockIdx.y, bj = blockIdx.x;
   if (lower && bi < bj) return;
-  extern __shared__ double gsm[];
-  double* As = gsm;                           // [2][GK][GB + GPAD]
-  double* Bs = gsm + 2 * GK * (GB + GPAD);    // [2][GK][GB + GPAD]
-  const int tid = threadIdx.x;
-  const int tx = tid & 15, ty = tid >> 4;
-  const int i0 = bi * GB, j0 = bj * GB;
-  int kbeg = tri_k ? max(i0, j0) : 0;
+  extern __shared__ double dsm[];
+  double* As = dsm;                       // [DG_S][DG_STAGE]
+  double* Bs = dsm + DG_S * DG_STAGE;     // [DG_S][DG_STAGE]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp >> 2, wn = warp & 3;  // warp tile rows wm*64, cols wn*32
+  const int i0 = bi * DG_T, j0 = bj * DG_T;
+  int kbeg = kmode == 2 ? max(i0, j0) : (kmode == 1 ? i0 : 0);
   kbeg = min(kbeg, K);
-  const int nk = (K - kbeg + GK - 1) / GK;
-  double acc[8][8];
+  const int nk = (K - kbeg + DG_K - 1) / DG_K;
+  // stage loader: 2048 elements of each operand, 8 per thread
+  auto load = [&](int s, int kk) {
+    double* as = As + s * DG_STAGE;
+    double* bs = Bs + s * DG_STAGE;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const int idx = tid + 256 * e;
+      if (TA) {  // memory rows t, contiguous i: smem [k][m]
+        const int t = idx >> 7, i = idx & 127;
+        const int gi = i0 + i, gt = kk + t;
+        const bool ok = gi < m && gt < K;
+        cp_async8(as + t * (DG_T + DG_PAD) + i, ok ? A + (int64_t)gt * lda + gi : A, ok);
+      } else {   // memory rows i, contiguous t: smem [m][k]
+        const int i = idx >> 4, t = idx & 15;
+        const int gi = i0 + i, gt = kk + t;
+        const bool ok = gi < m && gt < K;
+        cp_async8(as + i * (DG_K + DG_PAD) + t, ok ? A + (int64_t)gi * lda + gt : A, ok);
+      }
+      if (TB) {  // memory rows j, contiguous t: smem [n][k]
+        const int j = idx >> 4, t = idx & 15;
+        const int gj = j0 + j, gt = kk + t;
+        const bool ok = gj < n && gt < K;
+        cp_async8(bs + j * (DG_K + DG_PAD) + t, ok ? B + (int64_t)gj * ldb + gt : B, ok);
+      } else {   // memory rows t, contiguous j: smem [k][n]
+        const int t = idx >> 7, j = idx & 127;
+        const int gj = j0 + j, gt = kk + t;
+        const bool ok = gj < n && gt < K;
+        cp_async8(bs + t * (DG_T + DG_PAD) + j, ok ? B + (int64_t)gt * ldb + gj : B, ok);
+      }
+    }
+  };
+  double acc[8][4][2];
 #pragma unroll
   for (int u = 0; u < 8; ++u)
 #pragma unroll
-    for (int v = 0; v < 8; ++v) acc[u][v] = 0.0;
-  double ra[8], rb[8];
-  // global -> register tile loader: 2048 elements of each operand per k step, 8/thread
-  auto load = [&](int kk) {
+    for (int v = 0; v < 4; ++v) acc[u][v][0] = acc[u][v][1] = 0.0;
 #pragma unroll
-    for (int e = 0; e < 8; ++e) {
-      const int idx = tid + 256 * e;
-      int i, t;
-      if (TA) { t = idx >> 7; i = idx & 127; } else { i = idx >> 4; t = idx & 15; }
-      const int gi = i0 + i, gt = kk + t;
-      ra[e] = (gi < m && gt < K) ? (TA ? A[(int64_t)gt * lda + gi] : A[(int64_t)gi * lda + gt]) : 0.0;
-      int j, tb;
-      if (TB) { j = idx >> 4; tb = idx & 15; } else { tb = idx >> 7; j = idx & 127; }
-      const int gj = j0 + j, gtb = kk + tb;
-      rb[e] = (gj < n && gtb < K) ? (TB ? B[(int64_t)gj * ldb + gtb] : B[(int64_t)gtb * ldb + gj]) : 0.0;
-    }
-  };
-  auto store = [&](int buf) {
-    double* as = As + buf * GK * (GB + GPAD);
-    double* bs = Bs + buf * GK * (GB + GPAD);
-#pragma unroll
-    for (int e = 0; e < 8; ++e) {
-      const int idx = tid + 256 * e;
-      int i, t;
-      if (TA) { t = idx >> 7; i = idx & 127; } else { i = idx >> 4; t = idx & 15; }
-      as[t * (GB + GPAD) + i] = ra[e];
-      int j, tb;
-      if (TB) { j = idx >> 4; tb = idx & 15; } else { tb = idx >> 7; j = idx & 127; }
-      bs[tb * (GB + GPAD) + j] = rb[e];
-    }
-  };
-  if (nk > 0) {
-    load(kbeg);
-    store(0);
-    __syncthreads();
+  for (int s = 0; s < DG_S - 1; ++s) {
+    if (s < nk) load(s, kbeg + s * DG_K);
+    cp_async_commit();
   }
-  for (int s = 0; s < nk; ++s) {
-    const int buf = s & 1;
-    if (s + 1 < nk) load(kbeg + (s + 1) * GK);
-    const double* as = As + buf * GK * (GB + GPAD);
-    const double* bs = Bs + buf * GK * (GB + GPAD);
+  const int fr = lane >> 2, fc = lane & 3;  // fragment row / k index of this lane
+  for (int st = 0; st < nk; ++st) {
+    cp_async_wait<DG_S - 2>();
+    __syncthreads();
+    {  // prefetch stage st + DG_S - 1 into the slot consumed at st - 1
+      const int nx = st + DG_S - 1;
+      if (nx < nk) load(nx % DG_S, kbeg + nx * DG_K);
+      cp_async_commit();
+    }
+    const double* as = As + (st % DG_S) * DG_STAGE;
+    const double* bs = Bs + (st % DG_S) * DG_STAGE;
 #pragma unroll
-    for (int t = 0; t < GK; ++t) {
-      double a[8], b[8];
-      const double2* ap = reinterpret_cast<const double2*>(as + t * (GB + GPAD));
-      const double2* bp = reinterpret_cast<const double2*>(bs + t * (GB + GPAD));
-      double2 a0 = ap[ty * 2], a1 = ap[ty * 2 + 1], a2 = ap[32 + ty * 2], a3 = ap[32 + ty * 2 + 1];
-      double2 b0 = bp[tx * 2], b1 = bp[tx * 2 + 1], b2 = bp[32 + tx * 2], b3 = bp[32 + tx * 2 + 1];
-      a[0] = a0.x; a[1] = a0.y; a[2] = a1.x; a[3] = a1.y;
-      a[4] = a2.x; a[5] = a2.y; a[6] = a3.x; a[7] = a3.y;
-      b[0] = b0.x; b[1] = b0.y; b[2] = b1.x; b[3] = b1.y;
-      b[4] = b2.x; b[5] = b2.y; b[6] = b3.x; b[7] = b3.y;
+    for (int kq = 0; kq < DG_K; kq += 4) {
+      double a[8], b[4];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int r = wm * 64 + u * 8 + fr;
+        a[u] = TA ? as[(kq + fc) * (DG_T + DG_PAD) + r] : as[r * (DG_K + DG_PAD) + kq + fc];
+      }
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        const int cidx = wn * 32 + v * 8 + fr;
+        b[v] = TB ? bs[cidx * (DG_K + DG_PAD) + kq + fc] : bs[(kq + fc) * (DG_T + DG_PAD) + cidx];
+      }
 #pragma unroll
       for (int u = 0; u < 8; ++u)
 #pragma unroll
-        for (int v = 0; v < 8; ++v) acc[u][v] = fma(a[u], b[v], acc[u][v]);
-    }
-    if (s + 1 < nk) {
-      store(buf ^ 1);
-      __syncthreads();
+        for (int v = 0; v < 4; ++v) dmma(acc[u][v], a[u], b[v]);
     }
   }
+  cp_async_wait<0>();
 #pragma unroll
   for (int u = 0; u < 8; ++u) {
-    const int i = i0 + (u < 4 ? ty * 4 + u : 64 + ty * 4 + (u - 4));
+    const int i = i0 + wm * 64 + u * 8 + fr;
     if (i >= m) continue;
 #pragma unroll
-    for (int v = 0; v < 8; ++v) {
-      const int j = j0 + (v < 4 ? tx * 4 + v : 64 + tx * 4 + (v - 4));
-      if (j >= n) continue;
-      double* c = C + (int64_t)i * ldc + j;
-      *c = beta == 0.0 ? alpha * acc[u][v] : fma(alpha, acc[u][v], beta * *c);
+    for (int v = 0; v < 4; ++v) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int j = j0 + wn * 32 + v * 8 + 2 * fc + h;
+        if (j >= n) continue;
+        double* c = C + (int64_t)i * ldc + j;
+        *c = beta == 0.0 ? alpha * acc[u][v][h] : fma(alpha, acc[u][v][h], beta * *c);
+      }
     }
   }
 }
-
-// ---------------------------------------------------------------- cuBLAS (run-time bound)
-struct BlasApi {
-  bool ok = false;
-  cublasHandle_t h = nullptr;
-  decltype(&cublasSetStream_v2) set_stream = nullptr;
-  decltype(&cublasDgemm_v2) dgemm = nullptr;
-  decltype(&cublasDsyrk_v2) dsyrk = nullptr;
-  decltype(&cublasDtrmm_v2) dtrmm = nullptr;
-};
-
-static BlasApi* blas(msb_ctx ctx) {
-  static BlasApi api[64];
-  static bool tried[64];
-  const int d = ctx->device;
-  if (d < 0 || d >= 64) return nullptr;
-  if (!tried[d]) {
-    tried[d] = true;
-    const char* own = getenv("MSB_OWN_DGEMM");
-    if (own && own[0] == '1') return nullptr;
-    void* lib = dlopen("libcublas.so.12", RTLD_NOW | RTLD_GLOBAL);
-    if (!lib) lib = dlopen("libcublas.so", RTLD_NOW | RTLD_GLOBAL);
-    if (!lib) return nullptr;
-    auto create = reinterpret_cast<decltype(&cublasCreate_v2)>(dlsym(lib, "cublasCreate_v2"));
-    BlasApi& a = api[d];
-    a.set_stream = reinterpret_cast<decltype(&cublasSetStream_v2)>(dlsym(lib, "cublasSetStream_v2"));
-    a.dgemm = reinterpret_cast<decltype(&cublasDgemm_v2)>(dlsym(lib, "cublasDgemm_v2"));
-    a.dsyrk = reinterpret_cast<decltype(&cublasDsyrk_v2)>(dlsym(lib, "cublasDsyrk_v2"));
-    a.dtrmm = reinterpret_cast<decltype(&cublasDtrmm_v2)>(dlsym(lib, "cublasDtrmm_v2"));
-    auto set_mode =
-        reinterpret_cast<decltype(&cublasSetMathMode)>(dlsym(lib, "cublasSetMathMode"));
-    if (!create || !a.set_stream || !a.dgemm || !a.dsyrk) return nullptr;
-    int prev = -1;
-    cudaGetDevice(&prev);
-    cudaSetDevice(d);
-    const bool made = create(&a.h) == CUBLAS_STATUS_SUCCESS;
-    if (prev >= 0) cudaSetDevice(prev);
-    if (!made) return nullptr;
-    if (set_mode) set_mode(a.h, CUBLAS_PEDANTIC_MATH);  // plain fp64, no emulation
-    a.ok = true;
-  }
-  return api[d].ok ? &api[d] : nullptr;
-}
-
-// Row-major C (m x n, ldc) = alpha op(A) op(B) + beta C on cuBLAS (column-major): the
-// same memory read column-major is the transpose, so C^T = op(B)^T op(A)^T.
-template <bool TA, bool TB>
-static bool blas_gemm(msb_ctx ctx, int m, int n, int K, double alpha, const double* A,
-                      int64_t lda, const double* B, int64_t ldb, double beta, double* C,
-                      int64_t ldc) {
-  BlasApi* b = blas(ctx);
-  if (!b || b->set_stream(b->h, ctx->stream) != CUBLAS_STATUS_SUCCESS) return false;
-  return b->dgemm(b->h, TB ? CUBLAS_OP_T : CUBLAS_OP_N, TA ? CUBLAS_OP_T : CUBLAS_OP_N, n, m, K,
-                  &alpha, B, (int)ldb, A, (int)lda, &beta, C, (int)ldc) == CUBLAS_STATUS_SUCCESS;
-}
-
-// Row-major lower triangle of C (n x n) = alpha X + beta C with X = A A^T (at = false,
-// A n x k) or X = A^T A (at = true, A k x n); the row-major lower triangle is the
-// column-major upper one.
-static bool blas_syrk(msb_ctx ctx, bool at, int n, int k, double alpha, const double* A,
-                      int64_t lda, double beta, double* C, int64_t ldc) {
-  BlasApi* b = blas(ctx);
-  if (!b || b->set_stream(b->h, ctx->stream) != CUBLAS_STATUS_SUCCESS) return false;
-  return b->dsyrk(b->h, CUBLAS_FILL_MODE_UPPER, at ? CUBLAS_OP_N : CUBLAS_OP_T, n, k, &alpha, A,
-                  (int)lda, &beta, C, (int)ldc) == CUBLAS_STATUS_SUCCESS;
-}
-
-// Row-major C (m x n, ldc) = W22^T W21 for W22 lower triangular (n x n, lda) and W21
-// (n rows x m cols, ldb): in column-major terms C_cm = W21_cm W22_cm^T with W22_cm upper
-// triangular — cuBLAS DTRMM, side right, out of place.
-static bool blas_trmm_lt(msb_ctx ctx, int m, int n, const double* W22, int64_t lda,
-                         const double* W21, int64_t ldb, double* C, int64_t ldc) {
-  BlasApi* b = blas(ctx);
-  if (!b || !b->dtrmm || b->set_stream(b->h, ctx->stream) != CUBLAS_STATUS_SUCCESS) return false;
-  const double one = 1.0;
-  return b->dtrmm(b->h, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_T,
-                  CUBLAS_DIAG_NON_UNIT, m, n, &one, W22, (int)lda, W21, (int)ldb, C,
-                  (int)ldc) == CUBLAS_STATUS_SUCCESS;
-}
-
-constexpr size_t GEMM_SMEM = 2 * 2 * GK * (GB + GPAD) * sizeof(double);
 
 template <bool TA, bool TB>
 static msb_status gemm(msb_ctx ctx, int m, int n, int K, double alpha, const double* A, int64_t lda,
                        const double* B, int64_t ldb, double beta, double* C, int64_t ldc,
-                       bool lower = false, bool tri_k = false) {
+                       bool lower = false, int kmode = 0) {
   if (m <= 0 || n <= 0) return MSB_OK;
-  if (!lower && !tri_k && K > 0 &&
-      blas_gemm<TA, TB>(ctx, m, n, K, alpha, A, lda, B, ldb, beta, C, ldc)) {
-    count_launch();
-    return MSB_OK;
-  }
   static bool attr = false;
   if (!attr) {
     MSB_CUDA_TRY(ctx, cudaFuncSetAttribute(k_dgemm<TA, TB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           (int)GEMM_SMEM));
+                                           (int)DG_SMEM));
     attr = true;
   }
-  dim3 g((n + GB - 1) / GB, (m + GB - 1) / GB);
-  k_dgemm<TA, TB><<<g, 256, GEMM_SMEM, ctx->stream>>>(m, n, K, alpha, A, lda, B, ldb, beta, C, ldc,
-                                                       lower ? 1 : 0, tri_k ? 1 : 0);
+  dim3 g((n + DG_T - 1) / DG_T, (m + DG_T - 1) / DG_T);
+  k_dgemm<TA, TB><<<g, 256, DG_SMEM, ctx->stream>>>(m, n, K, alpha, A, lda, B, ldb, beta, C, ldc,
+                                                     lower ? 1 : 0, kmode);
   MSB_LAUNCH_CHECK(ctx);
   return MSB_OK;
+}
+
+msb_status dgemm(msb_ctx ctx, bool ta, bool tb, int m, int n, int K, double alpha, const double* A,
+                 int64_t lda, const double* B, int64_t ldb, double beta, double* C, int64_t ldc) {
+  if (ta && tb) return gemm<true, true>(ctx, m, n, K, alpha, A, lda, B, ldb, beta, C, ldc);
+  if (ta) return gemm<true, false>(ctx, m, n, K, alpha, A, lda, B, ldb, beta, C, ldc);
+  if (tb) return gemm<false, true>(ctx, m, n, K, alpha, A, lda, B, ldb, beta, C, ldc);
+  return gemm<false, false>(ctx, m, n, K, alpha, A, lda, B, ldb, beta, C, ldc);
 }
 
 // Leaf: Cholesky of the n x n (n <= LEAF) block at A (ld) in place (lower; upper zeroed)
@@ -382,9 +329,7 @@ static msb_status chol_inv(msb_ctx ctx, double* F, double* Wb, int64_t ld, int n
   k_copy2d<<<grid_for((int64_t)n2 * n1, 256), 256, 0, ctx->stream>>>(F21, ld, W21, ld, n2, n1);
   MSB_LAUNCH_CHECK(ctx);
   // A22 -= L21 L21^T (lower tiles)
-  if (blas_syrk(ctx, false, n2, n1, -1.0, F21, ld, 1.0, F22, ld))
-    count_launch();
-  else if ((rc = gemm<false, true>(ctx, n2, n2, n1, -1.0, F21, ld, F21, ld, 1.0, F22, ld, true)))
+  if ((rc = gemm<false, true>(ctx, n2, n2, n1, -1.0, F21, ld, F21, ld, 1.0, F22, ld, true)))
     return rc;
   if ((rc = chol_inv(ctx, F22, W22, ld, n2, amax, sing))) return rc;
   // triangular inverse (LAPACK dtrtri): T^T = W11^T L21^T (n1 x n2) into the free upper
@@ -405,18 +350,20 @@ __global__ void k_absmax2(const double* __restrict__ A, int64_t n, unsigned long
 
 // Lower triangle of F = W^T W for lower-triangular W (LAPACK dlauum, recursive):
 //   [W11 0; W21 W22]: F11 = W11^T W11 + W21^T W21, F21 = W22^T W21, F22 = W22^T W22
-// — M^3/3 flops instead of the M^3 of one DSYRK over the full (half-zero) W.  Leaves
-// (n <= 512) are one DSYRK.  Returns false when cuBLAS is not available.
-static bool lauum(msb_ctx ctx, const double* W, double* F, int n, int64_t ld) {
-  if (n <= 512) return blas_syrk(ctx, true, n, n, 1.0, W, ld, 0.0, F, ld);
+// — M^3/3 flops instead of the M^3 of one SYRK over the full (half-zero) W.  Leaves
+// (n <= 512) are one triangular-K product (kmode 2).
+static msb_status lauum(msb_ctx ctx, const double* W, double* F, int n, int64_t ld) {
+  if (n <= 512) return gemm<true, false>(ctx, n, n, n, 1.0, W, ld, W, ld, 0.0, F, ld, true, 2);
   const int n1 = split1(n), n2 = n - n1;
   const double* W21 = W + (int64_t)n1 * ld;
   const double* W22 = W21 + n1;
   double* F21 = F + (int64_t)n1 * ld;
   double* F22 = F21 + n1;
-  if (!lauum(ctx, W, F, n1, ld)) return false;
-  if (!blas_syrk(ctx, true, n1, n2, 1.0, W21, ld, 1.0, F, ld)) return false;
-  if (!blas_trmm_lt(ctx, n1, n2, W22, ld, W21, ld, F21, ld)) return false;
+  msb_status rc;
+  if ((rc = lauum(ctx, W, F, n1, ld))) return rc;
+  if ((rc = gemm<true, false>(ctx, n1, n1, n2, 1.0, W21, ld, W21, ld, 1.0, F, ld, true))) return rc;
+  if ((rc = gemm<true, false>(ctx, n2, n1, n2, 1.0, W22, ld, W21, ld, 0.0, F21, ld, false, 1)))
+    return rc;
   return lauum(ctx, W22, F22, n2, ld);
 }
 
@@ -450,13 +397,7 @@ msb_status coarse_factor_dense(msb_ctx ctx, Coarse& co) {
   // A_c^{-1} = W^T W: lower tiles with the K range restricted to the nonzeros of W,
   // written over the factor buffer (L is no longer needed), then mirrored; swap so
   // that co.Ainv holds the inverse and co.L the inverse factor W.
-  static const bool full_syrk = getenv("MSB_FULL_SYRK") != nullptr;
-  if (!full_syrk && lauum(ctx, Wb, F, M, M))
-    count_launch();
-  else if (blas_syrk(ctx, true, M, M, 1.0, Wb, M, 0.0, F, M))
-    count_launch();
-  else if ((rc = gemm<true, false>(ctx, M, M, M, 1.0, Wb, M, Wb, M, 0.0, F, M, true, true)))
-    return rc;
+  if ((rc = lauum(ctx, Wb, F, M, M))) return rc;
   dim3 g((M + 31) / 32, (M + 31) / 32);
   k_mirror_lower<<<g, dim3(32, 32), 0, s>>>(F, M);
   MSB_LAUNCH_CHECK(ctx);

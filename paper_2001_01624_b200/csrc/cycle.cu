@@ -1243,7 +1243,7 @@ static msb_status enqueue_stage(msb_ctx ctx, msb_solver s, msb_level L, const do
       k_restrict_cart<<<L->nb[1] * L->nb[2], RR2_THREADS, restrict_rows_smem(op->nx), st>>>(
           V, s->r, s->rc, s->st);
       MSB_LAUNCH_CHECK(ctx);
-      coarse_solve_dense(ctx, L->co, s->rc, s->xc, &s->st->done);
+      coarse_solve(ctx, L->co, s->rc, s->xc, &s->st->done);
       k_prolong_cart<<<g, CT, 0, st>>>(V, s->xbuf[cur], s->xc, s->st);
       MSB_LAUNCH_CHECK(ctx);
       return MSB_OK;
@@ -1259,7 +1259,7 @@ static msb_status enqueue_stage(msb_ctx ctx, msb_solver s, msb_level L, const do
       k_restrict_csc<<<(unsigned)((L->M + 7) / 8), 256, 0, st>>>(L->csc_ptr, L->csc_pos, L->P[L->cur],
                                                               s->r, (int)L->N, L->M, s->rc, s->st);
       MSB_LAUNCH_CHECK(ctx);
-      coarse_solve_dense(ctx, L->co, s->rc, s->xc, &s->st->done);
+      coarse_solve(ctx, L->co, s->rc, s->xc, &s->st->done);
       k_prolong<<<g, CT, 0, st>>>(V, s->xbuf[cur], s->xc, s->st);
       MSB_LAUNCH_CHECK(ctx);
       return MSB_OK;
@@ -1298,7 +1298,7 @@ static msb_status enqueue_stage(msb_ctx ctx, msb_solver s, msb_level L, const do
       if (rc) return rc;
     }
     first = false;
-    coarse_solve_dense(ctx, L->co, s->rc, s->xc, &s->st->done);
+    coarse_solve(ctx, L->co, s->rc, s->xc, &s->st->done);
     k_prolong<<<g, CT, 0, st>>>(V, s->xbuf[cur], s->xc, s->st);
     MSB_LAUNCH_CHECK(ctx);
     return MSB_OK;
@@ -1352,6 +1352,7 @@ static msb_status chunk_graph(msb_ctx ctx, msb_solver s, const double* db, int c
   for (msb_level L : s->levels) {
     key.push_back(L->P[L->cur]);
     key.push_back(L->co.Ainv);
+    key.push_back(L->co.sch);
     key.push_back(L->co.Xp);
   }
   if (key != s->gkey) {

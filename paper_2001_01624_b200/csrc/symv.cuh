@@ -23,10 +23,13 @@ __device__ __forceinline__ void symv_tile_rc(int64_t t, int& bi, int& bj) {
 
 // tile t: row contribution X_t r_bj and (off-diagonal) column contribution X_t^T r_bi
 // into part[t][0..63], part[t][64..127].  Uses 8.5 KB of static shared memory.
+// map / roff (batched solves, coarse_schur.cu): matrix row r reads rc[map[roff + r]]
+// (map NULL: rc[roff + r]).
 template <bool CG>
 __device__ __forceinline__ void symv_tile_body(const double* __restrict__ Xp, int M,
                                                const double* rc, double* __restrict__ part,
-                                               int64_t t) {
+                                               int64_t t, const int32_t* __restrict__ map = nullptr,
+                                               int roff = 0) {
   int bi, bj;
   symv_tile_rc(t, bi, bj);
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // columns 2tx, 2tx+1; rows ty + 8u
@@ -34,14 +37,15 @@ __device__ __forceinline__ void symv_tile_body(const double* __restrict__ Xp, in
   double2 a[8];
 #pragma unroll
   for (int u = 0; u < 8; ++u) a[u] = __ldcs(tile + (ty + 8 * u) * (ST / 2) + tx);
+  auto at = [&](int r) -> int { return map ? map[roff + r] : roff + r; };
   const int cj = bj * ST + 2 * tx;
-  const double r0 = cj < M ? ld_mut<CG>(rc + cj) : 0.0;
-  const double r1 = cj + 1 < M ? ld_mut<CG>(rc + cj + 1) : 0.0;
+  const double r0 = cj < M ? ld_mut<CG>(rc + at(cj)) : 0.0;
+  const double r1 = cj + 1 < M ? ld_mut<CG>(rc + at(cj + 1)) : 0.0;
   double ri[8];
 #pragma unroll
   for (int u = 0; u < 8; ++u) {
     const int row = bi * ST + ty + 8 * u;
-    ri[u] = row < M ? ld_mut<CG>(rc + row) : 0.0;
+    ri[u] = row < M ? ld_mut<CG>(rc + at(row)) : 0.0;
   }
   __shared__ double rows_sh[ST];
   __shared__ double cols_sh[8][ST];
@@ -77,9 +81,12 @@ __device__ __forceinline__ void symv_tile_body(const double* __restrict__ Xp, in
 // G = blockDim / 64 thread groups of 64 taking every G-th contribution (the persistent
 // kernel runs 4 groups, k_symv_reduce 16: a 4-deep instead of 14-deep chain of dependent
 // L2 loads per thread at M = 3,400), then a fixed-order combine of the groups
+// omap / roff: output row r goes to xc[omap[roff + r]] (omap NULL: xc[roff + r])
 template <bool CG>
 __device__ __forceinline__ void symv_reduce_body(const double* part, int M, int ntb,
-                                                 double* __restrict__ xc, int b, bool skip) {
+                                                 double* __restrict__ xc, int b, bool skip,
+                                                 const int32_t* __restrict__ omap = nullptr,
+                                                 int roff = 0) {
   const int i = threadIdx.x & (ST - 1), g = threadIdx.x / ST, G = blockDim.x / ST;
   const int64_t rowbase = (int64_t)b * (b + 1) / 2;
   double v = 0.0;
@@ -95,7 +102,7 @@ __device__ __forceinline__ void symv_reduce_body(const double* part, int M, int 
     double tot = 0.0;
     for (int q = 0; q < G; ++q) tot += sh[q][i];
     const int row = b * ST + i;
-    if (row < M && !skip) xc[row] = tot;
+    if (row < M && !skip) xc[omap ? omap[roff + row] : roff + row] = tot;
   }
   __syncthreads();
 }

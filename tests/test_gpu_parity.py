@@ -877,12 +877,18 @@ def test_ilu_smoother_parity(ctx, name):
     xo1 = o1["sol"]["x"]
     e1 = np.linalg.norm(g1["x_host"] - xo1) / np.linalg.norm(xo1)
     # 1e-10 (tighter than the north-star 1e-9) absorbs the restriction's summation order:
-    # with one block P^T r = sum r, which nearly cancels on this Neumann problem, and the
+    # with one block P^T r = sum r, which nearly cancels on this Neumann problem.  The
     # ILU(0) pivots D~_b = a_bb - sum a_br^2 / a_rr cancel where a black cell hangs on one
-    # strong link (K contrast 1e3); a wrong ILU term is O(1e-3)
+    # strong link (K contrast 1e3), so the summation order of a_bb itself is amplified: the
+    # floor is the genuine alternate that sums A's diagonal face by face in ascending
+    # neighbour order (oracle.tpfa diag_order="faces"; the GPU's order) instead of scipy's
+    # assembly order.  A wrong ILU term is O(1e-3).
+    from oracle import pipeline as opl
+    oa = opl.run(p1, fixed_iters=2, levels_info=o1["levels_info"], diag_order="faces")
+    f1 = np.linalg.norm(oa["sol"]["x"] - xo1) / np.linalg.norm(xo1)
     from conftest import record_parity
-    record_parity(f"ilu_tight/{name}", err=e1, x_tol=1e-10)
-    assert e1 <= 1e-10, e1
+    record_parity(f"ilu_tight/{name}", err=e1, floor=f1, x_tol=max(1e-10, 2.0 * f1))
+    assert e1 <= max(1e-10, 2.0 * f1), (e1, f1)
     orc = _oracle_full(prob)
     assert orc["sol"]["converged"]
     k_or = orc["sol"]["iters"]
@@ -1039,3 +1045,157 @@ def test_error_paths_fail_loudly(ctx):
     x = torch.zeros(prob.N, dtype=torch.float64, device="cuda")
     out = s.iterate(x, None, 1e-300, 3)  # unreachable tolerance: MSB_NOT_CONVERGED, not an error
     assert out["iters"] == 3 and not out["converged"]
+
+
+# ---------------------------------------------------------------- round 2: coarse subsystem
+def _ell_vs_galerkin(lev, P, A, M):
+    """GPU box-stencil A_c (msb_level_export_coarse) against scipy P^T A P of the same P:
+    every stored entry, and every scipy nonzero inside the stored pattern."""
+    import scipy.sparse as sp
+    from oracle import coarse
+    r, c, v = lev.export_coarse()
+    ref = coarse.galerkin(P, A)
+    ref = sp.csr_matrix(ref)
+    scale = np.abs(ref.data).max()
+    err = np.max(np.abs(np.asarray(ref[r, c]).ravel() - v))
+    # nothing outside the stored pattern
+    got = sp.csr_matrix((v, (r, c)), shape=(M, M))
+    outside = (abs(ref) - abs(ref).multiply(got != 0)).max() if ref.nnz else 0.0
+    return err / scale, outside / scale
+
+
+SCHUR_CASES = {
+    # M = 24 x 22 x 10 = 5,280 > 4,096 blocks: the Schur-complement coarse solver;
+    # even x blocks (reach 2), odd y / z blocks (reach 1), ragged last z block
+    "even_odd_ragged": lambda: random_problem(31, 48, 66, 29, (2, 3, 3), sigma=1.5,
+                                              max_sweeps=30, fixed_sweeps=True),
+    # 4 x 4 x 2 blocks on the config-5 recipe's anisotropic field: reach 2 in x and y
+    "config5_recipe": lambda: make_problem(5, shape=(96, 88, 20), block=(4, 4, 2),
+                                           max_sweeps=30, fixed_sweeps=True),
+}
+
+
+@pytest.mark.parametrize("name", list(SCHUR_CASES))
+def test_schur_coarse_solver_parity(ctx, name):
+    """Cartesian level with M > 4,096: A_c assembled exactly into its box stencil (against
+    scipy P^T A P <= 1e-12 max|A_c|, nothing outside the stencil) and solved by the
+    one-level nested-dissection Schur solver; fixed 10 iterations against the oracle
+    (sparse LU) within max(1e-9, 2 x the band-Cholesky / natural-order alternates)."""
+    import scipy.sparse as sp
+    from conftest import record_parity
+    from oracle import pipeline as opl
+    prob = SCHUR_CASES[name]()
+    g = _gpu_full(ctx, prob, fixed_iters=10)
+    lev = g["levels"][0]
+    rowptr, cols, vals, _ = lev.export()
+    M = lev.info()["M"]
+    assert M > 4096
+    orc = opl.run(prob, fixed_iters=10)
+    P = sp.csr_matrix((vals, cols, rowptr), shape=(prob.N, M))
+    e_ac, e_out = _ell_vs_galerkin(lev, P, orc["A"], M)
+    xo = orc["sol"]["x"]
+    li = orc["levels_info"]
+    floors = [np.linalg.norm(opl.run(prob, fixed_iters=10, levels_info=li, coarse=cm,
+                                     assoc=asc)["sol"]["x"] - xo) / np.linalg.norm(xo)
+              for cm, asc in (("cholesky", "right"), ("splu_natural", "right"), ("lu", "left"))]
+    err = np.linalg.norm(g["x_host"] - xo) / np.linalg.norm(xo)
+    x_tol = max(X_RTOL, 2.0 * max(floors))
+    record_parity(f"schur/{name}", M=M, ac_err=e_ac, ac_outside=e_out, err=err,
+                  floor=max(floors), x_tol=x_tol)
+    assert e_ac <= 1e-12 and e_out == 0.0, (e_ac, e_out)
+    assert err <= x_tol, (err, floors)
+    assert np.allclose(g["sol"]["res"], orc["sol"]["res"], rtol=1e-6, atol=1e-13)
+
+
+def test_cartesian_ell_export_dense_path(ctx):
+    """The box-stencil dump of a dense-solver level (M <= 4,096) equals its dense A_c."""
+    from paper_2001_01624_b200 import Level
+    from paper_2001_01624_b200.pipeline import build_operator
+    prob = random_problem(5, 23, 17, 7, (5, 4, 3), sigma=2.0)
+    op = build_operator(ctx, prob)
+    lev = Level.cartesian(ctx, op, prob.block)
+    lev.smooth(op, 20, prob.omega, -1.0)
+    lev.assemble(op)
+    _, _, _, Ac = lev.export(with_Ac=True)
+    r, c, v = lev.export_coarse()
+    assert np.array_equal(Ac[r, c], v)
+    mask = np.zeros_like(Ac, dtype=bool)
+    mask[r, c] = True
+    assert np.all(Ac[~mask] == 0.0)
+
+
+def test_constant_level_import_assembles_imported_values(ctx):
+    """A W = 1 level whose values were imported (rows no longer known to be all ones) is
+    assembled from its P, not as a constant basis (k_rap_const_det ignored P)."""
+    import scipy.sparse as sp
+    from oracle import coarse, tpfa
+    from paper_2001_01624_b200 import Level
+    from paper_2001_01624_b200.pipeline import build_operator
+    prob = random_problem(8, 23, 17, 9, (5, 4, 3), sigma=2.0)
+    A_T, A, q, _ = tpfa.build(prob)
+    rng = np.random.default_rng(4)
+    M = 40
+    part = np.repeat(rng.integers(0, M, size=prob.N // 8 + 1), 8)[:prob.N]
+    part[:M] = np.arange(M)
+    part = part.astype(np.int32)
+    op = build_operator(ctx, prob)
+    lev = Level.constant(ctx, op, part, M)
+    vals = rng.uniform(0.5, 2.0, prob.N)
+    lev.import_values(np.ascontiguousarray(vals))
+    lev.assemble(op)
+    _, _, _, Ac = lev.export(with_Ac=True)
+    P = sp.csr_matrix((vals, (np.arange(prob.N), part)), shape=(prob.N, M))
+    ref = coarse.galerkin(P, A)
+    assert np.max(np.abs(Ac - ref)) <= 1e-12 * np.abs(ref).max()
+
+
+def test_inconsistent_compartment_rejected(ctx):
+    """Sealing faces (multiplier 0) that cut off a compartment without the gauge cell make
+    A singular: msb_solver_create returns MSB_EINCONSISTENT."""
+    from paper_2001_01624_b200 import Level, Solver
+    from paper_2001_01624_b200.api import MsbError
+    from paper_2001_01624_b200.pipeline import build_operator
+    prob = random_problem(12, 12, 8, 4, (4, 4, 2))
+    nx, ny, nz = prob.nx, prob.ny, prob.nz
+    mx = np.ones((nz, ny, nx - 1))
+    mx[:, :, 7] = 0.0  # the plane between i = 7 and i = 8 seals the grid in two
+    prob.mult_x = mx.ravel()
+    op = build_operator(ctx, prob)
+    lev = Level.cartesian(ctx, op, prob.block)
+    lev.smooth(op, 5, prob.omega, -1.0)
+    lev.assemble(op)
+    with pytest.raises(MsbError, match="EINCONSISTENT"):
+        Solver(ctx, op, [lev], prob.omega_s, prob.nu, prob.post_smooth)
+    mx[:, 3, 7] = 1.0  # one open face reconnects the compartments
+    prob.mult_x = mx.ravel()
+    op2 = build_operator(ctx, prob)
+    lev2 = Level.cartesian(ctx, op2, prob.block)
+    lev2.smooth(op2, 5, prob.omega, -1.0)
+    lev2.assemble(op2)
+    Solver(ctx, op2, [lev2], prob.omega_s, prob.nu, prob.post_smooth)
+
+
+def test_transport_step_size_and_initial_mobility(ctx):
+    """Config-4 helpers now in the library: dt (msb_transport_step_size) and the step-1
+    face mobility λ_t(S = 0) = 1/μ_o (msb_upstream_mobility with p = S = NULL)."""
+    import torch
+    from oracle import transport
+    from oracle.grid import all_faces
+    from paper_2001_01624_b200.pipeline import build_operator
+    prob = make_problem(4, shape=(14, 26, 9))
+    op = build_operator(ctx, prob)
+    phi = np.full(prob.N, prob.phi)
+    dt = op.step_size(torch.as_tensor(phi, device="cuda"), 0.005)
+    dt_or = transport.step_size(prob, prob.rhs(), phi, 0.005)
+    assert abs(dt - dt_or) <= 4 * np.finfo(float).eps * dt_or
+    mob = op.upstream_mobility(None, None, 1.0, 5.0,
+                               torch.empty(prob.n_faces, dtype=torch.float64, device="cuda"))
+    faces = all_faces(prob.nx, prob.ny, prob.nz)
+    ref = np.concatenate(transport.upstream_mobility(faces, np.zeros(prob.N), np.zeros(prob.N),
+                                                     1.0, 5.0))
+    assert np.array_equal(mob.cpu().numpy(), ref)
+    rng = np.random.default_rng(2)
+    p, S = rng.standard_normal(prob.N), rng.uniform(0, 1, prob.N)
+    mob2 = op.upstream_mobility(p, S, 1.0, 5.0, np.empty(prob.n_faces))
+    ref2 = np.concatenate(transport.upstream_mobility(faces, p, S, 1.0, 5.0))
+    assert np.allclose(mob2, ref2, rtol=2 * np.finfo(float).eps, atol=0.0)
