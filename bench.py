@@ -258,6 +258,8 @@ def run_gpu(args):
     K_dev = K_host.to(f"cuda:{local}")
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=f"cuda:{local}")  # 256 MB > L2
 
+    level_facts = {}
+
     def step(K, x_out=None, timers=None):
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
         ev[0].record(stream)
@@ -267,6 +269,8 @@ def run_gpu(args):
         n, last, deltas, _ = lev.smooth(op, prob.max_sweeps, prob.omega, prob.sweep_tol)
         ev[2].record(stream)
         lev.assemble(op)
+        if not level_facts:
+            level_facts.update(lev.info())
         solver = Solver(ctx, op, [lev], prob.omega_s, prob.nu, prob.post_smooth)
         x = torch.zeros(N, dtype=torch.float64, device=f"cuda:{local}")
         ev[3].record(stream)
@@ -324,7 +328,7 @@ def run_gpu(args):
     # algorithmic bytes: sweep = 16 nnz + 8 faces; cycle stage =
     # 16 nnz + 8 faces + 40 N + coarse solve, the coarse solve reading the lower
     # triangle of the symmetric A_c^{-1}: 8 M (M + 1) / 2
-    nnz, faces, M = 6964260, prob.n_faces, 3400
+    nnz, faces, M = level_facts["nnz"], prob.n_faces, level_facts["M"]
     b_sweep = 16 * nnz + 8 * faces
     b_iter = 16 * nnz + 8 * faces + 40 * N + 4 * M * (M + 1)
     peaks = _peaks()
@@ -360,6 +364,7 @@ def run_gpu(args):
                "sample": f"{args.cpu_sweeps} oracle sweeps + {args.cpu_iters} oracle cycles on "
                          f"the full config2 grid, single thread",
                "ms_per_iteration": s.get("ms_per_iteration"), "cpu": model, "host_cores": cores}
+    c5 = None if args.no_config5 else config5_measure(ctx, stream, local, peak, src)
     e2e_t = sum(t for t, _ in e2e) or float("nan")
     e2e_sw = sum(n for _, n in e2e)
     line = {
@@ -383,6 +388,7 @@ def run_gpu(args):
         "roofline": dominant,
         "roofline_sweep": roof_sweep,
         "roofline_cycle": roof_cycle,
+        "config5": c5,
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_sw / e2e_t, "unit": "sweeps/s",
                 "ms_per_step": 1e3 * e2e_t / max(1, len(e2e)),
@@ -396,6 +402,68 @@ def run_gpu(args):
     return 0
 
 
+def config5_measure(ctx, stream, local, peak, src):
+    """BASELINE.json configs[4] (200x400x125 = 10M cells, M = 20,000): the whole path once
+    untimed, then timed with CUDA events on the library stream — the smoothing phase to
+    δ <= 1e-3 (or 300 sweeps), the coarse setup, and the 20 fixed multiscale iterations.
+    Fractions use SURVEY.md §8.d's algorithmic bytes: sweep 16 nnz + 8 faces; iteration
+    16 nnz + 8 faces + 40 N + the band factor's two sweeps 2 * 8 M (bw + 1)."""
+    import numpy as np
+    import torch
+    from paper_2001_01624_b200 import Level, Operator, Solver
+    from paper_2001_01624_b200 import pipeline as gp
+    from synth.configs import make_problem
+
+    prob = make_problem(5)
+    K = torch.from_numpy(gp.problem_K(prob)).to(f"cuda:{local}")
+    res = {}
+    for rep in range(2):  # rep 0 warms up (allocator, graph instantiation)
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
+        ev[0].record(stream)
+        op = Operator(ctx, prob.nx, prob.ny, prob.nz, K, prob.src_cells, prob.src_rates)
+        lev = Level.cartesian(ctx, op, prob.block)
+        ev[1].record(stream)
+        n, _, _, _ = lev.smooth(op, prob.max_sweeps, prob.omega, prob.sweep_tol)
+        ev[2].record(stream)
+        lev.assemble(op)
+        solver = Solver(ctx, op, [lev], prob.omega_s, prob.nu, prob.post_smooth)
+        x = torch.zeros(prob.N, dtype=torch.float64, device=f"cuda:{local}")
+        ev[3].record(stream)
+        sol = solver.iterate(x, None, prob.cycle_tol, 100, prob.fixed_iters, history=True)
+        ev[4].record(stream)
+        torch.cuda.synchronize()
+        t = [ev[i].elapsed_time(ev[i + 1]) for i in range(4)]
+        info = lev.info()
+        if rep == 1:
+            r, c, _ = lev.export_coarse()
+            bw = int(np.max(np.abs(r.astype(np.int64) - c)))
+            N, nnz, M, faces = prob.N, info["nnz"], info["M"], prob.n_faces
+            b_sweep = 16 * nnz + 8 * faces
+            b_band = 2 * 8 * M * (bw + 1)
+            b_iter = 16 * nnz + 8 * faces + 40 * N + b_band
+            per_sweep = t[1] / 1e3 / n
+            per_iter = t[3] / 1e3 / sol["iters"]
+            res = {"workload": "config5: 200x400x125 (10M cells), log-normal K sigma=2, "
+                               "Kz/Kx in [0.01, 0.1], 10x10x5 blocks (M = 20,000)",
+                   "sweeps": n, "iterations": sol["iters"], "ms_per_sweep": 1e3 * per_sweep,
+                   "ms_per_iteration": 1e3 * per_iter, "setup_ms": t[0], "coarse_setup_ms": t[2],
+                   "final_rel_residual": float(sol["res"][-1]),
+                   "bytes": {"sweep": b_sweep, "iteration": b_iter, "coarse_band": b_band,
+                             "coarse_half_bandwidth": bw},
+                   "roofline_sweep": {"bound": "hbm", "achieved": b_sweep / per_sweep / 1e9,
+                                      "peak": peak, "unit": "GB/s",
+                                      "frac": b_sweep / per_sweep / 1e9 / peak,
+                                      "peak_source": src},
+                   "roofline_cycle": {"bound": "hbm", "achieved": b_iter / per_iter / 1e9,
+                                      "peak": peak, "unit": "GB/s",
+                                      "frac": b_iter / per_iter / 1e9 / peak,
+                                      "peak_source": src,
+                                      "coarse_solver": "Schur complement (one-level nested "
+                                                       "dissection), own fp64 kernels"}}
+        solver.close(); lev.close(); op.close()
+    return res
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -406,6 +474,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer e2e steps "
                     "(ncu launch-list runs)")
+    ap.add_argument("--no-config5", action="store_true", help="skip the 10M-cell config-5 "
+                    "sweep / cycle measurement")
     ap.add_argument("--cpu-sweeps", type=int, default=20)
     ap.add_argument("--cpu-iters", type=int, default=10)
     ap.add_argument("--ref-sweeps", type=int, default=5)

@@ -209,7 +209,9 @@ msb_status msb_smooth_basis(msb_ctx ctx, msb_level lev, msb_op op, int32_t max_s
  * rows of P sum to one (created or smoothed levels: MsRSB's partition of unity) each face
  * adds only the lower off-diagonal products and the diagonal is minus the row's
  * off-diagonal total plus the gauge term — the same matrix up to the rounding of P's row
- * sums.  Returns MSB_ESINGULAR if a pivot is <= 1e-14 * max|A_c|. */
+ * sums.  Returns MSB_ESINGULAR if a pivot is <= 1e-14 * max|A_c|, MSB_EINCONSISTENT when
+ * the faces with T > 0 leave a compartment without the gauge cell 0 (A, hence A_c, is
+ * then singular). */
 msb_status msb_coarse_assemble(msb_ctx ctx, msb_level lev, msb_op op);
 
 /* ---------------------------------------------------------------- solver (rows a6–a11)

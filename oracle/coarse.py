@@ -15,9 +15,12 @@ the yardstick any third implementation (the GPU's) is held to.  Each is one
 library call, no arithmetic of its own:
     "cholesky"      LAPACK potrf/potrs (dense) or banded Cholesky pbtrf/pbtrs on the
                     natural-order band (sparse M; the band solver of SURVEY §8.a5)
-    "inverse"       LAPACK getrf/getri explicit inverse + GEMV (reading B1)
-    "lu_reversed"   LAPACK LU of the coarse matrix with its unknowns in reverse order
-    "splu_natural"  SuperLU with natural column order (sparse M)
+    "inverse"       LAPACK getrf/getri explicit inverse + GEMV (reading B1; the sparse A_c
+                    densified first)
+    "lu_reversed"   LU of the coarse matrix with its unknowns in reverse order (LAPACK
+                    dense; SuperLU, natural order, sparse)
+    "splu_natural"  SuperLU with natural column order
+Every method works for dense (M <= DENSE_MAX) and sparse A_c.
 `galerkin(..., assoc="left")` forms (P^T A) P instead of P^T (A P): another
 summation order of the same product.
 TEST INFRASTRUCTURE ONLY.
@@ -83,8 +86,8 @@ class CoarseSolver:
                 self._f = np.linalg.inv(Ac)
             elif method == "lu_reversed":
                 self._f = la.lu_factor(Ac[::-1, ::-1])
-            else:
-                raise ValueError(f"{method} is a sparse-only alternate")
+            else:  # splu_natural
+                self._f = spla.splu(sp.csc_matrix(Ac), permc_spec="NATURAL")
         else:
             try:
                 if method == "lu":
@@ -93,8 +96,10 @@ class CoarseSolver:
                     self._f = spla.splu(sp.csc_matrix(Ac), permc_spec="NATURAL")
                 elif method == "cholesky":
                     self._f = la.cholesky_banded(_banded_lower(Ac), lower=True)
-                else:
-                    raise ValueError(f"{method} is a dense-only alternate")
+                elif method == "inverse":
+                    self._f = np.linalg.inv(Ac.toarray())
+                else:  # lu_reversed: SuperLU of the coarse matrix with its unknowns reversed
+                    self._f = spla.splu(sp.csc_matrix(Ac[::-1][:, ::-1]), permc_spec="NATURAL")
             except RuntimeError as e:  # exactly singular
                 raise SingularCoarse(str(e))
             except la.LinAlgError as e:
@@ -109,7 +114,13 @@ class CoarseSolver:
                 return la.cho_solve(self._f, rc)
             if m == "inverse":
                 return self._f @ rc
+            if m == "splu_natural":
+                return self._f.solve(rc)
             return la.lu_solve(self._f, rc[::-1])[::-1]
         if m == "cholesky":
             return la.cho_solve_banded((self._f, True), rc)
+        if m == "inverse":
+            return self._f @ rc
+        if m == "lu_reversed":
+            return self._f.solve(rc[::-1])[::-1]
         return self._f.solve(rc)

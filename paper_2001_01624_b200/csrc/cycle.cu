@@ -166,6 +166,8 @@ __global__ void __launch_bounds__(CT) k_jacobi(StencilT S, const double* __restr
                                                const double* __restrict__ b, double omega,
                                                int first, double* __restrict__ partials,
                                                const IterState* st) {
+  pdl_wait();
+  pdl_trigger();
   const bool done = is_done(st);
   const int N = S.g.nxy * S.g.nz;
   const int c0 = blockIdx.x * (CT * CPT) + threadIdx.x;
@@ -563,6 +565,8 @@ __global__ void __launch_bounds__(CT) k_residual(StencilT S, const double* __res
                                                  double* __restrict__ r, int first,
                                                  double* __restrict__ partials,
                                                  const IterState* st) {
+  pdl_wait();
+  pdl_trigger();
   const bool done = is_done(st);
   const int N = S.g.nxy * S.g.nz;
   const int c0 = blockIdx.x * (CT * CPT) + threadIdx.x;
@@ -615,8 +619,9 @@ __device__ __forceinline__ void support_range(int J, int b, int n, int nb, int& 
 // atomics).  Thread layout: XL lanes along x (XL = pow2 >= nx, <= 256) x RG row
 // groups; x positions beyond 256 take a second partial.
 constexpr int RR2_THREADS = 256;
-template <bool CG>
-__device__ __forceinline__ void restrict_row_body(const LevelView& L, const double* r,
+// XP x positions per lane (x = xo + XL * e, e < XP): XP = ceil(nx / XL), 1 for nx <= 256
+template <int XP>
+__device__ __forceinline__ void restrict_row_body(const LevelView& L, const double* __restrict__ r,
                                                   double* __restrict__ rc, int unit,
                                                   double* rsh, bool done) {
   const int N = L.g.nxy * L.g.nz;
@@ -629,26 +634,33 @@ __device__ __forceinline__ void restrict_row_body(const LevelView& L, const doub
   const int sy = ((Jy & 1) << 1) | ((Jz & 1) << 2);
   const double* __restrict__ P0 = L.P + (size_t)sy * N;        // x parity 0
   const double* __restrict__ P1 = L.P + (size_t)(sy | 1) * N;  // x parity 1
-  const int XL = nx <= 32 ? 32 : (nx <= 64 ? 64 : (nx <= 128 ? 128 : 256));
+  const int XL = XP > 1 ? 256 : (nx <= 32 ? 32 : (nx <= 64 ? 64 : (nx <= 128 ? 128 : 256)));
   const int RG = RR2_THREADS / XL;
   const int xo = threadIdx.x % XL, rg = threadIdx.x / XL;
-  const bool x0ok = xo < nx, x1ok = xo + 256 < nx;
-  double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;  // parity 0/1 at xo and xo + 256
+  double a0[XP], a1[XP];  // parity 0 / 1 partials at x = xo + XL e
+  bool xok[XP];
+#pragma unroll
+  for (int e = 0; e < XP; ++e) {
+    a0[e] = a1[e] = 0.0;
+    xok[e] = xo + XL * e < nx;
+  }
   int row = rg;
   int zz = row / wy, yy = row - zz * wy;
   const int dz = RG / wy, dy = RG - dz * wy;
+  constexpr int U = XP > 2 ? 2 : 4;  // rows in flight per lane
   while (row < rows) {
-    double p0[4], p1[4], rv[4], q0[4], q1[4], rw[4];
+    double p0[U][XP], p1[U][XP], rv[U][XP];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < U; ++u) {
       const bool ok = row < rows;
       const size_t c = (size_t)nx * (y0 + yy) + (size_t)sxy * (z0 + zz) + xo;
-      p0[u] = (ok && x0ok) ? P0[c] : 0.0;
-      p1[u] = (ok && x0ok) ? P1[c] : 0.0;
-      rv[u] = (ok && x0ok) ? ld_mut<CG>(r + c) : 0.0;
-      q0[u] = (ok && x1ok) ? P0[c + 256] : 0.0;
-      q1[u] = (ok && x1ok) ? P1[c + 256] : 0.0;
-      rw[u] = (ok && x1ok) ? ld_mut<CG>(r + c + 256) : 0.0;
+#pragma unroll
+      for (int e = 0; e < XP; ++e) {
+        const bool v = ok && xok[e];
+        p0[u][e] = v ? P0[c + XL * e] : 0.0;
+        p1[u][e] = v ? P1[c + XL * e] : 0.0;
+        rv[u][e] = v ? r[c + XL * e] : 0.0;
+      }
       row += RG;
       yy += dy;
       zz += dz;
@@ -658,19 +670,20 @@ __device__ __forceinline__ void restrict_row_body(const LevelView& L, const doub
       }
     }
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      a0 += p0[u] * rv[u];
-      a1 += p1[u] * rv[u];
-      b0 += q0[u] * rw[u];
-      b1 += q1[u] * rw[u];
-    }
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int e = 0; e < XP; ++e) {
+        a0[e] += p0[u][e] * rv[u][e];
+        a1[e] += p1[u][e] * rv[u][e];
+      }
   }
   // per-(row group, parity, x) partials -> shared, summed over row groups in order
-  const int XLX = 2 * XL;  // rsh: [RG][2][XLX] then totals [2][XLX]
-  rsh[(rg * 2 + 0) * XLX + xo] = a0;
-  rsh[(rg * 2 + 1) * XLX + xo] = a1;
-  rsh[(rg * 2 + 0) * XLX + XL + xo] = b0;
-  rsh[(rg * 2 + 1) * XLX + XL + xo] = b1;
+  const int XLX = XP * XL;  // rsh: [RG][2][XLX] then totals [2][XLX]
+#pragma unroll
+  for (int e = 0; e < XP; ++e) {
+    rsh[(rg * 2 + 0) * XLX + XL * e + xo] = a0[e];
+    rsh[(rg * 2 + 1) * XLX + XL * e + xo] = a1[e];
+  }
   __syncthreads();
   for (int t = threadIdx.x; t < 2 * XLX; t += blockDim.x) {
     double v = 0.0;
@@ -684,23 +697,31 @@ __device__ __forceinline__ void restrict_row_body(const LevelView& L, const doub
     support_range(Jx, L.b0, nx, L.nb0, x0, x1);
     const double* tp = tot + (Jx & 1) * XLX;
     double v = 0.0;
-    for (int x = x0; x < x1; ++x) v += tp[x < 256 ? x : XL + (x - 256)];
+    for (int x = x0; x < x1; ++x) v += tp[x];
     if (!done) rc[Jx + L.nb0 * (Jy + L.nb1 * Jz)] = v;
   }
 }
 
+template <int XP>
 __global__ void __launch_bounds__(RR2_THREADS) k_restrict_cart(LevelView L,
                                                                const double* __restrict__ r,
                                                                double* __restrict__ rc,
                                                                const IterState* st) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ double rsh[];
-  restrict_row_body<false>(L, r, rc, blockIdx.x, rsh, is_done(st));
+  restrict_row_body<XP>(L, r, rc, blockIdx.x, rsh, is_done(st));
+}
+
+static inline int restrict_xp(int nx) {
+  return nx <= 256 ? 1 : (nx <= 512 ? 2 : (nx <= 1024 ? 4 : 8));
 }
 
 static inline size_t restrict_rows_smem(int nx) {
-  const int XL = nx <= 32 ? 32 : (nx <= 64 ? 64 : (nx <= 128 ? 128 : 256));
+  const int XP = restrict_xp(nx);
+  const int XL = XP > 1 ? 256 : (nx <= 32 ? 32 : (nx <= 64 ? 64 : (nx <= 128 ? 128 : 256)));
   const int RG = RR2_THREADS / XL;
-  return (size_t)(RG + 1) * 2 * 2 * XL * sizeof(double);
+  return (size_t)(RG + 1) * 2 * XP * XL * sizeof(double);
 }
 
 // a9 (Cartesian level): x += P x_c, one thread per cell: the six per-axis block
@@ -711,6 +732,8 @@ static inline size_t restrict_rows_smem(int nx) {
 __global__ void __launch_bounds__(CT) k_prolong_cart(LevelView L, double* __restrict__ x,
                                                      const double* __restrict__ xc,
                                                      const IterState* st) {
+  pdl_wait();
+  pdl_trigger();
   const bool done = is_done(st);
   const int N = L.g.nxy * L.g.nz;
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
@@ -1174,6 +1197,11 @@ static msb_status enqueue_stage(msb_ctx ctx, msb_solver s, msb_level L, const do
   // (kernels that have not yet seen `done` then do harmless work).
   const bool side = s->levels.size() == 1 && s->nu == 1 && !s->post && L->kind == 0 &&
                     s->smoother == 0;
+  // programmatic dependent launches along the Cartesian / dense-coarse / Jacobi chain
+  // (every kernel on it starts with pdl_wait(): no read of a predecessor's output before
+  // that grid has completed)
+  static const bool no_pdl = getenv("MSB_NO_PDL") != nullptr;  // A/B during development
+  const bool pdl = !no_pdl && L->kind == 0 && L->co.kind == 0 && s->smoother == 0;
   auto fin = [&](unsigned np) -> msb_status {  // np = blocks of the kernel that wrote partials
     if (side) {
       if (!s->side_stream) {
@@ -1217,8 +1245,8 @@ static msb_status enqueue_stage(msb_ctx ctx, msb_solver s, msb_level L, const do
   auto jac = [&]() -> msb_status {
     if (s->smoother == 1) return ilu();
     for (int v = 0; v < s->nu; ++v) {
-      k_jacobi<<<g4, CT, 0, st>>>(S, s->xbuf[cur], s->xbuf[cur ^ 1], b, s->omega_s, first ? 1 : 0,
-                                 s->partials, s->st);
+      MSB_CUDA_TRY(ctx, launch_k(pdl, k_jacobi, g4, CT, 0, st, S, s->xbuf[cur], s->xbuf[cur ^ 1], b,
+                                 s->omega_s, first ? 1 : 0, s->partials, s->st));
       MSB_LAUNCH_CHECK(ctx);
       if (first) {
         msb_status rc = fin(g4);
@@ -1231,20 +1259,46 @@ static msb_status enqueue_stage(msb_ctx ctx, msb_solver s, msb_level L, const do
   };
   auto corr = [&]() -> msb_status {
     if (L->kind == 0) {
-      k_residual<<<g4, CT, 0, st>>>(S, s->xbuf[cur], b, s->r, first ? 1 : 0, s->partials, s->st);
+      MSB_CUDA_TRY(ctx, launch_k(pdl, k_residual, g4, CT, 0, st, S, s->xbuf[cur], b, s->r,
+                                 first ? 1 : 0, s->partials, s->st));
       MSB_LAUNCH_CHECK(ctx);
       if (first) {
         msb_status rc = fin(g4);
         if (rc) return rc;
       }
       first = false;
-      if (op->nx > 512)
-        return set_error(ctx, MSB_EINVAL, "Cartesian restriction supports nx <= 512 (nx=%d)", op->nx);
-      k_restrict_cart<<<L->nb[1] * L->nb[2], RR2_THREADS, restrict_rows_smem(op->nx), st>>>(
-          V, s->r, s->rc, s->st);
+      if (op->nx > 2048)
+        return set_error(ctx, MSB_EINVAL, "Cartesian restriction supports nx <= 2048 (nx=%d)", op->nx);
+      {
+        const int xp = restrict_xp(op->nx);
+        const size_t smem = restrict_rows_smem(op->nx);
+        const unsigned gr = (unsigned)(L->nb[1] * L->nb[2]);
+        if (xp == 1)
+          MSB_CUDA_TRY(ctx, launch_k(pdl, k_restrict_cart<1>, gr, RR2_THREADS, smem, st, V, s->r,
+                                     s->rc, s->st));
+        else if (xp == 2)
+          MSB_CUDA_TRY(ctx, launch_k(pdl, k_restrict_cart<2>, gr, RR2_THREADS, smem, st, V, s->r,
+                                     s->rc, s->st));
+        else if (xp == 4) {
+          static bool attr = false;
+          if (!attr) {
+            MSB_CUDA_TRY(ctx, cudaFuncSetAttribute(k_restrict_cart<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            attr = true;
+          }
+          k_restrict_cart<4><<<gr, RR2_THREADS, smem, st>>>(V, s->r, s->rc, s->st);
+        } else {
+          static bool attr = false;
+          if (!attr) {
+            MSB_CUDA_TRY(ctx, cudaFuncSetAttribute(k_restrict_cart<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            attr = true;
+          }
+          k_restrict_cart<8><<<gr, RR2_THREADS, smem, st>>>(V, s->r, s->rc, s->st);
+        }
+      }
       MSB_LAUNCH_CHECK(ctx);
-      coarse_solve(ctx, L->co, s->rc, s->xc, &s->st->done);
-      k_prolong_cart<<<g, CT, 0, st>>>(V, s->xbuf[cur], s->xc, s->st);
+      coarse_solve(ctx, L->co, s->rc, s->xc, &s->st->done, pdl);
+      MSB_CUDA_TRY(ctx, launch_k(pdl && L->co.kind == 0, k_prolong_cart, g, CT, 0, st, V,
+                                 s->xbuf[cur], s->xc, s->st));
       MSB_LAUNCH_CHECK(ctx);
       return MSB_OK;
     }

@@ -1151,7 +1151,8 @@ def test_constant_level_import_assembles_imported_values(ctx):
 
 def test_inconsistent_compartment_rejected(ctx):
     """Sealing faces (multiplier 0) that cut off a compartment without the gauge cell make
-    A singular: msb_solver_create returns MSB_EINCONSISTENT."""
+    A singular: msb_coarse_assemble (and msb_solver_create) return MSB_EINCONSISTENT
+    (SPEC.md:79 "pre: A nonsingular")."""
     from paper_2001_01624_b200 import Level, Solver
     from paper_2001_01624_b200.api import MsbError
     from paper_2001_01624_b200.pipeline import build_operator
@@ -1162,10 +1163,9 @@ def test_inconsistent_compartment_rejected(ctx):
     prob.mult_x = mx.ravel()
     op = build_operator(ctx, prob)
     lev = Level.cartesian(ctx, op, prob.block)
-    lev.smooth(op, 5, prob.omega, -1.0)
-    lev.assemble(op)
+    lev.smooth(op, 5, prob.omega, -1.0)  # A_T's compartments smooth independently: fine
     with pytest.raises(MsbError, match="EINCONSISTENT"):
-        Solver(ctx, op, [lev], prob.omega_s, prob.nu, prob.post_smooth)
+        lev.assemble(op)
     mx[:, 3, 7] = 1.0  # one open face reconnects the compartments
     prob.mult_x = mx.ravel()
     op2 = build_operator(ctx, prob)
