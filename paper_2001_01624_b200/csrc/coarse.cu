@@ -477,16 +477,12 @@ constexpr int SYMV_T = 256;  // threads per tile: 8 double2 of the tile per thre
 __global__ void __launch_bounds__(SYMV_T) k_symv_tiles(const double* __restrict__ Xp, int M,
                                                        const double* __restrict__ rc,
                                                        double* __restrict__ part) {
-  pdl_wait();
-  pdl_trigger();
   symv_tile_body<false>(Xp, M, rc, part, blockIdx.x);
 }
 
 __global__ void __launch_bounds__(16 * ST) k_symv_reduce(const double* __restrict__ part, int M,
                                                         int ntb, double* __restrict__ xc,
                                                         const int* done) {
-  pdl_wait();
-  pdl_trigger();
   const bool skip = done && *(volatile const int*)done;
   symv_reduce_body<false>(part, M, ntb, xc, blockIdx.x, skip);
 }
@@ -522,13 +518,12 @@ void symv_batched(msb_ctx ctx, const SymvTile* td, int ntile, const SymvRow* rd,
   count_launch();
 }
 
-void coarse_solve(msb_ctx ctx, const Coarse& co, const double* rc, double* xc, const int* done,
-                  bool pdl) {
+void coarse_solve(msb_ctx ctx, const Coarse& co, const double* rc, double* xc, const int* done) {
   if (co.kind == 1) {
     coarse_schur_solve(ctx, co, rc, xc, done);
     return;
   }
-  coarse_solve_dense(ctx, co, rc, xc, done, pdl);
+  coarse_solve_dense(ctx, co, rc, xc, done);
 }
 
 msb_status coarse_pack_symmetric(msb_ctx ctx, Coarse& co) {
@@ -549,10 +544,10 @@ msb_status coarse_pack_symmetric(msb_ctx ctx, Coarse& co) {
 }
 
 void coarse_solve_dense(msb_ctx ctx, const Coarse& co, const double* rc, double* xc,
-                        const int* done, bool pdl) {
+                        const int* done) {
   const int64_t nt = (int64_t)co.ntb * (co.ntb + 1) / 2;
-  launch_k(pdl, k_symv_tiles, (unsigned)nt, SYMV_T, 0, ctx->stream, co.Xp, co.M, rc, co.part);
-  launch_k(pdl, k_symv_reduce, co.ntb, 16 * ST, 0, ctx->stream, co.part, co.M, co.ntb, xc, done);
+  k_symv_tiles<<<(unsigned)nt, SYMV_T, 0, ctx->stream>>>(co.Xp, co.M, rc, co.part);
+  k_symv_reduce<<<co.ntb, 16 * ST, 0, ctx->stream>>>(co.part, co.M, co.ntb, xc, done);
   count_launch();
   count_launch();
 }

@@ -67,7 +67,7 @@ __global__ void __launch_bounds__(256) k_dgemm(int m, int n, int K, double alpha
                                                const double* __restrict__ A, int64_t lda,
                                                const double* __restrict__ B, int64_t ldb,
                                                double beta, double* __restrict__ C, int64_t ldc,
-                                               int lower, int kmode) {
+                                               int lower, int kmode, double* __restrict__ ws) {
   const int bi = blockIdx.y, bj = blockIdx.x;
   if (lower && bi < bj) return;
   extern __shared__ double dsm[];
@@ -78,7 +78,14 @@ __global__ void __launch_bounds__(256) k_dgemm(int m, int n, int K, double alpha
   const int i0 = bi * DG_T, j0 = bj * DG_T;
   int kbeg = kmode == 2 ? max(i0, j0) : (kmode == 1 ? i0 : 0);
   kbeg = min(kbeg, K);
-  const int nk = (K - kbeg + DG_K - 1) / DG_K;
+  int nk = (K - kbeg + DG_K - 1) / DG_K;
+  if (gridDim.z > 1) {  // split K: this CTA takes k-steps [z nk / S, (z + 1) nk / S)
+    const int z = blockIdx.z, S = gridDim.z;
+    const int s0 = (int)((int64_t)nk * z / S), s1 = (int)((int64_t)nk * (z + 1) / S);
+    kbeg += s0 * DG_K;
+    nk = s1 - s0;
+  }
+  const int kend = min(K, kbeg + nk * DG_K);
   // stage loader: 2048 elements of each operand, 8 per thread
   auto load = [&](int s, int kk) {
     double* as = As + s * DG_STAGE;
@@ -89,23 +96,23 @@ __global__ void __launch_bounds__(256) k_dgemm(int m, int n, int K, double alpha
       if (TA) {  // memory rows t, contiguous i: smem [k][m]
         const int t = idx >> 7, i = idx & 127;
         const int gi = i0 + i, gt = kk + t;
-        const bool ok = gi < m && gt < K;
+        const bool ok = gi < m && gt < kend;
         cp_async8(as + t * (DG_T + DG_PAD) + i, ok ? A + (int64_t)gt * lda + gi : A, ok);
       } else {   // memory rows i, contiguous t: smem [m][k]
         const int i = idx >> 4, t = idx & 15;
         const int gi = i0 + i, gt = kk + t;
-        const bool ok = gi < m && gt < K;
+        const bool ok = gi < m && gt < kend;
         cp_async8(as + i * (DG_K + DG_PAD) + t, ok ? A + (int64_t)gi * lda + gt : A, ok);
       }
       if (TB) {  // memory rows j, contiguous t: smem [n][k]
         const int j = idx >> 4, t = idx & 15;
         const int gj = j0 + j, gt = kk + t;
-        const bool ok = gj < n && gt < K;
+        const bool ok = gj < n && gt < kend;
         cp_async8(bs + j * (DG_K + DG_PAD) + t, ok ? B + (int64_t)gj * ldb + gt : B, ok);
       } else {   // memory rows t, contiguous j: smem [k][n]
         const int t = idx >> 7, j = idx & 127;
         const int gj = j0 + j, gt = kk + t;
-        const bool ok = gj < n && gt < K;
+        const bool ok = gj < n && gt < kend;
         cp_async8(bs + t * (DG_T + DG_PAD) + j, ok ? B + (int64_t)gt * ldb + gj : B, ok);
       }
     }
@@ -151,6 +158,17 @@ __global__ void __launch_bounds__(256) k_dgemm(int m, int n, int K, double alpha
     }
   }
   cp_async_wait<0>();
+  if (ws) {  // split K: the raw partial tile, summed in split order by k_dgemm_splitk_sum
+    double* wt = ws + (((int64_t)blockIdx.z * gridDim.y + bi) * gridDim.x + bj) * DG_T * DG_T;
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        const int li = wm * 64 + u * 8 + fr, lj = wn * 32 + v * 8 + 2 * fc;
+        *reinterpret_cast<double2*>(wt + li * DG_T + lj) = make_double2(acc[u][v][0], acc[u][v][1]);
+      }
+    return;
+  }
 #pragma unroll
   for (int u = 0; u < 8; ++u) {
     const int i = i0 + wm * 64 + u * 8 + fr;
@@ -168,6 +186,25 @@ __global__ void __launch_bounds__(256) k_dgemm(int m, int n, int K, double alpha
   }
 }
 
+// C = alpha * (sum over the S split partials, in split order) + beta * C
+__global__ void k_dgemm_splitk_sum(const double* __restrict__ ws, int S, int gx, int gy, int m,
+                                   int n, double alpha, double beta, double* __restrict__ C,
+                                   int64_t ldc, int lower) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (int64_t)m * n) return;
+  const int i = (int)(e / n), j = (int)(e - (int64_t)i * n);
+  const int bi = i / DG_T, bj = j / DG_T;
+  if (lower && bi < bj) return;
+  const int64_t tile = (int64_t)bi * gx + bj, off = (i - bi * DG_T) * DG_T + (j - bj * DG_T);
+  double v = 0.0;
+  for (int z = 0; z < S; ++z) v += ws[((int64_t)z * gy * gx + tile) * DG_T * DG_T + off];
+  double* c = C + (int64_t)i * ldc + j;
+  *c = beta == 0.0 ? alpha * v : fma(alpha, v, beta * *c);
+}
+
+// One CTA per SM (the 101 KB ring and 64 fp64 accumulators per thread) and ~70 fp64 FMA
+// per clock per SM: a product with few output tiles (the narrow panels of the recursion)
+// splits its K range over more CTAs, partial tiles to a workspace summed in a fixed order.
 template <bool TA, bool TB>
 static msb_status gemm(msb_ctx ctx, int m, int n, int K, double alpha, const double* A, int64_t lda,
                        const double* B, int64_t ldb, double beta, double* C, int64_t ldc,
@@ -179,10 +216,33 @@ static msb_status gemm(msb_ctx ctx, int m, int n, int K, double alpha, const dou
                                            (int)DG_SMEM));
     attr = true;
   }
-  dim3 g((n + DG_T - 1) / DG_T, (m + DG_T - 1) / DG_T);
+  const int gx = (n + DG_T - 1) / DG_T, gy = (m + DG_T - 1) / DG_T;
+  const int tiles = lower ? (gx * (gx + 1)) / 2 + (gy - gx) * gx : gx * gy;
+  int S = 1;
+  if (kmode == 0 && K >= 8 * DG_K && tiles < 2 * ctx->sm_count) {
+    S = std::min((2 * ctx->sm_count + tiles - 1) / tiles, K / (4 * DG_K));
+    S = std::max(1, std::min(S, 32));
+  }
+  double* ws = nullptr;
+  if (S > 1) {
+    const size_t need = (size_t)S * gx * gy * DG_T * DG_T;
+    if (ctx->gemm_ws_cap < need) {
+      dfree(ctx, ctx->gemm_ws);
+      ctx->gemm_ws = dalloc_n<double>(ctx, need);
+      ctx->gemm_ws_cap = ctx->gemm_ws ? need : 0;
+    }
+    ws = ctx->gemm_ws;
+    if (!ws) S = 1;
+  }
+  dim3 g(gx, gy, S);
   k_dgemm<TA, TB><<<g, 256, DG_SMEM, ctx->stream>>>(m, n, K, alpha, A, lda, B, ldb, beta, C, ldc,
-                                                     lower ? 1 : 0, kmode);
+                                                     lower ? 1 : 0, kmode, S > 1 ? ws : nullptr);
   MSB_LAUNCH_CHECK(ctx);
+  if (S > 1) {
+    k_dgemm_splitk_sum<<<grid_for((int64_t)m * n, 256), 256, 0, ctx->stream>>>(
+        ws, S, gx, gy, m, n, alpha, beta, C, ldc, lower ? 1 : 0);
+    MSB_LAUNCH_CHECK(ctx);
+  }
   return MSB_OK;
 }
 
@@ -195,64 +255,61 @@ msb_status dgemm(msb_ctx ctx, bool ta, bool tb, int m, int n, int K, double alph
 }
 
 // Leaf: Cholesky of the n x n (n <= LEAF) block at A (ld) in place (lower; upper zeroed)
-// and its triangular inverse into W (ld, lower; upper zeroed).  One CTA, LEAF^2 smem.
-__global__ void __launch_bounds__(1024) k_chol_inv_leaf(double* __restrict__ A, int64_t ld, int n,
-                                                        double* __restrict__ W,
-                                                        const unsigned long long* amax_bits,
-                                                        int* __restrict__ singular) {
-  static_assert(LEAF == 64, "thread-element map assumes 64 x 64 leaves and 1024 threads");
+// and its triangular inverse into W (ld, lower; upper zeroed).  One CTA of 256 threads,
+// thread (r = tid / 4, q = tid % 4) owns row r's columns c = q (mod 4) of both L and W.
+// Right-looking Cholesky fused with the forward substitution W = L^{-1}, with the scaling
+// of column j of L and row j of W deferred: at step j every update uses the scaled values
+// L_rj = a_rj / l_jj and W_jc = w_jc / l_jj formed on the fly from the stored reciprocal,
+//   a_rc -= L_rj L_cj  (j < c <= r),   w_rc -= L_rj W_jc  (c <= j < r),
+// and nothing read in step j is written in step j, so ONE barrier per step suffices: the
+// owner of a_{j+1,j+1} takes the next pivot right after its last update.  The scaling is
+// applied once at the end.
+__global__ void __launch_bounds__(256) k_chol_inv_leaf(double* __restrict__ A, int64_t ld, int n,
+                                                       double* __restrict__ W,
+                                                       const unsigned long long* amax_bits,
+                                                       int* __restrict__ singular) {
+  static_assert(LEAF == 64, "thread-element map assumes 64 x 64 leaves and 256 threads");
   extern __shared__ double lsm[];
   double (*a)[LEAF + 1] = reinterpret_cast<double (*)[LEAF + 1]>(lsm);
   double (*w)[LEAF + 1] = reinterpret_cast<double (*)[LEAF + 1]>(lsm + LEAF * (LEAF + 1));
+  double* rinv = lsm + 2 * LEAF * (LEAF + 1);  // [LEAF] 1 / l_jj
   const int tid = threadIdx.x;
   for (int e = tid; e < LEAF * LEAF; e += blockDim.x) {
     const int r = e >> 6, c = e & 63;
     a[r][c] = (r < n && c < n) ? A[(int64_t)r * ld + c] : 0.0;
     w[r][c] = (r == c) ? 1.0 : 0.0;
   }
-  __syncthreads();
   const double amax = __longlong_as_double((long long)*amax_bits);
-  // Right-looking Cholesky fused with the forward substitution W = L^{-1}: at step j the
-  // pivot is taken, column j of L is scaled and row j of W finished (w[j][c] / L_jj), then
-  // every later row receives its rank-1 updates of L and of W (w[r][c] -= L_rj W_jc, c <= j)
-  // in parallel — the same operations in the same order as a column-by-column forward
-  // substitution, so the result is unchanged, with 3 barriers per step instead of an
-  // O(n^2) serial loop per column.
+  auto pivot = [&](int j) {  // l_jj = sqrt(a_jj) (pivot test SPEC.md:81), its reciprocal
+    double d = a[j][j];
+    if (!(d > 1e-14 * amax)) {
+      atomicExch(singular, 1);
+      d = 1.0;
+    }
+    const double l = sqrt(d);
+    a[j][j] = l;
+    rinv[j] = 1.0 / l;
+  };
+  __syncthreads();
+  if (tid == 0 && n > 0) pivot(0);
+  __syncthreads();
+  const int r = tid >> 2, q = tid & 3;
   for (int j = 0; j < n; ++j) {
-    if (tid == 0) {
-      double d = a[j][j];
-      if (!(d > 1e-14 * amax)) {
-        atomicExch(singular, 1);
-        d = 1.0;
-      }
-      a[j][j] = sqrt(d);
-    }
-    __syncthreads();
-    const double ljj = a[j][j];
-    if (tid < LEAF) {
-      if (tid > j && tid < n) a[tid][j] /= ljj;
-    } else if (tid < 2 * LEAF) {
-      const int c = tid - LEAF;
-      if (c <= j) w[j][c] = w[j][c] / ljj;
-    }
-    __syncthreads();
-#pragma unroll
-    for (int u = 0; u < (LEAF * LEAF) / 1024; ++u) {
-      const int e = tid + 1024 * u, r = e >> 6, c = e & 63;
-      if (r > j && r < n) {
-        if (c > j) {
-          if (c <= r) a[r][c] -= a[r][j] * a[c][j];
-        } else {
-          w[r][c] -= a[r][j] * w[j][c];
-        }
-      }
+    if (r > j && r < n) {
+      const double ri = rinv[j];
+      const double lrj = a[r][j] * ri;
+      int c = j + 1 + ((q - (j + 1)) & 3);  // first c > j with c = q (mod 4)
+      for (; c <= r; c += 4) a[r][c] -= lrj * (a[c][j] * ri);
+      for (int cc = q; cc <= j; cc += 4) w[r][cc] -= lrj * (w[j][cc] * ri);
+      if (r == j + 1 && q == (r & 3)) pivot(r);  // a_rr received its last update above
     }
     __syncthreads();
   }
   for (int e = tid; e < n * n; e += blockDim.x) {
-    const int r = e / n, c = e % n;
-    A[(int64_t)r * ld + c] = c <= r ? a[r][c] : 0.0;
-    W[(int64_t)r * ld + c] = c <= r ? w[r][c] : 0.0;
+    const int rr = e / n, c = e % n;
+    // L_rc = a_rc / l_cc below the diagonal, W_rc = w_rc / l_rr (row r of W scaled at step r)
+    A[(int64_t)rr * ld + c] = c < rr ? a[rr][c] * rinv[c] : (c == rr ? a[rr][rr] : 0.0);
+    W[(int64_t)rr * ld + c] = c <= rr ? w[rr][c] * rinv[rr] : 0.0;
   }
 }
 
@@ -303,14 +360,14 @@ static msb_status rtrsm(msb_ctx ctx, double* B, double* X, int m, int n, const d
 static msb_status chol_inv(msb_ctx ctx, double* F, double* Wb, int64_t ld, int n,
                            const unsigned long long* amax, int* sing) {
   if (n <= LEAF) {
-    constexpr size_t smem = 2 * LEAF * (LEAF + 1) * sizeof(double);
+    constexpr size_t smem = (2 * LEAF * (LEAF + 1) + LEAF) * sizeof(double);
     static bool attr = false;
     if (!attr) {
       MSB_CUDA_TRY(ctx, cudaFuncSetAttribute(k_chol_inv_leaf, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)smem));
       attr = true;
     }
-    k_chol_inv_leaf<<<1, 1024, smem, ctx->stream>>>(F, ld, n, Wb, amax, sing);
+    k_chol_inv_leaf<<<1, 256, smem, ctx->stream>>>(F, ld, n, Wb, amax, sing);
     MSB_LAUNCH_CHECK(ctx);
     return MSB_OK;
   }

@@ -98,47 +98,60 @@ __global__ void k_scatter_sub(double* __restrict__ C, int ldc, const int32_t* __
   C[(int64_t)idx[i] * ldc + idx[j]] -= G[e];
 }
 
-// t_q = r_c[s_q] - sum over s_q's domain neighbours K of A_c(s_q, K) y[pos(K)]
-__global__ void k_schur_t(const double* __restrict__ Aell, int n0, int n1, int n2,
-                          const int32_t* __restrict__ sep_nodes, int nS,
-                          const int32_t* __restrict__ node_pos, const double* __restrict__ rc,
-                          const double* __restrict__ y, double* __restrict__ t) {
-  const int q = blockIdx.x * blockDim.x + threadIdx.x;
-  if (q >= nS) return;
+// t_q = r_c[s_q] - sum over s_q's domain neighbours K of A_c(s_q, K) y[pos(K)]: one warp
+// per separator node, lanes over the 125 stencil slots (coalesced row of A_c, the
+// neighbour loads of all slots in flight together), then a fixed shuffle tree
+__global__ void __launch_bounds__(256) k_schur_t(const double* __restrict__ Aell, int n0, int n1,
+                                                 int n2, const int32_t* __restrict__ sep_nodes,
+                                                 int nS, const int32_t* __restrict__ node_pos,
+                                                 const double* __restrict__ rc,
+                                                 const double* __restrict__ y,
+                                                 double* __restrict__ t) {
+  const int q = (int)((blockIdx.x * (unsigned)blockDim.x + threadIdx.x) >> 5);
+  const int lane = threadIdx.x & 31;
+  if (q >= nS) return;  // warp-uniform
   const int s = sep_nodes[q];
-  double v = rc[s];
-  for (int d = 0; d < SW; ++d) {
-    const int K = box_nb(s, d, n0, n1, n2);
-    if (K < 0) continue;
-    const int p = node_pos[K];
-    if (p >= 0) v -= Aell[(int64_t)s * SW + d] * y[p];
+  double v = 0.0;
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int d = lane + 32 * u;
+    const int K = d < SW ? box_nb(s, d, n0, n1, n2) : -1;
+    const int p = K >= 0 ? node_pos[K] : -1;
+    if (p >= 0) v = fma(Aell[(int64_t)s * SW + d], y[p], v);
   }
-  t[q] = v;
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if (lane == 0) t[q] = rc[s] - v;
 }
 
-// u_p = r_c[J_p] - sum over J_p's separator neighbours K of A_c(J_p, K) x_S[q(K)];
-// threads past nD write the separator part of x_c (x_S scattered), done-guarded
-__global__ void k_schur_u(const double* __restrict__ Aell, int n0, int n1, int n2,
-                          const int32_t* __restrict__ dom_nodes, int nD,
-                          const int32_t* __restrict__ sep_nodes, int nS,
-                          const int32_t* __restrict__ node_pos, const double* __restrict__ rc,
-                          const double* __restrict__ xs, double* __restrict__ u,
-                          double* __restrict__ xc, const int* done) {
-  const int p = blockIdx.x * blockDim.x + threadIdx.x;
-  if (p < nD) {
-    const int J = dom_nodes[p];
-    double v = rc[J];
-    for (int d = 0; d < SW; ++d) {
-      const int K = box_nb(J, d, n0, n1, n2);
-      if (K < 0) continue;
-      const int q = node_pos[K];
-      if (q < 0) v -= Aell[(int64_t)J * SW + d] * xs[-q - 1];
+// u_p = r_c[J_p] - sum over J_p's separator neighbours K of A_c(J_p, K) x_S[q(K)] (one warp
+// per domain node, as k_schur_t); warps past nD write the separator part of x_c (x_S
+// scattered), done-guarded
+__global__ void __launch_bounds__(256) k_schur_u(const double* __restrict__ Aell, int n0, int n1,
+                                                 int n2, const int32_t* __restrict__ dom_nodes,
+                                                 int nD, const int32_t* __restrict__ sep_nodes,
+                                                 int nS, const int32_t* __restrict__ node_pos,
+                                                 const double* __restrict__ rc,
+                                                 const double* __restrict__ xs,
+                                                 double* __restrict__ u, double* __restrict__ xc,
+                                                 const int* done) {
+  const int w = (int)((blockIdx.x * (unsigned)blockDim.x + threadIdx.x) >> 5);
+  const int lane = threadIdx.x & 31;
+  if (w < nD) {
+    const int J = dom_nodes[w];
+    double v = 0.0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int d = lane + 32 * k;
+      const int K = d < SW ? box_nb(J, d, n0, n1, n2) : -1;
+      const int q = K >= 0 ? node_pos[K] : 0;
+      if (q < 0) v = fma(Aell[(int64_t)J * SW + d], xs[-q - 1], v);
     }
-    u[p] = v;
-  } else if (p < nD + nS) {
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) u[w] = rc[J] - v;
+  } else {
     const bool skip = done && *(volatile const int*)done;
-    const int q = p - nD;
-    if (!skip) xc[sep_nodes[q]] = xs[q];
+    const int q = (w - nD) * 32 + lane;  // 32 separator entries per trailing warp
+    if (q < nS && !skip) xc[sep_nodes[q]] = xs[q];
   }
 }
 
@@ -464,14 +477,16 @@ void coarse_schur_solve(msb_ctx ctx, const Coarse& co, const double* rc, double*
   // y_d = A_dd^{-1} r_d (r_c read through the domain node map)
   symv_batched(ctx, S->td, S->ntd, S->rd, S->nrd, S->Xd, rc, S->dom_nodes, S->partd, S->y, nullptr,
                nullptr);
-  k_schur_t<<<grid_for(S->nS, 128), 128, 0, st>>>(co.Aell, n0, n1, n2, S->sep_nodes, S->nS,
-                                                  S->node_pos, rc, S->y, S->t);
+  k_schur_t<<<grid_for((int64_t)S->nS * 32, 256), 256, 0, st>>>(co.Aell, n0, n1, n2, S->sep_nodes,
+                                                                 S->nS, S->node_pos, rc, S->y,
+                                                                 S->t);
   count_launch();
   symv_batched(ctx, S->tc, S->ntc, S->rcd, S->nrc, S->C.Xp, S->t, nullptr, S->C.part, S->xs,
                nullptr, nullptr);
-  k_schur_u<<<grid_for(S->nD + S->nS, 128), 128, 0, st>>>(co.Aell, n0, n1, n2, S->dom_nodes, S->nD,
-                                                          S->sep_nodes, S->nS, S->node_pos, rc,
-                                                          S->xs, S->u, xc, done);
+  const int64_t wu = (int64_t)S->nD + (S->nS + 31) / 32;  // warps
+  k_schur_u<<<grid_for(wu * 32, 256), 256, 0, st>>>(co.Aell, n0, n1, n2, S->dom_nodes, S->nD,
+                                                     S->sep_nodes, S->nS, S->node_pos, rc, S->xs,
+                                                     S->u, xc, done);
   count_launch();
   symv_batched(ctx, S->td, S->ntd, S->rd, S->nrd, S->Xd, S->u, nullptr, S->partd, xc, S->dom_nodes,
                done);

@@ -226,6 +226,7 @@ msb_status msb_ctx_destroy(msb_ctx ctx) {
   if (!ctx) return MSB_EINVAL;
   if (ctx->pinned) cudaFreeHost(ctx->pinned);
   msb::dfree(ctx, ctx->scan_scr);
+  msb::dfree(ctx, ctx->gemm_ws);
   delete ctx;
   return MSB_OK;
 }

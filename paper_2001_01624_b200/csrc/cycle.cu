@@ -166,8 +166,6 @@ __global__ void __launch_bounds__(CT) k_jacobi(StencilT S, const double* __restr
                                                const double* __restrict__ b, double omega,
                                                int first, double* __restrict__ partials,
                                                const IterState* st) {
-  pdl_wait();
-  pdl_trigger();
   const bool done = is_done(st);
   const int N = S.g.nxy * S.g.nz;
   const int c0 = blockIdx.x * (CT * CPT) + threadIdx.x;
@@ -565,8 +563,6 @@ __global__ void __launch_bounds__(CT) k_residual(StencilT S, const double* __res
                                                  double* __restrict__ r, int first,
                                                  double* __restrict__ partials,
                                                  const IterState* st) {
-  pdl_wait();
-  pdl_trigger();
   const bool done = is_done(st);
   const int N = S.g.nxy * S.g.nz;
   const int c0 = blockIdx.x * (CT * CPT) + threadIdx.x;
@@ -707,8 +703,6 @@ __global__ void __launch_bounds__(RR2_THREADS) k_restrict_cart(LevelView L,
                                                                const double* __restrict__ r,
                                                                double* __restrict__ rc,
                                                                const IterState* st) {
-  pdl_wait();
-  pdl_trigger();
   extern __shared__ double rsh[];
   restrict_row_body<XP>(L, r, rc, blockIdx.x, rsh, is_done(st));
 }
@@ -732,8 +726,6 @@ static inline size_t restrict_rows_smem(int nx) {
 __global__ void __launch_bounds__(CT) k_prolong_cart(LevelView L, double* __restrict__ x,
                                                      const double* __restrict__ xc,
                                                      const IterState* st) {
-  pdl_wait();
-  pdl_trigger();
   const bool done = is_done(st);
   const int N = L.g.nxy * L.g.nz;
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
@@ -1197,11 +1189,7 @@ static msb_status enqueue_stage(msb_ctx ctx, msb_solver s, msb_level L, const do
   // (kernels that have not yet seen `done` then do harmless work).
   const bool side = s->levels.size() == 1 && s->nu == 1 && !s->post && L->kind == 0 &&
                     s->smoother == 0;
-  // programmatic dependent launches along the Cartesian / dense-coarse / Jacobi chain
-  // (every kernel on it starts with pdl_wait(): no read of a predecessor's output before
-  // that grid has completed)
-  static const bool no_pdl = getenv("MSB_NO_PDL") != nullptr;  // A/B during development
-  const bool pdl = !no_pdl && L->kind == 0 && L->co.kind == 0 && s->smoother == 0;
+
   auto fin = [&](unsigned np) -> msb_status {  // np = blocks of the kernel that wrote partials
     if (side) {
       if (!s->side_stream) {
@@ -1245,8 +1233,8 @@ static msb_status enqueue_stage(msb_ctx ctx, msb_solver s, msb_level L, const do
   auto jac = [&]() -> msb_status {
     if (s->smoother == 1) return ilu();
     for (int v = 0; v < s->nu; ++v) {
-      MSB_CUDA_TRY(ctx, launch_k(pdl, k_jacobi, g4, CT, 0, st, S, s->xbuf[cur], s->xbuf[cur ^ 1], b,
-                                 s->omega_s, first ? 1 : 0, s->partials, s->st));
+      k_jacobi<<<g4, CT, 0, st>>>(S, s->xbuf[cur], s->xbuf[cur ^ 1], b, s->omega_s, first ? 1 : 0,
+                                 s->partials, s->st);
       MSB_LAUNCH_CHECK(ctx);
       if (first) {
         msb_status rc = fin(g4);
@@ -1259,8 +1247,7 @@ static msb_status enqueue_stage(msb_ctx ctx, msb_solver s, msb_level L, const do
   };
   auto corr = [&]() -> msb_status {
     if (L->kind == 0) {
-      MSB_CUDA_TRY(ctx, launch_k(pdl, k_residual, g4, CT, 0, st, S, s->xbuf[cur], b, s->r,
-                                 first ? 1 : 0, s->partials, s->st));
+      k_residual<<<g4, CT, 0, st>>>(S, s->xbuf[cur], b, s->r, first ? 1 : 0, s->partials, s->st);
       MSB_LAUNCH_CHECK(ctx);
       if (first) {
         msb_status rc = fin(g4);
@@ -1273,12 +1260,8 @@ static msb_status enqueue_stage(msb_ctx ctx, msb_solver s, msb_level L, const do
         const int xp = restrict_xp(op->nx);
         const size_t smem = restrict_rows_smem(op->nx);
         const unsigned gr = (unsigned)(L->nb[1] * L->nb[2]);
-        if (xp == 1)
-          MSB_CUDA_TRY(ctx, launch_k(pdl, k_restrict_cart<1>, gr, RR2_THREADS, smem, st, V, s->r,
-                                     s->rc, s->st));
-        else if (xp == 2)
-          MSB_CUDA_TRY(ctx, launch_k(pdl, k_restrict_cart<2>, gr, RR2_THREADS, smem, st, V, s->r,
-                                     s->rc, s->st));
+        if (xp == 1) k_restrict_cart<1><<<gr, RR2_THREADS, smem, st>>>(V, s->r, s->rc, s->st);
+        else if (xp == 2) k_restrict_cart<2><<<gr, RR2_THREADS, smem, st>>>(V, s->r, s->rc, s->st);
         else if (xp == 4) {
           static bool attr = false;
           if (!attr) {
@@ -1296,9 +1279,8 @@ static msb_status enqueue_stage(msb_ctx ctx, msb_solver s, msb_level L, const do
         }
       }
       MSB_LAUNCH_CHECK(ctx);
-      coarse_solve(ctx, L->co, s->rc, s->xc, &s->st->done, pdl);
-      MSB_CUDA_TRY(ctx, launch_k(pdl && L->co.kind == 0, k_prolong_cart, g, CT, 0, st, V,
-                                 s->xbuf[cur], s->xc, s->st));
+      coarse_solve(ctx, L->co, s->rc, s->xc, &s->st->done);
+      k_prolong_cart<<<g, CT, 0, st>>>(V, s->xbuf[cur], s->xc, s->st);
       MSB_LAUNCH_CHECK(ctx);
       return MSB_OK;
     }
