@@ -286,9 +286,18 @@ __global__ void __launch_bounds__(256) k_chol_inv_leaf(double* __restrict__ A, i
       atomicExch(singular, 1);
       d = 1.0;
     }
-    const double l = sqrt(d);
-    a[j][j] = l;
-    rinv[j] = 1.0 / l;
+    // 1/sqrt(d) from the MUFU seed and two Newton steps, l = d / sqrt(d): both within an
+    // ulp (one dependent chain instead of a square root and a division)
+    double y;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(d));
+    double h = 0.5 * y;
+    double e = fma(-d * y, h, 0.5);
+    y = fma(y, e, y);
+    h = 0.5 * y;
+    e = fma(-d * y, h, 0.5);
+    y = fma(y, e, y);
+    a[j][j] = d * y;
+    rinv[j] = y;
   };
   __syncthreads();
   if (tid == 0 && n > 0) pivot(0);
@@ -298,9 +307,17 @@ __global__ void __launch_bounds__(256) k_chol_inv_leaf(double* __restrict__ A, i
     if (r > j && r < n) {
       const double ri = rinv[j];
       const double lrj = a[r][j] * ri;
-      int c = j + 1 + ((q - (j + 1)) & 3);  // first c > j with c = q (mod 4)
-      for (; c <= r; c += 4) a[r][c] -= lrj * (a[c][j] * ri);
-      for (int cc = q; cc <= j; cc += 4) w[r][cc] -= lrj * (w[j][cc] * ri);
+      // columns c = q + 4t: L part for j < c <= r, W part for c <= j (fixed trip count,
+      // predicated: all sixteen loads of a step are in flight together)
+#pragma unroll
+      for (int t = 0; t < LEAF / 4; ++t) {
+        const int c = q + 4 * t;
+        if (c > j) {
+          if (c <= r) a[r][c] -= lrj * (a[c][j] * ri);
+        } else {
+          w[r][c] -= lrj * (w[j][c] * ri);
+        }
+      }
       if (r == j + 1 && q == (r & 3)) pivot(r);  // a_rr received its last update above
     }
     __syncthreads();
@@ -334,8 +351,13 @@ __global__ void k_mirror_lower(double* __restrict__ X, int M) {
   if (i2 < M && j2 < M && j2 > i2) X[(int64_t)i2 * M + j2] = t[threadIdx.x][threadIdx.y];
 }
 
-// Split rule shared by chol_inv and rtrsm, so that rtrsm's leaves are exactly the
-// diagonal blocks whose inverses chol_inv's leaves stored in W.
+// Split rule shared by chol_inv and rtrsm, so that rtrsm's leaves are diagonal blocks
+// whose inverses chol_inv stored in W (the inverse factor of every recursion node is
+// complete when rtrsm runs: W_aa = (L_aa)^{-1} for a diagonal block of a lower-triangular
+// factor).  rtrsm stops at RT_LEAF: blocked TRSM with explicit inverses of <= 256-wide
+// diagonal blocks (LAPACK's dtrtri applies inverse blocks the same way), one product
+// per 256 columns instead of a recursion down to the 64-wide leaves.
+constexpr int RT_LEAF = 256;
 static inline int split1(int n) { return ((n / 2 + LEAF - 1) / LEAF) * LEAF; }
 
 // X = B L^{-T} (solve X L^T = B) for B: m x n (ld), L: n x n lower (ld), recursively:
@@ -346,7 +368,7 @@ static inline int split1(int n) { return ((n / 2 + LEAF - 1) / LEAF) * LEAF; }
 // full inverse of L11.
 static msb_status rtrsm(msb_ctx ctx, double* B, double* X, int m, int n, const double* L,
                         const double* W, int64_t ld) {
-  if (n <= LEAF) return gemm<false, true>(ctx, m, n, n, 1.0, B, ld, W, ld, 0.0, X, ld);
+  if (n <= RT_LEAF) return gemm<false, true>(ctx, m, n, n, 1.0, B, ld, W, ld, 0.0, X, ld);
   const int na = split1(n), nc = n - na;
   msb_status rc;
   if ((rc = rtrsm(ctx, B, X, m, na, L, W, ld))) return rc;

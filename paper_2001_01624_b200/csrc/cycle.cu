@@ -183,7 +183,7 @@ __global__ void __launch_bounds__(CT) k_jacobi(StencilT S, const double* __restr
   for (int u = 0; u < CPT; ++u) {
     const int c = c0 + u * CT;
     if (c < N) {
-      if (!done) xo[c] = xv[u] + omega * (r[u] / dA[u]);
+      if (!done) xo[c] = xv[u] + omega * div_rn(r[u], dA[u], rcp_fast(dA[u]));
       v += r[u] * r[u];
     }
   }

@@ -175,23 +175,6 @@ __device__ __forceinline__ double mask_d(double v, unsigned bit) {
   return __longlong_as_double(__double_as_longlong(v) & -(long long)bit);
 }
 
-// 1/x from the fp64 reciprocal seed (MUFU.RCP64H) and two Newton steps: accurate to
-// ~1 ulp (not correctly rounded) for the normal, positive D and row sums of the sweep;
-// div_rn below still returns the correctly rounded quotient from it.
-__device__ __forceinline__ double rcp_fast(double x) {
-  double r;
-  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
-  double e = fma(-x, r, 1.0);
-  r = fma(r, e, r);
-  e = fma(-x, r, 1.0);
-  return fma(r, e, r);
-}
-
-__device__ __forceinline__ double div_rn(double a, double b, double rb) {
-  double q = a * rb;
-  double e = fma(-q, b, a);
-  return fma(e, rb, q);
-}
 
 // One thread per cell owns all 8 slots: the per-cell work (five T reads, D, 1/D, the
 // twelve masked weights, the row sum, 1/sum, the store address) is done once (a

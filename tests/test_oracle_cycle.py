@@ -169,3 +169,38 @@ def test_cost_model_spec():
     r = [cost.cost_per_iteration(1, 2, 15, 4, nc) / cost.cost_per_iteration(1, 1, 15, 4, nc)
          for nc in (1, 2, 3, 4)]
     assert all(a > b for a, b in zip(r, r[1:]))         # PAPER.md:430 "diminishes"
+
+
+def test_dynamic_stage_wiring():
+    """Pins the dynamic-stage wiring of O11 (readings A12, A14, A15):
+    (i) no stage at k = 1; (ii) the k-th partition is dynamic_partition of
+    x_start(k) - x_start(k-1), the update over the PREVIOUS full iteration, with both
+    iterates re-run independently (fixed_iters = k-1, k-2); (iii) the stage runs after the
+    static levels — the iterate after 3 iterations equals a hand-sequenced chain of
+    cycle.stage() calls in that order.  An x_end(k) - x_start(k) reading, a start at k = 1,
+    or the dynamic stage placed first each fail one of these."""
+    p = make_problem(1, shape=(24, 24), block=(6, 6, 1), max_sweeps=40, dynamic=True)
+    r = pipeline.run(p, fixed_iters=3, record_dynamic=True)
+    A, q, levels = r["A"], r["q"], r["levels"]
+    recs = r["sol"]["dyn"]
+    assert [k for k, _, _ in recs] == [2, 3]                                     # (i)
+    xs = [np.zeros(p.N)] + [pipeline.run(p, fixed_iters=k, levels_info=r["levels_info"])
+                            ["sol"]["x"] for k in (1, 2)]
+    for k, part, M in recs:                                                      # (ii)
+        ref, Mr = partition.dynamic_partition(xs[k - 1] - xs[k - 2], p.nx, p.ny, p.nz,
+                                              p.dyn_edges, p.dyn_max_blocks)
+        assert Mr == M and np.array_equal(part, ref)
+    DA = A.diagonal()                                                            # (iii)
+    x = np.zeros(p.N)
+    starts = []
+    for k in (1, 2, 3):
+        starts.append(x.copy())
+        for lev in levels:
+            x = cycle.stage(A, DA, q, x, lev, p.omega_s, p.nu, p.post_smooth)
+        if k >= 2:
+            part, M = partition.dynamic_partition(starts[k - 1] - starts[k - 2], p.nx, p.ny,
+                                                  p.nz, p.dyn_edges, p.dyn_max_blocks)
+            dl = cycle.Level(cycle.constant_basis(part, M), A)
+            # the dynamic stage is built from x_start(k) but applied after the static ones
+            x = cycle.stage(A, DA, q, x, dl, p.omega_s, p.nu, p.post_smooth)
+    assert np.array_equal(x, r["sol"]["x"])

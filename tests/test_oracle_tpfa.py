@@ -93,3 +93,31 @@ def test_gauge_closed_form():
     assert abs(x[0]) < 1e-12 * np.abs(x).max()
     assert np.linalg.norm(A_T @ x - q) < 1e-11 * np.linalg.norm(q)
     assert A[0, 0] == 2 * A_T[0, 0]
+
+
+def test_anisotropic_per_axis_closed_form():
+    """Per-axis K selection (config 5 has Kz != Kx): heterogeneous kx, ky, kz fields with
+    distinct values per axis give T_f = 2 K_a,i K_a,l / (K_a,i + K_a,l) * A_a / Δ_a on each
+    axis from THAT axis' permeability — a kx-on-every-axis slip fails."""
+    nx, ny, nz = 3, 2, 2
+    n = nx * ny * nz
+    c = np.arange(n)
+    kx = 1.0 + c            # 1..12
+    ky = 100.0 + 10.0 * c   # distinct from kx everywhere
+    kz = 0.01 * (1.0 + c)
+    p = Problem("a", nx, ny, nz, kx, ky, kz, np.array([0]), np.array([0.0]), (1, 1, 1),
+                dx=1.0, dy=2.0, dz=4.0)
+    tr = tpfa.transmissibilities(p)
+    areas = (2.0 * 4.0, 1.0 * 4.0, 1.0 * 2.0)   # A_x = dy dz, A_y = dx dz, A_z = dx dy
+    dists = (1.0, 2.0, 4.0)
+    for a, (left, right, T) in enumerate(tr):
+        K = (kx, ky, kz)[a]
+        # harmonic mean of the two half-transmissibilities K A / (Δ / 2), written out
+        t_l = K[left] * areas[a] / (dists[a] / 2.0)
+        t_r = K[right] * areas[a] / (dists[a] / 2.0)
+        expect = 1.0 / (1.0 / t_l + 1.0 / t_r)
+        assert np.allclose(T, expect, rtol=1e-15, atol=0.0), a
+        # and by hand for the first face of each axis
+    assert np.isclose(tr[0][2][0], 1.0 / (1.0 / (1 * 8 / 0.5) + 1.0 / (2 * 8 / 0.5)))  # kx 1 | 2
+    assert np.isclose(tr[1][2][0], 1.0 / (1.0 / (100 * 4 / 1.0) + 1.0 / (130 * 4 / 1.0)))  # ky 100 | 130
+    assert np.isclose(tr[2][2][0], 1.0 / (1.0 / (0.01 * 2 / 2.0) + 1.0 / (0.07 * 2 / 2.0)))  # kz .01 | .07
