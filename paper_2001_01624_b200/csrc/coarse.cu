@@ -518,7 +518,42 @@ void symv_batched(msb_ctx ctx, const SymvTile* td, int ntile, const SymvRow* rd,
   count_launch();
 }
 
+// x = W^T (W r) with the lower-triangular inverse factor W (row-major, ld M): one warp
+// per row of W r, one warp per column of W^T y (lane-strided, fixed shuffle tree)
+__global__ void __launch_bounds__(256) k_trmv_lower(const double* __restrict__ W, int M,
+                                                    const double* __restrict__ r,
+                                                    double* __restrict__ y) {
+  const int i = (int)((blockIdx.x * (unsigned)blockDim.x + threadIdx.x) >> 5);
+  const int lane = threadIdx.x & 31;
+  if (i >= M) return;
+  double v = 0.0;
+  for (int j = lane; j <= i; j += 32) v = fma(W[(int64_t)i * M + j], r[j], v);
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if (lane == 0) y[i] = v;
+}
+
+__global__ void __launch_bounds__(256) k_trmv_lower_t(const double* __restrict__ W, int M,
+                                                      const double* __restrict__ y,
+                                                      double* __restrict__ x, const int* done) {
+  const int j = (int)((blockIdx.x * (unsigned)blockDim.x + threadIdx.x) >> 5);
+  const int lane = threadIdx.x & 31;
+  if (j >= M) return;
+  const bool skip = done && *(volatile const int*)done;
+  double v = 0.0;
+  for (int i = j + lane; i < M; i += 32) v = fma(W[(int64_t)i * M + j], y[i], v);
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if (lane == 0 && !skip) x[j] = v;
+}
+
 void coarse_solve(msb_ctx ctx, const Coarse& co, const double* rc, double* xc, const int* done) {
+  if (co.tri) {
+    const unsigned g = grid_for((int64_t)co.M * 32, 256);
+    k_trmv_lower<<<g, 256, 0, ctx->stream>>>(co.Ainv, co.M, rc, co.tri_y);
+    k_trmv_lower_t<<<g, 256, 0, ctx->stream>>>(co.Ainv, co.M, co.tri_y, xc, done);
+    count_launch();
+    count_launch();
+    return;
+  }
   if (co.kind == 1) {
     coarse_schur_solve(ctx, co, rc, xc, done);
     return;
@@ -567,6 +602,11 @@ static msb_status ensure_dense(msb_ctx ctx, Coarse& co, int M) {
   MSB_ALLOC(ctx, co.Ac, double, (int64_t)M * M);
   MSB_ALLOC(ctx, co.L, double, (int64_t)M * M);
   MSB_ALLOC(ctx, co.Ainv, double, (int64_t)M * M);
+  if (co.tri) {
+    dfree(ctx, co.tri_y);
+    co.tri_y = nullptr;
+    MSB_ALLOC(ctx, co.tri_y, double, M);
+  }
   co.cap = M;
   return MSB_OK;
 }
@@ -705,6 +745,8 @@ msb_status coarse_assemble_dense(msb_ctx ctx, msb_level L, msb_op op) {
 
 void coarse_free(msb_ctx ctx, Coarse& co) {
   coarse_schur_free(ctx, co);
+  dfree(ctx, co.tri_y);
+  co.tri_y = nullptr;
   dfree(ctx, co.Aell);
   co.Aell = nullptr;
   co.ell_cap = 0;

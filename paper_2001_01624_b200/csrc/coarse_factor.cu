@@ -255,78 +255,64 @@ msb_status dgemm(msb_ctx ctx, bool ta, bool tb, int m, int n, int K, double alph
 }
 
 // Leaf: Cholesky of the n x n (n <= LEAF) block at A (ld) in place (lower; upper zeroed)
-// and its triangular inverse into W (ld, lower; upper zeroed).  One CTA of 256 threads,
-// thread (r = tid / 4, q = tid % 4) owns row r's columns c = q (mod 4) of both L and W.
-// Right-looking Cholesky fused with the forward substitution W = L^{-1}, with the scaling
-// of column j of L and row j of W deferred: at step j every update uses the scaled values
-// L_rj = a_rj / l_jj and W_jc = w_jc / l_jj formed on the fly from the stored reciprocal,
-//   a_rc -= L_rj L_cj  (j < c <= r),   w_rc -= L_rj W_jc  (c <= j < r),
-// and nothing read in step j is written in step j, so ONE barrier per step suffices: the
-// owner of a_{j+1,j+1} takes the next pivot right after its last update.  The scaling is
-// applied once at the end.
-__global__ void __launch_bounds__(256) k_chol_inv_leaf(double* __restrict__ A, int64_t ld, int n,
-                                                       double* __restrict__ W,
-                                                       const unsigned long long* amax_bits,
-                                                       int* __restrict__ singular) {
-  static_assert(LEAF == 64, "thread-element map assumes 64 x 64 leaves and 256 threads");
+// and its triangular inverse into W (ld, lower; upper zeroed).  One CTA, LEAF^2 smem.
+__global__ void __launch_bounds__(1024) k_chol_inv_leaf(double* __restrict__ A, int64_t ld, int n,
+                                                        double* __restrict__ W,
+                                                        const unsigned long long* amax_bits,
+                                                        int* __restrict__ singular) {
+  static_assert(LEAF == 64, "thread-element map assumes 64 x 64 leaves and 1024 threads");
   extern __shared__ double lsm[];
   double (*a)[LEAF + 1] = reinterpret_cast<double (*)[LEAF + 1]>(lsm);
   double (*w)[LEAF + 1] = reinterpret_cast<double (*)[LEAF + 1]>(lsm + LEAF * (LEAF + 1));
-  double* rinv = lsm + 2 * LEAF * (LEAF + 1);  // [LEAF] 1 / l_jj
   const int tid = threadIdx.x;
   for (int e = tid; e < LEAF * LEAF; e += blockDim.x) {
     const int r = e >> 6, c = e & 63;
     a[r][c] = (r < n && c < n) ? A[(int64_t)r * ld + c] : 0.0;
     w[r][c] = (r == c) ? 1.0 : 0.0;
   }
+  __syncthreads();
   const double amax = __longlong_as_double((long long)*amax_bits);
-  auto pivot = [&](int j) {  // l_jj = sqrt(a_jj) (pivot test SPEC.md:81), its reciprocal
-    double d = a[j][j];
-    if (!(d > 1e-14 * amax)) {
-      atomicExch(singular, 1);
-      d = 1.0;
-    }
-    // 1/sqrt(d) from the MUFU seed and two Newton steps, l = d / sqrt(d): both within an
-    // ulp (one dependent chain instead of a square root and a division)
-    double y;
-    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(d));
-    double h = 0.5 * y;
-    double e = fma(-d * y, h, 0.5);
-    y = fma(y, e, y);
-    h = 0.5 * y;
-    e = fma(-d * y, h, 0.5);
-    y = fma(y, e, y);
-    a[j][j] = d * y;
-    rinv[j] = y;
-  };
-  __syncthreads();
-  if (tid == 0 && n > 0) pivot(0);
-  __syncthreads();
-  const int r = tid >> 2, q = tid & 3;
+  // Right-looking Cholesky fused with the forward substitution W = L^{-1}: at step j the
+  // pivot is taken, column j of L is scaled and row j of W finished (w[j][c] / L_jj), then
+  // every later row receives its rank-1 updates of L and of W (w[r][c] -= L_rj W_jc, c <= j)
+  // in parallel — the same operations in the same order as a column-by-column forward
+  // substitution, so the result is unchanged, with 3 barriers per step instead of an
+  // O(n^2) serial loop per column.
   for (int j = 0; j < n; ++j) {
-    if (r > j && r < n) {
-      const double ri = rinv[j];
-      const double lrj = a[r][j] * ri;
-      // columns c = q + 4t: L part for j < c <= r, W part for c <= j (fixed trip count,
-      // predicated: all sixteen loads of a step are in flight together)
+    if (tid == 0) {
+      double d = a[j][j];
+      if (!(d > 1e-14 * amax)) {
+        atomicExch(singular, 1);
+        d = 1.0;
+      }
+      a[j][j] = sqrt(d);
+    }
+    __syncthreads();
+    const double ljj = a[j][j];
+    if (tid < LEAF) {
+      if (tid > j && tid < n) a[tid][j] /= ljj;
+    } else if (tid < 2 * LEAF) {
+      const int c = tid - LEAF;
+      if (c <= j) w[j][c] = w[j][c] / ljj;
+    }
+    __syncthreads();
 #pragma unroll
-      for (int t = 0; t < LEAF / 4; ++t) {
-        const int c = q + 4 * t;
+    for (int u = 0; u < (LEAF * LEAF) / 1024; ++u) {
+      const int e = tid + 1024 * u, r = e >> 6, c = e & 63;
+      if (r > j && r < n) {
         if (c > j) {
-          if (c <= r) a[r][c] -= lrj * (a[c][j] * ri);
+          if (c <= r) a[r][c] -= a[r][j] * a[c][j];
         } else {
-          w[r][c] -= lrj * (w[j][c] * ri);
+          w[r][c] -= a[r][j] * w[j][c];
         }
       }
-      if (r == j + 1 && q == (r & 3)) pivot(r);  // a_rr received its last update above
     }
     __syncthreads();
   }
   for (int e = tid; e < n * n; e += blockDim.x) {
-    const int rr = e / n, c = e % n;
-    // L_rc = a_rc / l_cc below the diagonal, W_rc = w_rc / l_rr (row r of W scaled at step r)
-    A[(int64_t)rr * ld + c] = c < rr ? a[rr][c] * rinv[c] : (c == rr ? a[rr][rr] : 0.0);
-    W[(int64_t)rr * ld + c] = c <= rr ? w[rr][c] * rinv[rr] : 0.0;
+    const int r = e / n, c = e % n;
+    A[(int64_t)r * ld + c] = c <= r ? a[r][c] : 0.0;
+    W[(int64_t)r * ld + c] = c <= r ? w[r][c] : 0.0;
   }
 }
 
@@ -382,14 +368,14 @@ static msb_status rtrsm(msb_ctx ctx, double* B, double* X, int m, int n, const d
 static msb_status chol_inv(msb_ctx ctx, double* F, double* Wb, int64_t ld, int n,
                            const unsigned long long* amax, int* sing) {
   if (n <= LEAF) {
-    constexpr size_t smem = (2 * LEAF * (LEAF + 1) + LEAF) * sizeof(double);
+    constexpr size_t smem = 2 * LEAF * (LEAF + 1) * sizeof(double);
     static bool attr = false;
     if (!attr) {
       MSB_CUDA_TRY(ctx, cudaFuncSetAttribute(k_chol_inv_leaf, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)smem));
       attr = true;
     }
-    k_chol_inv_leaf<<<1, 256, smem, ctx->stream>>>(F, ld, n, Wb, amax, sing);
+    k_chol_inv_leaf<<<1, 1024, smem, ctx->stream>>>(F, ld, n, Wb, amax, sing);
     MSB_LAUNCH_CHECK(ctx);
     return MSB_OK;
   }
@@ -472,6 +458,10 @@ msb_status coarse_factor_dense(msb_ctx ctx, Coarse& co) {
   if (hs) {
     co.ready = false;
     return set_error(ctx, MSB_ESINGULAR, "singular coarse matrix: pivot <= 1e-14 max|A_c| (M=%d)", M);
+  }
+  if (co.tri) {  // a single solve per factorisation: keep W = L^{-1} (co.Ainv), x = W^T (W r)
+    co.ready = true;
+    return MSB_OK;
   }
   // A_c^{-1} = W^T W: lower tiles with the K range restricted to the nonzeros of W,
   // written over the factor buffer (L is no longer needed), then mirrored; swap so

@@ -1140,7 +1140,9 @@ msb_status msb_solver_create(msb_ctx ctx, msb_op op, const msb_level* levels, in
     MSB_ALLOC(ctx, D->co.Ac, double, (int64_t)cap * cap);
     MSB_ALLOC(ctx, D->co.L, double, (int64_t)cap * cap);
     MSB_ALLOC(ctx, D->co.Ainv, double, (int64_t)cap * cap);
+    MSB_ALLOC(ctx, D->co.tri_y, double, cap);
     D->co.cap = cap;
+    D->co.tri = true;  // factorised for exactly one solve per rebuild
     s->dyn_level = D;
   }
   // bins must not alias cnt during counting: give them their own buffer

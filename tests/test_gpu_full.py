@@ -213,7 +213,9 @@ def test_full_config4_first_steps(ctx):
     steps = int(g["steps"])
     free = gp.run_sequential(ctx, prob, steps=steps)
     assert free["init_sweeps"] == int(g["init_sweeps"])
-    assert abs(free["dt"] - float(g["dt"])) <= 4 * np.finfo(float).eps * float(g["dt"])
+    # dt = pv Σφ|Ω| / Σq⁺ (reading A18): a device sum of 1.12M terms in another order than
+    # numpy's pairwise sum — the rounding bound of the longest addition chain (~330 adds)
+    assert abs(free["dt"] - float(g["dt"])) <= 1e-12 * float(g["dt"])
     k_or = [int(k) for k in g["k"]]
     names = [str(n) for n in g["alt_names"]]
     spread = max(abs(int(a) - b) for i in range(len(names)) for a, b in zip(g[f"alt_{i}_k"], k_or))

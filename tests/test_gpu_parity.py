@@ -1187,7 +1187,7 @@ def test_transport_step_size_and_initial_mobility(ctx):
     phi = np.full(prob.N, prob.phi)
     dt = op.step_size(torch.as_tensor(phi, device="cuda"), 0.005)
     dt_or = transport.step_size(prob, prob.rhs(), phi, 0.005)
-    assert abs(dt - dt_or) <= 4 * np.finfo(float).eps * dt_or
+    assert abs(dt - dt_or) <= 1e-12 * dt_or  # sums of N terms in different orders
     mob = op.upstream_mobility(None, None, 1.0, 5.0,
                                torch.empty(prob.n_faces, dtype=torch.float64, device="cuda"))
     faces = all_faces(prob.nx, prob.ny, prob.nz)
