@@ -1215,6 +1215,24 @@ static msb_status enqueue_stage(msb_ctx ctx, msb_solver s, msb_level L, const do
     MSB_CUDA_TRY(ctx, cudaStreamWaitEvent(st, s->ev_join, 0));
     s->pending_join = false;
   }
+  // fused Jacobi + residual (jacres_tma.cu): Cartesian level, pre-smoothing, ν = 1, on grids
+  // whose x, b, T working set is far beyond L2 (config 5); bit-identical to the two passes
+  bool jq = false;
+  if (L->kind == 0 && !s->post && s->nu == 1 && s->smoother == 0 && jacres_fused_wanted(ctx, op)) {
+    if (!s->jq) s->jq = new JQPlan();
+    if (!s->jq->ok || s->jq->b != b || s->jq->x[0] != s->xbuf[0] || s->jq->x[1] != s->xbuf[1])
+      jacres_tma_plan(ctx, op, s->xbuf[0], s->xbuf[1], b, s->jq);
+    jq = s->jq->ok;
+  }
+  auto jqres = [&]() -> msb_status {
+    msb_status rc = jacres_tma_launch(ctx, op, *s->jq, cur, s->xbuf[cur ^ 1], s->r, s->omega_s,
+                                      first ? 1 : 0, s->partials, &s->st->done);
+    if (rc) return rc;
+    if (first && (rc = fin(s->jq->grid))) return rc;
+    first = false;
+    cur ^= 1;
+    return MSB_OK;
+  };
   auto ilu = [&]() -> msb_status {  // ν red-black ILU(0) steps on x in place (NEXT-2)
     for (int v = 0; v < s->nu; ++v) {
       k_residual<<<g4, CT, 0, st>>>(S, s->xbuf[cur], b, s->r, first ? 1 : 0, s->partials, s->st);
@@ -1249,13 +1267,15 @@ static msb_status enqueue_stage(msb_ctx ctx, msb_solver s, msb_level L, const do
   };
   auto corr = [&]() -> msb_status {
     if (L->kind == 0) {
-      k_residual<<<g4, CT, 0, st>>>(S, s->xbuf[cur], b, s->r, first ? 1 : 0, s->partials, s->st);
-      MSB_LAUNCH_CHECK(ctx);
-      if (first) {
-        msb_status rc = fin(g4);
-        if (rc) return rc;
+      if (!jq) {  // the fused pass has already written r
+        k_residual<<<g4, CT, 0, st>>>(S, s->xbuf[cur], b, s->r, first ? 1 : 0, s->partials, s->st);
+        MSB_LAUNCH_CHECK(ctx);
+        if (first) {
+          msb_status rc = fin(g4);
+          if (rc) return rc;
+        }
+        first = false;
       }
-      first = false;
       if (op->nx > 2048)
         return set_error(ctx, MSB_EINVAL, "Cartesian restriction supports nx <= 2048 (nx=%d)", op->nx);
       {
@@ -1346,7 +1366,7 @@ static msb_status enqueue_stage(msb_ctx ctx, msb_solver s, msb_level L, const do
     if ((rc = corr())) return rc;
     if ((rc = jac())) return rc;
   } else {
-    if ((rc = jac())) return rc;
+    if ((rc = jq ? jqres() : jac())) return rc;
     if ((rc = corr())) return rc;
   }
   return MSB_OK;
@@ -1665,6 +1685,7 @@ msb_status msb_solver_destroy(msb_solver s) {
   dfree(ctx, s->mhist);
   if (s->dyn_level) level_free(s->dyn_level);
   dfree(ctx, s->ilu_d);
+  delete s->jq;
   drop_graphs(s);
   if (s->cap_stream) cudaStreamDestroy(s->cap_stream);
   if (s->side_stream) cudaStreamDestroy(s->side_stream);

@@ -41,7 +41,8 @@ def ctx():
 def _gold(cfg):
     path = os.path.join(GOLD, f"full_config{cfg}.npz")
     assert os.path.exists(path), f"missing golden {path} (scripts/make_goldens.py {cfg})"
-    return np.load(path, allow_pickle=False)
+    with np.load(path, allow_pickle=False) as z:  # decompress every array once
+        return {k: z[k] for k in z.files}
 
 
 def _inputs_sha(prob):
