@@ -292,3 +292,39 @@ def random_problem(seed: int, nx: int, ny: int, nz: int, block, sigma: float = 1
     if faults:
         p.mult_x, p.mult_y, p.mult_z = fault_multipliers(nx, ny, nz, faults)
     return _override(p, overrides)
+
+
+# ----------------------------------------------------------------------------- NEXT-4 state
+
+
+@dataclasses.dataclass
+class CprState:
+    """A synthetic Newton state of the compressible two-phase model (NEXT-4): current
+    iterate (p, S), previous time level (p_n, S_n), well cells and volumetric rates."""
+    p: np.ndarray
+    S: np.ndarray
+    p_n: np.ndarray
+    S_n: np.ndarray
+    well_cells: np.ndarray
+    well_rates: np.ndarray
+
+
+def cpr_state(prob: Problem, seed: int = 11, p_ref: float = 100.0, dp: float = 20.0,
+              rate: float = 2.0) -> CprState:
+    """Seeded smooth random pressure (p_ref ± dp) and saturation (0.05..0.95) fields on the
+    problem's grid, a previous time level a small random step away, and the problem's
+    5-spot cells with rates scaled by `rate`.  Random numbers only."""
+    rng = np.random.default_rng(seed)
+    shape = (prob.nz, prob.ny, prob.nx)
+    sig = max(1.0, min(prob.nx, prob.ny) / 8.0)
+
+    def field():
+        g = _gauss_smooth(rng.standard_normal(shape), sig)
+        return _standardise(g).ravel() if g.std() > 0 else g.ravel()
+
+    p = p_ref + dp * np.tanh(field() / 2.0)
+    S = 0.05 + 0.9 / (1.0 + np.exp(-field()))
+    p_n = p - 0.5 * np.abs(field())
+    S_n = np.clip(S - 0.05 * rng.uniform(0.0, 1.0, size=S.size), 0.0, 1.0)
+    return CprState(p=p, S=S, p_n=p_n, S_n=S_n, well_cells=prob.src_cells.copy(),
+                    well_rates=rate * prob.src_rates)
