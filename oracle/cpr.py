@@ -222,10 +222,28 @@ def quasi_impes_weights(J, N):
 
 
 def premultiply(J, F, w):
-    """J* = W J, F* = W F with W = [[W_1, W_2], [0, I]]."""
+    """J* = W J, F* = W F with W = [[W_1, W_2], [0, I]].
+
+    Row i of the first block row is w_1,i J_w(i, :) + w_2,i J_o(i, :), formed entry by entry
+    on J's block 7-point pattern so that entries which cancel to 0 (quasi-IMPES's diagonal
+    coupling) stay in the pattern (reading C4: ILU(0)'s pattern is the block stencil)."""
+    J = sp.csr_matrix(J)
+    J.sort_indices()
     N = w.shape[1]
-    W = sp.bmat([[sp.diags(w[0]), sp.diags(w[1])], [None, sp.identity(N)]]).tocsr()
-    return (W @ sp.csr_matrix(J)).tocsr(), W @ np.asarray(F)
+    n = 2 * N
+    ip, ix, dv = J.indptr, J.indices, J.data
+    rows = np.repeat(np.arange(n), np.diff(ip))
+    if not np.array_equal(np.diff(ip[:N + 1]), np.diff(ip[N:])):
+        raise ValueError("the two block rows of J do not share a pattern")
+    a0, a1 = ip[0], ip[N]
+    if not np.array_equal(ix[a0:a1], ix[a1:]):
+        raise ValueError("the two block rows of J do not share a pattern")
+    r0 = rows[a0:a1]
+    top = w[0][r0] * dv[a0:a1] + w[1][r0] * dv[a1:]
+    Js = sp.csr_matrix((np.concatenate([top, dv[a1:]]), ix.copy(), ip.copy()), shape=(n, n))
+    F = np.asarray(F, dtype=np.float64)
+    Fs = np.concatenate([w[0] * F[:N] + w[1] * F[N:], F[N:]])
+    return Js, Fs
 
 
 def block_rb_ilu0(Js, nx, ny, nz):

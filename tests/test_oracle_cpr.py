@@ -196,6 +196,7 @@ def test_premultiply_identity_and_second_row_and_equivalence():
     w = cpr.quasi_impes_weights(J, N)
     Js, Fs = cpr.premultiply(J, F, w)
     assert (Js[N:] != J[N:]).nnz == 0 and np.array_equal(Fs[N:], F[N:])
+    assert Js.nnz == J.nnz  # the block stencil pattern survives exact cancellation (C4)
     dx = np.linalg.solve(J.toarray(), -F)
     dxs = np.linalg.solve(Js.toarray(), -Fs)
     assert np.max(np.abs(dx - dxs)) <= 1e-9 * np.max(np.abs(dx))
