@@ -297,6 +297,72 @@ msb_status msb_upstream_mobility(msb_ctx ctx, msb_op op, const double* p, const 
 msb_status msb_transport_step_size(msb_ctx ctx, msb_op op, const double* phi,
                                    double pv_per_step, double* dt_out);
 
+/* ---------------------------------------------------------------- CPR two-stage (§8 NEXT-4)
+ * Constrained-pressure-residual preconditioning of the fully implicit compressible
+ * two-phase system (PAPER.md:122-203 §4, :287-292), readings C1-C6.
+ * Model: phases w, o with one component each, no gravity / capillarity;
+ * unknowns x = (p_1..p_N | S_1..S_N), S = S_w; equations F = (F_w | F_o),
+ *   F_a^i = (φ ρ_a S_a)_i - (φ ρ_a S_a)_i^n + (Δt/|Ω_i|) Σ_faces T_f (ρ_a λ_a)_up (p_i - p_j)
+ *           - (Δt/|Ω_i|) q_a^i,
+ *   ρ_a(p) = rho_a exp(c_a (p - p_ref)), φ(p) = phi exp(c_r (p - p_ref)),
+ *   λ_w = S^n/mu_w, λ_o = (1-S)^n/mu_o (n = nrel in {1, 2}), upstream cell = the face's
+ *   left/lower cell when p_l >= p_r (reading A17); per-cell rate Q: Q > 0 injects water
+ *   (q_w = ρ_w Q), Q < 0 produces at the cell's fractional flow (q_a = ρ_a f_a Q).
+ * T_f = the operator's base transmissibility (K, cell sizes, multipliers; no mobility).
+ * Jacobian storage (msb_cpr_export): 28 planes of N doubles, plane (2 b + v) * 7 + d holds
+ * ∂F_b(c)/∂x_v(nb_d(c)) for b, v in {0 (w | p), 1 (o | S)} and stencil slot d = 0 centre,
+ * 1 -x, 2 +x, 3 -y, 4 +y, 5 -z, 6 +z (0 where the neighbour does not exist). */
+typedef struct msb_cpr_s* msb_cpr;
+typedef struct {
+  double mu_w, mu_o;    /* viscosities                                */
+  double rho_w, rho_o;  /* densities at p_ref                         */
+  double c_w, c_o, c_r; /* fluid and rock compressibilities           */
+  double phi;           /* porosity at p_ref                          */
+  double p_ref, dt;     /* reference pressure, time step Δt           */
+  int32_t nrel;         /* relative-permeability exponent (1 or 2)    */
+} msb_fluid;
+
+/* Create a CPR object on `op` (grid + base T) whose predictor runs n_cycles Eq.-(8) cycles
+ * (pre-smoothing damped Jacobi ω_s, ν = 1, then the coarse correction of `lev`) on
+ * J*_pp ("one or a few cycles").  `lev` must be a Cartesian level of the same
+ * grid (its smoothed basis P is used as prolongation, R = P^T; reading C5); it is not
+ * owned and must outlive the CPR object.  Errors: MSB_EINVAL (nrel, n_cycles < 1,
+ * explicit level), MSB_EDIM (other grid). */
+msb_status msb_cpr_create(msb_ctx ctx, msb_op op, msb_level lev, const msb_fluid* fl,
+                          int32_t n_cycles, double omega_s, msb_cpr* out);
+/* Linearize at (p, S) with previous time level (p_n, S_n) (host|dev, N doubles each) and
+ * per-cell well rates q (host|dev N doubles, or NULL = none): F and J on the device. */
+msb_status msb_cpr_linearize(msb_ctx ctx, msb_cpr c, const double* p, const double* S,
+                             const double* p_n, const double* S_n, const double* q);
+/* Decouple: method 0 = no weights (w = (1, 0)), 1 = IMPES
+ * (Σ_b W_b ∂A_b/∂S = 0), 2 = quasi-IMPES (Σ_b W_b diag ∂F_b/∂S = 0); per cell the system
+ * [m_1 m_2; 1 1] w = [0; 1], w = (1, 0) where m_1 = m_2 = 0.  Then
+ * J* = W J, F* = W F (first block row W_1 row_w + W_2 row_o, second row unchanged), the
+ * predictor's coarse operator A_c = P^T J*_pp P (exact 128-bit fixed point) and its
+ * explicit inverse (blocked Gauss–Jordan without pivoting on the fp64 tensor cores;
+ * reading C5), and the corrector's ILU(0) of the full J* (2 x 2 cell blocks, red-black
+ * cell order, reading C4).  Errors: MSB_ESINGULAR for a singular weight system, a coarse
+ * pivot <= 1e-14 max|A_c| or a singular ILU(0) pivot block; MSB_EINVAL before linearize. */
+msb_status msb_cpr_decouple(msb_ctx ctx, msb_cpr c, int32_t method);
+/* dx = M_CPR^{-1} r: Δp = predictor(r_p); r' = r - J*[:, p] Δp;
+ * dx = (Δp, 0) + (L U)^{-1} r'.  r, dx: dev, 2N doubles (may not alias). */
+msb_status msb_cpr_apply(msb_ctx ctx, msb_cpr c, const double* r, double* dx);
+/* y = J* x (dev, 2N doubles). */
+msb_status msb_cpr_apply_system(msb_ctx ctx, msb_cpr c, const double* x, double* y);
+/* Parity dumps (host|dev, NULL skips): F (2N), J (28 N planes, layout above), w (2N:
+ * w_1 | w_2), F* (2N), J*'s first block row (14 N planes: pp slots 0..6 | ps slots 0..6). */
+msb_status msb_cpr_export(msb_ctx ctx, msb_cpr c, double* F, double* J, double* w,
+                          double* Fs, double* Js_row0);
+/* The predictor's coarse operator A_c = P^T J*_pp P (dense M*M row-major, host|dev). */
+msb_status msb_cpr_export_coarse(msb_ctx ctx, msb_cpr c, double* Ac, int32_t* M_out);
+/* Flexible GMRES(restart) on J* dx = b (b host|dev 2N or NULL = -F*; x host|dev 2N, in x0,
+ * out x), right-preconditioned by precond 1 = the CPR two-stage, 2 = the ILU(0) corrector
+ * alone; same stopping rule and outputs as msb_fgmres. */
+msb_status msb_cpr_fgmres(msb_ctx ctx, msb_cpr c, const double* b, double* x, double tol,
+                          int32_t restart, int32_t max_iter, int32_t fixed_iters,
+                          int32_t precond, int32_t* iters_out, double* res_hist);
+msb_status msb_cpr_destroy(msb_cpr c);
+
 #ifdef __cplusplus
 }
 #endif

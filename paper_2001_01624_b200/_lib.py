@@ -18,6 +18,13 @@ class Source(C.Structure):
     _fields_ = [("cell", C.c_int32), ("rate", C.c_double)]
 
 
+class Fluid(C.Structure):
+    _fields_ = [("mu_w", C.c_double), ("mu_o", C.c_double), ("rho_w", C.c_double),
+                ("rho_o", C.c_double), ("c_w", C.c_double), ("c_o", C.c_double),
+                ("c_r", C.c_double), ("phi", C.c_double), ("p_ref", C.c_double),
+                ("dt", C.c_double), ("nrel", C.c_int32)]
+
+
 ALLOC_FN = C.CFUNCTYPE(C.c_void_p, C.c_size_t, C.c_void_p)
 FREE_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_void_p)
 
@@ -66,6 +73,15 @@ SIGNATURES = {
     "msb_transport_upwind": (i32, [p, p, p, p, p, f64, f64, f64, p, pi32]),
     "msb_upstream_mobility": (i32, [p, p, p, p, f64, f64, p]),
     "msb_transport_step_size": (i32, [p, p, p, f64, pf64]),
+    "msb_cpr_create": (i32, [p, p, p, C.POINTER(Fluid), i32, f64, C.POINTER(p)]),
+    "msb_cpr_linearize": (i32, [p, p, p, p, p, p, p]),
+    "msb_cpr_decouple": (i32, [p, p, i32]),
+    "msb_cpr_apply": (i32, [p, p, p, p]),
+    "msb_cpr_apply_system": (i32, [p, p, p, p]),
+    "msb_cpr_export": (i32, [p, p, p, p, p, p, p]),
+    "msb_cpr_export_coarse": (i32, [p, p, p, pi32]),
+    "msb_cpr_fgmres": (i32, [p, p, p, p, f64, i32, i32, i32, i32, pi32, p]),
+    "msb_cpr_destroy": (i32, [p]),
 }
 
 _lib = None

@@ -427,3 +427,88 @@ class Solver:
             self.close()
         except Exception:
             pass
+
+
+class Cpr:
+    """§8 NEXT-4: the CPR two-stage preconditioner of the compressible two-phase system
+    (PAPER.md:122-203, :287-292).  `fluid`: a mapping with the msb_fluid fields."""
+
+    METHODS = {"none": 0, "impes": 1, "quasi": 2}
+    PRECONDS = {"cpr": 1, "ilu0": 2}
+
+    def __init__(self, ctx: Context, op: Operator, level: Level, fluid, n_cycles=1,
+                 omega_s=2.0 / 3.0):
+        self.ctx = ctx
+        self.op = op
+        self.level = level  # kept alive: the CPR object reads its basis
+        f = fluid if isinstance(fluid, dict) else vars(fluid)
+        fl = L.Fluid(*[float(f[k]) for k in ("mu_w", "mu_o", "rho_w", "rho_o", "c_w", "c_o",
+                                              "c_r", "phi", "p_ref", "dt")], int(f["nrel"]))
+        h = C.c_void_p()
+        ctx.check(ctx.lib.msb_cpr_create(ctx.h, op.h, level.h, C.byref(fl), int(n_cycles),
+                                         float(omega_s), C.byref(h)), "msb_cpr_create")
+        self.h = h
+        self.N = op.N
+
+    def linearize(self, p, S, p_n, S_n, q=None):
+        self.ctx.check(self.ctx.lib.msb_cpr_linearize(self.ctx.h, self.h, _ptr(p), _ptr(S),
+                                                      _ptr(p_n), _ptr(S_n), _ptr(q)),
+                       "msb_cpr_linearize")
+
+    def decouple(self, method="quasi"):
+        self.ctx.check(self.ctx.lib.msb_cpr_decouple(self.ctx.h, self.h, self.METHODS[method]),
+                       "msb_cpr_decouple")
+
+    def apply(self, r, dx):
+        self.ctx.check(self.ctx.lib.msb_cpr_apply(self.ctx.h, self.h, _ptr(r), _ptr(dx)),
+                       "msb_cpr_apply")
+
+    def apply_system(self, x, y):
+        self.ctx.check(self.ctx.lib.msb_cpr_apply_system(self.ctx.h, self.h, _ptr(x), _ptr(y)),
+                       "msb_cpr_apply_system")
+
+    def export(self, decoupled=True):
+        N = self.N
+        F, J = np.empty(2 * N), np.empty(28 * N)
+        w = Fs = Js = None
+        if decoupled:
+            w, Fs, Js = np.empty(2 * N), np.empty(2 * N), np.empty(14 * N)
+        self.ctx.check(self.ctx.lib.msb_cpr_export(self.ctx.h, self.h, _ptr(F), _ptr(J), _ptr(w),
+                                                   _ptr(Fs), _ptr(Js)), "msb_cpr_export")
+        out = dict(F=F, J=J.reshape(2, 2, 7, N))
+        if decoupled:
+            out.update(w=w.reshape(2, N), Fs=Fs, Js=Js.reshape(2, 7, N))
+        return out
+
+    def export_coarse(self):
+        M = C.c_int32()
+        self.ctx.check(self.ctx.lib.msb_cpr_export_coarse(self.ctx.h, self.h, None, C.byref(M)),
+                       "msb_cpr_export_coarse")
+        Ac = np.empty(M.value * M.value)
+        self.ctx.check(self.ctx.lib.msb_cpr_export_coarse(self.ctx.h, self.h, _ptr(Ac),
+                                                          C.byref(M)), "msb_cpr_export_coarse")
+        return Ac.reshape(M.value, M.value)
+
+    def fgmres(self, x, b=None, tol=1e-8, restart=40, max_iter=200, fixed_iters=0,
+               precond="cpr"):
+        n = C.c_int32()
+        cap = max(max_iter, fixed_iters) + 2 + max(max_iter, fixed_iters) // max(1, restart) + 2
+        res = np.zeros(cap)
+        st = self.ctx.lib.msb_cpr_fgmres(self.ctx.h, self.h, _ptr(b), _ptr(x), float(tol),
+                                         int(restart), int(max_iter), int(fixed_iters),
+                                         self.PRECONDS[precond], C.byref(n), _ptr(res))
+        self.ctx.check(st, "msb_cpr_fgmres")
+        k = n.value
+        return dict(iters=k, status=st, converged=(st == OK and fixed_iters == 0),
+                    res=res[:k + 1].copy())
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.ctx.lib.msb_cpr_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -159,8 +159,7 @@ __global__ void __launch_bounds__(CT) k_norm(StencilT S, const double* __restric
 // CPT cells per thread (strided by the block size, so every load instruction stays
 // coalesced): the loads of all CPT cells are in flight together and the grid is CPT
 // times shorter, which is what a short stencil pass needs to approach HBM bandwidth.
-constexpr int CPT = 4;
-
+template <int CPT>
 __global__ void __launch_bounds__(CT) k_jacobi(StencilT S, const double* __restrict__ x,
                                                double* __restrict__ xo,
                                                const double* __restrict__ b, double omega,
@@ -190,7 +189,25 @@ __global__ void __launch_bounds__(CT) k_jacobi(StencilT S, const double* __restr
   if (first) warp_partial(v, partials);
 }
 
+// L2 eviction-priority hints (createpolicy + ld.global.L2::cache_hint)
+__device__ __forceinline__ uint64_t pol_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t pol_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ double ld_pol(const double* a, uint64_t pol) {
+  double v;
+  asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(a), "l"(pol));
+  return v;
+}
+
 struct LevelView {
+  int hint;  // experiment: 1 = P kept in L2 by the restriction, dropped by the prolongation
   int kind, W, nb0, nb1, nb2, b0, b1, b2;
   Grid3 g;
   const int32_t* tab;
@@ -558,6 +575,7 @@ __global__ void __launch_bounds__(CT) k_prolong(LevelView L, double* __restrict_
 
 // a6: r = b - A x (materialised for the gather restriction); `first` also emits the
 // ||r||^2 partials of the stop test (post-smoothing order starts a cycle here).
+template <int CPT>
 __global__ void __launch_bounds__(CT) k_residual(StencilT S, const double* __restrict__ x,
                                                  const double* __restrict__ b,
                                                  double* __restrict__ r, int first,
@@ -615,8 +633,11 @@ __device__ __forceinline__ void support_range(int J, int b, int n, int nb, int& 
 // atomics).  Thread layout: XL lanes along x (XL = pow2 >= nx, <= 256) x RG row
 // groups; x positions beyond 256 take a second partial.
 constexpr int RR2_THREADS = 256;
-// XP x positions per lane (x = xo + XL * e, e < XP): XP = ceil(nx / XL), 1 for nx <= 256
-template <int XP>
+// XP x positions per lane (x = xo + XL * e, e < XP): XP = ceil(nx / XL), 1 for nx <= 256.
+// CS CTAs (one thread-block cluster) share one (Jy, Jz) unit: rank q walks the rows
+// q, q + CS, ... of each row group; the CTAs' per-(parity, x) totals are summed by rank 0
+// over distributed shared memory in rank order (deterministic).
+template <int XP, int CS>
 __device__ __forceinline__ void restrict_row_body(const LevelView& L, const double* __restrict__ r,
                                                   double* __restrict__ rc, int unit,
                                                   double* rsh, bool done) {
@@ -633,6 +654,8 @@ __device__ __forceinline__ void restrict_row_body(const LevelView& L, const doub
   const int XL = XP > 1 ? 256 : (nx <= 32 ? 32 : (nx <= 64 ? 64 : (nx <= 128 ? 128 : 256)));
   const int RG = RR2_THREADS / XL;
   const int xo = threadIdx.x % XL, rg = threadIdx.x / XL;
+  int rank = 0;
+  if constexpr (CS > 1) rank = (int)cooperative_groups::this_cluster().block_rank();
   double a0[XP], a1[XP];  // parity 0 / 1 partials at x = xo + XL e
   bool xok[XP];
 #pragma unroll
@@ -640,9 +663,11 @@ __device__ __forceinline__ void restrict_row_body(const LevelView& L, const doub
     a0[e] = a1[e] = 0.0;
     xok[e] = xo + XL * e < nx;
   }
-  int row = rg;
+  const uint64_t pol = L.hint ? pol_evict_last() : 0;
+  int row = rg + RG * rank;
   int zz = row / wy, yy = row - zz * wy;
-  const int dz = RG / wy, dy = RG - dz * wy;
+  const int step = RG * CS;
+  const int dz = step / wy, dy = step - dz * wy;
   constexpr int U = XP > 2 ? 2 : 4;  // rows in flight per lane
   while (row < rows) {
     double p0[U][XP], p1[U][XP], rv[U][XP];
@@ -653,11 +678,16 @@ __device__ __forceinline__ void restrict_row_body(const LevelView& L, const doub
 #pragma unroll
       for (int e = 0; e < XP; ++e) {
         const bool v = ok && xok[e];
-        p0[u][e] = v ? P0[c + XL * e] : 0.0;
-        p1[u][e] = v ? P1[c + XL * e] : 0.0;
+        if (L.hint) {
+          p0[u][e] = v ? ld_pol(P0 + c + XL * e, pol) : 0.0;
+          p1[u][e] = v ? ld_pol(P1 + c + XL * e, pol) : 0.0;
+        } else {
+          p0[u][e] = v ? P0[c + XL * e] : 0.0;
+          p1[u][e] = v ? P1[c + XL * e] : 0.0;
+        }
         rv[u][e] = v ? r[c + XL * e] : 0.0;
       }
-      row += RG;
+      row += step;
       yy += dy;
       zz += dz;
       if (yy >= wy) {
@@ -681,13 +711,30 @@ __device__ __forceinline__ void restrict_row_body(const LevelView& L, const doub
     rsh[(rg * 2 + 1) * XLX + XL * e + xo] = a1[e];
   }
   __syncthreads();
+  double* tot = rsh + RG * 2 * XLX;
   for (int t = threadIdx.x; t < 2 * XLX; t += blockDim.x) {
     double v = 0.0;
     for (int g = 0; g < RG; ++g) v += rsh[g * 2 * XLX + t];
-    rsh[RG * 2 * XLX + t] = v;
+    tot[t] = v;
+  }
+  if constexpr (CS > 1) {
+    auto cl = cooperative_groups::this_cluster();
+    cl.sync();  // every rank's totals are complete
+    if (rank == 0) {
+      for (int t = threadIdx.x; t < 2 * XLX; t += blockDim.x) {
+        double v = tot[t];
+#pragma unroll
+        for (int q = 1; q < CS; ++q) v += cl.map_shared_rank(tot, q)[t];
+        rsh[t] = v;  // the row-group partials are dead: reuse their space
+      }
+    }
+    cl.sync();  // remote reads done before any rank exits
+    if (rank != 0) return;
+    tot = rsh;
+  } else {
+    __syncthreads();
   }
   __syncthreads();
-  const double* tot = rsh + RG * 2 * XLX;
   for (int Jx = threadIdx.x; Jx < L.nb0; Jx += blockDim.x) {
     int x0, x1;
     support_range(Jx, L.b0, nx, L.nb0, x0, x1);
@@ -698,13 +745,13 @@ __device__ __forceinline__ void restrict_row_body(const LevelView& L, const doub
   }
 }
 
-template <int XP>
+template <int XP, int CS>
 __global__ void __launch_bounds__(RR2_THREADS) k_restrict_cart(LevelView L,
                                                                const double* __restrict__ r,
                                                                double* __restrict__ rc,
                                                                const IterState* st) {
   extern __shared__ double rsh[];
-  restrict_row_body<XP>(L, r, rc, blockIdx.x, rsh, is_done(st));
+  restrict_row_body<XP, CS>(L, r, rc, blockIdx.x / CS, rsh, is_done(st));
 }
 
 static inline int restrict_xp(int nx) {
@@ -716,6 +763,38 @@ static inline size_t restrict_rows_smem(int nx) {
   const int XL = XP > 1 ? 256 : (nx <= 32 ? 32 : (nx <= 64 ? 64 : (nx <= 128 ? 128 : 256)));
   const int RG = RR2_THREADS / XL;
   return (size_t)(RG + 1) * 2 * XP * XL * sizeof(double);
+}
+
+// k_restrict_cart<XP, CS> over `units` (Jy, Jz) rows, CS CTAs per unit in one cluster
+template <int XP, int CS>
+static msb_status launch_restrict(msb_ctx ctx, cudaStream_t st, unsigned units, size_t smem,
+                                  const LevelView& V, const double* r, double* rc,
+                                  const IterState* ist) {
+  static size_t attr = 48 * 1024;
+  if (smem > attr) {
+    MSB_CUDA_TRY(ctx, cudaFuncSetAttribute(k_restrict_cart<XP, CS>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = smem;
+  }
+  if constexpr (CS == 1) {
+    k_restrict_cart<XP, 1><<<units, RR2_THREADS, smem, st>>>(V, r, rc, ist);
+  } else {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(units * CS);
+    cfg.blockDim = dim3(RR2_THREADS);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = CS;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    MSB_CUDA_TRY(ctx, cudaLaunchKernelEx(&cfg, k_restrict_cart<XP, CS>, V, r, rc, ist));
+  }
+  return MSB_OK;  // the caller's MSB_LAUNCH_CHECK counts the launch
+
 }
 
 // a9 (Cartesian level): x += P x_c, one thread per cell: the six per-axis block
@@ -736,13 +815,14 @@ __global__ void __launch_bounds__(CT) k_prolong_cart(LevelView L, double* __rest
   const int2 ty = reinterpret_cast<const int2*>(L.tab)[L.g.nx + j];
   const int2 tz = reinterpret_cast<const int2*>(L.tab)[L.g.nx + L.g.ny + k];
   const double* __restrict__ base = L.P + c;
+  const uint64_t pol = L.hint ? pol_evict_first() : 0;
   double v[8], xv[8];
 #pragma unroll
   for (int s = 0; s < 8; ++s) {
     const int jx = (s & 1) ? tx.y : tx.x, jy = (s & 2) ? ty.y : ty.x, jz = (s & 4) ? tz.y : tz.x;
     const bool act = (jx | jy | jz) >= 0;
     const int col = jx + L.nb0 * (jy + L.nb1 * jz);
-    v[s] = act ? base[(size_t)s * N] : 0.0;
+    v[s] = act ? (L.hint ? ld_pol(base + (size_t)s * N, pol) : base[(size_t)s * N]) : 0.0;
     xv[s] = act ? xc[col] : 0.0;
   }
   double acc = 0.0;
@@ -927,7 +1007,7 @@ static StencilT stencil(msb_op op) {
 }
 
 static LevelView view(msb_level L) {
-  return LevelView{L->kind, L->W, L->nb[0], L->nb[1], L->nb[2], L->bs[0], L->bs[1], L->bs[2],
+  return LevelView{xknob("MSB_X_L2HINT", 0), L->kind, L->W, L->nb[0], L->nb[1], L->nb[2], L->bs[0], L->bs[1], L->bs[2],
                    make_grid3(L->nx, L->ny, L->nz), L->tab, L->col, L->P[L->cur],
                    (L->kind == 1 && L->W == 1 && L->unity) ? 1 : 0};
 }
@@ -1176,6 +1256,15 @@ msb_status msb_add_dynamic_basis(msb_ctx ctx, msb_solver s, const double* dp, in
 // Enqueue one stage (level L) on x buffers; `first` marks the iteration's first kernel.
 // Enqueue one stage (level L) on the x double buffer; `first` marks the iteration's
 // first kernel, which also emits the stop-test partials (finalised right after).
+#define RES_LAUNCH(...)                                                   \
+  (cpt == 8   ? k_residual<8><<<g4, CT, 0, st>>>(__VA_ARGS__)              \
+   : cpt == 2 ? k_residual<2><<<g4, CT, 0, st>>>(__VA_ARGS__)              \
+              : k_residual<4><<<g4, CT, 0, st>>>(__VA_ARGS__))
+#define JAC_LAUNCH(...)                                                   \
+  (cpt == 8   ? k_jacobi<8><<<g4, CT, 0, st>>>(__VA_ARGS__)                \
+   : cpt == 2 ? k_jacobi<2><<<g4, CT, 0, st>>>(__VA_ARGS__)                \
+              : k_jacobi<4><<<g4, CT, 0, st>>>(__VA_ARGS__))
+
 static msb_status enqueue_stage(msb_ctx ctx, msb_solver s, msb_level L, const double* b, int& cur,
                                 bool& first) {
   msb_op op = s->op;
@@ -1184,7 +1273,8 @@ static msb_status enqueue_stage(msb_ctx ctx, msb_solver s, msb_level L, const do
   StencilT S = stencil(op);
   LevelView V = view(L);
   unsigned g = grid_for(N, CT);
-  const unsigned g4 = grid_for(N, CT * CPT);  // multi-cell stencil kernels
+  const int cpt = xknob("MSB_X_CPT", 4);
+  const unsigned g4 = grid_for(N, CT * cpt);  // multi-cell stencil kernels
   // With one pre-smoothed level and nu = 1 no kernel of an iteration writes the buffer
   // holding x_{k-1}, so the stop test's finalize runs on a side branch in parallel with
   // the rest of the iteration and is joined before the next iteration's first kernel
@@ -1235,7 +1325,7 @@ static msb_status enqueue_stage(msb_ctx ctx, msb_solver s, msb_level L, const do
   };
   auto ilu = [&]() -> msb_status {  // ν red-black ILU(0) steps on x in place (NEXT-2)
     for (int v = 0; v < s->nu; ++v) {
-      k_residual<<<g4, CT, 0, st>>>(S, s->xbuf[cur], b, s->r, first ? 1 : 0, s->partials, s->st);
+      RES_LAUNCH(S, s->xbuf[cur], b, s->r, first ? 1 : 0, s->partials, s->st);
       MSB_LAUNCH_CHECK(ctx);
       if (first) {
         msb_status rc = fin(g4);
@@ -1253,7 +1343,7 @@ static msb_status enqueue_stage(msb_ctx ctx, msb_solver s, msb_level L, const do
   auto jac = [&]() -> msb_status {
     if (s->smoother == 1) return ilu();
     for (int v = 0; v < s->nu; ++v) {
-      k_jacobi<<<g4, CT, 0, st>>>(S, s->xbuf[cur], s->xbuf[cur ^ 1], b, s->omega_s, first ? 1 : 0,
+      JAC_LAUNCH(S, s->xbuf[cur], s->xbuf[cur ^ 1], b, s->omega_s, first ? 1 : 0,
                                  s->partials, s->st);
       MSB_LAUNCH_CHECK(ctx);
       if (first) {
@@ -1268,7 +1358,7 @@ static msb_status enqueue_stage(msb_ctx ctx, msb_solver s, msb_level L, const do
   auto corr = [&]() -> msb_status {
     if (L->kind == 0) {
       if (!jq) {  // the fused pass has already written r
-        k_residual<<<g4, CT, 0, st>>>(S, s->xbuf[cur], b, s->r, first ? 1 : 0, s->partials, s->st);
+        RES_LAUNCH(S, s->xbuf[cur], b, s->r, first ? 1 : 0, s->partials, s->st);
         MSB_LAUNCH_CHECK(ctx);
         if (first) {
           msb_status rc = fin(g4);
@@ -1282,23 +1372,18 @@ static msb_status enqueue_stage(msb_ctx ctx, msb_solver s, msb_level L, const do
         const int xp = restrict_xp(op->nx);
         const size_t smem = restrict_rows_smem(op->nx);
         const unsigned gr = (unsigned)(L->nb[1] * L->nb[2]);
-        if (xp == 1) k_restrict_cart<1><<<gr, RR2_THREADS, smem, st>>>(V, s->r, s->rc, s->st);
-        else if (xp == 2) k_restrict_cart<2><<<gr, RR2_THREADS, smem, st>>>(V, s->r, s->rc, s->st);
-        else if (xp == 4) {
-          static bool attr = false;
-          if (!attr) {
-            MSB_CUDA_TRY(ctx, cudaFuncSetAttribute(k_restrict_cart<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            attr = true;
-          }
-          k_restrict_cart<4><<<gr, RR2_THREADS, smem, st>>>(V, s->r, s->rc, s->st);
-        } else {
-          static bool attr = false;
-          if (!attr) {
-            MSB_CUDA_TRY(ctx, cudaFuncSetAttribute(k_restrict_cart<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            attr = true;
-          }
-          k_restrict_cart<8><<<gr, RR2_THREADS, smem, st>>>(V, s->r, s->rc, s->st);
-        }
+        const int cs = xknob("MSB_X_RCS", 1);
+        msb_status rc = MSB_OK;
+#define MSB_RESTRICT_CS(XPV)                                                              \
+  rc = cs == 4 ? launch_restrict<XPV, 4>(ctx, st, gr, smem, V, s->r, s->rc, s->st)        \
+       : cs == 2 ? launch_restrict<XPV, 2>(ctx, st, gr, smem, V, s->r, s->rc, s->st)      \
+                 : launch_restrict<XPV, 1>(ctx, st, gr, smem, V, s->r, s->rc, s->st)
+        if (xp == 1) MSB_RESTRICT_CS(1);
+        else if (xp == 2) MSB_RESTRICT_CS(2);
+        else if (xp == 4) MSB_RESTRICT_CS(4);
+        else MSB_RESTRICT_CS(8);
+#undef MSB_RESTRICT_CS
+        if (rc) return rc;
       }
       MSB_LAUNCH_CHECK(ctx);
       coarse_solve(ctx, L->co, s->rc, s->xc, &s->st->done);
@@ -1307,7 +1392,7 @@ static msb_status enqueue_stage(msb_ctx ctx, msb_solver s, msb_level L, const do
       return MSB_OK;
     }
     if (use_csc(s, L)) {
-      k_residual<<<g4, CT, 0, st>>>(S, s->xbuf[cur], b, s->r, first ? 1 : 0, s->partials, s->st);
+      RES_LAUNCH(S, s->xbuf[cur], b, s->r, first ? 1 : 0, s->partials, s->st);
       MSB_LAUNCH_CHECK(ctx);
       if (first) {
         msb_status rc = fin(g4);
@@ -1708,6 +1793,34 @@ msb_status solver_smoother_setup(msb_ctx ctx, msb_solver s) {
   return MSB_OK;
 }
 
+
+// Cartesian level's r_c = P^T r and x += P x_c outside a solver (NEXT-4 predictor,
+// cpr.cu); `done` is a device int kept 0 (the kernels' stop-test flag)
+msb_status level_restrict(msb_ctx ctx, msb_level L, const double* r, double* rc, const int* done) {
+  if (L->kind != 0) return set_error(ctx, MSB_EINVAL, "level_restrict: Cartesian level only");
+  if (L->nx > 2048) return set_error(ctx, MSB_EINVAL, "Cartesian restriction supports nx <= 2048");
+  const LevelView V = view(L);
+  const IterState* ist = reinterpret_cast<const IterState*>(done);  // `done` is its first member
+  const size_t smem = restrict_rows_smem(L->nx);
+  const unsigned gr = (unsigned)(L->nb[1] * L->nb[2]);
+  const int xp = restrict_xp(L->nx);
+  cudaStream_t st = ctx->stream;
+  msb_status rc2 = xp == 1   ? launch_restrict<1, 1>(ctx, st, gr, smem, V, r, rc, ist)
+                   : xp == 2 ? launch_restrict<2, 1>(ctx, st, gr, smem, V, r, rc, ist)
+                   : xp == 4 ? launch_restrict<4, 1>(ctx, st, gr, smem, V, r, rc, ist)
+                             : launch_restrict<8, 1>(ctx, st, gr, smem, V, r, rc, ist);
+  if (rc2) return rc2;
+  MSB_LAUNCH_CHECK(ctx);
+  return MSB_OK;
+}
+
+msb_status level_prolong_add(msb_ctx ctx, msb_level L, double* x, const double* xc, const int* done) {
+  if (L->kind != 0) return set_error(ctx, MSB_EINVAL, "level_prolong_add: Cartesian level only");
+  const IterState* ist = reinterpret_cast<const IterState*>(done);
+  k_prolong_cart<<<grid_for(L->N, CT), CT, 0, ctx->stream>>>(view(L), x, xc, ist);
+  MSB_LAUNCH_CHECK(ctx);
+  return MSB_OK;
+}
 
 msb_status solver_precondition(msb_ctx ctx, msb_solver s, const double* v, double* z) {
   cudaStream_t st = ctx->stream;

@@ -8,6 +8,7 @@
 // Reductions are block partials summed in a fixed order: deterministic.
 #include <algorithm>
 #include <cmath>
+#include <functional>
 #include <vector>
 
 #include "internal.cuh"
@@ -98,39 +99,29 @@ __global__ void k_scale(double a, const double* x, double* y, int64_t N) {
 
 }  // namespace msb
 
-using namespace msb;
+namespace msb {
 
-extern "C" msb_status msb_fgmres(msb_ctx ctx, msb_solver s, const double* b, double* x, double tol,
-                                 int32_t restart, int32_t max_iter, int32_t fixed_iters,
-                                 int32_t* iters_out, double* res_hist) {
-  if (!ctx || !s || !x) return set_error(ctx, MSB_EINVAL, "msb_fgmres: null");
+// Flexible GMRES(m) on a device operator: ops.A (y = A x) and ops.M (z = M^{-1} v) over
+// vectors of length N; db the device rhs, x host|dev in x0 / out x.
+msb_status fgmres_core(msb_ctx ctx, int64_t N, const FgOps& ops, const double* db, double* x,
+                       double tol, int32_t restart, int32_t max_iter, int32_t fixed_iters,
+                       int32_t* iters_out, double* res_hist) {
   if (restart < 1 || restart > 64 || max_iter < 0 || fixed_iters < 0)
-    return set_error(ctx, MSB_EINVAL, "msb_fgmres: restart must be in [1, 64]");
-  if (s->levels.empty() && !(s->dyn && s->dyn_level && s->dyn_level->M > 0))
-    return set_error(ctx, MSB_EINVAL, "msb_fgmres: solver has no stage to precondition with");
-  msb_op op = s->op;
-  const int64_t N = op->N;
+    return set_error(ctx, MSB_EINVAL, "fgmres: restart must be in [1, 64]");
   cudaStream_t st = ctx->stream;
   const int m = restart;
-  // the Krylov workspace (and the staged rhs) is released on every return path: the
-  // stream is drained first, so no enqueued kernel still reads a freed buffer
+  // the Krylov workspace is released on every return path: the stream is drained first,
+  // so no enqueued kernel still reads a freed buffer
   struct Workspace {
     msb_ctx ctx;
-    void* ob = nullptr;
     double *V = nullptr, *Z = nullptr, *w = nullptr, *xd = nullptr, *part = nullptr,
            *dots = nullptr;
     ~Workspace() {
       cudaStreamSynchronize(ctx->stream);
-      for (void* p : {(void*)V, (void*)Z, (void*)w, (void*)xd, (void*)part, (void*)dots, ob})
+      for (void* p : {(void*)V, (void*)Z, (void*)w, (void*)xd, (void*)part, (void*)dots})
         dfree(ctx, p);
     }
   } ws{ctx};
-  const double* db = b ? (const double*)stage_in(ctx, b, N * sizeof(double), &ws.ob) : op->q;
-  if (!db) return set_error(ctx, MSB_ENOMEM, "rhs staging");
-  {
-    msb_status r0 = solver_smoother_setup(ctx, s);
-    if (r0) return r0;
-  }
   double *&V = ws.V, *&Z = ws.Z, *&w = ws.w, *&xd = ws.xd, *&part = ws.part, *&dots = ws.dots;
   MSB_ALLOC(ctx, V, double, (size_t)(m + 1) * N);
   MSB_ALLOC(ctx, Z, double, (size_t)m * N);
@@ -166,7 +157,7 @@ extern "C" msb_status msb_fgmres(msb_ctx ctx, msb_solver s, const double* b, dou
   };
   // residual r = b - A x into V_0
   auto residual = [&](double* r) -> msb_status {
-    msb_status r2 = msb_op_apply(ctx, op, xd, r);
+    msb_status r2 = ops.A(xd, r);
     if (r2) return r2;
     k_xmy<<<ge, FG_T, 0, st>>>(db, r, N);
     MSB_LAUNCH_CHECK(ctx);
@@ -200,8 +191,8 @@ extern "C" msb_status msb_fgmres(msb_ctx ctx, msb_solver s, const double* b, dou
     for (int j = 0; j < m; ++j) {
       double* vj = V + (size_t)j * N;
       double* zj = Z + (size_t)j * N;
-      if ((rc = solver_precondition(ctx, s, vj, zj))) return rc;
-      if ((rc = msb_op_apply(ctx, op, zj, w))) return rc;
+      if ((rc = ops.M(vj, zj))) return rc;
+      if ((rc = ops.A(zj, w))) return rc;
       // CGS2: h = V^T w; w -= V h; twice — all on the device, then ||w||, the Arnoldi
       // column and v_{j+1}; one host round trip per step reads the column for the rotations
       for (int pass = 0; pass < 2; ++pass) {
@@ -263,4 +254,38 @@ extern "C" msb_status msb_fgmres(msb_ctx ctx, msb_solver s, const double* b, dou
   if (iters_out) *iters_out = k;
   if (fixed_iters > 0) return MSB_OK;
   return converged ? MSB_OK : MSB_NOT_CONVERGED;
+}
+
+}  // namespace msb
+
+using namespace msb;
+
+extern "C" msb_status msb_fgmres(msb_ctx ctx, msb_solver s, const double* b, double* x, double tol,
+                                 int32_t restart, int32_t max_iter, int32_t fixed_iters,
+                                 int32_t* iters_out, double* res_hist) {
+  if (!ctx || !s || !x) return set_error(ctx, MSB_EINVAL, "msb_fgmres: null");
+  if (restart < 1 || restart > 64 || max_iter < 0 || fixed_iters < 0)
+    return set_error(ctx, MSB_EINVAL, "msb_fgmres: restart must be in [1, 64]");
+  if (s->levels.empty() && !(s->dyn && s->dyn_level && s->dyn_level->M > 0))
+    return set_error(ctx, MSB_EINVAL, "msb_fgmres: solver has no stage to precondition with");
+  msb_op op = s->op;
+  const int64_t N = op->N;
+  struct Staged {
+    msb_ctx ctx;
+    void* ob = nullptr;
+    ~Staged() {
+      cudaStreamSynchronize(ctx->stream);
+      dfree(ctx, ob);
+    }
+  } sb{ctx};
+  const double* db = b ? (const double*)stage_in(ctx, b, N * sizeof(double), &sb.ob) : op->q;
+  if (!db) return set_error(ctx, MSB_ENOMEM, "rhs staging");
+  {
+    msb_status r0 = solver_smoother_setup(ctx, s);
+    if (r0) return r0;
+  }
+  FgOps ops;
+  ops.A = [&](const double* xv, double* yv) { return msb_op_apply(ctx, op, xv, yv); };
+  ops.M = [&](const double* v, double* z) { return solver_precondition(ctx, s, v, z); };
+  return fgmres_core(ctx, N, ops, db, x, tol, restart, max_iter, fixed_iters, iters_out, res_hist);
 }

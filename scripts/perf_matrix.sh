@@ -5,7 +5,7 @@ OUT=gpurun_out/$TAG; mkdir -p $OUT
 timeout 300 python -c "import __graft_entry__ as g; g.build()" > $OUT/build.log 2>&1
 i=0
 for E in "$@"; do
-  env $E timeout 300 python bench.py --steps 3 --warmup 3 --no-cpu-baseline > $OUT/b$i.log 2>&1
+  env $E timeout 300 python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-e2e --no-config5 > $OUT/b$i.log 2>&1
   python - "$OUT/b$i.log" "$E" <<'PY' >> $OUT/summary.txt
 import json, sys
 try:
