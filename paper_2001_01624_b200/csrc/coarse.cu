@@ -445,37 +445,6 @@ __global__ void __launch_bounds__(16 * ST) k_symv_reduce(const double* __restric
   symv_reduce_body<false>(part, M, ntb, xc, blockIdx.x, skip);
 }
 
-// k_symv_tiles + k_symv_reduce in one launch: every tile CTA publishes its partials
-// (fence, then one counter increment per output block it feeds); the CTA that brings an
-// output block's counter to ntb is the last contributor and sums that block's ntb
-// partial slots in the same fixed order k_symv_reduce uses (deterministic), then resets
-// the counter for the next solve.  Counters live after the partial slots (co.part).
-__global__ void __launch_bounds__(SYMV_T) k_symv_fused(const double* __restrict__ Xp, int M,
-                                                       int ntb, const double* __restrict__ rc,
-                                                       double* part, unsigned* cnt,
-                                                       double* __restrict__ xc, const int* done) {
-  symv_tile_body<false>(Xp, M, rc, part, blockIdx.x);
-  __threadfence();  // this CTA's partial slots are visible before its counter increments
-  __syncthreads();
-  __shared__ int last[2];
-  if (threadIdx.x == 0) {
-    int bi, bj;
-    symv_tile_rc(blockIdx.x, bi, bj);
-    last[0] = atomicAdd(cnt + bi, 1u) == (unsigned)ntb - 1 ? bi : -1;
-    last[1] = (bi != bj && atomicAdd(cnt + bj, 1u) == (unsigned)ntb - 1) ? bj : -1;
-  }
-  __syncthreads();
-  const bool skip = done && *(volatile const int*)done;
-#pragma unroll 1
-  for (int q = 0; q < 2; ++q) {
-    const int b = last[q];
-    if (b < 0) continue;
-    __threadfence();
-    symv_reduce_body<true>(part, M, ntb, xc, b, skip);
-    if (threadIdx.x == 0) cnt[b] = 0u;
-  }
-}
-
 // batched form (several packed matrices, vector rows through an optional index map):
 // one CTA per tile descriptor, one CTA per output-block descriptor
 __global__ void __launch_bounds__(SYMV_T) k_symv_tiles_b(const SymvTile* __restrict__ td,
@@ -498,52 +467,9 @@ __global__ void __launch_bounds__(16 * ST) k_symv_reduce_b(const SymvRow* __rest
   symv_reduce_body<false>(part + d.tile_base * 2 * ST, d.M, d.ntb, out, d.b, skip, omap, d.roff);
 }
 
-// batched k_symv_fused: tile CTAs count per output-block descriptor; the last contributor
-// of a block reduces it (fixed order, deterministic) and resets its counter
-__global__ void __launch_bounds__(SYMV_T) k_symv_fused_b(const SymvTile* __restrict__ td,
-                                                         const SymvRow* __restrict__ rd,
-                                                         const double* __restrict__ Xp,
-                                                         const double* __restrict__ vec,
-                                                         const int32_t* __restrict__ map,
-                                                         double* part, unsigned* cnt,
-                                                         double* __restrict__ out,
-                                                         const int32_t* __restrict__ omap,
-                                                         const int* done) {
-  const SymvTile d = td[blockIdx.x];
-  symv_tile_body<false>(Xp + d.tile_base * ST * ST, d.M, vec, part + d.tile_base * 2 * ST, d.t,
-                        map, d.roff);
-  __threadfence();
-  __syncthreads();
-  __shared__ int last[2];
-  if (threadIdx.x == 0) {
-    int bi, bj;
-    symv_tile_rc(d.t, bi, bj);
-    const unsigned ntb = (unsigned)((d.M + ST - 1) / ST);
-    last[0] = atomicAdd(cnt + d.rbase + bi, 1u) == ntb - 1 ? d.rbase + bi : -1;
-    last[1] = (bi != bj && atomicAdd(cnt + d.rbase + bj, 1u) == ntb - 1) ? d.rbase + bj : -1;
-  }
-  __syncthreads();
-  const bool skip = done && *(volatile const int*)done;
-#pragma unroll 1
-  for (int q = 0; q < 2; ++q) {
-    const int r = last[q];
-    if (r < 0) continue;
-    __threadfence();
-    const SymvRow R = rd[r];
-    symv_reduce_body<true>(part + R.tile_base * 2 * ST, R.M, R.ntb, out, R.b, skip, omap, R.roff);
-    if (threadIdx.x == 0) cnt[r] = 0u;
-  }
-}
-
 void symv_batched(msb_ctx ctx, const SymvTile* td, int ntile, const SymvRow* rd, int nrow,
                   const double* Xp, const double* vec, const int32_t* map, double* part,
-                  double* out, const int32_t* omap, const int* done, unsigned* cnt) {
-  if (cnt && xknob("MSB_X_SYMV", 1)) {
-    k_symv_fused_b<<<ntile, SYMV_T, 0, ctx->stream>>>(td, rd, Xp, vec, map, part, cnt, out, omap,
-                                                      done);
-    count_launch();
-    return;
-  }
+                  double* out, const int32_t* omap, const int* done) {
   k_symv_tiles_b<<<ntile, SYMV_T, 0, ctx->stream>>>(td, Xp, vec, map, part);
   k_symv_reduce_b<<<nrow, 16 * ST, 0, ctx->stream>>>(rd, part, out, omap, done);
   count_launch();
@@ -578,6 +504,10 @@ __global__ void __launch_bounds__(256) k_trmv_lower_t(const double* __restrict__
 }
 
 void coarse_solve(msb_ctx ctx, const Coarse& co, const double* rc, double* xc, const int* done) {
+  if (co.tri && co.small) {
+    coarse_solve_small(ctx, co, rc, xc, done);
+    return;
+  }
   if (co.tri) {
     const unsigned g = grid_for((int64_t)co.M * 32, 256);
     k_trmv_lower<<<g, 256, 0, ctx->stream>>>(co.Ainv, co.M, rc, co.tri_y);
@@ -601,10 +531,8 @@ msb_status coarse_pack_symmetric(msb_ctx ctx, Coarse& co) {
     dfree(ctx, co.Xp);
     dfree(ctx, co.part);
     MSB_ALLOC(ctx, co.Xp, double, nt * ST * ST);
-    MSB_ALLOC(ctx, co.part, double, nt * 2 * ST + ntb + 1);  // + k_symv_fused counters
+    MSB_ALLOC(ctx, co.part, double, nt * 2 * ST);
     co.xp_cap = nt;
-    MSB_CUDA_TRY(ctx, cudaMemsetAsync(co.part + nt * 2 * ST, 0, (ntb + 1) * sizeof(double),
-                                      ctx->stream));
   }
   co.ntb = ntb;
   k_pack_lower<<<(unsigned)nt, 256, 0, ctx->stream>>>(co.Ainv, M, ntb, co.Xp);
@@ -615,13 +543,6 @@ msb_status coarse_pack_symmetric(msb_ctx ctx, Coarse& co) {
 void coarse_solve_dense(msb_ctx ctx, const Coarse& co, const double* rc, double* xc,
                         const int* done) {
   const int64_t nt = (int64_t)co.ntb * (co.ntb + 1) / 2;
-  if (xknob("MSB_X_SYMV", 1)) {
-    unsigned* cnt = reinterpret_cast<unsigned*>(co.part + co.xp_cap * 2 * ST);
-    k_symv_fused<<<(unsigned)nt, SYMV_T, 0, ctx->stream>>>(co.Xp, co.M, co.ntb, rc, co.part, cnt,
-                                                           xc, done);
-    count_launch();
-    return;
-  }
   k_symv_tiles<<<(unsigned)nt, SYMV_T, 0, ctx->stream>>>(co.Xp, co.M, rc, co.part);
   k_symv_reduce<<<co.ntb, 16 * ST, 0, ctx->stream>>>(co.part, co.M, co.ntb, xc, done);
   count_launch();

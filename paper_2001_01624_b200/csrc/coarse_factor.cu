@@ -432,12 +432,123 @@ static msb_status lauum(msb_ctx ctx, const double* W, double* F, int n, int64_t 
   return lauum(ctx, W22, F22, n2, ld);
 }
 
+// ---------------------------------------------------------------- small SPD systems
+// One CTA: right-looking Cholesky of the M x M (M <= SMALL_CHOL_M) matrix A (row-major)
+// in shared memory, packed lower rows a[i (i+1)/2 + j]; column scaled by the pivot's
+// reciprocal (as LAPACK's potf2); the factor is written packed to Lp.  Pivot test as the
+// recursive path (d_jj <= 1e-14 max|A_c| -> singular).
+constexpr int SC_T = 512;
+__global__ void __launch_bounds__(SC_T) k_chol_small(const double* __restrict__ A, int M,
+                                                     double* __restrict__ Lp,
+                                                     const unsigned long long* amax_bits,
+                                                     int* __restrict__ singular) {
+  extern __shared__ double a[];
+  __shared__ double rinv;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int np = M * (M + 1) / 2;
+  for (int i = warp; i < M; i += SC_T / 32)
+    for (int j = lane; j <= i; j += 32) a[i * (i + 1) / 2 + j] = A[(int64_t)i * M + j];
+  __syncthreads();
+  const double tol = 1e-14 * __longlong_as_double((long long)*amax_bits);
+  for (int j = 0; j < M; ++j) {
+    const int jj = j * (j + 1) / 2 + j;
+    if (tid == 0) {
+      double d = a[jj];
+      if (!(d > tol)) {
+        *singular = 1;
+        d = 1.0;
+      }
+      const double p = sqrt(d);
+      a[jj] = p;
+      rinv = 1.0 / p;
+    }
+    __syncthreads();
+    for (int i = j + 1 + tid; i < M; i += SC_T) a[i * (i + 1) / 2 + j] *= rinv;
+    __syncthreads();
+    for (int i = j + 1 + warp; i < M; i += SC_T / 32) {
+      const int ri = i * (i + 1) / 2;
+      const double lij = a[ri + j];
+      for (int k = j + 1 + lane; k <= i; k += 32) a[ri + k] -= lij * a[k * (k + 1) / 2 + j];
+    }
+    __syncthreads();
+  }
+  for (int e = tid; e < np; e += SC_T) Lp[e] = a[e];
+}
+
+// x = L^{-T} L^{-1} r with the packed factor, one warp (forward then backward substitution)
+__global__ void __launch_bounds__(32) k_chol_small_solve(const double* __restrict__ Lp, int M,
+                                                         const double* __restrict__ r,
+                                                         double* __restrict__ x, const int* done) {
+  extern __shared__ double sm[];
+  double* L = sm;
+  double* y = sm + M * (M + 1) / 2;
+  const int lane = threadIdx.x;
+  const int np = M * (M + 1) / 2;
+  for (int e = lane; e < np; e += 32) L[e] = Lp[e];
+  for (int i = lane; i < M; i += 32) y[i] = r[i];
+  __syncwarp();
+  for (int j = 0; j < M; ++j) {  // L y = r, column-oriented
+    const double yj = y[j] / L[j * (j + 1) / 2 + j];
+    __syncwarp();
+    if (lane == 0) y[j] = yj;
+    for (int i = j + 1 + lane; i < M; i += 32) y[i] -= L[i * (i + 1) / 2 + j] * yj;
+    __syncwarp();
+  }
+  for (int j = M - 1; j >= 0; --j) {  // L^T x = y, row j of L holds column j of L^T
+    const int rj = j * (j + 1) / 2;
+    const double xj = y[j] / L[rj + j];
+    __syncwarp();
+    if (lane == 0) y[j] = xj;
+    for (int i = lane; i < j; i += 32) y[i] -= L[rj + i] * xj;
+    __syncwarp();
+  }
+  const bool skip = done && *(volatile const int*)done;
+  if (!skip)
+    for (int i = lane; i < M; i += 32) x[i] = y[i];
+}
+
+void coarse_solve_small(msb_ctx ctx, const Coarse& co, const double* rc, double* xc,
+                        const int* done) {
+  const int M = co.M;
+  const size_t smem = ((size_t)M * (M + 1) / 2 + M) * sizeof(double);
+  k_chol_small_solve<<<1, 32, smem, ctx->stream>>>(co.L, M, rc, xc, done);
+  count_launch();
+}
+
 msb_status coarse_factor_dense(msb_ctx ctx, Coarse& co) {
   const int M = co.M;
   cudaStream_t s = ctx->stream;
   if (!co.flags) MSB_ALLOC(ctx, co.flags, unsigned long long, 2);
   unsigned long long* amax = co.flags;
   int* sing = reinterpret_cast<int*>(co.flags + 1);
+  co.small = co.tri && M <= SMALL_CHOL_M;
+  if (co.small) {
+    if (!co.L) MSB_ALLOC(ctx, co.L, double, (int64_t)co.cap * co.cap);
+    MSB_CUDA_TRY(ctx, cudaMemsetAsync(co.flags, 0, 16, s));
+    k_absmax2<<<std::min<int64_t>(grid_for((int64_t)M * M, 256), 4 * ctx->sm_count), 256, 0, s>>>(
+        co.Ac, (int64_t)M * M, amax);
+    MSB_LAUNCH_CHECK(ctx);
+    static bool attr = false;
+    if (!attr) {
+      const int mx = (int)(((size_t)SMALL_CHOL_M * (SMALL_CHOL_M + 1) / 2 + SMALL_CHOL_M) * sizeof(double));
+      MSB_CUDA_TRY(ctx, cudaFuncSetAttribute(k_chol_small, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+      MSB_CUDA_TRY(ctx, cudaFuncSetAttribute(k_chol_small_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+      attr = true;
+    }
+    k_chol_small<<<1, SC_T, (size_t)M * (M + 1) / 2 * sizeof(double), s>>>(co.Ac, M, co.L, amax, sing);
+    MSB_LAUNCH_CHECK(ctx);
+    int hs = 0;
+    if (!co.defer_check) {
+      MSB_CUDA_TRY(ctx, cudaMemcpyAsync(&hs, sing, 4, cudaMemcpyDeviceToHost, s));
+      MSB_CUDA_TRY(ctx, cudaStreamSynchronize(s));
+    }
+    if (hs) {
+      co.ready = false;
+      return set_error(ctx, MSB_ESINGULAR, "singular coarse matrix: pivot <= 1e-14 max|A_c| (M=%d)", M);
+    }
+    co.ready = true;
+    return MSB_OK;
+  }
   if (!co.L) MSB_ALLOC(ctx, co.L, double, (int64_t)M * M);
   if (!co.Ainv) MSB_ALLOC(ctx, co.Ainv, double, (int64_t)M * M);
   double* F = co.L;

@@ -42,7 +42,6 @@ struct Schur {
   int32_t* sep_nodes = nullptr;  // [nS]
   double* Xd = nullptr;          // packed tiles of every A_dd^{-1}
   double* partd = nullptr;
-  unsigned* cntd = nullptr;      // fused-SYMV counters (inside partd)
   SymvTile* td = nullptr;        // domain tile / row descriptors
   SymvRow* rd = nullptr;
   int ntd = 0, nrd = 0;
@@ -259,8 +258,7 @@ static void describe(int m, int64_t tile_base, int roff, std::vector<SymvTile>& 
                      std::vector<SymvRow>& rd) {
   const int ntb = (m + ST - 1) / ST;
   const int64_t nt = (int64_t)ntb * (ntb + 1) / 2;
-  const int rbase = (int)rd.size();
-  for (int64_t t = 0; t < nt; ++t) td.push_back(SymvTile{tile_base, m, roff, (int)t, rbase});
+  for (int64_t t = 0; t < nt; ++t) td.push_back(SymvTile{tile_base, m, roff, (int)t});
   for (int b = 0; b < ntb; ++b) rd.push_back(SymvRow{tile_base, m, ntb, b, roff});
 }
 
@@ -370,11 +368,7 @@ msb_status coarse_schur_setup(msb_ctx ctx, Coarse& co, const msb_level_s& L) {
   S->rd = upload(ctx, rd);
   S->ntd = (int)td.size();
   S->nrd = (int)rd.size();
-  // partial slots, then the fused SYMV's per-output-block counters (zeroed; every solve
-  // leaves them zero)
-  MSB_ALLOC(ctx, S->partd, double, tbase[pl.nd] * 2 * ST + S->nrd + 1);
-  S->cntd = reinterpret_cast<unsigned*>(S->partd + tbase[pl.nd] * 2 * ST);
-  MSB_CUDA_TRY(ctx, cudaMemsetAsync(S->cntd, 0, (S->nrd + 1) * sizeof(double), st));
+  MSB_ALLOC(ctx, S->partd, double, tbase[pl.nd] * 2 * ST);
   if (!S->td || !S->rd) return set_error(ctx, MSB_ENOMEM, "schur descriptors");
   // the Schur complement starts as A_SS
   Coarse& C = S->C;
@@ -482,21 +476,20 @@ void coarse_schur_solve(msb_ctx ctx, const Coarse& co, const double* rc, double*
   const int n0 = co.nb[0], n1 = co.nb[1], n2 = co.nb[2];
   // y_d = A_dd^{-1} r_d (r_c read through the domain node map)
   symv_batched(ctx, S->td, S->ntd, S->rd, S->nrd, S->Xd, rc, S->dom_nodes, S->partd, S->y, nullptr,
-               nullptr, S->cntd);
+               nullptr);
   k_schur_t<<<grid_for((int64_t)S->nS * 32, 256), 256, 0, st>>>(co.Aell, n0, n1, n2, S->sep_nodes,
                                                                  S->nS, S->node_pos, rc, S->y,
                                                                  S->t);
   count_launch();
   symv_batched(ctx, S->tc, S->ntc, S->rcd, S->nrc, S->C.Xp, S->t, nullptr, S->C.part, S->xs,
-               nullptr, nullptr,
-               reinterpret_cast<unsigned*>(S->C.part + S->C.xp_cap * 2 * ST));
+               nullptr, nullptr);
   const int64_t wu = (int64_t)S->nD + (S->nS + 31) / 32;  // warps
   k_schur_u<<<grid_for(wu * 32, 256), 256, 0, st>>>(co.Aell, n0, n1, n2, S->dom_nodes, S->nD,
                                                      S->sep_nodes, S->nS, S->node_pos, rc, S->xs,
                                                      S->u, xc, done);
   count_launch();
   symv_batched(ctx, S->td, S->ntd, S->rd, S->nrd, S->Xd, S->u, nullptr, S->partd, xc, S->dom_nodes,
-               done, S->cntd);
+               done);
 }
 
 }  // namespace msb

@@ -1,24 +1,9 @@
-#include <map>
-#include <mutex>
-#include <cstdlib>
 // Context, allocation, host|dev staging, error reporting, device scan.
 #include "internal.cuh"
 
 namespace msb {
 
 std::atomic<int64_t> g_launches{0};
-
-int xknob(const char* name, int def) {
-  static std::mutex mu;
-  static std::map<std::string, int> cache;
-  std::lock_guard<std::mutex> lk(mu);
-  auto it = cache.find(name);
-  if (it != cache.end()) return it->second;
-  const char* v = getenv(name);
-  const int r = v ? atoi(v) : def;
-  cache[name] = r;
-  return r;
-}
 
 msb_status set_error(msb_ctx ctx, msb_status code, const char* fmt, ...) {
   if (ctx) {

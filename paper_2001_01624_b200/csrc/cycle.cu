@@ -159,6 +159,8 @@ __global__ void __launch_bounds__(CT) k_norm(StencilT S, const double* __restric
 // CPT cells per thread (strided by the block size, so every load instruction stays
 // coalesced): the loads of all CPT cells are in flight together and the grid is CPT
 // times shorter, which is what a short stencil pass needs to approach HBM bandwidth.
+constexpr int CPT = 4;
+
 template <int CPT>
 __global__ void __launch_bounds__(CT) k_jacobi(StencilT S, const double* __restrict__ x,
                                                double* __restrict__ xo,
@@ -189,25 +191,7 @@ __global__ void __launch_bounds__(CT) k_jacobi(StencilT S, const double* __restr
   if (first) warp_partial(v, partials);
 }
 
-// L2 eviction-priority hints (createpolicy + ld.global.L2::cache_hint)
-__device__ __forceinline__ uint64_t pol_evict_last() {
-  uint64_t p;
-  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
-  return p;
-}
-__device__ __forceinline__ uint64_t pol_evict_first() {
-  uint64_t p;
-  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
-  return p;
-}
-__device__ __forceinline__ double ld_pol(const double* a, uint64_t pol) {
-  double v;
-  asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(a), "l"(pol));
-  return v;
-}
-
 struct LevelView {
-  int hint;  // experiment: 1 = P kept in L2 by the restriction, dropped by the prolongation
   int kind, W, nb0, nb1, nb2, b0, b1, b2;
   Grid3 g;
   const int32_t* tab;
@@ -663,7 +647,6 @@ __device__ __forceinline__ void restrict_row_body(const LevelView& L, const doub
     a0[e] = a1[e] = 0.0;
     xok[e] = xo + XL * e < nx;
   }
-  const uint64_t pol = L.hint ? pol_evict_last() : 0;
   int row = rg + RG * rank;
   int zz = row / wy, yy = row - zz * wy;
   const int step = RG * CS;
@@ -678,13 +661,8 @@ __device__ __forceinline__ void restrict_row_body(const LevelView& L, const doub
 #pragma unroll
       for (int e = 0; e < XP; ++e) {
         const bool v = ok && xok[e];
-        if (L.hint) {
-          p0[u][e] = v ? ld_pol(P0 + c + XL * e, pol) : 0.0;
-          p1[u][e] = v ? ld_pol(P1 + c + XL * e, pol) : 0.0;
-        } else {
-          p0[u][e] = v ? P0[c + XL * e] : 0.0;
-          p1[u][e] = v ? P1[c + XL * e] : 0.0;
-        }
+        p0[u][e] = v ? P0[c + XL * e] : 0.0;
+        p1[u][e] = v ? P1[c + XL * e] : 0.0;
         rv[u][e] = v ? r[c + XL * e] : 0.0;
       }
       row += step;
@@ -754,6 +732,10 @@ __global__ void __launch_bounds__(RR2_THREADS) k_restrict_cart(LevelView L,
   restrict_row_body<XP, CS>(L, r, rc, blockIdx.x / CS, rsh, is_done(st));
 }
 
+// CTAs (one cluster) per (Jy, Jz) unit: 680 instead of 340 CTAs on config 2's 148 SMs
+// (measured 70.6 against 72.0 us per iteration; 4 per unit gave no further gain)
+constexpr int RCS = 2;
+
 static inline int restrict_xp(int nx) {
   return nx <= 256 ? 1 : (nx <= 512 ? 2 : (nx <= 1024 ? 4 : 8));
 }
@@ -815,14 +797,13 @@ __global__ void __launch_bounds__(CT) k_prolong_cart(LevelView L, double* __rest
   const int2 ty = reinterpret_cast<const int2*>(L.tab)[L.g.nx + j];
   const int2 tz = reinterpret_cast<const int2*>(L.tab)[L.g.nx + L.g.ny + k];
   const double* __restrict__ base = L.P + c;
-  const uint64_t pol = L.hint ? pol_evict_first() : 0;
   double v[8], xv[8];
 #pragma unroll
   for (int s = 0; s < 8; ++s) {
     const int jx = (s & 1) ? tx.y : tx.x, jy = (s & 2) ? ty.y : ty.x, jz = (s & 4) ? tz.y : tz.x;
     const bool act = (jx | jy | jz) >= 0;
     const int col = jx + L.nb0 * (jy + L.nb1 * jz);
-    v[s] = act ? (L.hint ? ld_pol(base + (size_t)s * N, pol) : base[(size_t)s * N]) : 0.0;
+    v[s] = act ? base[(size_t)s * N] : 0.0;
     xv[s] = act ? xc[col] : 0.0;
   }
   double acc = 0.0;
@@ -1007,7 +988,7 @@ static StencilT stencil(msb_op op) {
 }
 
 static LevelView view(msb_level L) {
-  return LevelView{xknob("MSB_X_L2HINT", 0), L->kind, L->W, L->nb[0], L->nb[1], L->nb[2], L->bs[0], L->bs[1], L->bs[2],
+  return LevelView{L->kind, L->W, L->nb[0], L->nb[1], L->nb[2], L->bs[0], L->bs[1], L->bs[2],
                    make_grid3(L->nx, L->ny, L->nz), L->tab, L->col, L->P[L->cur],
                    (L->kind == 1 && L->W == 1 && L->unity) ? 1 : 0};
 }
@@ -1256,14 +1237,8 @@ msb_status msb_add_dynamic_basis(msb_ctx ctx, msb_solver s, const double* dp, in
 // Enqueue one stage (level L) on x buffers; `first` marks the iteration's first kernel.
 // Enqueue one stage (level L) on the x double buffer; `first` marks the iteration's
 // first kernel, which also emits the stop-test partials (finalised right after).
-#define RES_LAUNCH(...)                                                   \
-  (cpt == 8   ? k_residual<8><<<g4, CT, 0, st>>>(__VA_ARGS__)              \
-   : cpt == 2 ? k_residual<2><<<g4, CT, 0, st>>>(__VA_ARGS__)              \
-              : k_residual<4><<<g4, CT, 0, st>>>(__VA_ARGS__))
-#define JAC_LAUNCH(...)                                                   \
-  (cpt == 8   ? k_jacobi<8><<<g4, CT, 0, st>>>(__VA_ARGS__)                \
-   : cpt == 2 ? k_jacobi<2><<<g4, CT, 0, st>>>(__VA_ARGS__)                \
-              : k_jacobi<4><<<g4, CT, 0, st>>>(__VA_ARGS__))
+#define RES_LAUNCH(...) k_residual<CPT><<<g4, CT, 0, st>>>(__VA_ARGS__)
+#define JAC_LAUNCH(...) k_jacobi<CPT><<<g4, CT, 0, st>>>(__VA_ARGS__)
 
 static msb_status enqueue_stage(msb_ctx ctx, msb_solver s, msb_level L, const double* b, int& cur,
                                 bool& first) {
@@ -1273,8 +1248,7 @@ static msb_status enqueue_stage(msb_ctx ctx, msb_solver s, msb_level L, const do
   StencilT S = stencil(op);
   LevelView V = view(L);
   unsigned g = grid_for(N, CT);
-  const int cpt = xknob("MSB_X_CPT", 4);
-  const unsigned g4 = grid_for(N, CT * cpt);  // multi-cell stencil kernels
+  const unsigned g4 = grid_for(N, CT * CPT);  // multi-cell stencil kernels
   // With one pre-smoothed level and nu = 1 no kernel of an iteration writes the buffer
   // holding x_{k-1}, so the stop test's finalize runs on a side branch in parallel with
   // the rest of the iteration and is joined before the next iteration's first kernel
@@ -1372,12 +1346,9 @@ static msb_status enqueue_stage(msb_ctx ctx, msb_solver s, msb_level L, const do
         const int xp = restrict_xp(op->nx);
         const size_t smem = restrict_rows_smem(op->nx);
         const unsigned gr = (unsigned)(L->nb[1] * L->nb[2]);
-        const int cs = xknob("MSB_X_RCS", 1);
         msb_status rc = MSB_OK;
-#define MSB_RESTRICT_CS(XPV)                                                              \
-  rc = cs == 4 ? launch_restrict<XPV, 4>(ctx, st, gr, smem, V, s->r, s->rc, s->st)        \
-       : cs == 2 ? launch_restrict<XPV, 2>(ctx, st, gr, smem, V, s->r, s->rc, s->st)      \
-                 : launch_restrict<XPV, 1>(ctx, st, gr, smem, V, s->r, s->rc, s->st)
+#define MSB_RESTRICT_CS(XPV) \
+  rc = launch_restrict<XPV, RCS>(ctx, st, gr, smem, V, s->r, s->rc, s->st)
         if (xp == 1) MSB_RESTRICT_CS(1);
         else if (xp == 2) MSB_RESTRICT_CS(2);
         else if (xp == 4) MSB_RESTRICT_CS(4);
@@ -1698,6 +1669,11 @@ msb_status msb_ms_iterate(msb_ctx ctx, msb_solver s, const double* b, double* x,
     // a singular flag left by an earlier call (a failed rebuild) must not fail this one
     // before it has rebuilt anything: only this call's rebuilds may set it
     if (D->co.flags) MSB_CUDA_TRY(ctx, cudaMemsetAsync(D->co.flags + 1, 0, sizeof(int), st));
+    if (!s->dyn_stream) {
+      MSB_CUDA_TRY(ctx, cudaStreamCreateWithFlags(&s->dyn_stream, cudaStreamNonBlocking));
+      MSB_CUDA_TRY(ctx, cudaEventCreateWithFlags(&s->ev_dp, cudaEventDisableTiming));
+      MSB_CUDA_TRY(ctx, cudaEventCreateWithFlags(&s->ev_dyn, cudaEventDisableTiming));
+    }
     while (true) {
       if ((rc = enqueue_norm(ctx, s, s->xbuf[cur], db, 0))) return rc;
       MSB_CUDA_TRY(ctx, cudaMemcpyAsync(&hs, s->st, sizeof(hs), cudaMemcpyDeviceToHost, st));
@@ -1711,20 +1687,34 @@ msb_status msb_ms_iterate(msb_ctx ctx, msb_solver s, const double* b, double* x,
       if (hs.done) break;
       int k = hs.k;  // iteration about to run (1-based)
       int32_t M = 0;
-      if (k >= 2) {
+      const bool rebuild = k >= 2;
+      if (rebuild) {
         k_dp<<<grid_for(N, 256), 256, 0, st>>>(s->xbuf[cur], s->xprev, N, s->dpbuf);
         MSB_LAUNCH_CHECK(ctx);
-        D->co.defer_check = true;
-        rc = build_dynamic(ctx, s, s->dpbuf, &M, nullptr);
-        D->co.defer_check = false;
-        if (rc) return rc;
+        MSB_CUDA_TRY(ctx, cudaEventRecord(s->ev_dp, st));
       }
-      dynM.push_back(M);
       MSB_CUDA_TRY(ctx, cudaMemcpyAsync(s->xprev, s->xbuf[cur], N * sizeof(double),
                                         cudaMemcpyDeviceToDevice, st));
+      // The static stages do not depend on the new partition: they are enqueued first and
+      // run on the context stream while the rebuild (bins, components, merge, numbering,
+      // A_c, factor) runs on the solver's rebuild stream; the dynamic stage waits for both.
+      // The rebuild only touches its own scratch and the dynamic level, whose last reader
+      // (the previous iteration's dynamic stage) precedes the Δp kernel the rebuild waits on.
       bool first = false;  // norm already taken
       for (msb_level L : s->levels)
         if ((rc = enqueue_stage(ctx, s, L, db, cur, first))) return rc;
+      if (rebuild) {
+        MSB_CUDA_TRY(ctx, cudaStreamWaitEvent(s->dyn_stream, s->ev_dp, 0));
+        D->co.defer_check = true;
+        ctx->stream = s->dyn_stream;
+        rc = build_dynamic(ctx, s, s->dpbuf, &M, nullptr);
+        ctx->stream = st;
+        D->co.defer_check = false;
+        if (rc) return rc;
+        MSB_CUDA_TRY(ctx, cudaEventRecord(s->ev_dyn, s->dyn_stream));
+        MSB_CUDA_TRY(ctx, cudaStreamWaitEvent(st, s->ev_dyn, 0));
+      }
+      dynM.push_back(M);
       if (M > 0)
         if ((rc = enqueue_stage(ctx, s, s->dyn_level, db, cur, first))) return rc;
       cur_after.push_back(cur);
@@ -1776,6 +1766,9 @@ msb_status msb_solver_destroy(msb_solver s) {
   if (s->side_stream) cudaStreamDestroy(s->side_stream);
   if (s->ev_fork) cudaEventDestroy(s->ev_fork);
   if (s->ev_join) cudaEventDestroy(s->ev_join);
+  if (s->dyn_stream) cudaStreamDestroy(s->dyn_stream);
+  if (s->ev_dp) cudaEventDestroy(s->ev_dp);
+  if (s->ev_dyn) cudaEventDestroy(s->ev_dyn);
   delete s;
   return MSB_OK;
 }
@@ -1805,10 +1798,10 @@ msb_status level_restrict(msb_ctx ctx, msb_level L, const double* r, double* rc,
   const unsigned gr = (unsigned)(L->nb[1] * L->nb[2]);
   const int xp = restrict_xp(L->nx);
   cudaStream_t st = ctx->stream;
-  msb_status rc2 = xp == 1   ? launch_restrict<1, 1>(ctx, st, gr, smem, V, r, rc, ist)
-                   : xp == 2 ? launch_restrict<2, 1>(ctx, st, gr, smem, V, r, rc, ist)
-                   : xp == 4 ? launch_restrict<4, 1>(ctx, st, gr, smem, V, r, rc, ist)
-                             : launch_restrict<8, 1>(ctx, st, gr, smem, V, r, rc, ist);
+  msb_status rc2 = xp == 1   ? launch_restrict<1, RCS>(ctx, st, gr, smem, V, r, rc, ist)
+                   : xp == 2 ? launch_restrict<2, RCS>(ctx, st, gr, smem, V, r, rc, ist)
+                   : xp == 4 ? launch_restrict<4, RCS>(ctx, st, gr, smem, V, r, rc, ist)
+                             : launch_restrict<8, RCS>(ctx, st, gr, smem, V, r, rc, ist);
   if (rc2) return rc2;
   MSB_LAUNCH_CHECK(ctx);
   return MSB_OK;

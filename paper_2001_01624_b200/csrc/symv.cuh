@@ -90,10 +90,20 @@ __device__ __forceinline__ void symv_reduce_body(const double* part, int M, int 
   const int i = threadIdx.x & (ST - 1), g = threadIdx.x / ST, G = blockDim.x / ST;
   const int64_t rowbase = (int64_t)b * (b + 1) / 2;
   double v = 0.0;
-  for (int e = g; e < ntb; e += G) {
-    const int64_t off = e <= b ? (rowbase + e) * 2 * ST + i
-                               : ((int64_t)e * (e + 1) / 2 + b) * 2 * ST + ST + i;
-    v += ld_mut<CG>(part + off);
+  // batches of 8 independent loads in flight, then summed in order (the same order as one
+  // load at a time: deterministic, identical result)
+  for (int e0 = g; e0 < ntb; e0 += 8 * G) {
+    double t[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int e = e0 + u * G;
+      const int64_t off = e <= b ? (rowbase + e) * 2 * ST + i
+                                 : ((int64_t)e * (e + 1) / 2 + b) * 2 * ST + ST + i;
+      t[u] = e < ntb ? ld_mut<CG>(part + off) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (e0 + u * G < ntb) v += t[u];
   }
   __shared__ double sh[16][ST];
   sh[g][i] = v;

@@ -165,6 +165,60 @@ def config4(args):
     print(json.dumps(rec), flush=True)
 
 
+def config_cpr(cfg, args):
+    """§8 NEXT-4 on config `cfg`'s grid (default the 1.122M-cell config-2 grid): the
+    compressible two-phase Newton system at a synthetic state (synth.configs.cpr_state),
+    linearize, quasi-IMPES decoupling + predictor/corrector setup, one CPR application,
+    FGMRES(40) to 1e-8 with CPR and with ILU(0) alone; CUDA events on the library stream."""
+    from paper_2001_01624_b200 import Cpr
+    from synth.configs import cpr_state
+    prob = make_problem(cfg)
+    st_ = cpr_state(prob)
+    ctx = Context(0)
+    st = torch.cuda.current_stream()
+    op = gp.build_operator(ctx, prob)
+    lev = Level.cartesian(ctx, op, prob.block)
+    lev.smooth(op, prob.max_sweeps, prob.omega, prob.sweep_tol)
+    fl = dict(mu_w=1.0, mu_o=5.0, rho_w=1000.0, rho_o=800.0, c_w=4e-5, c_o=1e-4, c_r=3e-5,
+              phi=0.2, p_ref=100.0, dt=0.05, nrel=2)
+    c = Cpr(ctx, op, lev, fl, n_cycles=args.cycles)
+    N = prob.N
+    q = np.zeros(N)
+    np.add.at(q, st_.well_cells, st_.well_rates)
+    dev = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
+    p, S, pn, Sn, qd = dev(st_.p), dev(st_.S), dev(st_.p_n), dev(st_.S_n), dev(q)
+    c.linearize(p, S, pn, Sn, qd)
+    c.decouple("quasi")  # warm-up
+    torch.cuda.synchronize()
+    e0 = ev(st)
+    c.linearize(p, S, pn, Sn, qd)
+    e1 = ev(st)
+    c.decouple("quasi")
+    e2 = ev(st)
+    r = torch.randn(2 * N, dtype=torch.float64, device="cuda")
+    dx = torch.empty_like(r)
+    c.apply(r, dx)
+    torch.cuda.synchronize()
+    e3 = ev(st)
+    for _ in range(10):
+        c.apply(r, dx)
+    e4 = ev(st)
+    torch.cuda.synchronize()
+    out = {}
+    for pre in ("cpr", "ilu0"):
+        x = torch.zeros(2 * N, dtype=torch.float64, device="cuda")
+        a = ev(st)
+        g = c.fgmres(x, None, tol=1e-8, restart=40, max_iter=args.max_iter or 400, precond=pre)
+        b = ev(st)
+        torch.cuda.synchronize()
+        out[pre] = dict(iters=g["iters"], converged=g["converged"], ms=a.elapsed_time(b),
+                        final=float(g["res"][-1]))
+    rec = dict(workload=f"cpr on config{cfg} grid", N=N, M=lev.info()["M"], n_cycles=args.cycles,
+               linearize_ms=e0.elapsed_time(e1), decouple_setup_ms=e1.elapsed_time(e2),
+               apply_ms=e3.elapsed_time(e4) / 10, fgmres=out)
+    print(json.dumps(rec), flush=True)
+
+
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("config", type=int)
@@ -172,8 +226,13 @@ if __name__ == "__main__":
     ap.add_argument("--sweeps", type=int, default=0)
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--static", action="store_true", help="NEXT-3 static levels vs none")
+    ap.add_argument("--cpr", action="store_true", help="NEXT-4 CPR on the config's grid")
+    ap.add_argument("--cycles", type=int, default=1)
+    ap.add_argument("--max-iter", type=int, default=0)
     a = ap.parse_args()
-    if a.static:
+    if a.cpr:
+        config_cpr(a.config, a)
+    elif a.static:
         config_static(a.config, a)
     elif a.config in (1, 3):
         config_pipeline(a.config, a)
