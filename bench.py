@@ -365,6 +365,7 @@ def run_gpu(args):
                          f"the full config2 grid, single thread",
                "ms_per_iteration": s.get("ms_per_iteration"), "cpu": model, "host_cores": cores}
     c5 = None if args.no_config5 else config5_measure(ctx, stream, local, peak, src)
+    cpr = None if args.no_cpr else cpr_measure(ctx, stream, local)
     e2e_t = sum(t for t, _ in e2e) or float("nan")
     e2e_sw = sum(n for _, n in e2e)
     line = {
@@ -389,6 +390,7 @@ def run_gpu(args):
         "roofline_sweep": roof_sweep,
         "roofline_cycle": roof_cycle,
         "config5": c5,
+        "next4_cpr": cpr,
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_sw / e2e_t, "unit": "sweeps/s",
                 "ms_per_step": 1e3 * e2e_t / max(1, len(e2e)),
@@ -471,6 +473,58 @@ def config5_measure(ctx, stream, local, peak, src):
     return res
 
 
+def cpr_measure(ctx, stream, local):
+    """SURVEY §8.f NEXT-4 on the config-2 grid (1.122M cells, M = 3,400): the compressible
+    two-phase Newton system at a seeded synthetic state (synth.configs.cpr_state), timed with
+    CUDA events on the library stream after one untimed pass — linearize (F, J), quasi-IMPES
+    decoupling + predictor (A_c = P^T J*_pp P, Gauss–Jordan inverse) + corrector (ILU(0))
+    setup, one CPR application, and FGMRES(40) to 1e-8 with the CPR preconditioner."""
+    import numpy as np
+    import torch
+    from paper_2001_01624_b200 import Cpr, Level
+    from paper_2001_01624_b200 import pipeline as gp
+    from synth.configs import cpr_state, make_problem
+
+    prob = make_problem(2)
+    stt = cpr_state(prob)
+    op = gp.build_operator(ctx, prob)
+    lev = Level.cartesian(ctx, op, prob.block)
+    lev.smooth(op, prob.max_sweeps, prob.omega, prob.sweep_tol)
+    fl = dict(mu_w=1.0, mu_o=5.0, rho_w=1000.0, rho_o=800.0, c_w=4e-5, c_o=1e-4, c_r=3e-5,
+              phi=0.2, p_ref=100.0, dt=0.05, nrel=2)
+    c = Cpr(ctx, op, lev, fl)
+    N = prob.N
+    q = np.zeros(N)
+    np.add.at(q, stt.well_cells, stt.well_rates)
+    dev = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(f"cuda:{local}")
+    p, S, pn, Sn, qd = dev(stt.p), dev(stt.S), dev(stt.p_n), dev(stt.S_n), dev(q)
+    r = torch.from_numpy(np.random.default_rng(0).standard_normal(2 * N)).to(f"cuda:{local}")
+    dx = torch.empty_like(r)
+    out = {}
+    for rep in range(2):
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(6)]
+        ev[0].record(stream)
+        c.linearize(p, S, pn, Sn, qd)
+        ev[1].record(stream)
+        c.decouple("quasi")
+        ev[2].record(stream)
+        c.apply(r, dx)
+        ev[3].record(stream)
+        x = torch.zeros(2 * N, dtype=torch.float64, device=f"cuda:{local}")
+        ev[4].record(stream)
+        g = c.fgmres(x, None, tol=1e-8, restart=40, max_iter=400, precond="cpr")
+        ev[5].record(stream)
+        torch.cuda.synchronize()
+        t = [ev[i].elapsed_time(ev[i + 1]) for i in range(5)]
+        out = {"workload": "config-2 grid (1.122M cells), compressible two-phase Newton system "
+                           "at a seeded synthetic state, quasi-IMPES, M = 3,400",
+               "linearize_ms": t[0], "decouple_setup_ms": t[1], "cpr_apply_ms": t[2],
+               "fgmres_iterations": g["iters"], "fgmres_converged": bool(g["converged"]),
+               "fgmres_ms": t[4], "fgmres_final_rel_residual": float(g["res"][-1])}
+    c.close(); lev.close(); op.close()
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -481,6 +535,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer e2e steps "
                     "(ncu launch-list runs)")
+    ap.add_argument("--no-cpr", action="store_true", help="skip the NEXT-4 CPR block")
     ap.add_argument("--no-config5", action="store_true", help="skip the 10M-cell config-5 "
                     "sweep / cycle measurement")
     ap.add_argument("--cpu-sweeps", type=int, default=20)

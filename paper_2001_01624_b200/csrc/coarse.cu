@@ -595,12 +595,11 @@ static msb_status coarse_assemble_cart(msb_ctx ctx, msb_level L, msb_op op) {
     MSB_ALLOC(ctx, co.Aell, double, n);
     co.ell_cap = M;
   }
-  unsigned long long* tmax = co.acc + 2 * n;
   int* bad = reinterpret_cast<int*>(co.acc + 2 * n + 1);
   MSB_CUDA_TRY(ctx, cudaMemsetAsync(co.acc, 0, (2 * n + 2) * sizeof(unsigned long long), st));
-  k_absmax_t<<<std::min<int64_t>(grid_for(3 * op->N, 256), 4 * ctx->sm_count), 256, 0, st>>>(
-      op->Tx, 3 * op->N, tmax);
-  MSB_LAUNCH_CHECK(ctx);
+  const unsigned long long* tmax_c = nullptr;
+  if (msb_status r0 = op_tmax(ctx, op, &tmax_c)) return r0;
+  unsigned long long* tmax = const_cast<unsigned long long*>(tmax_c);
   if (L->unity)
     k_rap<true, true, true><<<grid_for(L->N, 128), 128, 0, st>>>(*L, L->P[L->cur], op->Tx, op->Ty,
                                                                 op->Tz, nullptr, co.acc, tmax, bad);
@@ -646,6 +645,19 @@ msb_status coarse_assemble(msb_ctx ctx, msb_level L, msb_op op) {
   return coarse_assemble_dense(ctx, L, op);
 }
 
+msb_status op_tmax(msb_ctx ctx, msb_op op, const unsigned long long** out) {
+  if (!op->tmax) MSB_ALLOC(ctx, op->tmax, unsigned long long, 1);
+  if (!op->tmax_valid) {
+    MSB_CUDA_TRY(ctx, cudaMemsetAsync(op->tmax, 0, 8, ctx->stream));
+    k_absmax_t<<<std::min<int64_t>(grid_for(3 * op->N, 256), 4 * ctx->sm_count), 256, 0, ctx->stream>>>(
+        op->Tx, 3 * op->N, op->tmax);
+    MSB_LAUNCH_CHECK(ctx);
+    op->tmax_valid = true;
+  }
+  *out = op->tmax;
+  return MSB_OK;
+}
+
 msb_status coarse_assemble_dense(msb_ctx ctx, msb_level L, msb_op op) {
   int M = L->M;
   Coarse& co = L->co;
@@ -674,9 +686,9 @@ msb_status coarse_assemble_dense(msb_ctx ctx, msb_level L, msb_op op) {
     }
     unsigned long long* tmax = co.acc + 2 * n;
     MSB_CUDA_TRY(ctx, cudaMemsetAsync(co.acc, 0, (2 * n + 1) * sizeof(unsigned long long), st));
-    k_absmax_t<<<std::min<int64_t>(grid_for(3 * op->N, 256), 4 * ctx->sm_count), 256, 0, st>>>(
-        op->Tx, 3 * op->N, tmax);
-    MSB_LAUNCH_CHECK(ctx);
+    const unsigned long long* tmax_c = nullptr;
+    if (msb_status r0 = op_tmax(ctx, op, &tmax_c)) return r0;
+    tmax = const_cast<unsigned long long*>(tmax_c);
     if (constant) {
       k_rap_const_det<<<grid_for(op->N, 256), 256, 0, st>>>(
           L->col, make_grid3(op->nx, op->ny, op->nz), M, op->Tx, op->Ty, op->Tz, tmax, co.acc);

@@ -157,13 +157,7 @@ __global__ void k_scan_total(const int32_t* __restrict__ in, const int32_t* __re
 
 // Exclusive prefix sum of n int32 (device); *total (host, optional) = sum of all, read
 // back with one synchronisation.  Scratch is the context's, reused across calls.
-msb_status scan_exclusive(msb_ctx ctx, const int32_t* in, int32_t* out, int64_t n,
-                          int32_t* total, const void* extra_dev, void* extra_host,
-                          size_t extra_bytes) {
-  if (n <= 0) {
-    if (total) *total = 0;
-    return MSB_OK;
-  }
+msb_status scan_reserve(msb_ctx ctx, int64_t n) {
   int64_t need = 1;  // the total word, then sums|offs of every level scan_level visits
   for (int64_t m = n;;) {
     const int64_t nb = (m + SCAN_BLOCK - 1) / SCAN_BLOCK;
@@ -178,6 +172,32 @@ msb_status scan_exclusive(msb_ctx ctx, const int32_t* in, int32_t* out, int64_t 
     MSB_ALLOC(ctx, ctx->scan_scr, int32_t, need);
     ctx->scan_cap = need;
   }
+  return MSB_OK;
+}
+
+// scan_exclusive without the readback: the total is left in device memory (*total_dev,
+// valid until the next scan); no host synchronisation, so it can be graph-captured.  The
+// scratch must have been sized by scan_reserve(n) first.
+msb_status scan_exclusive_async(msb_ctx ctx, const int32_t* in, int32_t* out, int64_t n,
+                                const int32_t** total_dev) {
+  if (n <= 0 || ctx->scan_cap < 1) return set_error(ctx, MSB_EINVAL, "scan_exclusive_async: scratch");
+  msb_status st = scan_level(ctx, in, out, n, ctx->scan_scr + 1);
+  if (st != MSB_OK) return st;
+  k_scan_total<<<1, 1, 0, ctx->stream>>>(in, out, n, ctx->scan_scr);
+  MSB_LAUNCH_CHECK(ctx);
+  *total_dev = ctx->scan_scr;
+  return MSB_OK;
+}
+
+msb_status scan_exclusive(msb_ctx ctx, const int32_t* in, int32_t* out, int64_t n,
+                          int32_t* total, const void* extra_dev, void* extra_host,
+                          size_t extra_bytes) {
+  if (n <= 0) {
+    if (total) *total = 0;
+    return MSB_OK;
+  }
+  msb_status rs = scan_reserve(ctx, n);
+  if (rs != MSB_OK) return rs;
   int32_t* tot = ctx->scan_scr;
   msb_status st = scan_level(ctx, in, out, n, ctx->scan_scr + 1);
   if (st != MSB_OK) return st;

@@ -993,8 +993,10 @@ static LevelView view(msb_level L) {
                    (L->kind == 1 && L->W == 1 && L->unity) ? 1 : 0};
 }
 // Build the dynamic constant-basis stage from dp (device, length N) into s->dyn_level.
-static msb_status build_dynamic(msb_ctx ctx, msb_solver s, const double* dp, int32_t* M_out,
-                                int32_t* part_out) {
+// The N-sized part of the dynamic rebuild (no host synchronisation; graph-capturable):
+// max|Δp|, bins (A14), connected components, sizes, the merge threshold and merged labels
+// (A15), canonical numbering; M_dyn and max|Δp| are copied to the pinned s->dyn_pin.
+static msb_status dyn_labels(msb_ctx ctx, msb_solver s, const double* dp) {
   msb_op op = s->op;
   int64_t N = op->N;
   cudaStream_t st = ctx->stream;
@@ -1002,8 +1004,6 @@ static msb_status build_dynamic(msb_ctx ctx, msb_solver s, const double* dp, int
   MSB_CUDA_TRY(ctx, cudaMemsetAsync(mx, 0, 8, st));
   k_absmax_vec<<<(unsigned)std::min<int64_t>(grid_for(N, 256), 2 * ctx->sm_count), 256, 0, st>>>(dp, N, mx);
   MSB_LAUNCH_CHECK(ctx);
-  // max|Δp| is read back with the block count (no synchronisation of its own); when it is
-  // 0 the stage is skipped there
   k_bins<<<grid_for(N, 256), 256, 0, st>>>(dp, N, mx, s->edge0, s->edge1, s->bins);
   MSB_LAUNCH_CHECK(ctx);
   msb_status rc = cc_label(ctx, op, s->bins, s->lab, nullptr);
@@ -1023,21 +1023,28 @@ static msb_status build_dynamic(msb_ctx ctx, msb_solver s, const double* dp, int
   k_merge_label<<<grid_for(N, 256), 256, 0, st>>>(s->lab, s->cnt, s->bins, N, 1, s->mhist + 129,
                                                   s->ids, s->mhist + 128);
   MSB_LAUNCH_CHECK(ctx);
-  int32_t M = 0;
-  // canonical numbering: labels are minimum cells of their blocks; max|Δp| comes back with
-  // its count (one synchronisation for both)
-  unsigned long long hm = 0;
-  rc = canonical_number(ctx, N, s->ids, s->lab, s->cnt /* 2N scratch: cnt|bins reused */, &M, mx,
-                        &hm, sizeof(hm));
+  // canonical numbering: labels are minimum cells of their blocks
+  const int32_t* Md = nullptr;
+  rc = canonical_number_async(ctx, N, s->ids, s->lab, s->cnt /* 2N scratch: cnt|bins reused */, &Md);
   if (rc) return rc;
-  {
-    double m;
-    memcpy(&m, &hm, 8);
-    if (!(m > 0.0)) {  // max|Δp| = 0: stage skipped
-      *M_out = 0;
-      return MSB_OK;
-    }
-  }
+  char* pin = static_cast<char*>(s->dyn_pin);
+  MSB_CUDA_TRY(ctx, cudaMemcpyAsync(pin, Md, 4, cudaMemcpyDeviceToHost, st));
+  MSB_CUDA_TRY(ctx, cudaMemcpyAsync(pin + 8, mx, 8, cudaMemcpyDeviceToHost, st));
+  return MSB_OK;
+}
+
+// M_dyn and max|Δp| from the pinned buffer (after dyn_labels has completed)
+static void dyn_read(msb_solver s, int32_t* M, double* mxv) {
+  const char* pin = static_cast<const char*>(s->dyn_pin);
+  memcpy(M, pin, 4);
+  memcpy(mxv, pin + 8, 8);
+}
+
+// The M-sized part: the constant basis of the labels, A_c (exact) and its factorisation.
+static msb_status dyn_finish(msb_ctx ctx, msb_solver s, int32_t M, int32_t* part_out) {
+  msb_op op = s->op;
+  int64_t N = op->N;
+  cudaStream_t st = ctx->stream;
   msb_level D = s->dyn_level;
   k_refill_const<<<grid_for(N, 256), 256, 0, st>>>(s->lab, N, D->col, D->P[0]);
   MSB_LAUNCH_CHECK(ctx);
@@ -1045,8 +1052,28 @@ static msb_status build_dynamic(msb_ctx ctx, msb_solver s, const double* dp, int
   D->cur = 0;
   D->M = M;
   if (part_out) MSB_CUDA_TRY(ctx, copy_out(ctx, part_out, D->part, N * sizeof(int32_t)));
-  rc = coarse_assemble_dense(ctx, D, op);
+  return coarse_assemble_dense(ctx, D, op);
+}
+
+static msb_status ensure_dyn_pin(msb_ctx ctx, msb_solver s) {
+  if (!s->dyn_pin) MSB_CUDA_TRY(ctx, cudaHostAlloc(&s->dyn_pin, 64, cudaHostAllocDefault));
+  return scan_reserve(ctx, s->op->N);
+}
+
+static msb_status build_dynamic(msb_ctx ctx, msb_solver s, const double* dp, int32_t* M_out,
+                                int32_t* part_out) {
+  msb_status rc = ensure_dyn_pin(ctx, s);
   if (rc) return rc;
+  if ((rc = dyn_labels(ctx, s, dp))) return rc;
+  MSB_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  int32_t M = 0;
+  double m = 0.0;
+  dyn_read(s, &M, &m);
+  if (!(m > 0.0)) {  // max|Δp| = 0: stage skipped
+    *M_out = 0;
+    return MSB_OK;
+  }
+  if ((rc = dyn_finish(ctx, s, M, part_out))) return rc;
   *M_out = M;
   return MSB_OK;
 }
@@ -1453,7 +1480,10 @@ static void drop_graphs(msb_solver s) {
     if (s->gexec[t]) cudaGraphExecDestroy(s->gexec[t]);
     s->gexec[t] = nullptr;
     s->glaunches[t] = 0;
+    if (s->sgexec[t]) cudaGraphExecDestroy(s->sgexec[t]);
+    s->sgexec[t] = nullptr;
   }
+  s->sgkey.clear();
 }
 
 // Capture `n` iterations of the static stages starting from x buffer `cur0` into a
@@ -1513,6 +1543,94 @@ static msb_status chunk_graph(msb_ctx ctx, msb_solver s, const double* db, int c
     return set_error(ctx, MSB_ECUDA, "graph capture: %s", cudaGetErrorString(e));
   }
   *out = s->gexec[cur0];
+  return MSB_OK;
+}
+
+// Dynamic loop: one iteration of the static stages (norm already taken: no stop-test
+// partials) from x buffer cur0, captured once and replayed; *cur_out = the buffer it ends in.
+static msb_status static_graph(msb_ctx ctx, msb_solver s, const double* db, int cur0,
+                               cudaGraphExec_t* out, int* cur_out) {
+  *out = nullptr;
+  std::vector<const void*> key = {db};
+  for (msb_level L : s->levels) {
+    key.push_back(L->P[L->cur]);
+    key.push_back(L->co.Ainv);
+    key.push_back(L->co.sch);
+    key.push_back(L->co.Xp);
+  }
+  if (key != s->sgkey) {
+    for (int t = 0; t < 2; ++t) {
+      if (s->sgexec[t]) cudaGraphExecDestroy(s->sgexec[t]);
+      s->sgexec[t] = nullptr;
+    }
+    s->sgkey = key;
+  }
+  if (!s->sgexec[cur0]) {
+    if (!s->cap_stream)
+      MSB_CUDA_TRY(ctx, cudaStreamCreateWithFlags(&s->cap_stream, cudaStreamNonBlocking));
+    cudaStream_t user = ctx->stream;
+    ctx->stream = s->cap_stream;
+    const int64_t l0 = g_launches.load();
+    msb_status rc = MSB_OK;
+    int cur = cur0;
+    cudaError_t e = cudaStreamBeginCapture(s->cap_stream, cudaStreamCaptureModeThreadLocal);
+    if (e == cudaSuccess) {
+      bool first = false;
+      for (msb_level L : s->levels)
+        if ((rc = enqueue_stage(ctx, s, L, db, cur, first))) break;
+      cudaGraph_t graph = nullptr;
+      cudaError_t e2 = cudaStreamEndCapture(s->cap_stream, &graph);
+      if (!rc && e2 == cudaSuccess) e = cudaGraphInstantiate(&s->sgexec[cur0], graph, 0);
+      else if (e2 != cudaSuccess) e = e2;
+      if (graph) cudaGraphDestroy(graph);
+    }
+    ctx->stream = user;
+    s->sglaunches[cur0] = g_launches.load() - l0;
+    g_launches.fetch_sub(s->sglaunches[cur0]);  // captured, not launched
+    s->scur_after[cur0] = cur;
+    if (rc) return rc;
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      s->sgexec[cur0] = nullptr;
+      return set_error(ctx, MSB_ECUDA, "static-stage graph: %s", cudaGetErrorString(e));
+    }
+  }
+  *out = s->sgexec[cur0];
+  *cur_out = s->scur_after[cur0];
+  return MSB_OK;
+}
+
+// Dynamic loop: the N-sized rebuild (dyn_labels on s->dpbuf) as one graph.
+static msb_status labels_graph(msb_ctx ctx, msb_solver s, cudaGraphExec_t* out) {
+  *out = nullptr;
+  if (!s->lgexec) {
+    msb_status rc = ensure_dyn_pin(ctx, s);
+    if (rc) return rc;
+    if (!s->cap_stream)
+      MSB_CUDA_TRY(ctx, cudaStreamCreateWithFlags(&s->cap_stream, cudaStreamNonBlocking));
+    cudaStream_t user = ctx->stream;
+    ctx->stream = s->cap_stream;
+    const int64_t l0 = g_launches.load();
+    cudaError_t e = cudaStreamBeginCapture(s->cap_stream, cudaStreamCaptureModeThreadLocal);
+    if (e == cudaSuccess) {
+      rc = dyn_labels(ctx, s, s->dpbuf);
+      cudaGraph_t graph = nullptr;
+      cudaError_t e2 = cudaStreamEndCapture(s->cap_stream, &graph);
+      if (!rc && e2 == cudaSuccess) e = cudaGraphInstantiate(&s->lgexec, graph, 0);
+      else if (e2 != cudaSuccess) e = e2;
+      if (graph) cudaGraphDestroy(graph);
+    }
+    ctx->stream = user;
+    s->lglaunches = g_launches.load() - l0;
+    g_launches.fetch_sub(s->lglaunches);
+    if (rc) return rc;
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      s->lgexec = nullptr;
+      return set_error(ctx, MSB_ECUDA, "rebuild graph: %s", cudaGetErrorString(e));
+    }
+  }
+  *out = s->lgexec;
   return MSB_OK;
 }
 
@@ -1673,6 +1791,7 @@ msb_status msb_ms_iterate(msb_ctx ctx, msb_solver s, const double* b, double* x,
       MSB_CUDA_TRY(ctx, cudaStreamCreateWithFlags(&s->dyn_stream, cudaStreamNonBlocking));
       MSB_CUDA_TRY(ctx, cudaEventCreateWithFlags(&s->ev_dp, cudaEventDisableTiming));
       MSB_CUDA_TRY(ctx, cudaEventCreateWithFlags(&s->ev_dyn, cudaEventDisableTiming));
+      MSB_CUDA_TRY(ctx, cudaEventCreateWithFlags(&s->ev_lab, cudaEventDisableTiming));
     }
     while (true) {
       if ((rc = enqueue_norm(ctx, s, s->xbuf[cur], db, 0))) return rc;
@@ -1700,21 +1819,38 @@ msb_status msb_ms_iterate(msb_ctx ctx, msb_solver s, const double* b, double* x,
       // A_c, factor) runs on the solver's rebuild stream; the dynamic stage waits for both.
       // The rebuild only touches its own scratch and the dynamic level, whose last reader
       // (the previous iteration's dynamic stage) precedes the Δp kernel the rebuild waits on.
-      bool first = false;  // norm already taken
-      for (msb_level L : s->levels)
-        if ((rc = enqueue_stage(ctx, s, L, db, cur, first))) return rc;
+      {
+        cudaGraphExec_t ge = nullptr;
+        int cur_next = cur;
+        if ((rc = static_graph(ctx, s, db, cur, &ge, &cur_next))) return rc;
+        MSB_CUDA_TRY(ctx, cudaGraphLaunch(ge, st));
+        g_launches.fetch_add(s->sglaunches[cur], std::memory_order_relaxed);
+        cur = cur_next;
+      }
       if (rebuild) {
+        cudaGraphExec_t lg = nullptr;
+        if ((rc = labels_graph(ctx, s, &lg))) return rc;
         MSB_CUDA_TRY(ctx, cudaStreamWaitEvent(s->dyn_stream, s->ev_dp, 0));
-        D->co.defer_check = true;
-        ctx->stream = s->dyn_stream;
-        rc = build_dynamic(ctx, s, s->dpbuf, &M, nullptr);
-        ctx->stream = st;
-        D->co.defer_check = false;
-        if (rc) return rc;
+        MSB_CUDA_TRY(ctx, cudaGraphLaunch(lg, s->dyn_stream));
+        g_launches.fetch_add(s->lglaunches, std::memory_order_relaxed);
+        MSB_CUDA_TRY(ctx, cudaEventRecord(s->ev_lab, s->dyn_stream));
+        MSB_CUDA_TRY(ctx, cudaEventSynchronize(s->ev_lab));  // M_dyn, max|Δp| in dyn_pin
+        double mxv = 0.0;
+        dyn_read(s, &M, &mxv);
+        if (!(mxv > 0.0)) M = 0;
+        if (M > 0) {
+          D->co.defer_check = true;
+          ctx->stream = s->dyn_stream;
+          rc = dyn_finish(ctx, s, M, nullptr);
+          ctx->stream = st;
+          D->co.defer_check = false;
+          if (rc) return rc;
+        }
         MSB_CUDA_TRY(ctx, cudaEventRecord(s->ev_dyn, s->dyn_stream));
         MSB_CUDA_TRY(ctx, cudaStreamWaitEvent(st, s->ev_dyn, 0));
       }
       dynM.push_back(M);
+      bool first = false;  // norm already taken
       if (M > 0)
         if ((rc = enqueue_stage(ctx, s, s->dyn_level, db, cur, first))) return rc;
       cur_after.push_back(cur);
@@ -1769,6 +1905,9 @@ msb_status msb_solver_destroy(msb_solver s) {
   if (s->dyn_stream) cudaStreamDestroy(s->dyn_stream);
   if (s->ev_dp) cudaEventDestroy(s->ev_dp);
   if (s->ev_dyn) cudaEventDestroy(s->ev_dyn);
+  if (s->ev_lab) cudaEventDestroy(s->ev_lab);
+  if (s->lgexec) cudaGraphExecDestroy(s->lgexec);
+  if (s->dyn_pin) cudaFreeHost(s->dyn_pin);
   delete s;
   return MSB_OK;
 }

@@ -155,6 +155,19 @@ __global__ void k_gather_ids(const int32_t* __restrict__ lab, const int32_t* __r
 }
 
 // lab[i] must be a cell index that is its own label for the representative cell.
+msb_status canonical_number_async(msb_ctx ctx, int64_t N, const int32_t* lab, int32_t* out,
+                                  int32_t* scratch, const int32_t** M_dev) {
+  int32_t* flags = scratch;
+  int32_t* ids = scratch + N;
+  k_root_flags<<<grid_for(N, 256), 256, 0, ctx->stream>>>(lab, N, flags);
+  MSB_LAUNCH_CHECK(ctx);
+  msb_status st = scan_exclusive_async(ctx, flags, ids, N, M_dev);
+  if (st != MSB_OK) return st;
+  k_gather_ids<<<grid_for(N, 256), 256, 0, ctx->stream>>>(lab, ids, N, out);
+  MSB_LAUNCH_CHECK(ctx);
+  return MSB_OK;
+}
+
 msb_status canonical_number(msb_ctx ctx, int64_t N, const int32_t* lab, int32_t* out,
                             int32_t* scratch, int32_t* M_out, const void* extra_dev,
                             void* extra_host, size_t extra_bytes) {

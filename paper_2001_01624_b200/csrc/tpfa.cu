@@ -222,6 +222,7 @@ msb_status msb_build_tpfa(msb_ctx ctx, const msb_grid* g, const double* K, const
 
 msb_status msb_op_set_mobility(msb_ctx ctx, msb_op op, const double* mob) {
   if (!ctx || !op || !mob) return set_error(ctx, MSB_EINVAL, "msb_op_set_mobility: null");
+  op->tmax_valid = false;  // T changes below
   int64_t nf = (int64_t)(op->nx - 1) * op->ny * op->nz + (int64_t)op->nx * (op->ny - 1) * op->nz +
                (int64_t)op->nx * op->ny * (op->nz - 1);
   void* o = nullptr;
@@ -266,6 +267,7 @@ msb_status msb_op_destroy(msb_op op) {
   if (!op) return MSB_EINVAL;
   msb_ctx ctx = op->ctx;
   dfree(ctx, op->Tx);  // Ty, Tz live in the same block
+  dfree(ctx, op->tmax);
   dfree(ctx, op->Tb);
   dfree(ctx, op->q);
   dfree(ctx, op->open);

@@ -147,7 +147,9 @@ def config_pipeline(cfg, args):
                final_res=float(out["res"][-1]), setup_levels_ms=e0.elapsed_time(e1),
                solve_ms=e2.elapsed_time(e3),
                ms_per_iteration=e2.elapsed_time(e3) / max(1, out["iters"]),
-               dyn_M_median=float(np.median(dyn[dyn > 0])) if dyn is not None and np.any(dyn > 0) else 0)
+               dyn_M_median=float(np.median(dyn[dyn > 0])) if dyn is not None and np.any(dyn > 0) else 0,
+               dyn_M_pct=[float(np.percentile(dyn[dyn > 0], q)) for q in (10, 25, 75, 90, 100)]
+               if dyn is not None and np.any(dyn > 0) else [])
     print(json.dumps(rec), flush=True)
 
 
