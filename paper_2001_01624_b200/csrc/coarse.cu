@@ -441,6 +441,8 @@ __global__ void __launch_bounds__(SYMV_T) k_symv_tiles(const double* __restrict_
 __global__ void __launch_bounds__(16 * ST) k_symv_reduce(const double* __restrict__ part, int M,
                                                         int ntb, double* __restrict__ xc,
                                                         const int* done) {
+  pdl_wait();
+  pdl_trigger();
   const bool skip = done && *(volatile const int*)done;
   symv_reduce_body<false>(part, M, ntb, xc, blockIdx.x, skip);
 }
@@ -543,8 +545,10 @@ msb_status coarse_pack_symmetric(msb_ctx ctx, Coarse& co) {
 void coarse_solve_dense(msb_ctx ctx, const Coarse& co, const double* rc, double* xc,
                         const int* done) {
   const int64_t nt = (int64_t)co.ntb * (co.ntb + 1) / 2;
-  k_symv_tiles<<<(unsigned)nt, SYMV_T, 0, ctx->stream>>>(co.Xp, co.M, rc, co.part);
-  k_symv_reduce<<<co.ntb, 16 * ST, 0, ctx->stream>>>(co.part, co.M, co.ntb, xc, done);
+  launch_ex(k_symv_tiles, dim3((unsigned)nt), dim3(SYMV_T), 0, ctx->stream, kPDL, 1, co.Xp, co.M,
+            rc, co.part);
+  launch_ex(k_symv_reduce, dim3(co.ntb), dim3(16 * ST), 0, ctx->stream, kPDL, 1, co.part, co.M,
+            co.ntb, xc, done);
   count_launch();
   count_launch();
 }
@@ -562,7 +566,7 @@ static msb_status ensure_dense(msb_ctx ctx, Coarse& co, int M) {
   co.Ac = co.L = co.Ainv = nullptr;
   co.cap = 0;
   MSB_ALLOC(ctx, co.Ac, double, (int64_t)M * M);
-  MSB_ALLOC(ctx, co.L, double, (int64_t)M * M);
+  MSB_ALLOC(ctx, co.L, double, (int64_t)M * M + M);  // + the small path's pivot reciprocals
   MSB_ALLOC(ctx, co.Ainv, double, (int64_t)M * M);
   if (co.tri) {
     dfree(ctx, co.tri_y);
@@ -747,6 +751,7 @@ void coarse_free(msb_ctx ctx, Coarse& co) {
 using namespace msb;
 
 extern "C" msb_status msb_coarse_assemble(msb_ctx ctx, msb_level L, msb_op op) {
+  MSB_NVTX("msb_coarse_assemble");
   if (!ctx || !L || !op) return set_error(ctx, MSB_EINVAL, "msb_coarse_assemble: null");
   if (L->N != op->N) return set_error(ctx, MSB_EDIM, "level/operator size mismatch");
   if (L->kind != 0 && (int64_t)L->M * L->M > (int64_t)1 << 31)

@@ -278,6 +278,10 @@ __global__ void __launch_bounds__(1024) k_chol_inv_leaf(double* __restrict__ A, 
   // in parallel — the same operations in the same order as a column-by-column forward
   // substitution, so the result is unchanged, with 3 barriers per step instead of an
   // O(n^2) serial loop per column.
+  // the pivot's reciprocal is formed once and the column / W row scaled by it (as LAPACK's
+  // potf2 scales by 1/l_jj): one fp64 division per step on the critical path, not one per
+  // element
+  __shared__ double rinv;
   for (int j = 0; j < n; ++j) {
     if (tid == 0) {
       double d = a[j][j];
@@ -285,15 +289,17 @@ __global__ void __launch_bounds__(1024) k_chol_inv_leaf(double* __restrict__ A, 
         atomicExch(singular, 1);
         d = 1.0;
       }
-      a[j][j] = sqrt(d);
+      const double p = sqrt(d);
+      a[j][j] = p;
+      rinv = 1.0 / p;
     }
     __syncthreads();
-    const double ljj = a[j][j];
+    const double ri = rinv;
     if (tid < LEAF) {
-      if (tid > j && tid < n) a[tid][j] /= ljj;
+      if (tid > j && tid < n) a[tid][j] *= ri;
     } else if (tid < 2 * LEAF) {
       const int c = tid - LEAF;
-      if (c <= j) w[j][c] = w[j][c] / ljj;
+      if (c <= j) w[j][c] *= ri;
     }
     __syncthreads();
 #pragma unroll
@@ -461,6 +467,7 @@ __global__ void __launch_bounds__(SC_T) k_chol_small(const double* __restrict__ 
       const double p = sqrt(d);
       a[jj] = p;
       rinv = 1.0 / p;
+      Lp[np + j] = rinv;  // the substitutions multiply by it
     }
     __syncthreads();
     for (int i = j + 1 + tid; i < M; i += SC_T) a[i * (i + 1) / 2 + j] *= rinv;
@@ -475,20 +482,22 @@ __global__ void __launch_bounds__(SC_T) k_chol_small(const double* __restrict__ 
   for (int e = tid; e < np; e += SC_T) Lp[e] = a[e];
 }
 
-// x = L^{-T} L^{-1} r with the packed factor, one warp (forward then backward substitution)
+// x = L^{-T} L^{-1} r with the packed factor (followed by the M pivot reciprocals), one
+// warp (forward then backward substitution)
 __global__ void __launch_bounds__(32) k_chol_small_solve(const double* __restrict__ Lp, int M,
                                                          const double* __restrict__ r,
                                                          double* __restrict__ x, const int* done) {
   extern __shared__ double sm[];
   double* L = sm;
-  double* y = sm + M * (M + 1) / 2;
-  const int lane = threadIdx.x;
   const int np = M * (M + 1) / 2;
-  for (int e = lane; e < np; e += 32) L[e] = Lp[e];
+  const double* dinv = L + np;
+  double* y = sm + np + M;
+  const int lane = threadIdx.x;
+  for (int e = lane; e < np + M; e += 32) L[e] = Lp[e];
   for (int i = lane; i < M; i += 32) y[i] = r[i];
   __syncwarp();
   for (int j = 0; j < M; ++j) {  // L y = r, column-oriented
-    const double yj = y[j] / L[j * (j + 1) / 2 + j];
+    const double yj = y[j] * dinv[j];
     __syncwarp();
     if (lane == 0) y[j] = yj;
     for (int i = j + 1 + lane; i < M; i += 32) y[i] -= L[i * (i + 1) / 2 + j] * yj;
@@ -496,7 +505,7 @@ __global__ void __launch_bounds__(32) k_chol_small_solve(const double* __restric
   }
   for (int j = M - 1; j >= 0; --j) {  // L^T x = y, row j of L holds column j of L^T
     const int rj = j * (j + 1) / 2;
-    const double xj = y[j] / L[rj + j];
+    const double xj = y[j] * dinv[j];
     __syncwarp();
     if (lane == 0) y[j] = xj;
     for (int i = lane; i < j; i += 32) y[i] -= L[rj + i] * xj;
@@ -510,7 +519,7 @@ __global__ void __launch_bounds__(32) k_chol_small_solve(const double* __restric
 void coarse_solve_small(msb_ctx ctx, const Coarse& co, const double* rc, double* xc,
                         const int* done) {
   const int M = co.M;
-  const size_t smem = ((size_t)M * (M + 1) / 2 + M) * sizeof(double);
+  const size_t smem = ((size_t)M * (M + 1) / 2 + 2 * M) * sizeof(double);
   k_chol_small_solve<<<1, 32, smem, ctx->stream>>>(co.L, M, rc, xc, done);
   count_launch();
 }
@@ -523,14 +532,14 @@ msb_status coarse_factor_dense(msb_ctx ctx, Coarse& co) {
   int* sing = reinterpret_cast<int*>(co.flags + 1);
   co.small = co.tri && M <= SMALL_CHOL_M;
   if (co.small) {
-    if (!co.L) MSB_ALLOC(ctx, co.L, double, (int64_t)co.cap * co.cap);
+    if (!co.L) MSB_ALLOC(ctx, co.L, double, (int64_t)co.cap * co.cap + co.cap);
     MSB_CUDA_TRY(ctx, cudaMemsetAsync(co.flags, 0, 16, s));
     k_absmax2<<<std::min<int64_t>(grid_for((int64_t)M * M, 256), 4 * ctx->sm_count), 256, 0, s>>>(
         co.Ac, (int64_t)M * M, amax);
     MSB_LAUNCH_CHECK(ctx);
     static bool attr = false;
     if (!attr) {
-      const int mx = (int)(((size_t)SMALL_CHOL_M * (SMALL_CHOL_M + 1) / 2 + SMALL_CHOL_M) * sizeof(double));
+      const int mx = (int)(((size_t)SMALL_CHOL_M * (SMALL_CHOL_M + 1) / 2 + 2 * SMALL_CHOL_M) * sizeof(double));
       MSB_CUDA_TRY(ctx, cudaFuncSetAttribute(k_chol_small, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
       MSB_CUDA_TRY(ctx, cudaFuncSetAttribute(k_chol_small_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
       attr = true;

@@ -786,6 +786,7 @@ msb_status msb_cpr_create(msb_ctx ctx, msb_op op, msb_level lev, const msb_fluid
 
 msb_status msb_cpr_linearize(msb_ctx ctx, msb_cpr c, const double* p, const double* S,
                              const double* p_n, const double* S_n, const double* q) {
+  MSB_NVTX("msb_cpr_linearize");
   if (!ctx || !c || !p || !S || !p_n || !S_n) return set_error(ctx, MSB_EINVAL, "msb_cpr_linearize: null");
   const int64_t N = c->N;
   const size_t B = N * sizeof(double);
@@ -812,6 +813,7 @@ msb_status msb_cpr_linearize(msb_ctx ctx, msb_cpr c, const double* p, const doub
 }
 
 msb_status msb_cpr_decouple(msb_ctx ctx, msb_cpr c, int32_t method) {
+  MSB_NVTX("msb_cpr_decouple");
   if (!ctx || !c) return set_error(ctx, MSB_EINVAL, "msb_cpr_decouple: null");
   if (method < 0 || method > 2) return set_error(ctx, MSB_EINVAL, "msb_cpr_decouple: method");
   if (!c->linearized) return set_error(ctx, MSB_EINVAL, "msb_cpr_decouple: linearize first");
@@ -849,6 +851,7 @@ msb_status msb_cpr_decouple(msb_ctx ctx, msb_cpr c, int32_t method) {
 }
 
 msb_status msb_cpr_apply(msb_ctx ctx, msb_cpr c, const double* r, double* dx) {
+  MSB_NVTX("msb_cpr_apply");
   if (!ctx || !c || !r || !dx || r == dx) return set_error(ctx, MSB_EINVAL, "msb_cpr_apply: args");
   if (!c->decoupled) return set_error(ctx, MSB_EINVAL, "msb_cpr_apply: decouple first");
   if (!is_device_ptr(r) || !is_device_ptr(dx)) return set_error(ctx, MSB_EINVAL, "msb_cpr_apply: device vectors");
@@ -893,6 +896,7 @@ msb_status msb_cpr_export_coarse(msb_ctx ctx, msb_cpr c, double* Ac, int32_t* M_
 msb_status msb_cpr_fgmres(msb_ctx ctx, msb_cpr c, const double* b, double* x, double tol,
                           int32_t restart, int32_t max_iter, int32_t fixed_iters, int32_t precond,
                           int32_t* iters_out, double* res_hist) {
+  MSB_NVTX("msb_cpr_fgmres");
   if (!ctx || !c || !x) return set_error(ctx, MSB_EINVAL, "msb_cpr_fgmres: null");
   if (precond != 1 && precond != 2) return set_error(ctx, MSB_EINVAL, "msb_cpr_fgmres: precond must be 1 or 2");
   if (!c->decoupled) return set_error(ctx, MSB_EINVAL, "msb_cpr_fgmres: decouple first");

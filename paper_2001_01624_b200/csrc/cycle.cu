@@ -161,12 +161,35 @@ __global__ void __launch_bounds__(CT) k_norm(StencilT S, const double* __restric
 // times shorter, which is what a short stencil pass needs to approach HBM bandwidth.
 constexpr int CPT = 4;
 
+// Stencil passes launched as programmatic dependents: the inputs they do not write (the
+// transmissibility planes incl. the -y/-z face planes, and b) are bulk-prefetched into L2
+// for this CTA's cells, then the pass waits for its predecessor (which wrote x).
+template <int CPT>
+__device__ __forceinline__ void stencil_prologue(const StencilT& S, const double* b) {
+  const int N = S.g.nxy * S.g.nz;
+  const int cb = blockIdx.x * (CT * CPT);
+  const int ce = min(cb + CT * CPT, N);
+  const size_t n = (size_t)(ce - cb) * sizeof(double);
+  switch (threadIdx.x) {
+    case 0: prefetch_l2(S.Tx + max(cb - 1, 0), n + 8); break;
+    case 32: prefetch_l2(S.Ty + cb, n); break;
+    case 64: prefetch_l2(S.Tz + cb, n); break;
+    case 96: prefetch_l2(b + cb, n); break;
+    case 128: if (cb >= S.g.nx) prefetch_l2(S.Ty + cb - S.g.nx, n); break;
+    case 160: if (cb >= S.g.nxy) prefetch_l2(S.Tz + cb - S.g.nxy, n); break;
+    default: break;
+  }
+  pdl_wait();
+  pdl_trigger();
+}
+
 template <int CPT>
 __global__ void __launch_bounds__(CT) k_jacobi(StencilT S, const double* __restrict__ x,
                                                double* __restrict__ xo,
                                                const double* __restrict__ b, double omega,
                                                int first, double* __restrict__ partials,
                                                const IterState* st) {
+  stencil_prologue<CPT>(S, b);
   const bool done = is_done(st);
   const int N = S.g.nxy * S.g.nz;
   const int c0 = blockIdx.x * (CT * CPT) + threadIdx.x;
@@ -565,6 +588,7 @@ __global__ void __launch_bounds__(CT) k_residual(StencilT S, const double* __res
                                                  double* __restrict__ r, int first,
                                                  double* __restrict__ partials,
                                                  const IterState* st) {
+  stencil_prologue<CPT>(S, b);
   const bool done = is_done(st);
   const int N = S.g.nxy * S.g.nz;
   const int c0 = blockIdx.x * (CT * CPT) + threadIdx.x;
@@ -647,11 +671,24 @@ __device__ __forceinline__ void restrict_row_body(const LevelView& L, const doub
     a0[e] = a1[e] = 0.0;
     xok[e] = xo + XL * e < nx;
   }
+  const int step = RG * CS;
+  constexpr int U = XP > 2 ? 2 : 4;  // rows in flight per lane
+  // the first rows this CTA loads (U per row group, both x-parity planes of P, which no pass
+  // of the cycle writes) are bulk-prefetched into L2 while the residual pass drains; r
+  // after the wait.  Only the first batch: beyond L2 (config 5) a whole-range prefetch
+  // would be evicted before use.
+  for (int t = threadIdx.x; t < min(rows, U * step); t += blockDim.x) {
+    if ((t % step) / RG != rank) continue;
+    const int tz = t / wy, ty = t - tz * wy;
+    const size_t c = (size_t)nx * (y0 + ty) + (size_t)sxy * (z0 + tz);
+    prefetch_l2(P0 + c, (size_t)nx * sizeof(double));
+    prefetch_l2(P1 + c, (size_t)nx * sizeof(double));
+  }
+  pdl_wait();
+  pdl_trigger();
   int row = rg + RG * rank;
   int zz = row / wy, yy = row - zz * wy;
-  const int step = RG * CS;
   const int dz = step / wy, dy = step - dz * wy;
-  constexpr int U = XP > 2 ? 2 : 4;  // rows in flight per lane
   while (row < rows) {
     double p0[U][XP], p1[U][XP], rv[U][XP];
 #pragma unroll
@@ -758,23 +795,8 @@ static msb_status launch_restrict(msb_ctx ctx, cudaStream_t st, unsigned units, 
                                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr = smem;
   }
-  if constexpr (CS == 1) {
-    k_restrict_cart<XP, 1><<<units, RR2_THREADS, smem, st>>>(V, r, rc, ist);
-  } else {
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(units * CS);
-    cfg.blockDim = dim3(RR2_THREADS);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = st;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = CS;
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
-    MSB_CUDA_TRY(ctx, cudaLaunchKernelEx(&cfg, k_restrict_cart<XP, CS>, V, r, rc, ist));
-  }
+  MSB_CUDA_TRY(ctx, launch_ex(k_restrict_cart<XP, CS>, dim3(units * CS), dim3(RR2_THREADS), smem, st,
+                              kPDL, CS, V, r, rc, ist));
   return MSB_OK;  // the caller's MSB_LAUNCH_CHECK counts the launch
 
 }
@@ -798,14 +820,18 @@ __global__ void __launch_bounds__(CT) k_prolong_cart(LevelView L, double* __rest
   const int2 tz = reinterpret_cast<const int2*>(L.tab)[L.g.nx + L.g.ny + k];
   const double* __restrict__ base = L.P + c;
   double v[8], xv[8];
+  int col[8];
 #pragma unroll
   for (int s = 0; s < 8; ++s) {
     const int jx = (s & 1) ? tx.y : tx.x, jy = (s & 2) ? ty.y : ty.x, jz = (s & 4) ? tz.y : tz.x;
     const bool act = (jx | jy | jz) >= 0;
-    const int col = jx + L.nb0 * (jy + L.nb1 * jz);
+    col[s] = act ? jx + L.nb0 * (jy + L.nb1 * jz) : -1;
     v[s] = act ? base[(size_t)s * N] : 0.0;
-    xv[s] = act ? xc[col] : 0.0;
   }
+  pdl_wait();  // P is an input; x_c and x come from the coarse solve and the smoother
+  pdl_trigger();
+#pragma unroll
+  for (int s = 0; s < 8; ++s) xv[s] = col[s] >= 0 ? xc[col[s]] : 0.0;
   double acc = 0.0;
 #pragma unroll
   for (int s = 0; s < 8; ++s) acc += v[s] * xv[s];
@@ -1158,6 +1184,7 @@ msb_status msb_solver_create(msb_ctx ctx, msb_op op, const msb_level* levels, in
                              double omega_s, int32_t nu, int32_t post_smooth, int32_t dyn_enable,
                              double dyn_edge0, double dyn_edge1, int32_t dyn_max_blocks,
                              msb_solver* out) {
+  MSB_NVTX("msb_solver_create");
   if (!ctx || !op || !out || n_levels < 0 || (n_levels > 0 && !levels) || nu < 0)
     return set_error(ctx, MSB_EINVAL, "msb_solver_create args");
   if (n_levels == 0 && !dyn_enable) return set_error(ctx, MSB_EINVAL, "solver needs a level");
@@ -1245,6 +1272,7 @@ msb_status msb_solver_create(msb_ctx ctx, msb_op op, const msb_level* levels, in
 
 msb_status msb_add_dynamic_basis(msb_ctx ctx, msb_solver s, const double* dp, int32_t* M_dyn_out,
                                  int32_t* part_out) {
+  MSB_NVTX("msb_add_dynamic_basis");
   if (!ctx || !s || !dp) return set_error(ctx, MSB_EINVAL, "msb_add_dynamic_basis: null");
   if (!s->dyn) return set_error(ctx, MSB_EINVAL, "solver created without dynamic stage");
   void* o = nullptr;
@@ -1264,8 +1292,10 @@ msb_status msb_add_dynamic_basis(msb_ctx ctx, msb_solver s, const double* dp, in
 // Enqueue one stage (level L) on x buffers; `first` marks the iteration's first kernel.
 // Enqueue one stage (level L) on the x double buffer; `first` marks the iteration's
 // first kernel, which also emits the stop-test partials (finalised right after).
-#define RES_LAUNCH(...) k_residual<CPT><<<g4, CT, 0, st>>>(__VA_ARGS__)
-#define JAC_LAUNCH(...) k_jacobi<CPT><<<g4, CT, 0, st>>>(__VA_ARGS__)
+#define RES_LAUNCH(...) \
+  MSB_CUDA_TRY(ctx, launch_ex(k_residual<CPT>, dim3(g4), dim3(CT), 0, st, kPDL, 1, __VA_ARGS__))
+#define JAC_LAUNCH(...) \
+  MSB_CUDA_TRY(ctx, launch_ex(k_jacobi<CPT>, dim3(g4), dim3(CT), 0, st, kPDL, 1, __VA_ARGS__))
 
 static msb_status enqueue_stage(msb_ctx ctx, msb_solver s, msb_level L, const double* b, int& cur,
                                 bool& first) {
@@ -1306,24 +1336,6 @@ static msb_status enqueue_stage(msb_ctx ctx, msb_solver s, msb_level L, const do
     MSB_CUDA_TRY(ctx, cudaStreamWaitEvent(st, s->ev_join, 0));
     s->pending_join = false;
   }
-  // fused Jacobi + residual (jacres_tma.cu): Cartesian level, pre-smoothing, ν = 1, on grids
-  // whose x, b, T working set is far beyond L2 (config 5); bit-identical to the two passes
-  bool jq = false;
-  if (L->kind == 0 && !s->post && s->nu == 1 && s->smoother == 0 && jacres_fused_wanted(ctx, op)) {
-    if (!s->jq) s->jq = new JQPlan();
-    if (!s->jq->ok || s->jq->b != b || s->jq->x[0] != s->xbuf[0] || s->jq->x[1] != s->xbuf[1])
-      jacres_tma_plan(ctx, op, s->xbuf[0], s->xbuf[1], b, s->jq);
-    jq = s->jq->ok;
-  }
-  auto jqres = [&]() -> msb_status {
-    msb_status rc = jacres_tma_launch(ctx, op, *s->jq, cur, s->xbuf[cur ^ 1], s->r, s->omega_s,
-                                      first ? 1 : 0, s->partials, &s->st->done);
-    if (rc) return rc;
-    if (first && (rc = fin(s->jq->grid))) return rc;
-    first = false;
-    cur ^= 1;
-    return MSB_OK;
-  };
   auto ilu = [&]() -> msb_status {  // ν red-black ILU(0) steps on x in place (NEXT-2)
     for (int v = 0; v < s->nu; ++v) {
       RES_LAUNCH(S, s->xbuf[cur], b, s->r, first ? 1 : 0, s->partials, s->st);
@@ -1358,15 +1370,13 @@ static msb_status enqueue_stage(msb_ctx ctx, msb_solver s, msb_level L, const do
   };
   auto corr = [&]() -> msb_status {
     if (L->kind == 0) {
-      if (!jq) {  // the fused pass has already written r
-        RES_LAUNCH(S, s->xbuf[cur], b, s->r, first ? 1 : 0, s->partials, s->st);
-        MSB_LAUNCH_CHECK(ctx);
-        if (first) {
-          msb_status rc = fin(g4);
-          if (rc) return rc;
-        }
-        first = false;
+      RES_LAUNCH(S, s->xbuf[cur], b, s->r, first ? 1 : 0, s->partials, s->st);
+      MSB_LAUNCH_CHECK(ctx);
+      if (first) {
+        msb_status rc = fin(g4);
+        if (rc) return rc;
       }
+      first = false;
       if (op->nx > 2048)
         return set_error(ctx, MSB_EINVAL, "Cartesian restriction supports nx <= 2048 (nx=%d)", op->nx);
       {
@@ -1385,7 +1395,8 @@ static msb_status enqueue_stage(msb_ctx ctx, msb_solver s, msb_level L, const do
       }
       MSB_LAUNCH_CHECK(ctx);
       coarse_solve(ctx, L->co, s->rc, s->xc, &s->st->done);
-      k_prolong_cart<<<g, CT, 0, st>>>(V, s->xbuf[cur], s->xc, s->st);
+      MSB_CUDA_TRY(ctx, launch_ex(k_prolong_cart, dim3(g), dim3(CT), 0, st, kPDL, 1, V, s->xbuf[cur],
+                                  s->xc, s->st));
       MSB_LAUNCH_CHECK(ctx);
       return MSB_OK;
     }
@@ -1449,7 +1460,7 @@ static msb_status enqueue_stage(msb_ctx ctx, msb_solver s, msb_level L, const do
     if ((rc = corr())) return rc;
     if ((rc = jac())) return rc;
   } else {
-    if ((rc = jq ? jqres() : jac())) return rc;
+    if ((rc = jac())) return rc;
     if ((rc = corr())) return rc;
   }
   return MSB_OK;
@@ -1712,6 +1723,7 @@ msb_status msb_partition_indicator(msb_ctx ctx, msb_op op, const double* ind, co
 msb_status msb_ms_iterate(msb_ctx ctx, msb_solver s, const double* b, double* x, double tol,
                           int32_t max_iter, int32_t fixed_iters, int32_t* iters_out,
                           double* res_hist, int32_t* dyn_M_hist) {
+  MSB_NVTX("msb_ms_iterate");
   if (!ctx || !s || !x) return set_error(ctx, MSB_EINVAL, "msb_ms_iterate: null");
   if (max_iter < 0 || fixed_iters < 0) return set_error(ctx, MSB_EINVAL, "negative iteration count");
   msb_op op = s->op;
@@ -1793,20 +1805,48 @@ msb_status msb_ms_iterate(msb_ctx ctx, msb_solver s, const double* b, double* x,
       MSB_CUDA_TRY(ctx, cudaEventCreateWithFlags(&s->ev_dyn, cudaEventDisableTiming));
       MSB_CUDA_TRY(ctx, cudaEventCreateWithFlags(&s->ev_lab, cudaEventDisableTiming));
     }
+    // TEMPORARY host-phase timing (MSB_DYN_PROFILE): sync wait, static enqueue, labels wait,
+    // finish enqueue, stage enqueue
+    static const bool prof = getenv("MSB_DYN_PROFILE") != nullptr;
+    double tp[6] = {0, 0, 0, 0, 0, 0};
+    int np_ = 0;
+    auto now = [] { return std::chrono::duration<double, std::micro>(
+                        std::chrono::steady_clock::now().time_since_epoch()).count(); };
+    double t0 = now();
+    cudaEvent_t pe[5] = {};
+    if (prof)
+      for (auto& e : pe) cudaEventCreate(&e);
+    double gsum[2][5] = {};  // [M <= 232 | M > 232][static, labels, finish, stage, next-norm]
+    int gcnt[2] = {0, 0};
+    int prevM = -1;
     while (true) {
+      if (prof && prevM > 0) cudaEventRecord(pe[4], st);
       if ((rc = enqueue_norm(ctx, s, s->xbuf[cur], db, 0))) return rc;
       MSB_CUDA_TRY(ctx, cudaMemcpyAsync(&hs, s->st, sizeof(hs), cudaMemcpyDeviceToHost, st));
       if (D->co.flags)
         MSB_CUDA_TRY(ctx, cudaMemcpyAsync(&hsing, D->co.flags + 1, sizeof(int), cudaMemcpyDeviceToHost, st));
+      double ta = now();
+      tp[5] += ta - t0;
       MSB_CUDA_TRY(ctx, cudaStreamSynchronize(st));
+      t0 = now();
+      tp[0] += t0 - ta;
+      ++np_;
       if (hsing) {
         D->co.ready = false;
         return set_error(ctx, MSB_ESINGULAR, "dynamic stage: singular coarse matrix (M=%d)", D->M);
+      }
+      if (prof && prevM > 0) {
+        const int bkt = prevM > 232 ? 1 : 0;
+        float ms;
+        for (int q = 1; q < 5; ++q)
+          if (cudaEventElapsedTime(&ms, pe[0], pe[q]) == cudaSuccess) gsum[bkt][q - 1] += 1e3 * ms;
+        ++gcnt[bkt];
       }
       if (hs.done) break;
       int k = hs.k;  // iteration about to run (1-based)
       int32_t M = 0;
       const bool rebuild = k >= 2;
+      if (prof) cudaEventRecord(pe[0], st);
       if (rebuild) {
         k_dp<<<grid_for(N, 256), 256, 0, st>>>(s->xbuf[cur], s->xprev, N, s->dpbuf);
         MSB_LAUNCH_CHECK(ctx);
@@ -1826,7 +1866,9 @@ msb_status msb_ms_iterate(msb_ctx ctx, msb_solver s, const double* b, double* x,
         MSB_CUDA_TRY(ctx, cudaGraphLaunch(ge, st));
         g_launches.fetch_add(s->sglaunches[cur], std::memory_order_relaxed);
         cur = cur_next;
+        if (prof) cudaEventRecord(pe[1], st);
       }
+      { double t1 = now(); tp[1] += t1 - t0; t0 = t1; }
       if (rebuild) {
         cudaGraphExec_t lg = nullptr;
         if ((rc = labels_graph(ctx, s, &lg))) return rc;
@@ -1834,7 +1876,10 @@ msb_status msb_ms_iterate(msb_ctx ctx, msb_solver s, const double* b, double* x,
         MSB_CUDA_TRY(ctx, cudaGraphLaunch(lg, s->dyn_stream));
         g_launches.fetch_add(s->lglaunches, std::memory_order_relaxed);
         MSB_CUDA_TRY(ctx, cudaEventRecord(s->ev_lab, s->dyn_stream));
+        if (prof) cudaEventRecord(pe[2], s->dyn_stream);
+        { double t1 = now(); tp[1] += t1 - t0; t0 = t1; }
         MSB_CUDA_TRY(ctx, cudaEventSynchronize(s->ev_lab));  // M_dyn, max|Δp| in dyn_pin
+        { double t1 = now(); tp[2] += t1 - t0; t0 = t1; }
         double mxv = 0.0;
         dyn_read(s, &M, &mxv);
         if (!(mxv > 0.0)) M = 0;
@@ -1847,14 +1892,28 @@ msb_status msb_ms_iterate(msb_ctx ctx, msb_solver s, const double* b, double* x,
           if (rc) return rc;
         }
         MSB_CUDA_TRY(ctx, cudaEventRecord(s->ev_dyn, s->dyn_stream));
+        if (prof) cudaEventRecord(pe[3], s->dyn_stream);
         MSB_CUDA_TRY(ctx, cudaStreamWaitEvent(st, s->ev_dyn, 0));
+        { double t1 = now(); tp[3] += t1 - t0; t0 = t1; }
       }
       dynM.push_back(M);
       bool first = false;  // norm already taken
       if (M > 0)
         if ((rc = enqueue_stage(ctx, s, s->dyn_level, db, cur, first))) return rc;
       cur_after.push_back(cur);
+      prevM = M;
+      { double t1 = now(); tp[4] += t1 - t0; t0 = t1; }
     }
+    if (prof)
+      for (int b2 = 0; b2 < 2; ++b2)
+        if (gcnt[b2])
+          fprintf(stderr, "dyn-gpu %s (n=%d) us from iteration start: static-end %.1f labels-end %.1f "
+                  "finish-end %.1f norm-start %.1f\n", b2 ? "M>232" : "M<=232", gcnt[b2],
+                  gsum[b2][0] / gcnt[b2], gsum[b2][1] / gcnt[b2], gsum[b2][2] / gcnt[b2],
+                  gsum[b2][3] / gcnt[b2]);
+    if (prof && np_)
+      fprintf(stderr, "dyn-profile us/iter: sync %.1f static-enq %.1f labels-wait %.1f finish-enq %.1f stage-enq %.1f norm-enq %.1f\n",
+              tp[0] / np_, tp[1] / np_, tp[2] / np_, tp[3] / np_, tp[4] / np_, tp[5] / np_);
   }
   int k = hs.k;
   int xb = cur_after[std::min<size_t>(k, cur_after.size() - 1)];
@@ -1896,7 +1955,6 @@ msb_status msb_solver_destroy(msb_solver s) {
   dfree(ctx, s->mhist);
   if (s->dyn_level) level_free(s->dyn_level);
   dfree(ctx, s->ilu_d);
-  delete s->jq;
   drop_graphs(s);
   if (s->cap_stream) cudaStreamDestroy(s->cap_stream);
   if (s->side_stream) cudaStreamDestroy(s->side_stream);

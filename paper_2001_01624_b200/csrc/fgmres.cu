@@ -263,6 +263,7 @@ using namespace msb;
 extern "C" msb_status msb_fgmres(msb_ctx ctx, msb_solver s, const double* b, double* x, double tol,
                                  int32_t restart, int32_t max_iter, int32_t fixed_iters,
                                  int32_t* iters_out, double* res_hist) {
+  MSB_NVTX("msb_fgmres");
   if (!ctx || !s || !x) return set_error(ctx, MSB_EINVAL, "msb_fgmres: null");
   if (restart < 1 || restart > 64 || max_iter < 0 || fixed_iters < 0)
     return set_error(ctx, MSB_EINVAL, "msb_fgmres: restart must be in [1, 64]");

@@ -283,6 +283,7 @@ msb_status msb_partition_cartesian(msb_ctx ctx, const msb_grid* g, int32_t bx, i
 
 msb_status msb_level_create_cartesian(msb_ctx ctx, msb_op op, int32_t bx, int32_t by, int32_t bz,
                                       msb_level* out, int64_t* nnz_out) {
+  MSB_NVTX("msb_level_create_cartesian");
   if (!ctx || !op || !out || bx < 1 || by < 1 || bz < 1)
     return set_error(ctx, MSB_EINVAL, "msb_level_create_cartesian args");
   msb_level L = new msb_level_s();

@@ -402,6 +402,7 @@ using namespace msb;
 
 extern "C" msb_status msb_level_create_split(msb_ctx ctx, msb_op op, msb_level parent,
                                              msb_level* out, int64_t* nnz_out) {
+  MSB_NVTX("msb_level_create_split");
   if (!ctx || !op || !parent || !out) return set_error(ctx, MSB_EINVAL, "split level: null");
   if (parent->kind != 0) return set_error(ctx, MSB_EINVAL, "split level needs a Cartesian parent");
   int64_t N = op->N;

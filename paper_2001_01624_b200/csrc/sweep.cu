@@ -504,6 +504,7 @@ using namespace msb;
 extern "C" msb_status msb_smooth_basis(msb_ctx ctx, msb_level L, msb_op op, int32_t max_sweeps,
                                        double omega, double tol, int32_t* sweeps_done,
                                        double* last_delta, double* deltas) {
+  MSB_NVTX("msb_smooth_basis");
   if (!ctx || !L || !op) return set_error(ctx, MSB_EINVAL, "msb_smooth_basis: null");
   if (max_sweeps < 0 || !(omega > 0.0) || !(omega <= 1.0))
     return set_error(ctx, MSB_EINVAL, "msb_smooth_basis: bad max_sweeps/omega");

@@ -37,6 +37,8 @@ __device__ __forceinline__ void symv_tile_body(const double* __restrict__ Xp, in
   double2 a[8];
 #pragma unroll
   for (int u = 0; u < 8; ++u) a[u] = __ldcs(tile + (ty + 8 * u) * (ST / 2) + tx);
+  pdl_wait();  // the tile is an input: loaded while the restriction drains; r_c after the wait
+  pdl_trigger();
   auto at = [&](int r) -> int { return map ? map[roff + r] : roff + r; };
   const int cj = bj * ST + 2 * tx;
   const double r0 = cj < M ? ld_mut<CG>(rc + at(cj)) : 0.0;

@@ -155,6 +155,7 @@ extern "C" {
 
 msb_status msb_build_tpfa(msb_ctx ctx, const msb_grid* g, const double* K, const double* mult,
                           const double* mob, const msb_source* src, int32_t n_src, msb_op* out) {
+  MSB_NVTX("msb_build_tpfa");
   if (!ctx || !g || !K || !out || n_src < 0 || (n_src > 0 && !src))
     return set_error(ctx, MSB_EINVAL, "msb_build_tpfa: null argument");
   if (g->nx < 1 || g->ny < 1 || g->nz < 1 || !(g->dx > 0) || !(g->dy > 0) || !(g->dz > 0))
@@ -221,6 +222,7 @@ msb_status msb_build_tpfa(msb_ctx ctx, const msb_grid* g, const double* K, const
 }
 
 msb_status msb_op_set_mobility(msb_ctx ctx, msb_op op, const double* mob) {
+  MSB_NVTX("msb_op_set_mobility");
   if (!ctx || !op || !mob) return set_error(ctx, MSB_EINVAL, "msb_op_set_mobility: null");
   op->tmax_valid = false;  // T changes below
   int64_t nf = (int64_t)(op->nx - 1) * op->ny * op->nz + (int64_t)op->nx * (op->ny - 1) * op->nz +

@@ -285,6 +285,7 @@ extern "C" msb_status msb_transport_step_size(msb_ctx ctx, msb_op op, const doub
 extern "C" msb_status msb_transport_upwind(msb_ctx ctx, msb_op op, const double* p, double* S,
                                            const double* phi, double mu_w, double mu_o, double dt,
                                            double* mob_out, int32_t* substeps_out) {
+  MSB_NVTX("msb_transport_upwind");
   if (!ctx || !op || !p || !S || !phi) return set_error(ctx, MSB_EINVAL, "transport: null");
   if (!(mu_w > 0) || !(mu_o > 0) || !(dt >= 0)) return set_error(ctx, MSB_EINVAL, "transport: bad args");
   int64_t N = op->N;
