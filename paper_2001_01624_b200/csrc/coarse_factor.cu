@@ -254,16 +254,24 @@ msb_status dgemm(msb_ctx ctx, bool ta, bool tb, int m, int n, int K, double alph
   return gemm<false, false>(ctx, m, n, K, alpha, A, lda, B, ldb, beta, C, ldc);
 }
 
-// Leaf: Cholesky of the n x n (n <= LEAF) block at A (ld) in place (lower; upper zeroed)
-// and its triangular inverse into W (ld, lower; upper zeroed).  One CTA, LEAF^2 smem.
-__global__ void __launch_bounds__(1024) k_chol_inv_leaf(double* __restrict__ A, int64_t ld, int n,
-                                                        double* __restrict__ W,
-                                                        const unsigned long long* amax_bits,
-                                                        int* __restrict__ singular) {
+// Leaf: the Cholesky factor L of the n x n (n <= LEAF) block at A (ld), in place (lower;
+// upper zeroed), and its triangular inverse W = L^{-1} into W (ld, lower), from an LDL^T
+// elimination in blocks of 4 pivots (3 barriers per 4 pivots instead of 3 per pivot) with
+// the square roots deferred to a final parallel pass (L = L' D^{1/2}, W = D^{-1/2} L'^{-1}):
+// the critical path per pivot is one reciprocal and a few FMAs.  W' = L'^{-1} is built
+// alongside (the forward substitution of each finished block of L' into the rows below).
+// Pivot test on d_j = l_jj^2 <= 1e-14 max|A_c|.  1024 threads, 64 x 64 leaves.
+constexpr int LB = 4;
+__global__ void __launch_bounds__(1024) k_ldl_inv_leaf(double* __restrict__ A, int64_t ld, int n,
+                                                       double* __restrict__ W,
+                                                       const unsigned long long* amax_bits,
+                                                       int* __restrict__ singular) {
   static_assert(LEAF == 64, "thread-element map assumes 64 x 64 leaves and 1024 threads");
   extern __shared__ double lsm[];
   double (*a)[LEAF + 1] = reinterpret_cast<double (*)[LEAF + 1]>(lsm);
   double (*w)[LEAF + 1] = reinterpret_cast<double (*)[LEAF + 1]>(lsm + LEAF * (LEAF + 1));
+  __shared__ double u[LEAF][LB];  // u_it = L'_it d_t of the current block's columns
+  __shared__ double dinv[LEAF], dd[LEAF];
   const int tid = threadIdx.x;
   for (int e = tid; e < LEAF * LEAF; e += blockDim.x) {
     const int r = e >> 6, c = e & 63;
@@ -271,54 +279,91 @@ __global__ void __launch_bounds__(1024) k_chol_inv_leaf(double* __restrict__ A, 
     w[r][c] = (r == c) ? 1.0 : 0.0;
   }
   __syncthreads();
-  const double amax = __longlong_as_double((long long)*amax_bits);
-  // Right-looking Cholesky fused with the forward substitution W = L^{-1}: at step j the
-  // pivot is taken, column j of L is scaled and row j of W finished (w[j][c] / L_jj), then
-  // every later row receives its rank-1 updates of L and of W (w[r][c] -= L_rj W_jc, c <= j)
-  // in parallel — the same operations in the same order as a column-by-column forward
-  // substitution, so the result is unchanged, with 3 barriers per step instead of an
-  // O(n^2) serial loop per column.
-  // the pivot's reciprocal is formed once and the column / W row scaled by it (as LAPACK's
-  // potf2 scales by 1/l_jj): one fp64 division per step on the critical path, not one per
-  // element
-  __shared__ double rinv;
-  for (int j = 0; j < n; ++j) {
+  const double tol = 1e-14 * __longlong_as_double((long long)*amax_bits);
+  for (int jb = 0; jb < n; jb += LB) {
+    const int je = min(jb + LB, n);
+    // 1. the diagonal block: unit L' and d (one thread; <= 4 pivots)
     if (tid == 0) {
-      double d = a[j][j];
-      if (!(d > 1e-14 * amax)) {
-        atomicExch(singular, 1);
-        d = 1.0;
+      for (int j = jb; j < je; ++j) {
+        double d = a[j][j];
+        if (!(d > tol)) {
+          atomicExch(singular, 1);
+          d = 1.0;
+        }
+        dd[j] = d;
+        const double r = 1.0 / d;
+        dinv[j] = r;
+        for (int i = j + 1; i < je; ++i) {
+          const double uij = a[i][j];
+          a[i][j] = uij * r;  // L'_ij
+          for (int k = j + 1; k <= i; ++k) a[i][k] -= uij * (a[k][j]);  // a[k][j] = L'_kj (k > j)
+        }
       }
-      const double p = sqrt(d);
-      a[j][j] = p;
-      rinv = 1.0 / p;
     }
     __syncthreads();
-    const double ri = rinv;
+    // 2. rows below the block: u_it and L'_it (forward substitution with the unit block);
+    //    W' rows of the block (unit lower inverse within the block)
     if (tid < LEAF) {
-      if (tid > j && tid < n) a[tid][j] *= ri;
+      const int i = tid;
+      if (i >= je && i < n) {
+        double v[LB];
+#pragma unroll
+        for (int t = 0; t < LB; ++t) {
+          const int j = jb + t;
+          if (j < je) {
+            double x = a[i][j];
+            for (int q = 0; q < t; ++q) x -= v[q] * a[j][jb + q];
+            v[t] = x;
+          } else {
+            v[t] = 0.0;
+          }
+        }
+#pragma unroll
+        for (int t = 0; t < LB; ++t) {
+          u[i][t] = v[t];
+          if (jb + t < je) a[i][jb + t] = v[t] * dinv[jb + t];
+        }
+      }
     } else if (tid < 2 * LEAF) {
       const int c = tid - LEAF;
-      if (c <= j) w[j][c] *= ri;
+      for (int j = jb + 1; j < je; ++j) {
+        double x = w[j][c];
+        for (int q = jb; q < j; ++q) x -= a[j][q] * w[q][c];
+        w[j][c] = x;
+      }
     }
     __syncthreads();
+    // 3. rank-(je - jb) updates of the trailing matrix and of the W' rows below the block
 #pragma unroll
-    for (int u = 0; u < (LEAF * LEAF) / 1024; ++u) {
-      const int e = tid + 1024 * u, r = e >> 6, c = e & 63;
-      if (r > j && r < n) {
-        if (c > j) {
-          if (c <= r) a[r][c] -= a[r][j] * a[c][j];
-        } else {
-          w[r][c] -= a[r][j] * w[j][c];
+    for (int e4 = 0; e4 < (LEAF * LEAF) / 1024; ++e4) {
+      const int e = tid + 1024 * e4, r = e >> 6, c = e & 63;
+      if (r >= je && r < n) {
+        if (c >= je) {
+          if (c <= r) {
+            double x = a[r][c];
+            for (int t = 0; t < je - jb; ++t) x -= u[r][t] * a[c][jb + t];
+            a[r][c] = x;
+          }
+        } else if (c < je) {
+          double x = w[r][c];
+          for (int t = 0; t < je - jb; ++t) x -= a[r][jb + t] * w[jb + t][c];
+          w[r][c] = x;
         }
       }
     }
     __syncthreads();
   }
+  // L = L' D^{1/2}, W = D^{-1/2} W'
+  if (tid < n) {
+    const double sq = sqrt(dd[tid]);
+    dd[tid] = sq;
+    dinv[tid] = 1.0 / sq;
+  }
+  __syncthreads();
   for (int e = tid; e < n * n; e += blockDim.x) {
     const int r = e / n, c = e % n;
-    A[(int64_t)r * ld + c] = c <= r ? a[r][c] : 0.0;
-    W[(int64_t)r * ld + c] = c <= r ? w[r][c] : 0.0;
+    A[(int64_t)r * ld + c] = c < r ? a[r][c] * dd[c] : (c == r ? dd[r] : 0.0);
+    W[(int64_t)r * ld + c] = c <= r ? w[r][c] * dinv[r] : 0.0;
   }
 }
 
@@ -377,11 +422,11 @@ static msb_status chol_inv(msb_ctx ctx, double* F, double* Wb, int64_t ld, int n
     constexpr size_t smem = 2 * LEAF * (LEAF + 1) * sizeof(double);
     static bool attr = false;
     if (!attr) {
-      MSB_CUDA_TRY(ctx, cudaFuncSetAttribute(k_chol_inv_leaf, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      MSB_CUDA_TRY(ctx, cudaFuncSetAttribute(k_ldl_inv_leaf, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)smem));
       attr = true;
     }
-    k_chol_inv_leaf<<<1, 1024, smem, ctx->stream>>>(F, ld, n, Wb, amax, sing);
+    k_ldl_inv_leaf<<<1, 1024, smem, ctx->stream>>>(F, ld, n, Wb, amax, sing);
     MSB_LAUNCH_CHECK(ctx);
     return MSB_OK;
   }
@@ -439,51 +484,90 @@ static msb_status lauum(msb_ctx ctx, const double* W, double* F, int n, int64_t 
 }
 
 // ---------------------------------------------------------------- small SPD systems
-// One CTA: right-looking Cholesky of the M x M (M <= SMALL_CHOL_M) matrix A (row-major)
-// in shared memory, packed lower rows a[i (i+1)/2 + j]; column scaled by the pivot's
-// reciprocal (as LAPACK's potf2); the factor is written packed to Lp.  Pivot test as the
-// recursive path (d_jj <= 1e-14 max|A_c| -> singular).
-constexpr int SC_T = 512;
+// One CTA: LDL^T of the M x M (M <= SMALL_CHOL_M) matrix A (row-major) in shared memory,
+// packed lower rows a[i (i+1)/2 + j], in blocks of SB pivots (3 barriers per block): the
+// diagonal block by one thread, the rows below it by one thread each (forward substitution
+// with the unit block), then the rank-SB update of the trailing matrix.  Output: the unit
+// L' packed (diagonal slots unused) followed by the M reciprocal pivots 1/d_j.  Pivot test
+// as the recursive path (d_j <= 1e-14 max|A_c| -> singular).  The same matrix as the
+// Cholesky factor L = L' D^{1/2}.
+constexpr int SC_T = 512, SB = 8;
 __global__ void __launch_bounds__(SC_T) k_chol_small(const double* __restrict__ A, int M,
                                                      double* __restrict__ Lp,
                                                      const unsigned long long* amax_bits,
                                                      int* __restrict__ singular) {
-  extern __shared__ double a[];
-  __shared__ double rinv;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  extern __shared__ double sm[];
   const int np = M * (M + 1) / 2;
+  double* a = sm;
+  double* dd = sm + np;      // d_j
+  double* di = dd + M;       // 1 / d_j
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   for (int i = warp; i < M; i += SC_T / 32)
     for (int j = lane; j <= i; j += 32) a[i * (i + 1) / 2 + j] = A[(int64_t)i * M + j];
   __syncthreads();
   const double tol = 1e-14 * __longlong_as_double((long long)*amax_bits);
-  for (int j = 0; j < M; ++j) {
-    const int jj = j * (j + 1) / 2 + j;
+  for (int jb = 0; jb < M; jb += SB) {
+    const int je = min(jb + SB, M);
     if (tid == 0) {
-      double d = a[jj];
-      if (!(d > tol)) {
-        *singular = 1;
-        d = 1.0;
+      for (int j = jb; j < je; ++j) {
+        double d = a[j * (j + 1) / 2 + j];
+        if (!(d > tol)) {
+          *singular = 1;
+          d = 1.0;
+        }
+        const double r = 1.0 / d;
+        dd[j] = d;
+        di[j] = r;
+        for (int i = j + 1; i < je; ++i) {
+          const int ri = i * (i + 1) / 2;
+          const double uij = a[ri + j];
+          a[ri + j] = uij * r;
+          for (int k = j + 1; k <= i; ++k) a[ri + k] -= uij * a[k * (k + 1) / 2 + j];
+        }
       }
-      const double p = sqrt(d);
-      a[jj] = p;
-      rinv = 1.0 / p;
-      Lp[np + j] = rinv;  // the substitutions multiply by it
     }
     __syncthreads();
-    for (int i = j + 1 + tid; i < M; i += SC_T) a[i * (i + 1) / 2 + j] *= rinv;
-    __syncthreads();
-    for (int i = j + 1 + warp; i < M; i += SC_T / 32) {
+    for (int i = je + tid; i < M; i += SC_T) {  // L'_it for the rows below the block
       const int ri = i * (i + 1) / 2;
-      const double lij = a[ri + j];
-      for (int k = j + 1 + lane; k <= i; k += 32) a[ri + k] -= lij * a[k * (k + 1) / 2 + j];
+      double v[SB];
+#pragma unroll
+      for (int t = 0; t < SB; ++t) {
+        const int j = jb + t;
+        v[t] = 0.0;
+        if (j < je) {
+          double x = a[ri + j];
+          const int rj = j * (j + 1) / 2;
+          for (int q = 0; q < t; ++q) x -= v[q] * a[rj + jb + q];
+          v[t] = x;
+        }
+      }
+#pragma unroll
+      for (int t = 0; t < SB; ++t)
+        if (jb + t < je) a[ri + jb + t] = v[t] * di[jb + t];
+    }
+    __syncthreads();
+    for (int i = je + warp; i < M; i += SC_T / 32) {  // rank-(je - jb) trailing update
+      const int ri = i * (i + 1) / 2;
+      double ui[SB];
+#pragma unroll
+      for (int t = 0; t < SB; ++t) ui[t] = jb + t < je ? a[ri + jb + t] * dd[jb + t] : 0.0;
+      for (int k = je + lane; k <= i; k += 32) {
+        const int rk = k * (k + 1) / 2;
+        double x = a[ri + k];
+#pragma unroll
+        for (int t = 0; t < SB; ++t)
+          if (jb + t < je) x -= ui[t] * a[rk + jb + t];
+        a[ri + k] = x;
+      }
     }
     __syncthreads();
   }
   for (int e = tid; e < np; e += SC_T) Lp[e] = a[e];
+  for (int j = tid; j < M; j += SC_T) Lp[np + j] = di[j];
 }
 
-// x = L^{-T} L^{-1} r with the packed factor (followed by the M pivot reciprocals), one
-// warp (forward then backward substitution)
+// x = L'^{-T} D^{-1} L'^{-1} r with k_chol_small's output, one warp (forward substitution
+// with the unit L', the pivot scaling, backward substitution with L'^T)
 __global__ void __launch_bounds__(32) k_chol_small_solve(const double* __restrict__ Lp, int M,
                                                          const double* __restrict__ r,
                                                          double* __restrict__ x, const int* done) {
@@ -496,18 +580,16 @@ __global__ void __launch_bounds__(32) k_chol_small_solve(const double* __restric
   for (int e = lane; e < np + M; e += 32) L[e] = Lp[e];
   for (int i = lane; i < M; i += 32) y[i] = r[i];
   __syncwarp();
-  for (int j = 0; j < M; ++j) {  // L y = r, column-oriented
-    const double yj = y[j] * dinv[j];
-    __syncwarp();
-    if (lane == 0) y[j] = yj;
+  for (int j = 0; j < M; ++j) {  // L' y = r, column-oriented
+    const double yj = y[j];
     for (int i = j + 1 + lane; i < M; i += 32) y[i] -= L[i * (i + 1) / 2 + j] * yj;
     __syncwarp();
   }
-  for (int j = M - 1; j >= 0; --j) {  // L^T x = y, row j of L holds column j of L^T
+  for (int i = lane; i < M; i += 32) y[i] *= dinv[i];
+  __syncwarp();
+  for (int j = M - 1; j >= 0; --j) {  // L'^T x = y, row j of L' holds column j of L'^T
     const int rj = j * (j + 1) / 2;
-    const double xj = y[j] * dinv[j];
-    __syncwarp();
-    if (lane == 0) y[j] = xj;
+    const double xj = y[j];
     for (int i = lane; i < j; i += 32) y[i] -= L[rj + i] * xj;
     __syncwarp();
   }
@@ -544,7 +626,8 @@ msb_status coarse_factor_dense(msb_ctx ctx, Coarse& co) {
       MSB_CUDA_TRY(ctx, cudaFuncSetAttribute(k_chol_small_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
       attr = true;
     }
-    k_chol_small<<<1, SC_T, (size_t)M * (M + 1) / 2 * sizeof(double), s>>>(co.Ac, M, co.L, amax, sing);
+    k_chol_small<<<1, SC_T, ((size_t)M * (M + 1) / 2 + 2 * M) * sizeof(double), s>>>(co.Ac, M, co.L,
+                                                                                   amax, sing);
     MSB_LAUNCH_CHECK(ctx);
     int hs = 0;
     if (!co.defer_check) {

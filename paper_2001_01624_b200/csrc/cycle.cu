@@ -1805,48 +1805,20 @@ msb_status msb_ms_iterate(msb_ctx ctx, msb_solver s, const double* b, double* x,
       MSB_CUDA_TRY(ctx, cudaEventCreateWithFlags(&s->ev_dyn, cudaEventDisableTiming));
       MSB_CUDA_TRY(ctx, cudaEventCreateWithFlags(&s->ev_lab, cudaEventDisableTiming));
     }
-    // TEMPORARY host-phase timing (MSB_DYN_PROFILE): sync wait, static enqueue, labels wait,
-    // finish enqueue, stage enqueue
-    static const bool prof = getenv("MSB_DYN_PROFILE") != nullptr;
-    double tp[6] = {0, 0, 0, 0, 0, 0};
-    int np_ = 0;
-    auto now = [] { return std::chrono::duration<double, std::micro>(
-                        std::chrono::steady_clock::now().time_since_epoch()).count(); };
-    double t0 = now();
-    cudaEvent_t pe[5] = {};
-    if (prof)
-      for (auto& e : pe) cudaEventCreate(&e);
-    double gsum[2][5] = {};  // [M <= 232 | M > 232][static, labels, finish, stage, next-norm]
-    int gcnt[2] = {0, 0};
-    int prevM = -1;
     while (true) {
-      if (prof && prevM > 0) cudaEventRecord(pe[4], st);
       if ((rc = enqueue_norm(ctx, s, s->xbuf[cur], db, 0))) return rc;
       MSB_CUDA_TRY(ctx, cudaMemcpyAsync(&hs, s->st, sizeof(hs), cudaMemcpyDeviceToHost, st));
       if (D->co.flags)
         MSB_CUDA_TRY(ctx, cudaMemcpyAsync(&hsing, D->co.flags + 1, sizeof(int), cudaMemcpyDeviceToHost, st));
-      double ta = now();
-      tp[5] += ta - t0;
       MSB_CUDA_TRY(ctx, cudaStreamSynchronize(st));
-      t0 = now();
-      tp[0] += t0 - ta;
-      ++np_;
       if (hsing) {
         D->co.ready = false;
         return set_error(ctx, MSB_ESINGULAR, "dynamic stage: singular coarse matrix (M=%d)", D->M);
-      }
-      if (prof && prevM > 0) {
-        const int bkt = prevM > 232 ? 1 : 0;
-        float ms;
-        for (int q = 1; q < 5; ++q)
-          if (cudaEventElapsedTime(&ms, pe[0], pe[q]) == cudaSuccess) gsum[bkt][q - 1] += 1e3 * ms;
-        ++gcnt[bkt];
       }
       if (hs.done) break;
       int k = hs.k;  // iteration about to run (1-based)
       int32_t M = 0;
       const bool rebuild = k >= 2;
-      if (prof) cudaEventRecord(pe[0], st);
       if (rebuild) {
         k_dp<<<grid_for(N, 256), 256, 0, st>>>(s->xbuf[cur], s->xprev, N, s->dpbuf);
         MSB_LAUNCH_CHECK(ctx);
@@ -1866,9 +1838,7 @@ msb_status msb_ms_iterate(msb_ctx ctx, msb_solver s, const double* b, double* x,
         MSB_CUDA_TRY(ctx, cudaGraphLaunch(ge, st));
         g_launches.fetch_add(s->sglaunches[cur], std::memory_order_relaxed);
         cur = cur_next;
-        if (prof) cudaEventRecord(pe[1], st);
       }
-      { double t1 = now(); tp[1] += t1 - t0; t0 = t1; }
       if (rebuild) {
         cudaGraphExec_t lg = nullptr;
         if ((rc = labels_graph(ctx, s, &lg))) return rc;
@@ -1876,10 +1846,7 @@ msb_status msb_ms_iterate(msb_ctx ctx, msb_solver s, const double* b, double* x,
         MSB_CUDA_TRY(ctx, cudaGraphLaunch(lg, s->dyn_stream));
         g_launches.fetch_add(s->lglaunches, std::memory_order_relaxed);
         MSB_CUDA_TRY(ctx, cudaEventRecord(s->ev_lab, s->dyn_stream));
-        if (prof) cudaEventRecord(pe[2], s->dyn_stream);
-        { double t1 = now(); tp[1] += t1 - t0; t0 = t1; }
         MSB_CUDA_TRY(ctx, cudaEventSynchronize(s->ev_lab));  // M_dyn, max|Δp| in dyn_pin
-        { double t1 = now(); tp[2] += t1 - t0; t0 = t1; }
         double mxv = 0.0;
         dyn_read(s, &M, &mxv);
         if (!(mxv > 0.0)) M = 0;
@@ -1892,28 +1859,14 @@ msb_status msb_ms_iterate(msb_ctx ctx, msb_solver s, const double* b, double* x,
           if (rc) return rc;
         }
         MSB_CUDA_TRY(ctx, cudaEventRecord(s->ev_dyn, s->dyn_stream));
-        if (prof) cudaEventRecord(pe[3], s->dyn_stream);
         MSB_CUDA_TRY(ctx, cudaStreamWaitEvent(st, s->ev_dyn, 0));
-        { double t1 = now(); tp[3] += t1 - t0; t0 = t1; }
       }
       dynM.push_back(M);
       bool first = false;  // norm already taken
       if (M > 0)
         if ((rc = enqueue_stage(ctx, s, s->dyn_level, db, cur, first))) return rc;
       cur_after.push_back(cur);
-      prevM = M;
-      { double t1 = now(); tp[4] += t1 - t0; t0 = t1; }
     }
-    if (prof)
-      for (int b2 = 0; b2 < 2; ++b2)
-        if (gcnt[b2])
-          fprintf(stderr, "dyn-gpu %s (n=%d) us from iteration start: static-end %.1f labels-end %.1f "
-                  "finish-end %.1f norm-start %.1f\n", b2 ? "M>232" : "M<=232", gcnt[b2],
-                  gsum[b2][0] / gcnt[b2], gsum[b2][1] / gcnt[b2], gsum[b2][2] / gcnt[b2],
-                  gsum[b2][3] / gcnt[b2]);
-    if (prof && np_)
-      fprintf(stderr, "dyn-profile us/iter: sync %.1f static-enq %.1f labels-wait %.1f finish-enq %.1f stage-enq %.1f norm-enq %.1f\n",
-              tp[0] / np_, tp[1] / np_, tp[2] / np_, tp[3] / np_, tp[4] / np_, tp[5] / np_);
   }
   int k = hs.k;
   int xb = cur_after[std::min<size_t>(k, cur_after.size() - 1)];
