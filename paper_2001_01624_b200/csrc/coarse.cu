@@ -464,6 +464,8 @@ __global__ void __launch_bounds__(16 * ST) k_symv_reduce_b(const SymvRow* __rest
                                                           double* __restrict__ out,
                                                           const int32_t* __restrict__ omap,
                                                           const int* done) {
+  pdl_wait();
+  pdl_trigger();
   const bool skip = done && *(volatile const int*)done;
   const SymvRow d = rd[blockIdx.x];
   symv_reduce_body<false>(part + d.tile_base * 2 * ST, d.M, d.ntb, out, d.b, skip, omap, d.roff);
@@ -472,8 +474,10 @@ __global__ void __launch_bounds__(16 * ST) k_symv_reduce_b(const SymvRow* __rest
 void symv_batched(msb_ctx ctx, const SymvTile* td, int ntile, const SymvRow* rd, int nrow,
                   const double* Xp, const double* vec, const int32_t* map, double* part,
                   double* out, const int32_t* omap, const int* done) {
-  k_symv_tiles_b<<<ntile, SYMV_T, 0, ctx->stream>>>(td, Xp, vec, map, part);
-  k_symv_reduce_b<<<nrow, 16 * ST, 0, ctx->stream>>>(rd, part, out, omap, done);
+  launch_ex(k_symv_tiles_b, dim3(ntile), dim3(SYMV_T), 0, ctx->stream, kPDL, 1, td, Xp, vec, map,
+            part);
+  launch_ex(k_symv_reduce_b, dim3(nrow), dim3(16 * ST), 0, ctx->stream, kPDL, 1, rd, part, out, omap,
+            done);
   count_launch();
   count_launch();
 }

@@ -107,6 +107,8 @@ __global__ void __launch_bounds__(256) k_schur_t(const double* __restrict__ Aell
                                                  const double* __restrict__ rc,
                                                  const double* __restrict__ y,
                                                  double* __restrict__ t) {
+  pdl_wait();  // y comes from the domain solve
+  pdl_trigger();
   const int q = (int)((blockIdx.x * (unsigned)blockDim.x + threadIdx.x) >> 5);
   const int lane = threadIdx.x & 31;
   if (q >= nS) return;  // warp-uniform
@@ -134,6 +136,8 @@ __global__ void __launch_bounds__(256) k_schur_u(const double* __restrict__ Aell
                                                  const double* __restrict__ xs,
                                                  double* __restrict__ u, double* __restrict__ xc,
                                                  const int* done) {
+  pdl_wait();  // x_S comes from the separator solve
+  pdl_trigger();
   const int w = (int)((blockIdx.x * (unsigned)blockDim.x + threadIdx.x) >> 5);
   const int lane = threadIdx.x & 31;
   if (w < nD) {
@@ -477,16 +481,14 @@ void coarse_schur_solve(msb_ctx ctx, const Coarse& co, const double* rc, double*
   // y_d = A_dd^{-1} r_d (r_c read through the domain node map)
   symv_batched(ctx, S->td, S->ntd, S->rd, S->nrd, S->Xd, rc, S->dom_nodes, S->partd, S->y, nullptr,
                nullptr);
-  k_schur_t<<<grid_for((int64_t)S->nS * 32, 256), 256, 0, st>>>(co.Aell, n0, n1, n2, S->sep_nodes,
-                                                                 S->nS, S->node_pos, rc, S->y,
-                                                                 S->t);
+  launch_ex(k_schur_t, dim3(grid_for((int64_t)S->nS * 32, 256)), dim3(256), 0, st, kPDL, 1, co.Aell,
+            n0, n1, n2, S->sep_nodes, S->nS, S->node_pos, rc, S->y, S->t);
   count_launch();
   symv_batched(ctx, S->tc, S->ntc, S->rcd, S->nrc, S->C.Xp, S->t, nullptr, S->C.part, S->xs,
                nullptr, nullptr);
   const int64_t wu = (int64_t)S->nD + (S->nS + 31) / 32;  // warps
-  k_schur_u<<<grid_for(wu * 32, 256), 256, 0, st>>>(co.Aell, n0, n1, n2, S->dom_nodes, S->nD,
-                                                     S->sep_nodes, S->nS, S->node_pos, rc, S->xs,
-                                                     S->u, xc, done);
+  launch_ex(k_schur_u, dim3(grid_for(wu * 32, 256)), dim3(256), 0, st, kPDL, 1, co.Aell, n0, n1, n2,
+            S->dom_nodes, S->nD, S->sep_nodes, S->nS, S->node_pos, rc, S->xs, S->u, xc, done);
   count_launch();
   symv_batched(ctx, S->td, S->ntd, S->rd, S->nrd, S->Xd, S->u, nullptr, S->partd, xc, S->dom_nodes,
                done);
