@@ -325,9 +325,11 @@ typedef struct {
 /* Create a CPR object on `op` (grid + base T) whose predictor runs n_cycles Eq.-(8) cycles
  * (pre-smoothing damped Jacobi ω_s, ν = 1, then the coarse correction of `lev`) on
  * J*_pp ("one or a few cycles").  `lev` must be a Cartesian level of the same
- * grid (its smoothed basis P is used as prolongation, R = P^T; reading C5); it is not
- * owned and must outlive the CPR object.  Errors: MSB_EINVAL (nrel, n_cycles < 1,
- * explicit level), MSB_EDIM (other grid). */
+ * grid (its smoothed basis P is used as prolongation, R = P^T; reading C5) with M <= 8192
+ * (the predictor inverts A_c densely); it is not owned, must outlive the CPR object, and
+ * must not be re-smoothed between msb_cpr_decouple and the applications that use it.
+ * Errors: MSB_EINVAL (nrel, n_cycles < 1, explicit level, M > 8192, dt or a viscosity
+ * <= 0), MSB_EDIM (other grid). */
 msb_status msb_cpr_create(msb_ctx ctx, msb_op op, msb_level lev, const msb_fluid* fl,
                           int32_t n_cycles, double omega_s, msb_cpr* out);
 /* Linearize at (p, S) with previous time level (p_n, S_n) (host|dev, N doubles each) and

@@ -735,6 +735,9 @@ msb_status msb_cpr_create(msb_ctx ctx, msb_op op, msb_level lev, const msb_fluid
   if (lev->kind != 0) return set_error(ctx, MSB_EINVAL, "msb_cpr_create: Cartesian level required");
   if (lev->nx != op->nx || lev->ny != op->ny || lev->nz != op->nz)
     return set_error(ctx, MSB_EDIM, "msb_cpr_create: level of another grid");
+  if (lev->M > 8192)
+    return set_error(ctx, MSB_EINVAL, "msb_cpr_create: the predictor's dense coarse inverse "
+                     "supports M <= 8192 (M=%d)", lev->M);
   if (!(fl->dt > 0.0) || !(fl->mu_w > 0.0) || !(fl->mu_o > 0.0))
     return set_error(ctx, MSB_EINVAL, "msb_cpr_create: dt and viscosities must be > 0");
   msb_cpr c = new msb_cpr_s();
