@@ -83,7 +83,12 @@ __global__ void __launch_bounds__(256) k_rap_const_det(const int32_t* __restrict
                                                        const double* __restrict__ Ty,
                                                        const double* __restrict__ Tz,
                                                        const unsigned long long* __restrict__ tmax_bits,
-                                                       unsigned long long* __restrict__ acc) {
+                                                       unsigned long long* __restrict__ acc,
+                                                       const int* Md) {
+  if (Md) {  // M from the device (the dynamic loop's graph-captured small path; 0 = skip)
+    M = *Md;
+    if (M == 0) return;
+  }
   const unsigned FULL = 0xffffffffu, NONE = 0xffffffffu;
   const int N = g.nxy * g.nz;
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
@@ -135,8 +140,10 @@ __global__ void __launch_bounds__(256) k_rap_const_det(const int32_t* __restrict
 __global__ void __launch_bounds__(256) k_fx_const_to_double(const unsigned long long* __restrict__ acc,
                                                             int M,
                                                             const unsigned long long* __restrict__ tmax_bits,
-                                                            double* __restrict__ Ac) {
+                                                            double* __restrict__ Ac, const int* Md) {
+  if (Md) M = *Md;
   const int a = blockIdx.x;
+  if (a >= M) return;
   const int F = 90 - ilogb(__longlong_as_double((long long)*tmax_bits));
   unsigned long long slo = 0, shi = 0;
   for (int b = threadIdx.x; b < M; b += blockDim.x) {
@@ -666,6 +673,21 @@ msb_status op_tmax(msb_ctx ctx, msb_op op, const unsigned long long** out) {
   return MSB_OK;
 }
 
+msb_status coarse_assemble_const_gated(msb_ctx ctx, msb_level L, msb_op op, const int* Md, int Mcap) {
+  Coarse& co = L->co;
+  cudaStream_t st = ctx->stream;
+  if (!co.acc || co.acc_cap < (size_t)Mcap * Mcap)
+    return set_error(ctx, MSB_EINVAL, "coarse_assemble_const_gated: accumulator not reserved");
+  if (!op->tmax_valid) return set_error(ctx, MSB_EINVAL, "coarse_assemble_const_gated: max|T| not cached");
+  MSB_CUDA_TRY(ctx, cudaMemsetAsync(co.acc, 0, (size_t)2 * Mcap * Mcap * sizeof(unsigned long long), st));
+  k_rap_const_det<<<grid_for(op->N, 256), 256, 0, st>>>(L->col, make_grid3(op->nx, op->ny, op->nz), 0,
+                                                        op->Tx, op->Ty, op->Tz, op->tmax, co.acc, Md);
+  MSB_LAUNCH_CHECK(ctx);
+  k_fx_const_to_double<<<Mcap, 256, 0, st>>>(co.acc, 0, op->tmax, co.Ac, Md);
+  MSB_LAUNCH_CHECK(ctx);
+  return MSB_OK;
+}
+
 msb_status coarse_assemble_dense(msb_ctx ctx, msb_level L, msb_op op) {
   int M = L->M;
   Coarse& co = L->co;
@@ -699,7 +721,8 @@ msb_status coarse_assemble_dense(msb_ctx ctx, msb_level L, msb_op op) {
     tmax = const_cast<unsigned long long*>(tmax_c);
     if (constant) {
       k_rap_const_det<<<grid_for(op->N, 256), 256, 0, st>>>(
-          L->col, make_grid3(op->nx, op->ny, op->nz), M, op->Tx, op->Ty, op->Tz, tmax, co.acc);
+          L->col, make_grid3(op->nx, op->ny, op->nz), M, op->Tx, op->Ty, op->Tz, tmax, co.acc,
+          nullptr);
     } else {
       if (L->unity)
         k_rap<true, true><<<grid_for(L->N, 128), 128, 0, st>>>(*L, L->P[L->cur], op->Tx, op->Ty,
@@ -710,7 +733,7 @@ msb_status coarse_assemble_dense(msb_ctx ctx, msb_level L, msb_op op) {
     }
     MSB_LAUNCH_CHECK(ctx);
     if (constant)
-      k_fx_const_to_double<<<M, 256, 0, st>>>(co.acc, M, tmax, co.Ac);
+      k_fx_const_to_double<<<M, 256, 0, st>>>(co.acc, M, tmax, co.Ac, nullptr);
     else if (L->unity)
       k_fx_sym_to_double<<<M, 256, 0, st>>>(co.acc, M, tmax, co.Ac);
     else

@@ -455,7 +455,9 @@ static msb_status chol_inv(msb_ctx ctx, double* F, double* Wb, int64_t ld, int n
   return MSB_OK;
 }
 
-__global__ void k_absmax2(const double* __restrict__ A, int64_t n, unsigned long long* out) {
+__global__ void k_absmax2(const double* __restrict__ A, int64_t n, unsigned long long* out,
+                          const int* Md = nullptr) {
+  if (Md) n = (int64_t)*Md * *Md;  // an M x M matrix, M from the device
   double m = 0.0;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
@@ -495,7 +497,11 @@ constexpr int SC_T = 512, SB = 8;
 __global__ void __launch_bounds__(SC_T) k_chol_small(const double* __restrict__ A, int M,
                                                      double* __restrict__ Lp,
                                                      const unsigned long long* amax_bits,
-                                                     int* __restrict__ singular) {
+                                                     int* __restrict__ singular, const int* Md) {
+  if (Md) {  // M from the device (graph-captured small path; 0 = skip)
+    M = *Md;
+    if (M == 0) return;
+  }
   extern __shared__ double sm[];
   const int np = M * (M + 1) / 2;
   double* a = sm;
@@ -568,18 +574,25 @@ __global__ void __launch_bounds__(SC_T) k_chol_small(const double* __restrict__ 
 
 // x = L'^{-T} D^{-1} L'^{-1} r with k_chol_small's output, one warp (forward substitution
 // with the unit L', the pivot scaling, backward substitution with L'^T)
-__global__ void __launch_bounds__(32) k_chol_small_solve(const double* __restrict__ Lp, int M,
-                                                         const double* __restrict__ r,
-                                                         double* __restrict__ x, const int* done) {
+constexpr int SS_T = 256;  // the whole CTA stages the factor into shared memory, warp 0 solves
+__global__ void __launch_bounds__(SS_T) k_chol_small_solve(const double* __restrict__ Lp, int M,
+                                                           const double* __restrict__ r,
+                                                           double* __restrict__ x, const int* done,
+                                                           const int* Md) {
+  if (Md) {
+    M = *Md;
+    if (M == 0) return;
+  }
   extern __shared__ double sm[];
   double* L = sm;
   const int np = M * (M + 1) / 2;
   const double* dinv = L + np;
   double* y = sm + np + M;
+  for (int e = threadIdx.x; e < np + M; e += SS_T) L[e] = Lp[e];
+  for (int i = threadIdx.x; i < M; i += SS_T) y[i] = r[i];
+  __syncthreads();
+  if (threadIdx.x >= 32) return;
   const int lane = threadIdx.x;
-  for (int e = lane; e < np + M; e += 32) L[e] = Lp[e];
-  for (int i = lane; i < M; i += 32) y[i] = r[i];
-  __syncwarp();
   for (int j = 0; j < M; ++j) {  // L' y = r, column-oriented
     const double yj = y[j];
     for (int i = j + 1 + lane; i < M; i += 32) y[i] -= L[i * (i + 1) / 2 + j] * yj;
@@ -602,7 +615,37 @@ void coarse_solve_small(msb_ctx ctx, const Coarse& co, const double* rc, double*
                         const int* done) {
   const int M = co.M;
   const size_t smem = ((size_t)M * (M + 1) / 2 + 2 * M) * sizeof(double);
-  k_chol_small_solve<<<1, 32, smem, ctx->stream>>>(co.L, M, rc, xc, done);
+  k_chol_small_solve<<<1, SS_T, smem, ctx->stream>>>(co.L, M, rc, xc, done, nullptr);
+  count_launch();
+}
+
+// The dynamic loop's graph-captured small path: the one-CTA factorisation of an M x M
+// system (M <= SMALL_CHOL_M) with M read from the device (*Md; 0 = nothing to do), and its
+// solve.  Launch shapes are those of M = SMALL_CHOL_M.
+msb_status coarse_factor_small_gated(msb_ctx ctx, Coarse& co, const int* Md) {
+  cudaStream_t s = ctx->stream;
+  unsigned long long* amax = co.flags;
+  int* sing = reinterpret_cast<int*>(co.flags + 1);
+  static bool attr = false;
+  const int mx = (int)(((size_t)SMALL_CHOL_M * (SMALL_CHOL_M + 1) / 2 + 2 * SMALL_CHOL_M) * sizeof(double));
+  if (!attr) {
+    MSB_CUDA_TRY(ctx, cudaFuncSetAttribute(k_chol_small, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+    MSB_CUDA_TRY(ctx, cudaFuncSetAttribute(k_chol_small_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+    attr = true;
+  }
+  MSB_CUDA_TRY(ctx, cudaMemsetAsync(co.flags, 0, 16, s));
+  k_absmax2<<<std::min<int64_t>(grid_for((int64_t)SMALL_CHOL_M * SMALL_CHOL_M, 256), 4 * ctx->sm_count),
+              256, 0, s>>>(co.Ac, 0, amax, Md);
+  MSB_LAUNCH_CHECK(ctx);
+  k_chol_small<<<1, SC_T, mx, s>>>(co.Ac, 0, co.L, amax, sing, Md);
+  MSB_LAUNCH_CHECK(ctx);
+  return MSB_OK;
+}
+
+void coarse_solve_small_gated(msb_ctx ctx, const Coarse& co, const double* rc, double* xc,
+                              const int* done, const int* Md) {
+  const size_t smem = ((size_t)SMALL_CHOL_M * (SMALL_CHOL_M + 1) / 2 + 2 * SMALL_CHOL_M) * sizeof(double);
+  k_chol_small_solve<<<1, SS_T, smem, ctx->stream>>>(co.L, 0, rc, xc, done, Md);
   count_launch();
 }
 
@@ -627,7 +670,7 @@ msb_status coarse_factor_dense(msb_ctx ctx, Coarse& co) {
       attr = true;
     }
     k_chol_small<<<1, SC_T, ((size_t)M * (M + 1) / 2 + 2 * M) * sizeof(double), s>>>(co.Ac, M, co.L,
-                                                                                   amax, sing);
+                                                                                   amax, sing, nullptr);
     MSB_LAUNCH_CHECK(ctx);
     int hs = 0;
     if (!co.defer_check) {

@@ -408,8 +408,9 @@ __global__ void __launch_bounds__(CT) k_res_restrict_det(StencilT S, LevelView L
                                                          const double* __restrict__ b,
                                                          double* __restrict__ rc_part, int first,
                                                          double* __restrict__ partials,
-                                                         const IterState* st) {
+                                                         const IterState* st, const int* Md) {
   if (is_done(st)) return;
+  if (Md) M = *Md;  // M from the device (graph-captured small dynamic path)
   extern __shared__ double acc[];  // [RRD_WARPS][M]
   for (int m = threadIdx.x; m < RRD_WARPS * M; m += blockDim.x) acc[m] = 0.0;
   __syncthreads();
@@ -465,9 +466,11 @@ __global__ void __launch_bounds__(CT) k_res_restrict_det(StencilT S, LevelView L
 // one CTA per column: strided partial sums then a shuffle/shared tree, all fixed-order
 __global__ void __launch_bounds__(256) k_rc_combine(const double* __restrict__ rc_part, int G,
                                                     int M, double* __restrict__ rc,
-                                                    const IterState* st) {
+                                                    const IterState* st, const int* Md) {
   if (is_done(st)) return;
+  if (Md) M = *Md;
   const int m = blockIdx.x;
+  if (m >= M) return;
   double t = 0.0;
   for (int g = threadIdx.x; g < G; g += blockDim.x) t += rc_part[(size_t)g * M + m];
   __shared__ double sh[8];
@@ -997,6 +1000,18 @@ __global__ void k_bins_abs(const double* __restrict__ ind, int64_t N, BinEdges E
   bins[c] = b;
 }
 
+// The dynamic loop's small-path gate (after the rebuild's numbering): gate[4] = M_dyn when
+// the stage runs on the graph-captured small path (max|Δp| > 0 and 0 < M_dyn <= SMALL_CHOL_M),
+// else 0; gate[0] (read as IterState::done by the stage kernels) = 1 when they must not store.
+__global__ void k_dyn_gate(const int32_t* __restrict__ Mtot, const unsigned long long* __restrict__ mx,
+                           const IterState* st, int* __restrict__ gate) {
+  const int M = *Mtot;
+  const double m = __longlong_as_double((long long)*mx);
+  const int Meff = (m > 0.0 && M > 0 && M <= SMALL_CHOL_M) ? M : 0;
+  gate[4] = Meff;
+  gate[0] = (Meff == 0 || st->done) ? 1 : 0;
+}
+
 __global__ void k_refill_const(const int32_t* __restrict__ part, int64_t N, int32_t* __restrict__ col,
                                double* __restrict__ P) {
   int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -1258,6 +1273,18 @@ msb_status msb_solver_create(msb_ctx ctx, msb_op op, const msb_level* levels, in
     MSB_ALLOC(ctx, D->co.tri_y, double, cap);
     D->co.cap = cap;
     D->co.tri = true;  // factorised for exactly one solve per rebuild
+    // the graph-captured small path needs fixed buffers: the exact-assembly accumulator and
+    // the factor flags at full capacity, the restriction partials for M <= RRD_MAX_M, the gate
+    MSB_ALLOC(ctx, D->co.acc, unsigned long long, 2 * (int64_t)cap * cap + 2);
+    D->co.acc_cap = (size_t)cap * cap;
+    MSB_ALLOC(ctx, D->co.flags, unsigned long long, 2);
+    {
+      const int64_t gpart = std::min<int64_t>(grid_for(N, CT), 4 * ctx->sm_count);
+      const size_t need = (size_t)gpart * RRD_MAX_M;
+      MSB_ALLOC(ctx, s->rc_part, double, need);
+      s->rc_part_cap = need;
+    }
+    MSB_ALLOC(ctx, s->dyn_gate, int, 8);
     s->dyn_level = D;
   }
   // bins must not alias cnt during counting: give them their own buffer
@@ -1437,9 +1464,9 @@ static msb_status enqueue_stage(msb_ctx ctx, msb_solver s, msb_level L, const do
         attr = true;
       }
       k_res_restrict_det<<<gpart, CT, smem, st>>>(S, V, L->M, s->xbuf[cur], b, s->rc_part,
-                                                  first ? 1 : 0, s->partials, s->st);
+                                                  first ? 1 : 0, s->partials, s->st, nullptr);
       MSB_LAUNCH_CHECK(ctx);
-      k_rc_combine<<<L->M, 256, 0, st>>>(s->rc_part, (int)gpart, L->M, s->rc, s->st);
+      k_rc_combine<<<L->M, 256, 0, st>>>(s->rc_part, (int)gpart, L->M, s->rc, s->st, nullptr);
     } else {
       k_res_restrict<<<g, CT, 0, st>>>(S, V, s->xbuf[cur], b, s->rc, first ? 1 : 0, s->partials,
                                        s->st);
@@ -1493,8 +1520,11 @@ static void drop_graphs(msb_solver s) {
     s->glaunches[t] = 0;
     if (s->sgexec[t]) cudaGraphExecDestroy(s->sgexec[t]);
     s->sgexec[t] = nullptr;
+    if (s->dgexec[t]) cudaGraphExecDestroy(s->dgexec[t]);
+    s->dgexec[t] = nullptr;
   }
   s->sgkey.clear();
+  s->dgkey.clear();
 }
 
 // Capture `n` iterations of the static stages starting from x buffer `cur0` into a
@@ -1614,6 +1644,10 @@ static msb_status static_graph(msb_ctx ctx, msb_solver s, const double* db, int 
 // Dynamic loop: the N-sized rebuild (dyn_labels on s->dpbuf) as one graph.
 static msb_status labels_graph(msb_ctx ctx, msb_solver s, cudaGraphExec_t* out) {
   *out = nullptr;
+  if (s->lgexec && s->lg_scan != (const void*)ctx->scan_scr) {  // the scan scratch moved
+    cudaGraphExecDestroy(s->lgexec);
+    s->lgexec = nullptr;
+  }
   if (!s->lgexec) {
     msb_status rc = ensure_dyn_pin(ctx, s);
     if (rc) return rc;
@@ -1634,6 +1668,7 @@ static msb_status labels_graph(msb_ctx ctx, msb_solver s, cudaGraphExec_t* out) 
     ctx->stream = user;
     s->lglaunches = g_launches.load() - l0;
     g_launches.fetch_sub(s->lglaunches);
+    s->lg_scan = ctx->scan_scr;
     if (rc) return rc;
     if (e != cudaSuccess) {
       cudaGetLastError();
@@ -1642,6 +1677,169 @@ static msb_status labels_graph(msb_ctx ctx, msb_solver s, cudaGraphExec_t* out) 
     }
   }
   *out = s->lgexec;
+  return MSB_OK;
+}
+
+// ---------------------------------------------------------------- graph-captured dynamic iteration
+// For M_dyn <= SMALL_CHOL_M (most rebuilds) the whole iteration runs as one CUDA graph with
+// M_dyn read on the device: Δp, then the static stages on the context stream in parallel with
+// the rebuild on the rebuild stream (labels, the gate, the constant basis, exact A_c and the
+// one-CTA factorisation), then the dynamic stage — no host enqueue after the M_dyn readback.
+// When the gate is 0 (M_dyn > SMALL_CHOL_M, or max|Δp| = 0) the gated kernels return and the
+// host runs the general path after the graph.  Launch shapes are those of M = SMALL_CHOL_M.
+static int* dyn_gate_ptr(msb_solver s) { return reinterpret_cast<int*>(s->dyn_gate); }
+
+static msb_status dyn_small_finish(msb_ctx ctx, msb_solver s) {
+  msb_op op = s->op;
+  const int64_t N = op->N;
+  cudaStream_t st = ctx->stream;
+  msb_level D = s->dyn_level;
+  const int* Md = dyn_gate_ptr(s) + 4;
+  k_refill_const<<<grid_for(N, 256), 256, 0, st>>>(s->lab, N, D->col, D->P[0]);
+  MSB_LAUNCH_CHECK(ctx);
+  MSB_CUDA_TRY(ctx, cudaMemcpyAsync(D->part, s->lab, N * sizeof(int32_t), cudaMemcpyDeviceToDevice, st));
+  msb_status rc = coarse_assemble_const_gated(ctx, D, op, Md, SMALL_CHOL_M);
+  if (rc) return rc;
+  return coarse_factor_small_gated(ctx, D->co, Md);
+}
+
+static msb_status dyn_small_stage(msb_ctx ctx, msb_solver s, const double* b, int& cur) {
+  msb_op op = s->op;
+  msb_level D = s->dyn_level;
+  cudaStream_t st = ctx->stream;
+  const int* gate = dyn_gate_ptr(s);
+  const int* Md = gate + 4;
+  const IterState* gst = reinterpret_cast<const IterState*>(gate);  // done = gate[0]
+  StencilT S = stencil(op);
+  LevelView V = view(D);
+  const int64_t N = op->N;
+  const unsigned g = grid_for(N, CT), g4 = grid_for(N, CT * CPT);
+  const unsigned gpart = (unsigned)std::min<int64_t>(g, 4 * ctx->sm_count);
+  auto jac = [&]() -> msb_status {
+    for (int v = 0; v < s->nu; ++v) {
+      k_jacobi<CPT><<<g4, CT, 0, st>>>(S, s->xbuf[cur], s->xbuf[cur ^ 1], b, s->omega_s, 0,
+                                       s->partials, gst);
+      MSB_LAUNCH_CHECK(ctx);
+      cur ^= 1;
+    }
+    return MSB_OK;
+  };
+  auto corr = [&]() -> msb_status {
+    k_zero_if<<<1, 256, 0, st>>>(s->rc, SMALL_CHOL_M, gst);
+    MSB_LAUNCH_CHECK(ctx);
+    static bool attr = false;
+    if (!attr) {
+      MSB_CUDA_TRY(ctx, cudaFuncSetAttribute(k_res_restrict_det,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)(RRD_WARPS * RRD_MAX_M * sizeof(double))));
+      attr = true;
+    }
+    k_res_restrict_det<<<gpart, CT, (size_t)RRD_WARPS * SMALL_CHOL_M * sizeof(double), st>>>(
+        S, V, 0, s->xbuf[cur], b, s->rc_part, 0, s->partials, gst, Md);
+    MSB_LAUNCH_CHECK(ctx);
+    k_rc_combine<<<SMALL_CHOL_M, 256, 0, st>>>(s->rc_part, (int)gpart, 0, s->rc, gst, Md);
+    MSB_LAUNCH_CHECK(ctx);
+    coarse_solve_small_gated(ctx, D->co, s->rc, s->xc, gate, Md);
+    k_prolong<<<g, CT, 0, st>>>(V, s->xbuf[cur], s->xc, gst);
+    MSB_LAUNCH_CHECK(ctx);
+    return MSB_OK;
+  };
+  msb_status rc;
+  if (s->post) {
+    if ((rc = corr())) return rc;
+    return jac();
+  }
+  if ((rc = jac())) return rc;
+  return corr();
+}
+
+// the whole rebuild iteration from x buffer cur0 as one graph (see above); *cur_static = the
+// buffer after the static stages, *cur_small = after the small dynamic stage
+static msb_status dyn_graph(msb_ctx ctx, msb_solver s, const double* db, int cur0,
+                            cudaGraphExec_t* out, int* cur_static, int* cur_small) {
+  *out = nullptr;
+  std::vector<const void*> key = {db, ctx->scan_scr, s->rc_part};
+  for (msb_level L : s->levels) {
+    key.push_back(L->P[L->cur]);
+    key.push_back(L->co.Ainv);
+    key.push_back(L->co.sch);
+    key.push_back(L->co.Xp);
+  }
+  if (key != s->dgkey) {
+    for (int t = 0; t < 2; ++t) {
+      if (s->dgexec[t]) cudaGraphExecDestroy(s->dgexec[t]);
+      s->dgexec[t] = nullptr;
+    }
+    s->dgkey = key;
+  }
+  if (!s->dgexec[cur0]) {
+    msb_status rc = ensure_dyn_pin(ctx, s);
+    if (rc) return rc;
+    const unsigned long long* tm = nullptr;
+    if ((rc = op_tmax(ctx, s->op, &tm))) return rc;  // cached before capture
+    if (!s->cap_stream)
+      MSB_CUDA_TRY(ctx, cudaStreamCreateWithFlags(&s->cap_stream, cudaStreamNonBlocking));
+    if (!s->cap_stream2)
+      MSB_CUDA_TRY(ctx, cudaStreamCreateWithFlags(&s->cap_stream2, cudaStreamNonBlocking));
+    if (!s->ev_cf) {
+      MSB_CUDA_TRY(ctx, cudaEventCreateWithFlags(&s->ev_cf, cudaEventDisableTiming));
+      MSB_CUDA_TRY(ctx, cudaEventCreateWithFlags(&s->ev_cj, cudaEventDisableTiming));
+    }
+    cudaStream_t user = ctx->stream;
+    const int64_t l0 = g_launches.load();
+    const int64_t N = s->op->N;
+    int cur = cur0, cs = cur0;
+    cudaError_t e = cudaStreamBeginCapture(s->cap_stream, cudaStreamCaptureModeThreadLocal);
+    if (e == cudaSuccess) {
+      do {
+        ctx->stream = s->cap_stream;
+        k_dp<<<grid_for(N, 256), 256, 0, s->cap_stream>>>(s->xbuf[cur], s->xprev, N, s->dpbuf);
+        count_launch();
+        if ((e = cudaEventRecord(s->ev_cf, s->cap_stream)) != cudaSuccess) break;
+        if ((e = cudaMemcpyAsync(s->xprev, s->xbuf[cur], N * sizeof(double), cudaMemcpyDeviceToDevice,
+                                 s->cap_stream)) != cudaSuccess) break;
+        // rebuild branch
+        if ((e = cudaStreamWaitEvent(s->cap_stream2, s->ev_cf, 0)) != cudaSuccess) break;
+        ctx->stream = s->cap_stream2;
+        if ((rc = dyn_labels(ctx, s, s->dpbuf))) break;
+        k_dyn_gate<<<1, 1, 0, s->cap_stream2>>>(ctx->scan_scr, reinterpret_cast<unsigned long long*>(s->scratch_i),
+                                                s->st, dyn_gate_ptr(s));
+        count_launch();
+        if ((e = cudaEventRecordWithFlags(s->ev_lab, s->cap_stream2, cudaEventRecordExternal)) != cudaSuccess)
+          break;
+        if ((rc = dyn_small_finish(ctx, s))) break;
+        if ((e = cudaEventRecord(s->ev_cj, s->cap_stream2)) != cudaSuccess) break;
+        // static stages, then the (gated) dynamic stage
+        ctx->stream = s->cap_stream;
+        bool first = false;
+        for (msb_level L : s->levels)
+          if ((rc = enqueue_stage(ctx, s, L, db, cur, first))) break;
+        if (rc) break;
+        cs = cur;
+        if ((e = cudaStreamWaitEvent(s->cap_stream, s->ev_cj, 0)) != cudaSuccess) break;
+        if ((rc = dyn_small_stage(ctx, s, db, cur))) break;
+      } while (false);
+      cudaGraph_t graph = nullptr;
+      cudaError_t e2 = cudaStreamEndCapture(s->cap_stream, &graph);
+      if (!rc && e == cudaSuccess && e2 == cudaSuccess) e = cudaGraphInstantiate(&s->dgexec[cur0], graph, 0);
+      else if (e == cudaSuccess && e2 != cudaSuccess) e = e2;
+      if (graph) cudaGraphDestroy(graph);
+    }
+    ctx->stream = user;
+    s->dglaunches[cur0] = g_launches.load() - l0;
+    g_launches.fetch_sub(s->dglaunches[cur0]);
+    s->dcur_static[cur0] = cs;
+    s->dcur_small[cur0] = cur;
+    if (rc) return rc;
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      s->dgexec[cur0] = nullptr;
+      return set_error(ctx, MSB_ECUDA, "dynamic-iteration graph: %s", cudaGetErrorString(e));
+    }
+  }
+  *out = s->dgexec[cur0];
+  *cur_static = s->dcur_static[cur0];
+  *cur_small = s->dcur_small[cur0];
   return MSB_OK;
 }
 
@@ -1819,6 +2017,39 @@ msb_status msb_ms_iterate(msb_ctx ctx, msb_solver s, const double* b, double* x,
       int k = hs.k;  // iteration about to run (1-based)
       int32_t M = 0;
       const bool rebuild = k >= 2;
+      if (rebuild && s->smoother == 0) {  // one graph; the general path only for large M_dyn
+        cudaGraphExec_t dg = nullptr;
+        int cs = cur, csm = cur;
+        if ((rc = dyn_graph(ctx, s, db, cur, &dg, &cs, &csm))) return rc;
+        MSB_CUDA_TRY(ctx, cudaGraphLaunch(dg, st));
+        g_launches.fetch_add(s->dglaunches[cur], std::memory_order_relaxed);
+        MSB_CUDA_TRY(ctx, cudaEventSynchronize(s->ev_lab));  // M_dyn, max|Δp| in dyn_pin
+        double mxv = 0.0;
+        dyn_read(s, &M, &mxv);
+        if (!(mxv > 0.0)) M = 0;
+        if (M > 0 && M <= SMALL_CHOL_M) {  // the graph ran the stage
+          cur = csm;
+          D->cur = 0;
+          D->M = M;
+          D->co.M = M;
+          D->co.kind = 0;
+          D->co.small = true;
+          D->co.ready = true;
+        } else {
+          cur = cs;
+          if (M > 0) {  // general path after the graph, on the context stream
+            D->co.defer_check = true;
+            rc = dyn_finish(ctx, s, M, nullptr);
+            D->co.defer_check = false;
+            if (rc) return rc;
+            bool first = false;
+            if ((rc = enqueue_stage(ctx, s, D, db, cur, first))) return rc;
+          }
+        }
+        dynM.push_back(M);
+        cur_after.push_back(cur);
+        continue;
+      }
       if (rebuild) {
         k_dp<<<grid_for(N, 256), 256, 0, st>>>(s->xbuf[cur], s->xprev, N, s->dpbuf);
         MSB_LAUNCH_CHECK(ctx);
@@ -1917,6 +2148,10 @@ msb_status msb_solver_destroy(msb_solver s) {
   if (s->ev_dp) cudaEventDestroy(s->ev_dp);
   if (s->ev_dyn) cudaEventDestroy(s->ev_dyn);
   if (s->ev_lab) cudaEventDestroy(s->ev_lab);
+  if (s->cap_stream2) cudaStreamDestroy(s->cap_stream2);
+  if (s->ev_cf) cudaEventDestroy(s->ev_cf);
+  if (s->ev_cj) cudaEventDestroy(s->ev_cj);
+  dfree(ctx, s->dyn_gate);
   if (s->lgexec) cudaGraphExecDestroy(s->lgexec);
   if (s->dyn_pin) cudaFreeHost(s->dyn_pin);
   delete s;
