@@ -521,6 +521,10 @@ void coarse_solve(msb_ctx ctx, const Coarse& co, const double* rc, double* xc, c
     coarse_solve_small(ctx, co, rc, xc, done);
     return;
   }
+  if (co.tri && co.coop) {
+    coarse_solve_coop(ctx, co, rc, xc, done);
+    return;
+  }
   if (co.tri) {
     const unsigned g = grid_for((int64_t)co.M * 32, 256);
     k_trmv_lower<<<g, 256, 0, ctx->stream>>>(co.Ainv, co.M, rc, co.tri_y);

@@ -619,6 +619,205 @@ void coarse_solve_small(msb_ctx ctx, const Coarse& co, const double* rc, double*
   count_launch();
 }
 
+// ---------------------------------------------------------------- mid-size SPD systems
+// M_dyn in (SMALL_CHOL_M, 1024] (the dynamic stage's larger partitions, factored for one
+// solve): a blocked right-looking LDL^T in ONE cooperative launch of persistent CTAs with
+// grid barriers between its phases, instead of the recursion's ~50 dependent launches.
+// Per panel of 32 columns: (1) one warp factors the 32 x 32 diagonal block in registers
+// (lane i owns row i; the pivot rows reach the other lanes by shuffles); (2) every row below
+// is forward-substituted with the unit block (u_i = the row's panel entries, L'_i = u_i D^-1;
+// u kept in a scratch); (3) the trailing lower triangle is updated by 32 x 32 tiles,
+// A_ik -= u_i . L'_k.  A (row-major, ld M) is overwritten by L' (strictly lower) and d (the
+// diagonal); dinv = 1/d.  Pivot test as the other factorisations.
+constexpr int CP_B = 32, CP_T2 = 256;
+
+__device__ __forceinline__ void coop_grid_sync(unsigned* bar, unsigned target) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(bar, 1u);
+    unsigned v;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
+    } while (v < target);
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(CP_T2) k_ldl_coop(double* __restrict__ A, int M, double* __restrict__ U,
+                                                    double* __restrict__ dinv,
+                                                    const unsigned long long* amax_bits,
+                                                    int* __restrict__ singular, unsigned* bar) {
+  __shared__ double lb[CP_B][CP_B + 1];
+  __shared__ double us[CP_B][CP_B + 1];
+  __shared__ double di[CP_B];
+  const double tol = 1e-14 * __longlong_as_double((long long)*amax_bits);
+  unsigned phase = 0;
+  for (int p = 0; p < M; p += CP_B) {
+    const int pe = min(p + CP_B, M), nb = pe - p;
+    // (1) the diagonal block, one warp of CTA 0
+    if (blockIdx.x == 0 && threadIdx.x < 32) {
+      const int i = threadIdx.x;
+      double row[CP_B];
+#pragma unroll
+      for (int k = 0; k < CP_B; ++k)
+        row[k] = (i < nb && k <= i) ? A[(int64_t)(p + i) * M + p + k] : (k == i ? 1.0 : 0.0);
+#pragma unroll
+      for (int j = 0; j < CP_B; ++j) {
+        double dj = __shfl_sync(0xffffffffu, row[j], j);
+        if (j < nb && !(dj > tol)) {
+          if (i == 0) *singular = 1;
+          dj = 1.0;
+          if (i == j) row[j] = 1.0;
+        }
+        const double rj = 1.0 / dj;
+        const double u = i > j ? row[j] : 0.0;
+        const double l = u * rj;
+#pragma unroll
+        for (int k = j + 1; k < CP_B; ++k) {
+          const double lk = __shfl_sync(0xffffffffu, l, k);
+          if (i >= k) row[k] -= u * lk;
+        }
+        if (i > j) row[j] = l;
+      }
+      if (i < nb) {
+#pragma unroll
+        for (int k = 0; k < CP_B; ++k)
+          if (k <= i) A[(int64_t)(p + i) * M + p + k] = row[k];
+        dinv[p + i] = 1.0 / row[i];
+      }
+    }
+    coop_grid_sync(bar, ++phase * gridDim.x);
+    // (2) the rows below the block
+    for (int e = threadIdx.x; e < CP_B * CP_B; e += CP_T2) {
+      const int r = e / CP_B, c = e % CP_B;
+      lb[r][c] = (r < nb && c < r) ? A[(int64_t)(p + r) * M + p + c] : 0.0;
+    }
+    if (threadIdx.x < CP_B) di[threadIdx.x] = threadIdx.x < nb ? dinv[p + threadIdx.x] : 0.0;
+    __syncthreads();
+    for (int i = pe + blockIdx.x * CP_T2 + threadIdx.x; i < M; i += gridDim.x * CP_T2) {
+      double v[CP_B];
+#pragma unroll
+      for (int t = 0; t < CP_B; ++t) {
+        double x = t < nb ? A[(int64_t)i * M + p + t] : 0.0;
+#pragma unroll
+        for (int q = 0; q < t; ++q) x -= v[q] * lb[t][q];
+        v[t] = x;
+      }
+#pragma unroll
+      for (int t = 0; t < CP_B; ++t)
+        if (t < nb) {
+          U[(int64_t)i * CP_B + t] = v[t];
+          A[(int64_t)i * M + p + t] = v[t] * di[t];
+        }
+    }
+    coop_grid_sync(bar, ++phase * gridDim.x);
+    // (3) the trailing lower triangle, 32 x 32 tiles
+    const int nbk = (M - pe + CP_B - 1) / CP_B;
+    const int ntile = nbk * (nbk + 1) / 2;
+    for (int t = blockIdx.x; t < ntile; t += gridDim.x) {
+      int I = (int)((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
+      while ((I + 1) * (I + 2) / 2 <= t) ++I;
+      while (I * (I + 1) / 2 > t) --I;
+      const int K = t - I * (I + 1) / 2;
+      const int i0 = pe + I * CP_B, k0 = pe + K * CP_B;
+      __syncthreads();
+      for (int e = threadIdx.x; e < CP_B * CP_B; e += CP_T2) {
+        const int r = e / CP_B, c = e % CP_B;
+        us[r][c] = (i0 + r < M && c < nb) ? U[(int64_t)(i0 + r) * CP_B + c] : 0.0;
+        lb[r][c] = (k0 + r < M && c < nb) ? A[(int64_t)(k0 + r) * M + p + c] : 0.0;
+      }
+      __syncthreads();
+      const int r = threadIdx.x / 8, c0 = threadIdx.x % 8;
+      const int gi = i0 + r;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int c = c0 + 8 * q, gk = k0 + c;
+        if (gi < M && gk < M && gk <= gi) {
+          double x = A[(int64_t)gi * M + gk];
+#pragma unroll
+          for (int tt = 0; tt < CP_B; ++tt) x -= us[r][tt] * lb[c][tt];
+          A[(int64_t)gi * M + gk] = x;
+        }
+      }
+    }
+    coop_grid_sync(bar, ++phase * gridDim.x);
+  }
+}
+
+// x = L'^{-T} D^{-1} L'^{-1} r with k_ldl_coop's output, one CTA of 1024 threads in panels of
+// 32: the panel's triangle by one warp (shuffles), the rest of the vector by all threads
+constexpr int CS_T = 1024;
+__global__ void __launch_bounds__(CS_T) k_ldl_coop_solve(const double* __restrict__ A, int M,
+                                                         const double* __restrict__ dinv,
+                                                         const double* __restrict__ r,
+                                                         double* __restrict__ x, const int* done) {
+  __shared__ double y[1024];
+  __shared__ double lb[CP_B][CP_B + 1];
+  const int tid = threadIdx.x;
+  if (tid < M) y[tid] = r[tid];
+  for (int p = 0; p < M; p += CP_B) {  // L' y = r
+    const int pe = min(p + CP_B, M), nb = pe - p;
+    {
+      const int rr = tid / CP_B, c = tid % CP_B;
+      lb[rr][c] = (rr < nb && c < rr) ? A[(int64_t)(p + rr) * M + p + c] : 0.0;
+    }
+    __syncthreads();
+    if (tid < 32) {
+      double yl = tid < nb ? y[p + tid] : 0.0;
+#pragma unroll
+      for (int j = 0; j < CP_B; ++j) {
+        const double yj = __shfl_sync(0xffffffffu, yl, j);
+        if (tid > j) yl -= lb[tid][j] * yj;
+      }
+      if (tid < nb) y[p + tid] = yl;
+    }
+    __syncthreads();
+    const int i = pe + tid;
+    if (i < M) {
+      double s = y[i];
+#pragma unroll 8
+      for (int t = 0; t < nb; ++t) s -= A[(int64_t)i * M + p + t] * y[p + t];
+      y[i] = s;
+    }
+    __syncthreads();
+  }
+  if (tid < M) y[tid] *= dinv[tid];
+  __syncthreads();
+  for (int p = ((M - 1) / CP_B) * CP_B; p >= 0; p -= CP_B) {  // L'^T x = y
+    const int pe = min(p + CP_B, M), nb = pe - p;
+    {
+      const int rr = tid / CP_B, c = tid % CP_B;
+      lb[rr][c] = (rr < nb && c < rr) ? A[(int64_t)(p + rr) * M + p + c] : 0.0;
+    }
+    __syncthreads();
+    if (tid < 32) {
+      double yl = tid < nb ? y[p + tid] : 0.0;
+#pragma unroll
+      for (int j = CP_B - 1; j >= 0; --j) {
+        const double xj = __shfl_sync(0xffffffffu, yl, j);
+        if (tid < j) yl -= lb[j][tid] * xj;
+      }
+      if (tid < nb) y[p + tid] = yl;
+    }
+    __syncthreads();
+    if (tid < p) {
+      double s = y[tid];
+#pragma unroll 8
+      for (int t = 0; t < nb; ++t) s -= A[(int64_t)(p + t) * M + tid] * y[p + t];
+      y[tid] = s;
+    }
+    __syncthreads();
+  }
+  const bool skip = done && *(volatile const int*)done;
+  if (!skip && tid < M) x[tid] = y[tid];
+}
+
+void coarse_solve_coop(msb_ctx ctx, const Coarse& co, const double* rc, double* xc, const int* done) {
+  k_ldl_coop_solve<<<1, CS_T, 0, ctx->stream>>>(co.L, co.M, co.tri_y, rc, xc, done);
+  count_launch();
+}
+
 // The dynamic loop's graph-captured small path: the one-CTA factorisation of an M x M
 // system (M <= SMALL_CHOL_M) with M read from the device (*Md; 0 = nothing to do), and its
 // solve.  Launch shapes are those of M = SMALL_CHOL_M.
@@ -656,6 +855,41 @@ msb_status coarse_factor_dense(msb_ctx ctx, Coarse& co) {
   unsigned long long* amax = co.flags;
   int* sing = reinterpret_cast<int*>(co.flags + 1);
   co.small = co.tri && M <= SMALL_CHOL_M;
+  co.coop = co.tri && !co.small && M <= 1024;
+  if (co.coop) {
+    if (!co.L || !co.Ainv || !co.tri_y || co.cap < M)
+      return set_error(ctx, MSB_EINVAL, "coarse_factor_dense: mid-size buffers");
+    unsigned* bar = reinterpret_cast<unsigned*>(co.flags) + 3;  // flags[1] high word
+    MSB_CUDA_TRY(ctx, cudaMemsetAsync(co.flags, 0, 16, s));
+    k_absmax2<<<std::min<int64_t>(grid_for((int64_t)M * M, 256), 4 * ctx->sm_count), 256, 0, s>>>(
+        co.Ac, (int64_t)M * M, amax);
+    MSB_LAUNCH_CHECK(ctx);
+    MSB_CUDA_TRY(ctx, cudaMemcpyAsync(co.L, co.Ac, (size_t)M * M * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    const int G = std::min(ctx->sm_count, 128);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(G);
+    cfg.blockDim = dim3(CP_T2);
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    MSB_CUDA_TRY(ctx, cudaLaunchKernelEx(&cfg, k_ldl_coop, co.L, M, co.Ainv, co.tri_y,
+                                         (const unsigned long long*)amax, sing, bar));
+    count_launch();
+    int hs = 0;
+    if (!co.defer_check) {
+      MSB_CUDA_TRY(ctx, cudaMemcpyAsync(&hs, sing, 4, cudaMemcpyDeviceToHost, s));
+      MSB_CUDA_TRY(ctx, cudaStreamSynchronize(s));
+    }
+    if (hs) {
+      co.ready = false;
+      return set_error(ctx, MSB_ESINGULAR, "singular coarse matrix: pivot <= 1e-14 max|A_c| (M=%d)", M);
+    }
+    co.ready = true;
+    return MSB_OK;
+  }
   if (co.small) {
     if (!co.L) MSB_ALLOC(ctx, co.L, double, (int64_t)co.cap * co.cap + co.cap);
     MSB_CUDA_TRY(ctx, cudaMemsetAsync(co.flags, 0, 16, s));
