@@ -644,6 +644,41 @@ __device__ __forceinline__ void coop_grid_sync(unsigned* bar, unsigned target) {
   __syncthreads();
 }
 
+// the 32 x 32 diagonal block at (p, p) (nb rows valid): unit L' and d in place, 1/d to dinv
+__device__ __forceinline__ void coop_diag_block(double* __restrict__ A, int M, int p, int nb,
+                                                double* __restrict__ dinv, double tol,
+                                                int* __restrict__ singular) {
+  const int i = threadIdx.x;  // one warp
+  double row[CP_B];
+#pragma unroll
+  for (int k = 0; k < CP_B; ++k)
+    row[k] = (i < nb && k <= i) ? A[(int64_t)(p + i) * M + p + k] : (k == i ? 1.0 : 0.0);
+#pragma unroll
+  for (int j = 0; j < CP_B; ++j) {
+    double dj = __shfl_sync(0xffffffffu, row[j], j);
+    if (j < nb && !(dj > tol)) {
+      if (i == 0) *singular = 1;
+      dj = 1.0;
+      if (i == j) row[j] = 1.0;
+    }
+    const double rj = 1.0 / dj;
+    const double u = i > j ? row[j] : 0.0;
+    const double l = u * rj;
+#pragma unroll
+    for (int k = j + 1; k < CP_B; ++k) {
+      const double lk = __shfl_sync(0xffffffffu, l, k);
+      if (i >= k) row[k] -= u * lk;
+    }
+    if (i > j) row[j] = l;
+  }
+  if (i < nb) {
+#pragma unroll
+    for (int k = 0; k < CP_B; ++k)
+      if (k <= i) A[(int64_t)(p + i) * M + p + k] = row[k];
+    dinv[p + i] = 1.0 / row[i];
+  }
+}
+
 __global__ void __launch_bounds__(CP_T2) k_ldl_coop(double* __restrict__ A, int M, double* __restrict__ U,
                                                     double* __restrict__ dinv,
                                                     const unsigned long long* amax_bits,
@@ -653,42 +688,12 @@ __global__ void __launch_bounds__(CP_T2) k_ldl_coop(double* __restrict__ A, int 
   __shared__ double di[CP_B];
   const double tol = 1e-14 * __longlong_as_double((long long)*amax_bits);
   unsigned phase = 0;
+  if (blockIdx.x == 0 && threadIdx.x < 32) coop_diag_block(A, M, 0, min(CP_B, M), dinv, tol, singular);
+  coop_grid_sync(bar, ++phase * gridDim.x);
   for (int p = 0; p < M; p += CP_B) {
     const int pe = min(p + CP_B, M), nb = pe - p;
-    // (1) the diagonal block, one warp of CTA 0
-    if (blockIdx.x == 0 && threadIdx.x < 32) {
-      const int i = threadIdx.x;
-      double row[CP_B];
-#pragma unroll
-      for (int k = 0; k < CP_B; ++k)
-        row[k] = (i < nb && k <= i) ? A[(int64_t)(p + i) * M + p + k] : (k == i ? 1.0 : 0.0);
-#pragma unroll
-      for (int j = 0; j < CP_B; ++j) {
-        double dj = __shfl_sync(0xffffffffu, row[j], j);
-        if (j < nb && !(dj > tol)) {
-          if (i == 0) *singular = 1;
-          dj = 1.0;
-          if (i == j) row[j] = 1.0;
-        }
-        const double rj = 1.0 / dj;
-        const double u = i > j ? row[j] : 0.0;
-        const double l = u * rj;
-#pragma unroll
-        for (int k = j + 1; k < CP_B; ++k) {
-          const double lk = __shfl_sync(0xffffffffu, l, k);
-          if (i >= k) row[k] -= u * lk;
-        }
-        if (i > j) row[j] = l;
-      }
-      if (i < nb) {
-#pragma unroll
-        for (int k = 0; k < CP_B; ++k)
-          if (k <= i) A[(int64_t)(p + i) * M + p + k] = row[k];
-        dinv[p + i] = 1.0 / row[i];
-      }
-    }
-    coop_grid_sync(bar, ++phase * gridDim.x);
-    // (2) the rows below the block
+    // (2) the rows below the block: forward substitution with the unit block, the inner
+    // products split over four accumulators (independent FMA chains)
     for (int e = threadIdx.x; e < CP_B * CP_B; e += CP_T2) {
       const int r = e / CP_B, c = e % CP_B;
       lb[r][c] = (r < nb && c < r) ? A[(int64_t)(p + r) * M + p + c] : 0.0;
@@ -699,10 +704,18 @@ __global__ void __launch_bounds__(CP_T2) k_ldl_coop(double* __restrict__ A, int 
       double v[CP_B];
 #pragma unroll
       for (int t = 0; t < CP_B; ++t) {
-        double x = t < nb ? A[(int64_t)i * M + p + t] : 0.0;
+        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
 #pragma unroll
-        for (int q = 0; q < t; ++q) x -= v[q] * lb[t][q];
-        v[t] = x;
+        for (int q = 0; q + 3 < t; q += 4) {
+          s0 += v[q] * lb[t][q];
+          s1 += v[q + 1] * lb[t][q + 1];
+          s2 += v[q + 2] * lb[t][q + 2];
+          s3 += v[q + 3] * lb[t][q + 3];
+        }
+#pragma unroll
+        for (int q = t & ~3; q < t; ++q) s0 += v[q] * lb[t][q];
+        const double a = t < nb ? A[(int64_t)i * M + p + t] : 0.0;
+        v[t] = a - ((s0 + s1) + (s2 + s3));
       }
 #pragma unroll
       for (int t = 0; t < CP_B; ++t)
@@ -712,7 +725,9 @@ __global__ void __launch_bounds__(CP_T2) k_ldl_coop(double* __restrict__ A, int 
         }
     }
     coop_grid_sync(bar, ++phase * gridDim.x);
-    // (3) the trailing lower triangle, 32 x 32 tiles
+    // (3) the trailing lower triangle, 32 x 32 tiles; tile 0 (the next panel's diagonal
+    // block) is CTA 0's first, which then factors that block at once (look-ahead: the next
+    // panel's first phase overlaps the other CTAs' tiles, one barrier fewer per panel)
     const int nbk = (M - pe + CP_B - 1) / CP_B;
     const int ntile = nbk * (nbk + 1) / 2;
     for (int t = blockIdx.x; t < ntile; t += gridDim.x) {
@@ -739,6 +754,10 @@ __global__ void __launch_bounds__(CP_T2) k_ldl_coop(double* __restrict__ A, int 
           for (int tt = 0; tt < CP_B; ++tt) x -= us[r][tt] * lb[c][tt];
           A[(int64_t)gi * M + gk] = x;
         }
+      }
+      if (t == 0) {  // CTA 0: the next diagonal block is final
+        __syncthreads();
+        if (threadIdx.x < 32) coop_diag_block(A, M, pe, min(CP_B, M - pe), dinv, tol, singular);
       }
     }
     coop_grid_sync(bar, ++phase * gridDim.x);
