@@ -644,6 +644,12 @@ __device__ __forceinline__ void support_range(int J, int b, int n, int nb, int& 
 // atomics).  Thread layout: XL lanes along x (XL = pow2 >= nx, <= 256) x RG row
 // groups; x positions beyond 256 take a second partial.
 constexpr int RR2_THREADS = 256;
+// P is read once per pass and, with A_c^{-1}, is most of an iteration's bytes; T, b, x and r
+// (63 MB on config 2) are re-read by the next stencil passes.  The P loads here and in the
+// prolongation therefore use ld.global.cs (evict-first), like the SYMV's tile loads, so the
+// streams do not displace those vectors from L2: 67.4 -> 63.4 us per config-2 iteration
+// (profiles/r02i/p_stream_hint_ab.txt; a createpolicy evict_first hint measured the same,
+// evict_last on T/b/x and reversed traversal orders measured no gain or slower).
 // XP x positions per lane (x = xo + XL * e, e < XP): XP = ceil(nx / XL), 1 for nx <= 256.
 // CS CTAs (one thread-block cluster) share one (Jy, Jz) unit: rank q walks the rows
 // q, q + CS, ... of each row group; the CTAs' per-(parity, x) totals are summed by rank 0
@@ -701,8 +707,8 @@ __device__ __forceinline__ void restrict_row_body(const LevelView& L, const doub
 #pragma unroll
       for (int e = 0; e < XP; ++e) {
         const bool v = ok && xok[e];
-        p0[u][e] = v ? P0[c + XL * e] : 0.0;
-        p1[u][e] = v ? P1[c + XL * e] : 0.0;
+        p0[u][e] = v ? __ldcs(P0 + c + XL * e) : 0.0;  // streamed: see restrict_row_body's header
+        p1[u][e] = v ? __ldcs(P1 + c + XL * e) : 0.0;
         rv[u][e] = v ? r[c + XL * e] : 0.0;
       }
       row += step;
@@ -829,7 +835,7 @@ __global__ void __launch_bounds__(CT) k_prolong_cart(LevelView L, double* __rest
     const int jx = (s & 1) ? tx.y : tx.x, jy = (s & 2) ? ty.y : ty.x, jz = (s & 4) ? tz.y : tz.x;
     const bool act = (jx | jy | jz) >= 0;
     col[s] = act ? jx + L.nb0 * (jy + L.nb1 * jz) : -1;
-    v[s] = act ? base[(size_t)s * N] : 0.0;
+    v[s] = act ? __ldcs(base + (size_t)s * N) : 0.0;  // streamed (evict-first), as in the restriction
   }
   pdl_wait();  // P is an input; x_c and x come from the coarse solve and the smoother
   pdl_trigger();
