@@ -254,6 +254,12 @@ __global__ void __launch_bounds__(32 * (TY + 1)) k_sweep_ws(
     mbar_fence_init();
   }
   uint32_t q = 0, seq = 0;  // ring sequence: producer issue count / consumer item base
+  // T (3 N doubles: 27 MB on config 2) is re-read by every sweep while both P buffers stream
+  // through L2: its boxes are loaded with an evict-last priority so they stay resident across
+  // the sweeps (35.2 -> 33.6 us per config-2 sweep; profiles/r02i/t_evict_last_ab.txt).  An
+  // evict-first hint on the P boxes measured slower (the halo rows shared by neighbouring
+  // CTAs are dropped before their second reader; profiles/r02i/sweep_tma_hint_ab.txt).
+  const unsigned long long pol_t = l2_policy_evict_last();
   for (int j = 0; j < cnt; ++j) {
     const int n = n0 + j;
     if (j > 0) sweep_grid_sync(gbar, (unsigned)j * gridDim.x);
@@ -272,7 +278,7 @@ __global__ void __launch_bounds__(32 * (TY + 1)) k_sweep_ws(
             double* st = sm + slot * B::STAGE;
             mbar_expect_tx(&full[slot], B::TX);
             tma_load_4d(st, mIn, &full[slot], xt * TT_X - 2, yt * TY - 1, k0 - 1 + p, 0);
-            tma_load_4d(st + B::P_DBL, &mT, &full[slot], xt * TT_X - 2, yt * TY - 1, k0 - 1 + p, 0);
+            tma_load_4d_hint(st + B::P_DBL, &mT, &full[slot], xt * TT_X - 2, yt * TY - 1, k0 - 1 + p, 0, pol_t);
           }
         }
       }
