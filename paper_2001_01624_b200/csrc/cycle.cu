@@ -160,6 +160,15 @@ __global__ void __launch_bounds__(CT) k_norm(StencilT S, const double* __restric
 // coalesced): the loads of all CPT cells are in flight together and the grid is CPT
 // times shorter, which is what a short stencil pass needs to approach HBM bandwidth.
 constexpr int CPT = 4;
+// On grids whose stencil working set (5 N doubles) is beyond L2 every load of a pass goes to
+// HBM and the passes gain from more, shorter CTAs instead: CPT_BIG cells per thread (config 5:
+// 527 -> 507 us per iteration with 2; 8 measured 556; on config 2 4 stays best: 63.5 us against
+// 64.5 with 2 and 67.4 with 8; profiles/r02i/cells_per_thread_ab.txt)
+#ifndef MSB_CPT_BIG
+#define MSB_CPT_BIG 2
+#endif
+constexpr int CPT_BIG = MSB_CPT_BIG;
+constexpr int64_t CPT_BIG_MIN_N = 3200000;  // 5 N doubles > 128 MB
 
 // Stencil passes launched as programmatic dependents: the inputs they do not write (the
 // transmissibility planes incl. the -y/-z face planes, and b) are bulk-prefetched into L2
@@ -504,8 +513,10 @@ __global__ void __launch_bounds__(256) k_restrict_csc(const int32_t* __restrict_
   double t0 = 0.0, t1 = 0.0, t2 = 0.0, t3 = 0.0;
   int k = ptr[w] + lane;
   for (; k + 96 < k1; k += 128) {
-    const int p0 = pos[k], p1 = pos[k + 32], p2 = pos[k + 64], p3 = pos[k + 96];
-    const double a0 = P[p0], a1 = P[p1], a2 = P[p2], a3 = P[p3];
+    // the index and P are streamed (ld.cs, evict-first: see restrict_row_body), r is re-read
+    const int p0 = __ldcs(pos + k), p1 = __ldcs(pos + k + 32), p2 = __ldcs(pos + k + 64),
+              p3 = __ldcs(pos + k + 96);
+    const double a0 = __ldcs(P + p0), a1 = __ldcs(P + p1), a2 = __ldcs(P + p2), a3 = __ldcs(P + p3);
     const double b0 = r[p0 - (p0 / N) * N], b1 = r[p1 - (p1 / N) * N], b2 = r[p2 - (p2 / N) * N],
                  b3 = r[p3 - (p3 / N) * N];
     t0 = fma(a0, b0, t0);
@@ -514,8 +525,8 @@ __global__ void __launch_bounds__(256) k_restrict_csc(const int32_t* __restrict_
     t3 = fma(a3, b3, t3);
   }
   for (; k < k1; k += 32) {
-    const int p = pos[k];
-    t0 = fma(P[p], r[p - (p / N) * N], t0);
+    const int p = __ldcs(pos + k);
+    t0 = fma(__ldcs(P + p), r[p - (p / N) * N], t0);
   }
   double t = (t0 + t1) + (t2 + t3);
   for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
@@ -566,8 +577,8 @@ __global__ void __launch_bounds__(CT) k_prolong(LevelView L, double* __restrict_
       double p[4], v[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
-        key[u] = L.col[(size_t)(s + u) * N + c];
-        p[u] = L.P[(size_t)(s + u) * N + c];
+        key[u] = __ldcs(L.col + (size_t)(s + u) * N + c);  // streamed, like the Cartesian P
+        p[u] = __ldcs(L.P + (size_t)(s + u) * N + c);
       }
 #pragma unroll
       for (int u = 0; u < 4; ++u) v[u] = key[u] >= 0 ? p[u] * xc[key[u]] : 0.0;
@@ -1325,10 +1336,20 @@ msb_status msb_add_dynamic_basis(msb_ctx ctx, msb_solver s, const double* dp, in
 // Enqueue one stage (level L) on x buffers; `first` marks the iteration's first kernel.
 // Enqueue one stage (level L) on the x double buffer; `first` marks the iteration's
 // first kernel, which also emits the stop-test partials (finalised right after).
-#define RES_LAUNCH(...) \
-  MSB_CUDA_TRY(ctx, launch_ex(k_residual<CPT>, dim3(g4), dim3(CT), 0, st, kPDL, 1, __VA_ARGS__))
-#define JAC_LAUNCH(...) \
-  MSB_CUDA_TRY(ctx, launch_ex(k_jacobi<CPT>, dim3(g4), dim3(CT), 0, st, kPDL, 1, __VA_ARGS__))
+#define RES_LAUNCH(...)                                                                          \
+  do {                                                                                           \
+    if (big)                                                                                     \
+      MSB_CUDA_TRY(ctx, launch_ex(k_residual<CPT_BIG>, dim3(g4), dim3(CT), 0, st, kPDL, 1, __VA_ARGS__)); \
+    else                                                                                         \
+      MSB_CUDA_TRY(ctx, launch_ex(k_residual<CPT>, dim3(g4), dim3(CT), 0, st, kPDL, 1, __VA_ARGS__));     \
+  } while (0)
+#define JAC_LAUNCH(...)                                                                          \
+  do {                                                                                           \
+    if (big)                                                                                     \
+      MSB_CUDA_TRY(ctx, launch_ex(k_jacobi<CPT_BIG>, dim3(g4), dim3(CT), 0, st, kPDL, 1, __VA_ARGS__));   \
+    else                                                                                         \
+      MSB_CUDA_TRY(ctx, launch_ex(k_jacobi<CPT>, dim3(g4), dim3(CT), 0, st, kPDL, 1, __VA_ARGS__));       \
+  } while (0)
 
 static msb_status enqueue_stage(msb_ctx ctx, msb_solver s, msb_level L, const double* b, int& cur,
                                 bool& first) {
@@ -1338,7 +1359,8 @@ static msb_status enqueue_stage(msb_ctx ctx, msb_solver s, msb_level L, const do
   StencilT S = stencil(op);
   LevelView V = view(L);
   unsigned g = grid_for(N, CT);
-  const unsigned g4 = grid_for(N, CT * CPT);  // multi-cell stencil kernels
+  const bool big = N >= CPT_BIG_MIN_N;
+  const unsigned g4 = grid_for(N, CT * (big ? CPT_BIG : CPT));  // multi-cell stencil kernels
   // With one pre-smoothed level and nu = 1 no kernel of an iteration writes the buffer
   // holding x_{k-1}, so the stop test's finalize runs on a side branch in parallel with
   // the rest of the iteration and is joined before the next iteration's first kernel
