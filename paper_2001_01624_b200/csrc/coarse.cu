@@ -439,7 +439,8 @@ __global__ void k_pack_lower(const double* __restrict__ X, int M, int ntb, doubl
 
 constexpr int SYMV_T = 256;  // threads per tile: 8 double2 of the tile per thread
 
-__global__ void __launch_bounds__(SYMV_T) k_symv_tiles(const double* __restrict__ Xp, int M,
+// 5 CTAs per SM (48 registers): config 2's 1,485 tiles are two resident waves instead of 2.5
+__global__ void __launch_bounds__(SYMV_T, 5) k_symv_tiles(const double* __restrict__ Xp, int M,
                                                        const double* __restrict__ rc,
                                                        double* __restrict__ part) {
   symv_tile_body<false>(Xp, M, rc, part, blockIdx.x);

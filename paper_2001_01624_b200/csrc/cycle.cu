@@ -168,6 +168,7 @@ constexpr int CPT = 4;
 #define MSB_CPT_BIG 2
 #endif
 constexpr int CPT_BIG = MSB_CPT_BIG;
+constexpr int CPT_WAVE = 6;
 constexpr int64_t CPT_BIG_MIN_N = 3200000;  // 5 N doubles > 128 MB
 
 // Stencil passes launched as programmatic dependents: the inputs they do not write (the
@@ -1338,10 +1339,12 @@ msb_status msb_add_dynamic_basis(msb_ctx ctx, msb_solver s, const double* dp, in
 // first kernel, which also emits the stop-test partials (finalised right after).
 #define RES_LAUNCH(...)                                                                          \
   do {                                                                                           \
-    if (big)                                                                                     \
-      MSB_CUDA_TRY(ctx, launch_ex(k_residual<CPT_BIG>, dim3(g4), dim3(CT), 0, st, kPDL, 1, __VA_ARGS__)); \
+    if (rcpt == CPT_BIG)                                                                         \
+      MSB_CUDA_TRY(ctx, launch_ex(k_residual<CPT_BIG>, dim3(gr), dim3(CT), 0, st, kPDL, 1, __VA_ARGS__)); \
+    else if (rcpt == CPT_WAVE)                                                                   \
+      MSB_CUDA_TRY(ctx, launch_ex(k_residual<CPT_WAVE>, dim3(gr), dim3(CT), 0, st, kPDL, 1, __VA_ARGS__)); \
     else                                                                                         \
-      MSB_CUDA_TRY(ctx, launch_ex(k_residual<CPT>, dim3(g4), dim3(CT), 0, st, kPDL, 1, __VA_ARGS__));     \
+      MSB_CUDA_TRY(ctx, launch_ex(k_residual<CPT>, dim3(gr), dim3(CT), 0, st, kPDL, 1, __VA_ARGS__));     \
   } while (0)
 #define JAC_LAUNCH(...)                                                                          \
   do {                                                                                           \
@@ -1360,7 +1363,18 @@ static msb_status enqueue_stage(msb_ctx ctx, msb_solver s, msb_level L, const do
   LevelView V = view(L);
   unsigned g = grid_for(N, CT);
   const bool big = N >= CPT_BIG_MIN_N;
-  const unsigned g4 = grid_for(N, CT * (big ? CPT_BIG : CPT));  // multi-cell stencil kernels
+  const unsigned g4 = grid_for(N, CT * (big ? CPT_BIG : CPT));  // blocks of the smoother pass
+  // the residual pass (48 registers at CPT_WAVE cells per thread: 5 CTAs per SM) takes CPT_WAVE
+  // cells per thread when that makes its grid exactly one resident wave and CPT does not
+  // (config 2: 731 CTAs on 740 slots instead of 1,096 on 888: 64.3 -> 61.9 us per iteration;
+  // 5, 7, 8 cells and the same for the smoother measured slower, profiles/r02i/per_kernel_cpt_occ_ab.txt)
+  const int64_t slots = 5 * (int64_t)ctx->sm_count;
+  const int rcpt = big ? CPT_BIG
+                       : ((int64_t)grid_for(N, CT * CPT) > slots &&
+                                  (int64_t)grid_for(N, CT * CPT_WAVE) <= slots
+                              ? CPT_WAVE
+                              : CPT);
+  const unsigned gr = grid_for(N, CT * rcpt);  // blocks of the residual pass
   // With one pre-smoothed level and nu = 1 no kernel of an iteration writes the buffer
   // holding x_{k-1}, so the stop test's finalize runs on a side branch in parallel with
   // the rest of the iteration and is joined before the next iteration's first kernel
@@ -1396,7 +1410,7 @@ static msb_status enqueue_stage(msb_ctx ctx, msb_solver s, msb_level L, const do
       RES_LAUNCH(S, s->xbuf[cur], b, s->r, first ? 1 : 0, s->partials, s->st);
       MSB_LAUNCH_CHECK(ctx);
       if (first) {
-        msb_status rc = fin(g4);
+        msb_status rc = fin(gr);
         if (rc) return rc;
       }
       first = false;
@@ -1428,7 +1442,7 @@ static msb_status enqueue_stage(msb_ctx ctx, msb_solver s, msb_level L, const do
       RES_LAUNCH(S, s->xbuf[cur], b, s->r, first ? 1 : 0, s->partials, s->st);
       MSB_LAUNCH_CHECK(ctx);
       if (first) {
-        msb_status rc = fin(g4);
+        msb_status rc = fin(gr);
         if (rc) return rc;
       }
       first = false;
@@ -1459,7 +1473,7 @@ static msb_status enqueue_stage(msb_ctx ctx, msb_solver s, msb_level L, const do
       RES_LAUNCH(S, s->xbuf[cur], b, s->r, first ? 1 : 0, s->partials, s->st);
       MSB_LAUNCH_CHECK(ctx);
       if (first) {
-        msb_status rc = fin(g4);
+        msb_status rc = fin(gr);
         if (rc) return rc;
       }
       first = false;
