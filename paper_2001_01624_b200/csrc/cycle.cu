@@ -1364,23 +1364,25 @@ static msb_status enqueue_stage(msb_ctx ctx, msb_solver s, msb_level L, const do
   unsigned g = grid_for(N, CT);
   const bool big = N >= CPT_BIG_MIN_N;
   const unsigned g4 = grid_for(N, CT * (big ? CPT_BIG : CPT));  // blocks of the smoother pass
-  // the residual pass (48 registers at CPT_WAVE cells per thread: 5 CTAs per SM) takes CPT_WAVE
-  // cells per thread when that makes its grid exactly one resident wave and CPT does not
-  // (config 2: 731 CTAs on 740 slots instead of 1,096 on 888: 64.3 -> 61.9 us per iteration;
-  // 5, 7, 8 cells and the same for the smoother measured slower, profiles/r02i/per_kernel_cpt_occ_ab.txt)
-  const int64_t slots = 5 * (int64_t)ctx->sm_count;
-  const int rcpt = big ? CPT_BIG
-                       : ((int64_t)grid_for(N, CT * CPT) > slots &&
-                                  (int64_t)grid_for(N, CT * CPT_WAVE) <= slots
-                              ? CPT_WAVE
-                              : CPT);
-  const unsigned gr = grid_for(N, CT * rcpt);  // blocks of the residual pass
   // With one pre-smoothed level and nu = 1 no kernel of an iteration writes the buffer
   // holding x_{k-1}, so the stop test's finalize runs on a side branch in parallel with
   // the rest of the iteration and is joined before the next iteration's first kernel
   // (kernels that have not yet seen `done` then do harmless work).
   const bool side = s->levels.size() == 1 && s->nu == 1 && !s->post && L->kind == 0 &&
                     s->smoother == 0;
+  // the residual pass (48 registers at CPT_WAVE cells per thread: 5 CTAs per SM) takes CPT_WAVE
+  // cells per thread when that makes its grid exactly one resident wave and CPT does not
+  // (config 2: 731 CTAs on 740 slots instead of 1,096 on 888: 64.3 -> 61.9 us per iteration;
+  // 5, 7, 8 cells and the same for the smoother measured slower, profiles/r02i/per_kernel_cpt_occ_ab.txt);
+  // only in the single-level iteration: with the dynamic rebuild running beside the static
+  // stages (config 3) 4 cells stay faster (0.710 against 0.719 ms per iteration)
+  const int64_t slots = 5 * (int64_t)ctx->sm_count;
+  const int rcpt = big ? CPT_BIG
+                       : (side && (int64_t)grid_for(N, CT * CPT) > slots &&
+                                  (int64_t)grid_for(N, CT * CPT_WAVE) <= slots
+                              ? CPT_WAVE
+                              : CPT);
+  const unsigned gr = grid_for(N, CT * rcpt);  // blocks of the residual pass
 
   auto fin = [&](unsigned np) -> msb_status {  // np = blocks of the kernel that wrote partials
     if (side) {
