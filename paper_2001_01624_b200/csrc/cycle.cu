@@ -827,7 +827,10 @@ static msb_status launch_restrict(msb_ctx ctx, cudaStream_t st, unsigned units, 
 // with no branches, so all sixteen are in flight together.  (Four cells per thread, as
 // the stencil passes use, measured 27 us against 17 us here: the dependent x_c gathers
 // need the occupancy more than the extra loads in flight.)
-__global__ void __launch_bounds__(CT) k_prolong_cart(LevelView L, double* __restrict__ x,
+// bounded to 40 registers (6 CTAs per SM): the dependent x_c gathers need the occupancy
+// (config 5 523 -> 501 us per iteration, config 2 61.9 -> 61.0; 7 and 8 CTAs per SM spill and
+// measured 561 / 73.6 us; profiles/r02i/prolong_occupancy_ab.txt)
+__global__ void __launch_bounds__(CT, 6) k_prolong_cart(LevelView L, double* __restrict__ x,
                                                      const double* __restrict__ xc,
                                                      const IterState* st) {
   const bool done = is_done(st);
