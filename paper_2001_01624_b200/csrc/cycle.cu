@@ -164,11 +164,8 @@ constexpr int CPT = 4;
 // HBM and the passes gain from more, shorter CTAs instead: CPT_BIG cells per thread (config 5:
 // 527 -> 507 us per iteration with 2; 8 measured 556; on config 2 4 stays best: 63.5 us against
 // 64.5 with 2 and 67.4 with 8; profiles/r02i/cells_per_thread_ab.txt)
-#ifndef MSB_CPT_BIG
-#define MSB_CPT_BIG 2
-#endif
-constexpr int CPT_BIG = MSB_CPT_BIG;
-constexpr int CPT_WAVE = 6;
+constexpr int CPT_BIG = 2;
+constexpr int CPT_WAVE = 6;  // residual pass of the single-level iteration: see enqueue_stage
 constexpr int64_t CPT_BIG_MIN_N = 3200000;  // 5 N doubles > 128 MB
 
 // Stencil passes launched as programmatic dependents: the inputs they do not write (the
